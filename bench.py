@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""bench.py — RgCSR SpMV GFLOP/s and achieved HBM GB/s (% of roofline) on B200.
+
+Headline workload (BASELINE.json configs[1]): 3D 27-point stencil 128^3
+(2,097,152 rows, 55,742,968 nnz), fp64, RgCSR group size 32.  One step = one
+y = A x over the whole matrix (K2, one kernel launch) with A and x resident in
+HBM; the 681 MB matrix exceeds the 126 MB L2, so no flush is needed between
+steps (x, 16.8 MB, stays L2-resident as it would in an iterated solver).
+fp32, Hybrid ELL+COO (the paper's comparison format) and the conversion time
+ride along in ``variants``.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload 27pt-128|5pt-1024|powerlaw-8M|7pt-512]
+
+N > 1 (torchrun, one rank per GPU): the matrix is cut into group-aligned row
+slabs (paper_1012_2270_b200.partition), each step is one slab SpMV plus the
+NCCL all-gather of the next x (x_{k+1} = y_k * 2^-4, fused into the SpMV
+epilogue), timed as the max over ranks; scaling "strong" (fixed matrix).
+
+``--impl reference`` times the reference's own CPU spmv_rgcsr (oracle/_ref:
+the unmodified reference compiled in place; the plain-C port when _ref is not
+present) on the same workload with all host threads, as row slabs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of roofline) fp32/fp64 at 1/2/4/8 B200"
+
+WORKLOADS = {
+    # name: (kind, n or rows, group size, description)
+    "27pt-128": ("stencil", 27, 128, "3D 27-point stencil 128^3 (BASELINE configs[1])"),
+    "5pt-1024": ("stencil", 5, 1024, "2D 5-point Poisson 1024^2 (BASELINE configs[0])"),
+    "7pt-512": ("stencil", 7, 512, "3D 7-point Poisson 512^3 (BASELINE configs[4])"),
+    "powerlaw-8M": ("powerlaw", None, 8_000_000, "power-law rows, 8M (BASELINE configs[2])"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def committed_traffic(key):
+    """ncu dram bytes per launch of the dominant kernel (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.REASONS.items() if self.reasons & b and b != 0x1]}
+
+
+# ---------------------------------------------------------------- inputs
+def make_csr(workload):
+    """Device CSR of the workload (stencils generated directly in HBM)."""
+    from paper_1012_2270_b200 import generators as gen
+    from paper_1012_2270_b200 import spmvkit as sk
+    kind, a, b, _ = WORKLOADS[workload]
+    if kind == "stencil":
+        return sk.CsrMatrix.stencil(a, b)
+    return sk.build_csr(gen.powerlaw(b, 7))
+
+
+def host_csr(workload):
+    """Host CSR of the same workload (for the CPU reference)."""
+    from paper_1012_2270_b200 import generators as gen
+    kind, a, b, _ = WORKLOADS[workload]
+    m = gen.stencil(a, b) if kind == "stencil" else gen.powerlaw(b, 7)
+    return m.num_rows, m.num_cols, m.row_ptr, m.col, m.val
+
+
+# ---------------------------------------------------------------- timing helpers
+def time_launches(fn, stream, steps, warmup):
+    """Warm up, then time `steps` launches with per-launch CUDA events on
+    `stream` (barrier+sync both sides).  Returns (total_ms, [per-launch ms])."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for s, e in ev:
+            s.record(stream)
+            fn()
+            e.record(stream)
+        t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1), [s.elapsed_time(e) for s, e in ev]
+
+
+def rg_bytes(info, sv):
+    """Algorithmic bytes per SpMV: FillReport bytes + x read + y write."""
+    fr = info.bytes_double if sv == 8 else info.bytes_single
+    return fr + sv * (info.num_cols + info.num_rows)
+
+
+def hy_bytes(info, sv):
+    fr = info.bytes_double if sv == 8 else info.bytes_single
+    return fr + sv * (info.num_cols + info.num_rows)
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(workload, sample_reps, threads=None, fmt="rgcsr", G=32, prec=8):
+    """Times the reference CPU SpMV on the host cores.  kind 'reference' = the
+    unmodified reference (oracle/_ref), else the plain-C port (oracle)."""
+    import ctypes as C
+    import oracle as orc
+    rows, cols, rp, col, val = host_csr(workload)
+    threads = threads or os.cpu_count() or 1
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(cols, 1).astype(dt)
+    y = np.empty(rows, dt)
+    m = orc.Csr(rows, cols, rp, col, val)
+    nnz = m.nnz
+    if orc.ref_available():
+        r = orc.RefMatrix.from_csr(m)
+        h = C.c_void_p()
+        orc._rcheck(orc.R().ref_slabs_build(r.h, 1 if fmt == "rgcsr" else 2, G, -1, prec,
+                                            threads, C.byref(h)))
+        run = lambda: orc._rcheck(orc.R().ref_slabs_spmv(h, x.ctypes.data, y.ctypes.data))  # noqa: E731
+        kind = "reference"
+        cleanup = lambda: orc.R().ref_slabs_free(h)  # noqa: E731
+        used = threads
+    else:
+        a = orc.build_rgcsr(m, G, prec)
+        run = lambda: orc.spmv_rgcsr(a, x)  # noqa: E731
+        kind, used, cleanup = "port", 1, (lambda: None)
+    run()
+    times = []
+    for _ in range(sample_reps):
+        t = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t)
+    cleanup()
+    med = statistics.median(times)
+    return {"value": 2.0 * nnz / med / 1e9, "unit": "GFLOP/s", "cores": used, "kind": kind,
+            "sample": f"{sample_reps} full {fmt} SpMVs of {workload} ({WORKLOADS[workload][3]}), "
+                      f"{'fp64' if prec == 8 else 'fp32'}, median; {used} row-slab threads of the "
+                      f"{'unmodified reference spmv_rgcsr' if kind == 'reference' else 'C port'}",
+            "seconds_per_spmv": med}
+
+
+# ---------------------------------------------------------------- arms
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = args.steps
+    base = cpu_reference(args.workload, max(steps, 1))
+    line = {"metric": METRIC, "value": base["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup,
+            "ms_per_step": base["seconds_per_spmv"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "format": "rgcsr", "group_size": 32,
+                       "description": WORKLOADS[args.workload][3]},
+            "impl": "reference", "cpu_baseline": {k: base[k] for k in
+                                                  ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    from paper_1012_2270_b200 import spmvkit as sk
+    from paper_1012_2270_b200._lib import lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_1012_2270_b200 import partition
+        return partition.bench_distributed(args, METRIC, WORKLOADS)
+
+    torch.cuda.set_device(0)
+    assert lib().spmvk_init(0) == 0, sk._lib.last_error()
+    peak, peak_kind = peaks()
+    stream = torch.cuda.Stream()
+    G = 32
+
+    t = time.perf_counter()
+    csr = make_csr(args.workload)
+    torch.cuda.synchronize()
+    t_csr = time.perf_counter() - t
+    t = time.perf_counter()
+    a = sk.build_rgcsr(csr, G, 8, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t_conv = time.perf_counter() - t
+    nnz = a.nnz()
+    from paper_1012_2270_b200 import generators as gen
+    xh = gen.random_vector(a.num_cols, 1)
+    x = torch.from_numpy(xh).cuda()
+    y = torch.empty(a.num_rows, dtype=torch.float64, device="cuda")
+    sp = stream.cuda_stream
+    L = lib()
+
+    def step():
+        L.spmvk_rgcsr_spmv_f64(a._h, x.data_ptr(), a.num_cols, y.data_ptr(), a.num_rows, sp)
+
+    clocks = ClockSampler(0)
+    torch.cuda.synchronize()
+    with clocks:
+        total_ms, per = time_launches(step, stream, args.steps, args.warmup)
+    ms = total_ms / args.steps
+    kern_ms = statistics.mean(per)
+    B = rg_bytes(a.info, 8)
+    achieved = B / (kern_ms * 1e-3) / 1e9
+    value = 2.0 * nnz / (ms * 1e-3) / 1e9
+
+    # parity gate on the measured output (checksum vs the committed golden)
+    ysum = float(np.cumsum(y.cpu().numpy())[-1])
+
+    # ---- e2e: reference-facing C-ABI span overload with pinned HOST buffers
+    xpin = torch.from_numpy(xh).pin_memory()
+    ypin = torch.empty(a.num_rows, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    for _ in range(2):
+        L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols, ypin.data_ptr(),
+                                    a.num_rows, None)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        rc = L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols, ypin.data_ptr(),
+                                         a.num_rows, None)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t) / e2e_steps
+    assert rc == 0, sk._lib.last_error()
+    assert float(np.cumsum(ypin.numpy())[-1]) == ysum
+
+    # ---- variants: fp32 RgCSR, Hybrid fp64/fp32 (same timing method)
+    variants = {}
+    for label, builder, prec in (("rgcsr_f32_g32", "rg", 4), ("hybrid_f64", "hy", 8),
+                                 ("hybrid_f32", "hy", 4)):
+        dt = torch.float64 if prec == 8 else torch.float32
+        xv = x.to(dt)
+        yv = torch.empty(a.num_rows, dtype=dt, device="cuda")
+        tt = time.perf_counter()
+        if builder == "rg":
+            h = sk.build_rgcsr(csr, G, prec, stream=sp)
+            fn = L.spmvk_rgcsr_spmv_f32
+            Bv = rg_bytes(h.info, prec)
+        else:
+            h = sk.build_hybrid(csr, None, prec, stream=sp)
+            fn = L.spmvk_hybrid_spmv_f64 if prec == 8 else L.spmvk_hybrid_spmv_f32
+            Bv = hy_bytes(h.info, prec)
+        torch.cuda.synchronize()
+        tconv = time.perf_counter() - tt
+        _, pv = time_launches(lambda: fn(h._h, xv.data_ptr(), h.num_cols, yv.data_ptr(),
+                                         h.num_rows, sp), stream, args.steps, args.warmup)
+        km = statistics.mean(pv)
+        variants[label] = {"gflops": 2.0 * nnz / (km * 1e-3) / 1e9, "kernel_us": km * 1e3,
+                           "bytes": Bv, "achieved_gbs": Bv / (km * 1e-3) / 1e9,
+                           "frac_of_peak": Bv / (km * 1e-3) / 1e9 / peak,
+                           "convert_ms": tconv * 1e3}
+        if builder == "hy":
+            variants[label]["ell_width"] = h.slots_per_row
+            variants[label]["coo_nnz"] = h.coo_nnz()
+        del h
+
+    cpu = cpu_reference(args.workload, args.cpu_reps)
+    traffic = committed_traffic(f"{args.workload}/rgcsr_f64_g32")
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload][3],
+                   "format": "rgcsr", "group_size": G, "nnz": nnz, "rows": a.num_rows,
+                   "slots": a.slot_count(), "parallelism": "single GPU",
+                   "l2": "inputs larger than L2: matrix %.0f MB vs 126 MB L2; x stays L2-resident"
+                         % (B / 1e6)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "bytes_per_launch": B, "kernel_us": kern_ms * 1e3,
+                     "traffic": traffic},
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,
+                "ms_per_step": e2e_s * 1e3,
+                "path": "spmvk_rgcsr_spmv_host_f64 (pinned host x,y; H2D + SpMV + D2H)"},
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+        "checksum": ysum,
+        "convert_ms": {"csr_ingest": t_csr * 1e3, "rgcsr_g32_f64": t_conv * 1e3},
+        "variants": variants,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="27pt-128", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-reps", type=int, default=10)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

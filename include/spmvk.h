@@ -1,0 +1,208 @@
+/* include/spmvk.h — the drop-in C-ABI of the B200-native RgCSR / Hybrid SpMV.
+ *
+ * The reference (arxiv/paper_1012_2270, /root/reference/proj/core) exposes its
+ * hot path as header-only C++ templates in namespace spmvkit; it has no FFI.
+ * Every entry point below replaces one of those templates (file:line relative
+ * to /root/reference/proj/) and keeps its argument meaning and its error
+ * behaviour: where the reference throws std::invalid_argument this returns
+ * SPMVK_EINVAL, where it throws std::runtime_error this returns SPMVK_ERANGE,
+ * with the reference's message (or a more specific one) in spmvk_last_error().
+ * include/spmvkit_gpu.hpp restores the reference's C++ names, signatures and
+ * exceptions on top of this header.
+ *
+ * Conventions
+ *  - return 0 on success; nonzero spmvk_status otherwise;
+ *  - handles are opaque, own their device memory and are immutable after
+ *    build, so concurrent SpMVs on different streams are safe;
+ *  - x / y in the *_spmv_* calls are DEVICE pointers owned by the caller,
+ *    with their element counts passed like the reference's std::span sizes;
+ *    *_spmv_host_* take HOST pointers and do H2D / D2H inside (the span
+ *    overloads' semantics, synchronous);
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *  - indices are uint32_t like spmvkit::index_t (spmvkit/triplet.hpp:12).
+ *    Unlike the reference, a slot count that overflows 32 bits is REPORTED
+ *    (SPMVK_ERANGE) instead of silently truncated (spmvkit/rgcsr.hpp:56).
+ *  - no CPU fallback: without a usable sm_100 device every call that needs
+ *    the GPU returns SPMVK_ECUDA.
+ */
+#ifndef SPMVK_H
+#define SPMVK_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMVK_ABI_VERSION 1
+
+typedef enum {
+  SPMVK_OK = 0,
+  SPMVK_EINVAL = 1, /* std::invalid_argument in the reference */
+  SPMVK_ERANGE = 2, /* std::runtime_error (size budget / 32-bit overflow) */
+  SPMVK_ECUDA = 3,  /* CUDA runtime / launch failure */
+  SPMVK_ENCCL = 4,  /* collective failure (distributed path) */
+  SPMVK_ENOMEM = 5  /* device allocation failure */
+} spmvk_status;
+
+/* Storage precision: the reference's Scalar template argument
+ * (spmvkit/memsim.hpp:14-16 Precision; instantiated at src/bench.cpp:135-137). */
+typedef enum { SPMVK_F32 = 4, SPMVK_F64 = 8 } spmvk_precision;
+
+typedef struct spmvk_csr spmvk_csr;
+typedef struct spmvk_rgcsr spmvk_rgcsr;
+typedef struct spmvk_hybrid spmvk_hybrid;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* spmvk_last_error(void);
+int spmvk_abi_version(void);
+/* Selects the CUDA device for subsequent calls on this thread and checks it
+ * is an sm_100-class part. */
+int spmvk_init(int device);
+
+/* ------------------------------------------------------------------ CSR ingest
+ * Replaces TripletMatrix(num_rows, num_cols, entries) validation
+ * (src/triplet.cpp:22-32) + build_csr<S> (spmvkit/csr.hpp:24-39): the input is
+ * a canonical matrix given as CSR arrays on the HOST (row_ptr[rows+1],
+ * col[nnz], val[nnz]); entries must be in bounds and strictly increasing in
+ * column within each row (EINVAL otherwise, validated on the device).
+ * `val_prec` says whether `val` holds double (the triplet's value type) or
+ * float (an already-cast CsrMatrix<float>). */
+int spmvk_csr_upload(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t* row_ptr,
+                     const uint32_t* col, const void* val, int val_prec, void* stream,
+                     spmvk_csr** out);
+/* Same, from DEVICE arrays (copied device-to-device; the caller keeps its own). */
+int spmvk_csr_upload_device(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t* row_ptr,
+                            const uint32_t* col, const void* val, int val_prec, void* stream,
+                            spmvk_csr** out);
+/* Synthetic shapes generated directly in HBM:
+ * kind 5 = 2D 5-point n x n, 7 = 3D 7-point n^3, 27 = 3D 27-point n^3. */
+int spmvk_csr_stencil(int kind, uint64_t n, void* stream, spmvk_csr** out);
+/* rows, cols, nnz, val precision */
+int spmvk_csr_shape(const spmvk_csr* a, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                    int* val_prec);
+int spmvk_csr_download(const spmvk_csr* a, uint32_t* row_ptr, uint32_t* col, void* val);
+/* Row-length statistics (src/triplet.cpp:51-69 row_lengths / matrix_stats):
+ * out[0]=max out[1]=min (rows>0). */
+int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2);
+/* spmv_csr (spmvkit/csr.hpp:41-53): thread-per-row, same accumulation order. */
+int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
+                       void* stream);
+int spmvk_csr_spmv_f32(const spmvk_csr* a, const float* x, uint64_t nx, float* y, uint64_t ny,
+                       void* stream);
+void spmvk_csr_destroy(spmvk_csr* a);
+
+/* ------------------------------------------------------------------ RgCSR */
+typedef struct {
+  uint64_t num_rows, num_cols, group_size, num_groups;
+  uint64_t slots;            /* RgcsrMatrix::slot_count (rgcsr.hpp:35) */
+  uint64_t nnz;              /* sum of row_lengths = multiply-adds per SpMV */
+  uint64_t artificial_zeros; /* FillReport (fill.hpp:90-95) */
+  uint64_t bytes_single, bytes_double;
+  int precision;
+} spmvk_rgcsr_info;
+
+/* build_rgcsr<S>(m, group_size) (spmvkit/rgcsr.hpp:38-70), on the device:
+ * row lengths -> per-group max -> scan of s*K_g -> group-interleaved scatter
+ * with every pad slot written (value 0, column 0).  EINVAL if group_size==0
+ * ("build_rgcsr: group size must be nonzero"); ERANGE if the slot count does
+ * not fit uint32 (silently truncated in the reference).  prec may narrow a
+ * double CSR to float (static_cast<float>, round-to-nearest-even). */
+int spmvk_rgcsr_build(const spmvk_csr* a, uint64_t group_size, int prec, void* stream,
+                      spmvk_rgcsr** out);
+/* Row slab [row_begin, row_end) of `a` (columns stay global), row_begin a
+ * multiple of group_size: the slab's arrays equal the global build's slice
+ * (group_pointers rebased).  Used by the row-slab partitioner. */
+int spmvk_rgcsr_build_rows(const spmvk_csr* a, uint64_t row_begin, uint64_t row_end,
+                           uint64_t group_size, int prec, void* stream, spmvk_rgcsr** out);
+int spmvk_rgcsr_get_info(const spmvk_rgcsr* h, spmvk_rgcsr_info* info);
+/* Copies the four RgcsrMatrix arrays (rgcsr.hpp:24-27) to HOST buffers of
+ * slots / slots / num_groups+1 / num_rows elements (any may be NULL). */
+int spmvk_rgcsr_download(const spmvk_rgcsr* h, void* values, uint32_t* columns,
+                         uint32_t* group_pointers, uint32_t* row_lengths);
+/* spmv_rgcsr(a, x, y) (spmvkit/rgcsr.hpp:75-97): y = A x with x, y in HBM.
+ * EINVAL "spmv_rgcsr: dimension mismatch" unless nx == num_cols and
+ * ny == num_rows, or if the handle's precision differs from the entry point. */
+int spmvk_rgcsr_spmv_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                         uint64_t ny, void* stream);
+int spmvk_rgcsr_spmv_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                         uint64_t ny, void* stream);
+/* Iterated form used by the distributed product: y = A x and, fused in the
+ * same kernel, x_next[i] = y[i] * scale (x_next may be NULL). */
+int spmvk_rgcsr_spmv_scaled_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                                uint64_t ny, double* x_next, double scale, void* stream);
+/* Span overloads on HOST memory: H2D(x), SpMV, D2H(y), synchronous.
+ * multiply_add_count (may be NULL) receives the reference's madds count
+ * (rgcsr.hpp:72-74: one per stored nonzero). */
+int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, uint64_t* multiply_add_count);
+int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, uint64_t* multiply_add_count);
+void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
+
+/* ------------------------------------------------------------------ Hybrid */
+typedef struct {
+  uint64_t num_rows, num_cols;
+  uint64_t ell_width;        /* K1 = EllpackMatrix::slots_per_row */
+  uint64_t ell_slots;        /* num_rows * K1 */
+  uint64_t coo_nnz;
+  uint64_t nnz;
+  uint64_t artificial_zeros; /* FillReport (fill.hpp:67-72) */
+  uint64_t bytes_single, bytes_double;
+  int precision;
+} spmvk_hybrid_info;
+
+/* hybrid_split_cost / choose_ell_width (spmvkit/ellpack.hpp:143-166) over the
+ * row lengths of `a`, computed from a device histogram + suffix sums: the same
+ * integer argmin (smallest k on ties) in O(N + max_len). */
+int spmvk_csr_choose_ell_width(const spmvk_csr* a, uint64_t* k1);
+/* Host helper with the reference signature (lens[n]); exact same result. */
+uint64_t spmvk_choose_ell_width(const uint64_t* lens, uint64_t n);
+uint64_t spmvk_hybrid_split_cost(const uint64_t* lens, uint64_t n, uint64_t k);
+/* build_hybrid<S>(m, k1) (spmvkit/ellpack.hpp:168-203); k1 < 0 means
+ * std::nullopt (choose_ell_width).  EINVAL if k1 > max row length. */
+int spmvk_hybrid_build(const spmvk_csr* a, int64_t k1, int prec, void* stream,
+                       spmvk_hybrid** out);
+int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info);
+/* EllpackMatrix values/columns (slot-major, rows*K1) + CooArrays
+ * rows/columns/values (coo_nnz); any pointer may be NULL. */
+int spmvk_hybrid_download(const spmvk_hybrid* h, void* ell_values, uint32_t* ell_columns,
+                          uint32_t* coo_rows, uint32_t* coo_columns, void* coo_values);
+/* spmv_hybrid (spmvkit/ellpack.hpp:205-210) = spmv_ellpack (:110-123) then
+ * spmv_coo (:132-141), fused in one kernel; y is bitwise the reference's. */
+int spmvk_hybrid_spmv_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                          uint64_t ny, void* stream);
+int spmvk_hybrid_spmv_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                          uint64_t ny, void* stream);
+int spmvk_hybrid_spmv_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                               uint64_t ny);
+int spmvk_hybrid_spmv_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                               uint64_t ny);
+void spmvk_hybrid_destroy(spmvk_hybrid* h);
+
+/* ------------------------------------------------------------------ host generators
+ * Seeded, platform-independent generators (std::mt19937_64 draws, the
+ * reference's unit_real convention src/synthetic.cpp:7-9).  Two-pass: pass
+ * col/val NULL to get nnz, then call again with buffers. */
+/* random_vector (src/synthetic.cpp:62-67) */
+void spmvk_gen_random_vector(uint64_t n, uint64_t seed, double* out);
+/* Stencils as spmvk_csr_stencil, on the host.  Returns nnz. */
+uint64_t spmvk_gen_stencil(int kind, uint64_t n, uint32_t* row_ptr, uint32_t* col, double* val);
+/* Power-law rows.  Returns nnz. */
+uint64_t spmvk_gen_powerlaw(uint64_t rows, uint64_t seed, uint32_t* row_ptr, uint32_t* col,
+                            double* val);
+/* Row-wise random matrix for the sweep: each row draws its length uniformly
+ * in [1, 2*mean_len-1] and distinct uniform columns.  Returns nnz. */
+uint64_t spmvk_gen_random_rows(uint64_t rows, uint64_t cols, uint64_t mean_len, uint64_t seed,
+                               uint32_t* row_ptr, uint32_t* col, double* val);
+/* b x b dense blocks on random block columns, nblk blocks per block row. */
+uint64_t spmvk_gen_block(uint64_t rows, uint64_t b, uint64_t nblk, uint64_t seed,
+                         uint32_t* row_ptr, uint32_t* col, double* val);
+/* banded_matrix (src/synthetic.cpp:48-60). */
+uint64_t spmvk_gen_banded(uint64_t n, uint64_t hbw, uint64_t seed, uint32_t* row_ptr,
+                          uint32_t* col, double* val);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,112 @@
+"""ctypes binding of libspmvk.so (the C-ABI declared in include/spmvk.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).
+There is no CPU fallback: if the library is missing this module raises on
+first use, and every compute entry point returns SPMVK_ECUDA without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspmvk.so")
+
+SPMVK_OK, SPMVK_EINVAL, SPMVK_ERANGE, SPMVK_ECUDA, SPMVK_ENCCL, SPMVK_ENOMEM = range(6)
+F32, F64 = 4, 8
+
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+vp = C.c_void_p
+u64 = C.c_uint64
+i64 = C.c_int64
+cint = C.c_int
+
+
+class RgcsrInfo(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "num_rows", "num_cols", "group_size", "num_groups", "slots", "nnz",
+        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int)]
+
+
+class HybridInfo(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "num_rows", "num_cols", "ell_width", "ell_slots", "coo_nnz", "nnz",
+        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int)]
+
+
+# name -> (restype, argtypes); every symbol include/spmvk.h declares.
+SIGNATURES = {
+    "spmvk_last_error": (C.c_char_p, []),
+    "spmvk_abi_version": (cint, []),
+    "spmvk_init": (cint, [cint]),
+    "spmvk_csr_upload": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
+    "spmvk_csr_upload_device": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
+    "spmvk_csr_stencil": (cint, [cint, u64, vp, C.POINTER(vp)]),
+    "spmvk_csr_shape": (cint, [vp, u64p, u64p, u64p, C.POINTER(cint)]),
+    "spmvk_csr_download": (cint, [vp, vp, vp, vp]),
+    "spmvk_csr_row_length_range": (cint, [vp, u64p]),
+    "spmvk_csr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_csr_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_csr_destroy": (None, [vp]),
+    "spmvk_rgcsr_build": (cint, [vp, u64, cint, vp, C.POINTER(vp)]),
+    "spmvk_rgcsr_build_rows": (cint, [vp, u64, u64, u64, cint, vp, C.POINTER(vp)]),
+    "spmvk_rgcsr_get_info": (cint, [vp, C.POINTER(RgcsrInfo)]),
+    "spmvk_rgcsr_download": (cint, [vp, vp, vp, vp, vp]),
+    "spmvk_rgcsr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_rgcsr_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_rgcsr_spmv_scaled_f64": (cint, [vp, vp, u64, vp, u64, vp, C.c_double, vp]),
+    "spmvk_rgcsr_spmv_host_f64": (cint, [vp, vp, u64, vp, u64, u64p]),
+    "spmvk_rgcsr_spmv_host_f32": (cint, [vp, vp, u64, vp, u64, u64p]),
+    "spmvk_rgcsr_destroy": (None, [vp]),
+    "spmvk_csr_choose_ell_width": (cint, [vp, u64p]),
+    "spmvk_choose_ell_width": (u64, [vp, u64]),
+    "spmvk_hybrid_split_cost": (u64, [vp, u64, u64]),
+    "spmvk_hybrid_build": (cint, [vp, i64, cint, vp, C.POINTER(vp)]),
+    "spmvk_hybrid_get_info": (cint, [vp, C.POINTER(HybridInfo)]),
+    "spmvk_hybrid_download": (cint, [vp, vp, vp, vp, vp, vp]),
+    "spmvk_hybrid_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_host_f64": (cint, [vp, vp, u64, vp, u64]),
+    "spmvk_hybrid_spmv_host_f32": (cint, [vp, vp, u64, vp, u64]),
+    "spmvk_hybrid_destroy": (None, [vp]),
+    "spmvk_gen_random_vector": (None, [u64, u64, vp]),
+    "spmvk_gen_stencil": (u64, [cint, u64, vp, vp, vp]),
+    "spmvk_gen_powerlaw": (u64, [u64, u64, vp, vp, vp]),
+    "spmvk_gen_random_rows": (u64, [u64, u64, u64, u64, vp, vp, vp]),
+    "spmvk_gen_block": (u64, [u64, u64, u64, u64, vp, vp, vp]),
+    "spmvk_gen_banded": (u64, [u64, u64, u64, vp, vp, vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """The loaded libspmvk.so with every signature bound (loads once)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise LibraryMissing(
+                    f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                    "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    m = lib().spmvk_last_error()
+    return m.decode() if m else ""

@@ -1,0 +1,168 @@
+// Device plumbing shared by all spmvk entry points: last-error slot, device
+// checks, and the uint64 exclusive scan used for group pointers / COO offsets.
+#include "common.cuh"
+
+#include <string>
+#include <vector>
+
+namespace spmvk {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  SPMVK_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int n = 0;
+  SPMVK_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  if (dev < 64) cached[dev] = n;
+  return n;
+}
+
+void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(SPMVK_ECUDA, std::string("no CUDA device available (") +
+                          (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                          "); spmvk has no CPU fallback");
+  }
+}
+
+HostStage& host_stage() {
+  static thread_local HostStage st;
+  return st;
+}
+
+// ---------------------------------------------------------------- scan
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr uint64_t kScanTile = kScanThreads * kScanItems;
+
+// Block-wide exclusive scan of one value per thread; returns the block total.
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t& excl) {
+  __shared__ uint64_t warp_tot[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < kScanThreads / 32) warp_tot[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const uint64_t warp_off = warp == 0 ? 0 : warp_tot[warp - 1];
+  const uint64_t total = warp_tot[kScanThreads / 32 - 1];
+  excl = warp_off + inc - v;
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_reduce(const uint64_t* __restrict__ d,
+                                                                 uint64_t n,
+                                                                 uint64_t* __restrict__ part) {
+  const uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) s += d[base + i];
+  uint64_t ex;
+  const uint64_t tot = block_exclusive_scan(s, ex);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// Single CTA: exclusive scan of the tile sums; part[nb] receives the total.
+__global__ void __launch_bounds__(kScanThreads) scan_partials(uint64_t* part, uint64_t nb) {
+  const uint64_t per = (nb + kScanThreads - 1) / kScanThreads;
+  const uint64_t b0 = threadIdx.x * per;
+  uint64_t s = 0;
+  for (uint64_t i = b0; i < b0 + per && i < nb; ++i) s += part[i];
+  uint64_t ex;
+  const uint64_t tot = block_exclusive_scan(s, ex);
+  for (uint64_t i = b0; i < b0 + per && i < nb; ++i) {
+    const uint64_t v = part[i];
+    part[i] = ex;
+    ex += v;
+  }
+  if (threadIdx.x == 0) part[nb] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_apply(uint64_t* __restrict__ d,
+                                                                uint64_t n,
+                                                                const uint64_t* __restrict__ part) {
+  const uint64_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  uint64_t v[kScanItems];
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? d[base + i] : 0;
+    s += v[i];
+  }
+  uint64_t ex;
+  block_exclusive_scan(s, ex);
+  ex += part[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) d[base + i] = ex;
+    ex += v[i];
+  }
+}
+
+}  // namespace
+
+uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s) {
+  if (n == 0) return 0;
+  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
+  DevBuf<uint64_t> part(nb + 1);
+  scan_tile_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(d, n, part.p);
+  SPMVK_LAUNCH("scan_tile_reduce");
+  scan_partials<<<1, kScanThreads, 0, s>>>(part.p, nb);
+  SPMVK_LAUNCH("scan_partials");
+  scan_tile_apply<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(d, n, part.p);
+  SPMVK_LAUNCH("scan_tile_apply");
+  uint64_t total = 0;
+  SPMVK_CUDA(cudaMemcpyAsync(&total, part.p + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  return total;
+}
+
+}  // namespace spmvk
+
+extern "C" {
+
+const char* spmvk_last_error(void) { return spmvk::last_error_cstr(); }
+
+int spmvk_abi_version(void) { return SPMVK_ABI_VERSION; }
+
+int spmvk_init(int device) {
+  return spmvk::guarded([&] {
+    spmvk::require_device();
+    SPMVK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp p{};
+    SPMVK_CUDA(cudaGetDeviceProperties(&p, device));
+    if (p.major != 10)
+      spmvk::fail(SPMVK_ECUDA, std::string("spmvk is built for sm_100a; device ") + p.name +
+                                   " is sm_" + std::to_string(p.major * 10 + p.minor));
+  });
+}
+
+}  // extern "C"

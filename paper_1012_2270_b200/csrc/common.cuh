@@ -1,0 +1,196 @@
+// Shared plumbing for the spmvk C-ABI: status/error handling, device buffers,
+// cache-hinted loads.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/spmvk.h"
+
+namespace spmvk {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+const char* last_error_cstr();
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? SPMVK_ENOMEM : SPMVK_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define SPMVK_CUDA(call) ::spmvk::cuda_check((call), #call)
+#define SPMVK_LAUNCH(what) ::spmvk::cuda_check(cudaGetLastError(), what)
+
+// Runs f, converting exceptions to status codes + thread-local message.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SPMVK_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return SPMVK_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return SPMVK_ECUDA;
+  }
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- device buffer
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  uint64_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(uint64_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(uint64_t count) {
+    release();
+    n = count;
+    // one extra element keeps zero-sized arrays valid, distinct pointers
+    SPMVK_CUDA(cudaMalloc(&p, sizeof(T) * (count + 1)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  uint64_t bytes() const { return n * sizeof(T); }
+};
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+// Ensures the current device is usable (throws ECUDA otherwise).
+void require_device();
+
+// ---------------------------------------------------------------- loads
+// L2 cache policies (createpolicy): matrix slots are streamed once
+// (evict-first) so that the gathered x vector (evict-last) keeps its L2
+// residency across the whole SpMV.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Streamed-once matrix arrays: read-only path, no L1 allocation.
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// Gathered vector x: read-only path, L1-allocating.
+__device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// Separately rounded multiply and add: the reference's `acc += v * x[c]`
+// compiled without FMA contraction (core/CMakeLists.txt has no -march).
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// Grid of `per_sm` CTAs per SM, capped by the work.
+inline unsigned persistent_grid(uint64_t work_ctas, int per_sm) {
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
+  const uint64_t g = work_ctas < cap ? work_ctas : cap;
+  return static_cast<unsigned>(g == 0 ? 1 : g);
+}
+
+// ---------------------------------------------------------------- scan
+// Exclusive prefix sum of n uint64 values in place; returns the total (synchronises
+// the stream to read it back).  Used for group pointers and COO offsets.
+uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s);
+
+// Per-thread staging (stream + x/y device buffers) for the host-span
+// overloads (*_spmv_host_*), reused across calls.
+struct HostStage {
+  cudaStream_t stream = nullptr;
+  DevBuf<unsigned char> x, y;
+  ~HostStage() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void reserve(uint64_t xb, uint64_t yb) {
+    if (!stream) SPMVK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    if (x.n < xb) x.alloc(xb);
+    if (y.n < yb) y.alloc(yb);
+  }
+};
+HostStage& host_stage();
+
+}  // namespace spmvk
+
+// ---------------------------------------------------------------- handles
+struct spmvk_csr {
+  uint64_t rows = 0, cols = 0, nnz = 0;
+  int val_prec = SPMVK_F64;
+  spmvk::DevBuf<uint32_t> row_ptr, col;
+  spmvk::DevBuf<unsigned char> val;  // nnz * val_prec bytes
+};
+
+struct spmvk_rgcsr {
+  uint64_t rows = 0, cols = 0, group_size = 0, groups = 0, slots = 0, nnz = 0;
+  int prec = SPMVK_F64;
+  spmvk::DevBuf<unsigned char> values;  // slots * prec bytes
+  spmvk::DevBuf<uint32_t> columns, group_pointers, row_lengths;
+};
+
+struct spmvk_hybrid {
+  uint64_t rows = 0, cols = 0, k1 = 0, coo = 0, nnz = 0;
+  int prec = SPMVK_F64;
+  spmvk::DevBuf<unsigned char> ell_values, coo_values;
+  spmvk::DevBuf<uint32_t> ell_columns, coo_rows, coo_columns;
+  // tile_ptr[t]: first COO entry of row tile t (256 rows); kernel metadata,
+  // (N/256 + 1) words, not part of the reference's arrays.
+  spmvk::DevBuf<uint32_t> tile_ptr;
+};

@@ -1,0 +1,339 @@
+// CSR ingest on the device: upload + canonical-form validation, stencil
+// generation directly in HBM, and the thread-per-row spmv_csr comparator.
+//
+// Reference: TripletMatrix ctor validation (src/triplet.cpp:22-32),
+// build_csr (spmvkit/csr.hpp:24-39), spmv_csr (spmvkit/csr.hpp:41-53).
+#include <algorithm>
+#include <memory>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spmvk {
+namespace {
+
+// ------------------------------------------------------------ validation
+// flag bit 1: row_ptr not monotone / ends wrong; 2: column out of bounds;
+// 4: columns not strictly increasing.  bad_row = smallest offending row.
+__global__ void validate_csr(uint64_t rows, uint64_t cols, uint64_t nnz,
+                             const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                             unsigned* flag, unsigned long long* bad_row) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rp[r], e = rp[r + 1];
+    unsigned f = 0;
+    if (r == 0 && b != 0) f |= 1;
+    if (r + 1 == rows && e != nnz) f |= 1;
+    if (e < b || e > nnz) {
+      f |= 1;
+    } else {
+      uint32_t prev = 0;
+      for (uint32_t k = b; k < e; ++k) {
+        const uint32_t c = col[k];
+        if (c >= cols) f |= 2;
+        if (k > b && c <= prev) f |= 4;
+        prev = c;
+      }
+    }
+    if (f) {
+      atomicOr(flag, f);
+      atomicMin(bad_row, (unsigned long long)r);
+    }
+  }
+}
+
+void validate(const spmvk_csr& a, cudaStream_t s) {
+  if (a.rows == 0) {
+    if (a.nnz != 0) fail(SPMVK_EINVAL, "entries given for a matrix with zero rows");
+    return;
+  }
+  DevBuf<unsigned long long> scratch(2);
+  unsigned long long init[2] = {0, ~0ull};
+  SPMVK_CUDA(cudaMemcpyAsync(scratch.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  validate_csr<<<persistent_grid((a.rows + 255) / 256, 8), 256, 0, s>>>(
+      a.rows, a.cols, a.nnz, a.row_ptr.p, a.col.p, reinterpret_cast<unsigned*>(scratch.p),
+      scratch.p + 1);
+  SPMVK_LAUNCH("validate_csr");
+  unsigned long long out[2];
+  SPMVK_CUDA(cudaMemcpyAsync(out, scratch.p, sizeof(out), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  const unsigned f = static_cast<unsigned>(out[0]);
+  if (f) {
+    std::string why = (f & 1)   ? "row pointers are not a monotone offset array ending at nnz"
+                      : (f & 2) ? "column index outside the matrix"
+                                : "entries not strictly increasing in (row, col)";
+    fail(SPMVK_EINVAL, why + " (first bad row " + std::to_string(out[1]) + ")");
+  }
+}
+
+// ------------------------------------------------------------ stencils in HBM
+struct StencilShape {
+  int kind;
+  uint64_t n, nz;
+};
+
+__device__ __forceinline__ uint32_t stencil_row(const StencilShape sh, uint64_t r, uint32_t* col,
+                                                double* val) {
+  const uint64_t x = r % sh.n, y = (r / sh.n) % sh.n, z = r / (sh.n * sh.n);
+  const double diag = sh.kind == 5 ? 4.0 : sh.kind == 7 ? 6.0 : 26.0;
+  uint32_t k = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (sh.kind == 5 && dz != 0) continue;
+        const int nnb = (dz != 0) + (dy != 0) + (dx != 0);
+        if (sh.kind != 27 && nnb > 1) continue;
+        const int64_t zz = (int64_t)z + dz, yy = (int64_t)y + dy, xx = (int64_t)x + dx;
+        if (zz < 0 || yy < 0 || xx < 0 || zz >= (int64_t)sh.nz || yy >= (int64_t)sh.n ||
+            xx >= (int64_t)sh.n)
+          continue;
+        if (col) {
+          col[k] = (uint32_t)(((uint64_t)zz * sh.n + (uint64_t)yy) * sh.n + (uint64_t)xx);
+          val[k] = nnb == 0 ? diag : -1.0;
+        }
+        ++k;
+      }
+  return k;
+}
+
+__global__ void stencil_lengths(StencilShape sh, uint64_t rows, uint64_t* len) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    len[r] = stencil_row(sh, r, nullptr, nullptr);
+}
+
+__global__ void stencil_fill(StencilShape sh, uint64_t rows, const uint64_t* __restrict__ off,
+                             uint32_t* __restrict__ rp, uint32_t* __restrict__ col,
+                             double* __restrict__ val) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t o = off[r];
+    rp[r] = (uint32_t)o;
+    const uint32_t k = stencil_row(sh, r, col + o, val + o);
+    if (r + 1 == rows) rp[rows] = (uint32_t)(o + k);
+  }
+}
+
+// ------------------------------------------------------------ row-length range
+__global__ void row_len_range(uint64_t rows, const uint32_t* __restrict__ rp,
+                              unsigned* out /* [0]=max [1]=min */) {
+  unsigned mx = 0, mn = 0xffffffffu;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned l = rp[r + 1] - rp[r];
+    mx = max(mx, l);
+    mn = min(mn, l);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    atomicMin(out + 1, mn);
+  }
+}
+
+// ------------------------------------------------------------ spmv_csr
+// Thread per row, entries in column order, separately rounded multiply/add:
+// bitwise the reference's spmv_csr (csr.hpp:45-51).
+template <class T>
+__global__ void __launch_bounds__(256) csr_spmv_kernel(uint64_t rows,
+                                                       const uint32_t* __restrict__ rp,
+                                                       const uint32_t* __restrict__ col,
+                                                       const T* __restrict__ val,
+                                                       const T* __restrict__ x,
+                                                       T* __restrict__ y) {
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rp[r], e = rp[r + 1];
+    T acc = T(0);
+    uint32_t k = b;
+    for (; k + 4 <= e; k += 4) {
+      uint32_t c[4];
+      T v[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = ld_stream(col + k + u, pf);
+        v[u] = ld_stream(val + k + u, pf);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = ld_x(x + c[u], pl);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    }
+    for (; k < e; ++k) acc = add_rn(acc, mul_rn(ld_stream(val + k, pf), ld_x(x + ld_stream(col + k, pf), pl)));
+    y[r] = acc;
+  }
+}
+
+spmvk_csr* make_csr(uint64_t rows, uint64_t cols, uint64_t nnz, int val_prec) {
+  if (val_prec != SPMVK_F32 && val_prec != SPMVK_F64)
+    fail(SPMVK_EINVAL, "value precision must be SPMVK_F32 (4) or SPMVK_F64 (8)");
+  if (rows >= 0xffffffffull || cols > 0x100000000ull)
+    fail(SPMVK_ERANGE, "matrix dimensions exceed the 32-bit index type");
+  if (nnz > 0xffffffffull) fail(SPMVK_ERANGE, "nnz exceeds the 32-bit row pointer type");
+  auto a = std::make_unique<spmvk_csr>();
+  a->rows = rows;
+  a->cols = cols;
+  a->nnz = nnz;
+  a->val_prec = val_prec;
+  a->row_ptr.alloc(rows + 1);
+  a->col.alloc(nnz);
+  a->val.alloc(nnz * static_cast<uint64_t>(val_prec));
+  return a.release();
+}
+
+template <class T>
+void csr_spmv(const spmvk_csr* a, const T* x, uint64_t nx, T* y, uint64_t ny, cudaStream_t s) {
+  if (!a) fail(SPMVK_EINVAL, "null CSR handle");
+  if (nx != a->cols || ny != a->rows) fail(SPMVK_EINVAL, "spmv_csr: dimension mismatch");
+  if (a->val_prec != static_cast<int>(sizeof(T)))
+    fail(SPMVK_EINVAL, "spmv_csr: handle precision differs from the entry point");
+  if (a->rows == 0) return;
+  csr_spmv_kernel<T><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
+      a->rows, a->row_ptr.p, a->col.p, reinterpret_cast<const T*>(a->val.p), x, y);
+  SPMVK_LAUNCH("csr_spmv_kernel");
+}
+
+}  // namespace
+
+// row lengths -> uint32 (used by rgcsr / hybrid builders)
+__global__ void csr_row_lengths(uint64_t r0, uint64_t rows, const uint32_t* __restrict__ rp,
+                                uint32_t* __restrict__ lens) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    lens[r] = rp[r0 + r + 1] - rp[r0 + r];
+}
+
+void row_length_range(const spmvk_csr* a, uint64_t r0, uint64_t r1, unsigned* mx, unsigned* mn,
+                      cudaStream_t s) {
+  DevBuf<unsigned> out(2);
+  unsigned init[2] = {0, 0xffffffffu};
+  SPMVK_CUDA(cudaMemcpyAsync(out.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (r1 > r0) {
+    row_len_range<<<persistent_grid((r1 - r0 + 255) / 256, 8), 256, 0, s>>>(
+        r1 - r0, a->row_ptr.p + r0, out.p);
+    SPMVK_LAUNCH("row_len_range");
+  }
+  unsigned h[2];
+  SPMVK_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  *mx = h[0];
+  *mn = r1 > r0 ? h[1] : 0;
+}
+
+}  // namespace spmvk
+
+using namespace spmvk;
+
+extern "C" {
+
+int spmvk_csr_upload(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t* row_ptr,
+                     const uint32_t* col, const void* val, int val_prec, void* stream,
+                     spmvk_csr** out) {
+  return guarded([&] {
+    require_device();
+    if (!out || !row_ptr || (nnz && (!col || !val))) fail(SPMVK_EINVAL, "null argument");
+    cudaStream_t s = as_stream(stream);
+    std::unique_ptr<spmvk_csr> a(make_csr(rows, cols, nnz, val_prec));
+    SPMVK_CUDA(cudaMemcpyAsync(a->row_ptr.p, row_ptr, sizeof(uint32_t) * (rows + 1),
+                               cudaMemcpyHostToDevice, s));
+    if (nnz) {
+      SPMVK_CUDA(cudaMemcpyAsync(a->col.p, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, s));
+      SPMVK_CUDA(cudaMemcpyAsync(a->val.p, val, a->val.bytes(), cudaMemcpyHostToDevice, s));
+    }
+    validate(*a, s);
+    *out = a.release();
+  });
+}
+
+int spmvk_csr_upload_device(uint64_t rows, uint64_t cols, uint64_t nnz, const uint32_t* row_ptr,
+                            const uint32_t* col, const void* val, int val_prec, void* stream,
+                            spmvk_csr** out) {
+  return guarded([&] {
+    require_device();
+    if (!out || !row_ptr || (nnz && (!col || !val))) fail(SPMVK_EINVAL, "null argument");
+    cudaStream_t s = as_stream(stream);
+    std::unique_ptr<spmvk_csr> a(make_csr(rows, cols, nnz, val_prec));
+    SPMVK_CUDA(cudaMemcpyAsync(a->row_ptr.p, row_ptr, sizeof(uint32_t) * (rows + 1),
+                               cudaMemcpyDeviceToDevice, s));
+    if (nnz) {
+      SPMVK_CUDA(
+          cudaMemcpyAsync(a->col.p, col, sizeof(uint32_t) * nnz, cudaMemcpyDeviceToDevice, s));
+      SPMVK_CUDA(cudaMemcpyAsync(a->val.p, val, a->val.bytes(), cudaMemcpyDeviceToDevice, s));
+    }
+    validate(*a, s);
+    *out = a.release();
+  });
+}
+
+int spmvk_csr_stencil(int kind, uint64_t n, void* stream, spmvk_csr** out) {
+  return guarded([&] {
+    require_device();
+    if (!out) fail(SPMVK_EINVAL, "null argument");
+    if (kind != 5 && kind != 7 && kind != 27) fail(SPMVK_EINVAL, "stencil kind must be 5, 7 or 27");
+    if (n == 0) fail(SPMVK_EINVAL, "stencil grid size must be nonzero");
+    cudaStream_t s = as_stream(stream);
+    const StencilShape sh{kind, n, kind == 5 ? 1 : n};
+    const uint64_t rows = n * n * sh.nz;
+    DevBuf<uint64_t> off(rows);
+    const unsigned grid = persistent_grid((rows + 255) / 256, 8);
+    stencil_lengths<<<grid, 256, 0, s>>>(sh, rows, off.p);
+    SPMVK_LAUNCH("stencil_lengths");
+    const uint64_t nnz = exclusive_scan_u64(off.p, rows, s);
+    std::unique_ptr<spmvk_csr> a(make_csr(rows, rows, nnz, SPMVK_F64));
+    stencil_fill<<<grid, 256, 0, s>>>(sh, rows, off.p, a->row_ptr.p, a->col.p,
+                                      reinterpret_cast<double*>(a->val.p));
+    SPMVK_LAUNCH("stencil_fill");
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    *out = a.release();
+  });
+}
+
+int spmvk_csr_shape(const spmvk_csr* a, uint64_t* rows, uint64_t* cols, uint64_t* nnz,
+                    int* val_prec) {
+  return guarded([&] {
+    if (!a) fail(SPMVK_EINVAL, "null CSR handle");
+    if (rows) *rows = a->rows;
+    if (cols) *cols = a->cols;
+    if (nnz) *nnz = a->nnz;
+    if (val_prec) *val_prec = a->val_prec;
+  });
+}
+
+int spmvk_csr_download(const spmvk_csr* a, uint32_t* row_ptr, uint32_t* col, void* val) {
+  return guarded([&] {
+    if (!a) fail(SPMVK_EINVAL, "null CSR handle");
+    if (row_ptr)
+      SPMVK_CUDA(cudaMemcpy(row_ptr, a->row_ptr.p, sizeof(uint32_t) * (a->rows + 1),
+                            cudaMemcpyDeviceToHost));
+    if (col && a->nnz)
+      SPMVK_CUDA(cudaMemcpy(col, a->col.p, sizeof(uint32_t) * a->nnz, cudaMemcpyDeviceToHost));
+    if (val && a->nnz) SPMVK_CUDA(cudaMemcpy(val, a->val.p, a->val.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2) {
+  return guarded([&] {
+    if (!a || !out2) fail(SPMVK_EINVAL, "null argument");
+    unsigned mx, mn;
+    row_length_range(a, 0, a->rows, &mx, &mn, nullptr);
+    out2[0] = mx;
+    out2[1] = mn;
+  });
+}
+
+int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
+                       void* stream) {
+  return guarded([&] { csr_spmv<double>(a, x, nx, y, ny, as_stream(stream)); });
+}
+
+int spmvk_csr_spmv_f32(const spmvk_csr* a, const float* x, uint64_t nx, float* y, uint64_t ny,
+                       void* stream) {
+  return guarded([&] { csr_spmv<float>(a, x, nx, y, ny, as_stream(stream)); });
+}
+
+void spmvk_csr_destroy(spmvk_csr* a) { delete a; }
+
+}  // extern "C"

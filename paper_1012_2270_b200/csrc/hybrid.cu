@@ -1,0 +1,420 @@
+// Hybrid ELL + COO (Bell & Garland) on the device: K3 width choice + build,
+// K4/K5 fused SpMV.
+//
+// Reference: hybrid_split_cost / choose_ell_width (spmvkit/ellpack.hpp:143-166),
+// build_hybrid (:168-203), spmv_ellpack (:110-123), spmv_coo (:132-141),
+// spmv_hybrid (:205-210).  ELL is slot-major (slot*N + row), pads (0, col 0);
+// COO holds each row's entries past the first K1, sorted by (row, col).
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spmvk {
+namespace {
+
+constexpr int kRowsPerTile = 256;  // rows per SpMV tile (= CTA size)
+constexpr int kCooTile = 1024;     // COO entries staged in smem per pass
+
+// ------------------------------------------------------------ K3a: histogram
+// hist[len] += 1 over all rows.  Warp-aggregated (match_any) into a shared
+// histogram, then one global atomic per non-empty bin per CTA.
+__global__ void len_hist_smem(uint64_t rows, const uint32_t* __restrict__ rp, uint32_t nbins,
+                              unsigned long long* __restrict__ hist) {
+  extern __shared__ uint32_t sh[];
+  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x; r0 < rows;
+       r0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = r0 + threadIdx.x;
+    const bool live = r < rows;
+    const uint32_t len = live ? rp[r + 1] - rp[r] : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, len);
+    if (live && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&sh[len], __popc(peers));
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], (unsigned long long)sh[b]);
+}
+
+__global__ void len_hist_global(uint64_t rows, const uint32_t* __restrict__ rp,
+                                unsigned long long* __restrict__ hist) {
+  for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x; r0 < rows;
+       r0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = r0 + threadIdx.x;
+    const bool live = r < rows;
+    const uint32_t len = live ? rp[r + 1] - rp[r] : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, len);
+    if (live && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
+      atomicAdd(&hist[len], (unsigned long long)__popc(peers));
+  }
+}
+
+// argmin_k 2*N*k + 3*sum_{len>k}(len-k), smallest k on ties, from the
+// histogram: with C(k) = #rows longer than k and S(k) = their total length,
+// overflow(k) = S(k) - k*C(k); both are suffix sums.  Exact integers.
+uint64_t width_from_hist(const std::vector<unsigned long long>& hist, uint64_t rows) {
+  const uint64_t max_len = hist.empty() ? 0 : hist.size() - 1;
+  std::vector<uint64_t> C(max_len + 2, 0), S(max_len + 2, 0);
+  for (uint64_t k = max_len + 1; k-- > 0;) {
+    // rows with len > k: those with len == k+1 plus len > k+1
+    const uint64_t cnt = k + 1 <= max_len ? hist[k + 1] : 0;
+    C[k] = C[k + 1] + cnt;
+    S[k] = S[k + 1] + cnt * (k + 1);
+  }
+  uint64_t best_k = 0, best = 3 * S[0];
+  for (uint64_t k = 1; k <= max_len; ++k) {
+    const uint64_t cost = 2 * rows * k + 3 * (S[k] - k * C[k]);
+    if (cost < best) {
+      best = cost;
+      best_k = k;
+    }
+  }
+  return best_k;
+}
+
+uint64_t choose_width_device(const spmvk_csr* a, uint64_t max_len, cudaStream_t s) {
+  if (a->rows == 0) return 0;
+  DevBuf<unsigned long long> hist(max_len + 1);
+  SPMVK_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(unsigned long long) * (max_len + 1), s));
+  const unsigned grid = persistent_grid((a->rows + 255) / 256, 4);
+  if (max_len + 1 <= 12288) {
+    len_hist_smem<<<grid, 256, sizeof(uint32_t) * (max_len + 1), s>>>(
+        a->rows, a->row_ptr.p, static_cast<uint32_t>(max_len + 1), hist.p);
+  } else {
+    len_hist_global<<<grid, 256, 0, s>>>(a->rows, a->row_ptr.p, hist.p);
+  }
+  SPMVK_LAUNCH("len_hist");
+  std::vector<unsigned long long> h(max_len + 1);
+  SPMVK_CUDA(cudaMemcpyAsync(h.data(), hist.p, sizeof(unsigned long long) * (max_len + 1),
+                             cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  return width_from_hist(h, a->rows);
+}
+
+// ------------------------------------------------------------ K3b: build
+// ELL: thread per row writes its K1 slots (coalesced across rows for each
+// slot); COO: overflow counts for the offset scan.
+template <class T, class V>
+__global__ void hybrid_ell_fill(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
+                                const uint32_t* __restrict__ col, const V* __restrict__ val,
+                                T* __restrict__ ev, uint32_t* __restrict__ ec,
+                                uint64_t* __restrict__ overflow) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rp[r], len = rp[r + 1] - b;
+    for (uint32_t j = 0; j < k1; ++j) {
+      const uint64_t idx = (uint64_t)j * rows + r;
+      if (j < len) {
+        ev[idx] = static_cast<T>(val[b + j]);
+        ec[idx] = col[b + j];
+      } else {
+        ev[idx] = T(0);
+        ec[idx] = 0;
+      }
+    }
+    overflow[r] = len > k1 ? len - k1 : 0;
+  }
+}
+
+// COO: one warp per row with overflow copies the row's tail (coalesced).
+template <class T, class V>
+__global__ void hybrid_coo_fill(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
+                                const uint32_t* __restrict__ col, const V* __restrict__ val,
+                                const uint64_t* __restrict__ off, uint32_t* __restrict__ cr,
+                                uint32_t* __restrict__ cc, T* __restrict__ cv) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += warps) {
+    const uint32_t b = rp[r], len = rp[r + 1] - b;
+    if (len <= k1) continue;
+    const uint64_t o = off[r];
+    for (uint32_t i = lane; i < len - k1; i += 32) {
+      cr[o + i] = (uint32_t)r;
+      cc[o + i] = col[b + k1 + i];
+      cv[o + i] = static_cast<T>(val[b + k1 + i]);
+    }
+  }
+}
+
+// tile_ptr[t] = first COO entry whose row >= t * kRowsPerTile (lower bound).
+__global__ void coo_tile_bounds(uint64_t ntiles, uint64_t rows, uint64_t n,
+                                const uint32_t* __restrict__ cr, uint32_t* __restrict__ tp) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = min(t * kRowsPerTile, rows);
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (cr[mid] < row) lo = mid + 1; else hi = mid;
+    }
+    tp[t] = (uint32_t)lo;
+  }
+}
+
+// ------------------------------------------------------------ K4/K5: SpMV
+// One CTA-tile of 256 rows: (1) thread per row walks its K1 ELL slots (pads
+// included, as spmv_ellpack does); (2) the tile's COO range is staged in
+// shared memory in chunks, products v*x[c] computed in parallel, and each row
+// then adds its own products sequentially in column order.  Per row this is
+// exactly the reference's sequence of roundings: ELL slots 0..K1-1, then the
+// row's COO entries in array order -> y bitwise equal to spmv_hybrid.
+template <class T>
+__global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
+    uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
+    const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
+    const uint32_t* __restrict__ cc, const T* __restrict__ cv, const T* __restrict__ x,
+    T* __restrict__ y) {
+  __shared__ T prod[kCooTile];
+  __shared__ uint32_t prow[kCooTile];
+  constexpr int U = sizeof(T) == 8 ? 4 : 8;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  const uint32_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r = tile * kRowsPerTile + threadIdx.x;
+    const bool live = r < rows;
+    T acc = T(0);
+    if (live) {
+      uint32_t j = 0;
+      for (; j + U <= k1; j += U) {
+        uint32_t c[U];
+        T v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const size_t idx = (size_t)(j + u) * rows + r;
+          c[u] = ld_stream(ec + idx, pf);
+          v[u] = ld_stream(ev + idx, pf);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pl);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+      }
+      for (; j < k1; ++j) {
+        const size_t idx = (size_t)j * rows + r;
+        const uint32_t c = ld_stream(ec + idx, pf);
+        acc = add_rn(acc, mul_rn(ld_stream(ev + idx, pf), ld_x(x + c, pl)));
+      }
+    }
+    if (tile_ptr) {
+      const uint32_t c0 = tile_ptr[tile], c1 = tile_ptr[tile + 1];
+      for (uint32_t t0 = c0; t0 < c1; t0 += kCooTile) {
+        const uint32_t n = min((uint32_t)kCooTile, c1 - t0);
+        for (uint32_t i = threadIdx.x; i < n; i += kRowsPerTile) {
+          prow[i] = ld_stream(cr + t0 + i, pf);
+          prod[i] = mul_rn(ld_stream(cv + t0 + i, pf), ld_x(x + ld_stream(cc + t0 + i, pf), pl));
+        }
+        __syncthreads();
+        if (live) {
+          uint32_t lo = 0, hi = n;  // first staged entry with row >= r
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (prow[mid] < r) lo = mid + 1; else hi = mid;
+          }
+          for (uint32_t i = lo; i < n && prow[i] == r; ++i) acc = add_rn(acc, prod[i]);
+        }
+        __syncthreads();
+      }
+    }
+    if (live) y[r] = acc;
+  }
+}
+
+template <class T, class V>
+void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
+  const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
+  DevBuf<uint64_t> off(a->rows);
+  hybrid_ell_fill<T, V><<<grid, 256, 0, s>>>(
+      a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+      reinterpret_cast<const V*>(a->val.p), reinterpret_cast<T*>(h->ell_values.p),
+      h->ell_columns.p, off.p);
+  SPMVK_LAUNCH("hybrid_ell_fill");
+  const uint64_t coo = exclusive_scan_u64(off.p, a->rows, s);
+  h->coo = coo;
+  h->coo_rows.alloc(coo);
+  h->coo_columns.alloc(coo);
+  h->coo_values.alloc(coo * sizeof(T));
+  if (coo) {
+    hybrid_coo_fill<T, V><<<persistent_grid((a->rows + 7) / 8, 8), 256, 0, s>>>(
+        a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+        reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
+        reinterpret_cast<T*>(h->coo_values.p));
+    SPMVK_LAUNCH("hybrid_coo_fill");
+    const uint64_t ntiles = (a->rows + kRowsPerTile - 1) / kRowsPerTile;
+    h->tile_ptr.alloc(ntiles + 1);
+    coo_tile_bounds<<<persistent_grid((ntiles + 256) / 256, 4), 256, 0, s>>>(
+        ntiles, a->rows, coo, h->coo_rows.p, h->tile_ptr.p);
+    SPMVK_LAUNCH("coo_tile_bounds");
+  }
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+}
+
+spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
+  if (!a) fail(SPMVK_EINVAL, "null CSR handle");
+  if (prec != SPMVK_F32 && prec != SPMVK_F64)
+    fail(SPMVK_EINVAL, "precision must be SPMVK_F32 (4) or SPMVK_F64 (8)");
+  if (a->val_prec == SPMVK_F32 && prec == SPMVK_F64)
+    fail(SPMVK_EINVAL, "cannot build a double Hybrid from a float CSR");
+  unsigned mx = 0, mn = 0;
+  row_length_range(a, 0, a->rows, &mx, &mn, s);
+  const uint64_t width = k1 < 0 ? choose_width_device(a, mx, s) : static_cast<uint64_t>(k1);
+  if (width > mx)
+    fail(SPMVK_EINVAL, "build_hybrid: k1 " + std::to_string(width) +
+                           " exceeds the maximum row length " + std::to_string(mx));
+  if (a->rows * width > 0xffffffffull)
+    fail(SPMVK_ERANGE, "build_hybrid: " + std::to_string(a->rows * width) +
+                           " ELL slots overflow the 32-bit index type");
+  auto h = std::make_unique<spmvk_hybrid>();
+  h->rows = a->rows;
+  h->cols = a->cols;
+  h->k1 = width;
+  h->prec = prec;
+  h->nnz = a->nnz;
+  h->ell_values.alloc(a->rows * width * prec);
+  h->ell_columns.alloc(a->rows * width);
+  if (prec == SPMVK_F64) fill<double, double>(h.get(), a, s);
+  else if (a->val_prec == SPMVK_F64) fill<float, double>(h.get(), a, s);
+  else fill<float, float>(h.get(), a, s);
+  return h.release();
+}
+
+template <class T>
+void check_args(const spmvk_hybrid* h, uint64_t nx, uint64_t ny) {
+  if (!h) fail(SPMVK_EINVAL, "null Hybrid handle");
+  if (nx != h->cols || ny != h->rows) fail(SPMVK_EINVAL, "spmv_ellpack: dimension mismatch");
+  if (h->prec != static_cast<int>(sizeof(T)))
+    fail(SPMVK_EINVAL, "spmv_hybrid: handle precision differs from the entry point");
+}
+
+template <class T>
+void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s) {
+  if (h->rows == 0) return;
+  const uint64_t ntiles = (h->rows + kRowsPerTile - 1) / kRowsPerTile;
+  hybrid_spmv_kernel<T><<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
+      static_cast<uint32_t>(h->rows), static_cast<uint32_t>(h->k1),
+      reinterpret_cast<const T*>(h->ell_values.p), h->ell_columns.p,
+      h->coo ? h->tile_ptr.p : nullptr, h->coo_rows.p, h->coo_columns.p,
+      reinterpret_cast<const T*>(h->coo_values.p), x, y);
+  SPMVK_LAUNCH("hybrid_spmv_kernel");
+}
+
+template <class T>
+void spmv_host(const spmvk_hybrid* h, const T* x, uint64_t nx, T* y, uint64_t ny) {
+  check_args<T>(h, nx, ny);
+  HostStage& st = host_stage();
+  st.reserve(nx * sizeof(T), ny * sizeof(T));
+  if (nx) SPMVK_CUDA(cudaMemcpyAsync(st.x.p, x, nx * sizeof(T), cudaMemcpyHostToDevice, st.stream));
+  launch<T>(h, reinterpret_cast<const T*>(st.x.p), reinterpret_cast<T*>(st.y.p), st.stream);
+  if (ny) SPMVK_CUDA(cudaMemcpyAsync(y, st.y.p, ny * sizeof(T), cudaMemcpyDeviceToHost, st.stream));
+  SPMVK_CUDA(cudaStreamSynchronize(st.stream));
+}
+
+}  // namespace
+}  // namespace spmvk
+
+using namespace spmvk;
+
+extern "C" {
+
+uint64_t spmvk_hybrid_split_cost(const uint64_t* lens, uint64_t n, uint64_t k) {
+  uint64_t overflow = 0;
+  for (uint64_t i = 0; i < n; ++i) overflow += lens[i] > k ? lens[i] - k : 0;
+  return 2 * n * k + 3 * overflow;
+}
+
+uint64_t spmvk_choose_ell_width(const uint64_t* lens, uint64_t n) {
+  uint64_t max_len = 0;
+  for (uint64_t i = 0; i < n; ++i) max_len = std::max(max_len, lens[i]);
+  std::vector<unsigned long long> hist(max_len + 1, 0);
+  for (uint64_t i = 0; i < n; ++i) ++hist[lens[i]];
+  return width_from_hist(hist, n);
+}
+
+int spmvk_csr_choose_ell_width(const spmvk_csr* a, uint64_t* k1) {
+  return guarded([&] {
+    if (!a || !k1) fail(SPMVK_EINVAL, "null argument");
+    unsigned mx = 0, mn = 0;
+    row_length_range(a, 0, a->rows, &mx, &mn, nullptr);
+    *k1 = choose_width_device(a, mx, nullptr);
+  });
+}
+
+int spmvk_hybrid_build(const spmvk_csr* a, int64_t k1, int prec, void* stream,
+                       spmvk_hybrid** out) {
+  return guarded([&] {
+    require_device();
+    if (!out) fail(SPMVK_EINVAL, "null argument");
+    *out = build(a, k1, prec, as_stream(stream));
+  });
+}
+
+int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info) {
+  return guarded([&] {
+    if (!h || !info) fail(SPMVK_EINVAL, "null argument");
+    info->num_rows = h->rows;
+    info->num_cols = h->cols;
+    info->ell_width = h->k1;
+    info->ell_slots = h->rows * h->k1;
+    info->coo_nnz = h->coo;
+    info->nnz = h->nnz;
+    const uint64_t slots = info->ell_slots + h->coo;
+    info->artificial_zeros = slots - h->nnz;
+    // fill.hpp:67-72: index words = ell slots + 2 * coo
+    const uint64_t words = info->ell_slots + 2 * h->coo;
+    info->bytes_single = slots * 4 + words * 4;
+    info->bytes_double = slots * 8 + words * 4;
+    info->precision = h->prec;
+  });
+}
+
+int spmvk_hybrid_download(const spmvk_hybrid* h, void* ell_values, uint32_t* ell_columns,
+                          uint32_t* coo_rows, uint32_t* coo_columns, void* coo_values) {
+  return guarded([&] {
+    if (!h) fail(SPMVK_EINVAL, "null Hybrid handle");
+    const uint64_t es = h->rows * h->k1;
+    if (ell_values && es)
+      SPMVK_CUDA(cudaMemcpy(ell_values, h->ell_values.p, es * h->prec, cudaMemcpyDeviceToHost));
+    if (ell_columns && es)
+      SPMVK_CUDA(cudaMemcpy(ell_columns, h->ell_columns.p, es * 4, cudaMemcpyDeviceToHost));
+    if (coo_rows && h->coo)
+      SPMVK_CUDA(cudaMemcpy(coo_rows, h->coo_rows.p, h->coo * 4, cudaMemcpyDeviceToHost));
+    if (coo_columns && h->coo)
+      SPMVK_CUDA(cudaMemcpy(coo_columns, h->coo_columns.p, h->coo * 4, cudaMemcpyDeviceToHost));
+    if (coo_values && h->coo)
+      SPMVK_CUDA(cudaMemcpy(coo_values, h->coo_values.p, h->coo * h->prec, cudaMemcpyDeviceToHost));
+  });
+}
+
+int spmvk_hybrid_spmv_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                          uint64_t ny, void* stream) {
+  return guarded([&] {
+    check_args<double>(h, nx, ny);
+    launch<double>(h, x, y, as_stream(stream));
+  });
+}
+
+int spmvk_hybrid_spmv_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                          uint64_t ny, void* stream) {
+  return guarded([&] {
+    check_args<float>(h, nx, ny);
+    launch<float>(h, x, y, as_stream(stream));
+  });
+}
+
+int spmvk_hybrid_spmv_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                               uint64_t ny) {
+  return guarded([&] { spmv_host<double>(h, x, nx, y, ny); });
+}
+
+int spmvk_hybrid_spmv_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                               uint64_t ny) {
+  return guarded([&] { spmv_host<float>(h, x, nx, y, ny); });
+}
+
+void spmvk_hybrid_destroy(spmvk_hybrid* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,15 @@
+// Cross-file kernel/host helpers of the spmvk library.
+#pragma once
+#include "common.cuh"
+
+namespace spmvk {
+
+// lens[r] = rp[r0 + r + 1] - rp[r0 + r] for r < rows
+__global__ void csr_row_lengths(uint64_t r0, uint64_t rows, const uint32_t* __restrict__ rp,
+                                uint32_t* __restrict__ lens);
+
+// max / min row length over rows [r0, r1) (synchronous)
+void row_length_range(const spmvk_csr* a, uint64_t r0, uint64_t r1, unsigned* mx, unsigned* mn,
+                      cudaStream_t s);
+
+}  // namespace spmvk

@@ -1,0 +1,339 @@
+// RgCSR on the device: K1 (CSR -> RgCSR conversion) and K2 (SpMV).
+//
+// Layout (identical to the reference, spmvkit/rgcsr.hpp:11-28): rows are cut
+// into groups of G (the last one s = N - g*G rows); group g owns the slab
+// [gp[g], gp[g+1]) of s * K_g slots, K_g its longest row; entry j of local row
+// t sits at gp[g] + t + j*s, pads hold (0, column 0).  For one step j the s
+// rows of a group read s CONTIGUOUS slots, so a warp of consecutive rows
+// issues fully coalesced loads with one thread per row.
+#include <algorithm>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spmvk {
+namespace {
+
+// ------------------------------------------------------------ K1: layout
+// slots[g] = s_g * max_{t<s_g} lens[g*G + t]
+__global__ void group_slots(uint64_t rows, uint64_t G, uint64_t groups,
+                            const uint32_t* __restrict__ lens, uint64_t* __restrict__ slots) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r0 = g * G, s = min(G, rows - r0);
+    uint32_t w = 0;
+    for (uint64_t t = 0; t < s; ++t) w = max(w, lens[r0 + t]);
+    slots[g] = s * w;
+  }
+}
+
+__global__ void narrow_pointers(uint64_t groups, const uint64_t* __restrict__ gp64,
+                                uint64_t total, uint32_t* __restrict__ gp) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g <= groups;
+       g += (uint64_t)gridDim.x * blockDim.x)
+    gp[g] = (uint32_t)(g == groups ? total : gp64[g]);
+}
+
+// ------------------------------------------------------------ K1: scatter
+// One warp per group.  Lane t owns local row t (+32 per chunk) and walks its
+// slots j = 0..K_g-1; for a fixed j the warp writes 32 contiguous slots, and
+// every pad slot is written (0, 0), so no separate zero-fill pass is needed.
+template <class T, class V>
+__global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows, uint64_t G,
+                                                     uint64_t groups,
+                                                     const uint32_t* __restrict__ rp,
+                                                     const uint32_t* __restrict__ col,
+                                                     const V* __restrict__ val,
+                                                     const uint32_t* __restrict__ gp,
+                                                     const uint32_t* __restrict__ lens,
+                                                     T* __restrict__ values,
+                                                     uint32_t* __restrict__ columns) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < groups;
+       g += warps) {
+    const uint64_t s = min(G, rows - g * G);
+    const uint32_t base = gp[g];
+    const uint64_t width = s ? (gp[g + 1] - base) / s : 0;
+    for (uint64_t t0 = 0; t0 < s; t0 += 32) {
+      const uint64_t t = t0 + lane;
+      const bool live = t < s;
+      const uint64_t row = g * G + t;
+      const uint32_t len = live ? lens[row] : 0;
+      const uint32_t start = live ? rp[r0 + row] : 0;
+      if (!live) continue;
+      for (uint64_t j = 0; j < width; ++j) {
+        const uint64_t idx = base + t + j * s;
+        if (j < len) {
+          values[idx] = static_cast<T>(val[start + j]);
+          columns[idx] = col[start + j];
+        } else {
+          values[idx] = T(0);
+          columns[idx] = 0;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ K2: SpMV
+// Thread per row inside its group; persistent grid-stride CTAs.  The j loop
+// keeps the reference's order: acc = ((0 + v0*x0) + v1*x1) + ..., each product
+// and sum rounded separately (no FMA), so y is bitwise spmv_rgcsr's y.
+// Matrix slots are streamed (L1 no-allocate, L2 evict-first); x is gathered
+// through the read-only path with L2 evict-last so it stays L2-resident.
+template <class T, bool kScaled>
+__global__ void __launch_bounds__(256) rgcsr_spmv_kernel(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale) {
+  constexpr int U = sizeof(T) == 8 ? 4 : 8;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t t = r - g * G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = lens[r];
+    const T* __restrict__ vp = values + gp[g] + t;
+    const uint32_t* __restrict__ cp = columns + gp[g] + t;
+    T acc = T(0);
+    uint32_t j = 0;
+    for (; j + U <= len; j += U) {
+      uint32_t c[U];
+      T v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = ld_stream(cp + (size_t)(j + u) * s, pf);
+        v[u] = ld_stream(vp + (size_t)(j + u) * s, pf);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pl);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    }
+    for (; j < len; ++j) {
+      const uint32_t c = ld_stream(cp + (size_t)j * s, pf);
+      acc = add_rn(acc, mul_rn(ld_stream(vp + (size_t)j * s, pf), ld_x(x + c, pl)));
+    }
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+}
+
+int pow2_shift(uint64_t G) {
+  if (G == 0 || (G & (G - 1))) return -1;
+  int s = 0;
+  while ((1ull << s) < G) ++s;
+  return s;
+}
+
+spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int prec,
+                   cudaStream_t s) {
+  if (!a) fail(SPMVK_EINVAL, "null CSR handle");
+  if (G == 0) fail(SPMVK_EINVAL, "build_rgcsr: group size must be nonzero");
+  if (prec != SPMVK_F32 && prec != SPMVK_F64)
+    fail(SPMVK_EINVAL, "precision must be SPMVK_F32 (4) or SPMVK_F64 (8)");
+  if (a->val_prec == SPMVK_F32 && prec == SPMVK_F64)
+    fail(SPMVK_EINVAL, "cannot build a double RgCSR from a float CSR");
+  if (r0 > r1 || r1 > a->rows) fail(SPMVK_EINVAL, "row range outside the matrix");
+  if (r0 % G) fail(SPMVK_EINVAL, "row slab must start on a group boundary");
+  auto h = std::make_unique<spmvk_rgcsr>();
+  h->rows = r1 - r0;
+  h->cols = a->cols;
+  h->group_size = G;
+  h->prec = prec;
+  h->groups = (h->rows + G - 1) / G;
+  h->row_lengths.alloc(h->rows);
+  h->group_pointers.alloc(h->groups + 1);
+  const unsigned rgrid = persistent_grid((h->rows + 255) / 256, 8);
+  if (h->rows) {
+    csr_row_lengths<<<rgrid, 256, 0, s>>>(r0, h->rows, a->row_ptr.p, h->row_lengths.p);
+    SPMVK_LAUNCH("csr_row_lengths");
+  }
+  uint64_t total = 0;
+  {
+    DevBuf<uint64_t> slots(h->groups);
+    if (h->groups) {
+      group_slots<<<persistent_grid((h->groups + 255) / 256, 8), 256, 0, s>>>(
+          h->rows, G, h->groups, h->row_lengths.p, slots.p);
+      SPMVK_LAUNCH("group_slots");
+    }
+    total = exclusive_scan_u64(slots.p, h->groups, s);
+    if (total > 0xffffffffull)
+      fail(SPMVK_ERANGE, "build_rgcsr: " + std::to_string(total) +
+                             " slots overflow the 32-bit group pointers (group size " +
+                             std::to_string(G) + ")");
+    narrow_pointers<<<persistent_grid((h->groups + 256) / 256, 8), 256, 0, s>>>(
+        h->groups, slots.p, total, h->group_pointers.p);
+    SPMVK_LAUNCH("narrow_pointers");
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+  }
+  h->slots = total;
+  {
+    uint32_t b = 0, e = 0;
+    SPMVK_CUDA(cudaMemcpy(&b, a->row_ptr.p + r0, 4, cudaMemcpyDeviceToHost));
+    SPMVK_CUDA(cudaMemcpy(&e, a->row_ptr.p + r1, 4, cudaMemcpyDeviceToHost));
+    h->nnz = e - b;
+  }
+  h->values.alloc(total * static_cast<uint64_t>(prec));
+  h->columns.alloc(total);
+  if (h->groups) {
+    const unsigned sgrid = persistent_grid((h->groups + 7) / 8, 16);
+    if (prec == SPMVK_F64) {
+      rgcsr_scatter<double, double><<<sgrid, 256, 0, s>>>(
+          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
+          reinterpret_cast<const double*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
+          reinterpret_cast<double*>(h->values.p), h->columns.p);
+    } else if (a->val_prec == SPMVK_F64) {
+      rgcsr_scatter<float, double><<<sgrid, 256, 0, s>>>(
+          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
+          reinterpret_cast<const double*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
+          reinterpret_cast<float*>(h->values.p), h->columns.p);
+    } else {
+      rgcsr_scatter<float, float><<<sgrid, 256, 0, s>>>(
+          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
+          reinterpret_cast<const float*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
+          reinterpret_cast<float*>(h->values.p), h->columns.p);
+    }
+    SPMVK_LAUNCH("rgcsr_scatter");
+  }
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  return h.release();
+}
+
+template <class T>
+void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
+  if (!h) fail(SPMVK_EINVAL, "null RgCSR handle");
+  if (nx != h->cols || ny != h->rows) fail(SPMVK_EINVAL, "spmv_rgcsr: dimension mismatch");
+  if (h->prec != static_cast<int>(sizeof(T)))
+    fail(SPMVK_EINVAL, "spmv_rgcsr: handle precision differs from the entry point");
+}
+
+template <class T, bool kScaled>
+void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
+  if (h->rows == 0) return;
+  const unsigned grid = persistent_grid((h->rows + 255) / 256, 8);
+  rgcsr_spmv_kernel<T, kScaled><<<grid, 256, 0, s>>>(
+      static_cast<uint32_t>(h->rows), static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull)),
+      pow2_shift(h->group_size), h->group_pointers.p, h->row_lengths.p,
+      reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, x_next, scale);
+  SPMVK_LAUNCH("rgcsr_spmv_kernel");
+}
+
+template <class T>
+void spmv_host(const spmvk_rgcsr* h, const T* x, uint64_t nx, T* y, uint64_t ny,
+               uint64_t* madds) {
+  check_spmv_args<T>(h, nx, ny);
+  HostStage& st = host_stage();
+  st.reserve(nx * sizeof(T), ny * sizeof(T));
+  if (nx) SPMVK_CUDA(cudaMemcpyAsync(st.x.p, x, nx * sizeof(T), cudaMemcpyHostToDevice, st.stream));
+  launch_spmv<T, false>(h, reinterpret_cast<const T*>(st.x.p), reinterpret_cast<T*>(st.y.p),
+                        nullptr, T(0), st.stream);
+  if (ny) SPMVK_CUDA(cudaMemcpyAsync(y, st.y.p, ny * sizeof(T), cudaMemcpyDeviceToHost, st.stream));
+  SPMVK_CUDA(cudaStreamSynchronize(st.stream));
+  if (madds) *madds = h->nnz;
+}
+
+}  // namespace
+}  // namespace spmvk
+
+using namespace spmvk;
+
+extern "C" {
+
+int spmvk_rgcsr_build(const spmvk_csr* a, uint64_t group_size, int prec, void* stream,
+                      spmvk_rgcsr** out) {
+  return guarded([&] {
+    require_device();
+    if (!out) fail(SPMVK_EINVAL, "null argument");
+    *out = build(a, 0, a ? a->rows : 0, group_size, prec, as_stream(stream));
+  });
+}
+
+int spmvk_rgcsr_build_rows(const spmvk_csr* a, uint64_t row_begin, uint64_t row_end,
+                           uint64_t group_size, int prec, void* stream, spmvk_rgcsr** out) {
+  return guarded([&] {
+    require_device();
+    if (!out) fail(SPMVK_EINVAL, "null argument");
+    *out = build(a, row_begin, row_end, group_size, prec, as_stream(stream));
+  });
+}
+
+int spmvk_rgcsr_get_info(const spmvk_rgcsr* h, spmvk_rgcsr_info* info) {
+  return guarded([&] {
+    if (!h || !info) fail(SPMVK_EINVAL, "null argument");
+    info->num_rows = h->rows;
+    info->num_cols = h->cols;
+    info->group_size = h->group_size;
+    info->num_groups = h->groups;
+    info->slots = h->slots;
+    info->nnz = h->nnz;
+    info->artificial_zeros = h->slots - h->nnz;
+    // fill.hpp:90-95: index words = slots + group_pointers + row_lengths
+    const uint64_t words = h->slots + (h->groups + 1) + h->rows;
+    info->bytes_single = h->slots * 4 + words * 4;
+    info->bytes_double = h->slots * 8 + words * 4;
+    info->precision = h->prec;
+  });
+}
+
+int spmvk_rgcsr_download(const spmvk_rgcsr* h, void* values, uint32_t* columns,
+                         uint32_t* group_pointers, uint32_t* row_lengths) {
+  return guarded([&] {
+    if (!h) fail(SPMVK_EINVAL, "null RgCSR handle");
+    if (values && h->slots)
+      SPMVK_CUDA(cudaMemcpy(values, h->values.p, h->values.bytes(), cudaMemcpyDeviceToHost));
+    if (columns && h->slots)
+      SPMVK_CUDA(cudaMemcpy(columns, h->columns.p, h->columns.bytes(), cudaMemcpyDeviceToHost));
+    if (group_pointers)
+      SPMVK_CUDA(cudaMemcpy(group_pointers, h->group_pointers.p, 4 * (h->groups + 1),
+                            cudaMemcpyDeviceToHost));
+    if (row_lengths && h->rows)
+      SPMVK_CUDA(cudaMemcpy(row_lengths, h->row_lengths.p, 4 * h->rows, cudaMemcpyDeviceToHost));
+  });
+}
+
+int spmvk_rgcsr_spmv_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                         uint64_t ny, void* stream) {
+  return guarded([&] {
+    check_spmv_args<double>(h, nx, ny);
+    launch_spmv<double, false>(h, x, y, nullptr, 0.0, as_stream(stream));
+  });
+}
+
+int spmvk_rgcsr_spmv_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                         uint64_t ny, void* stream) {
+  return guarded([&] {
+    check_spmv_args<float>(h, nx, ny);
+    launch_spmv<float, false>(h, x, y, nullptr, 0.0f, as_stream(stream));
+  });
+}
+
+int spmvk_rgcsr_spmv_scaled_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                                uint64_t ny, double* x_next, double scale, void* stream) {
+  return guarded([&] {
+    check_spmv_args<double>(h, nx, ny);
+    if (x_next)
+      launch_spmv<double, true>(h, x, y, x_next, scale, as_stream(stream));
+    else
+      launch_spmv<double, false>(h, x, y, nullptr, 0.0, as_stream(stream));
+  });
+}
+
+int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, uint64_t* multiply_add_count) {
+  return guarded([&] { spmv_host<double>(h, x, nx, y, ny, multiply_add_count); });
+}
+
+int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, uint64_t* multiply_add_count) {
+  return guarded([&] { spmv_host<float>(h, x, nx, y, ny, multiply_add_count); });
+}
+
+void spmvk_rgcsr_destroy(spmvk_rgcsr* h) { delete h; }
+
+}  // extern "C"

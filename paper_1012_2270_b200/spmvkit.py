@@ -1,0 +1,436 @@
+"""Host-side mirror of the reference's ``spmvkit`` hot-path API, backed by the
+B200 kernels of libspmvk.so through the C-ABI (include/spmvk.h).
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/core, paths below relative to proj/):
+
+=====================  =========================================================
+this module            reference
+=====================  =========================================================
+TripletMatrix          spmvkit::TripletMatrix (core/include/spmvkit/triplet.hpp:26-45)
+canonicalize           spmvkit::canonicalize (core/src/triplet.cpp:34-49)
+row_lengths            spmvkit::row_lengths (core/src/triplet.cpp:51-55)
+build_csr / spmv_csr   spmvkit/csr.hpp:24-53
+build_rgcsr            spmvkit/rgcsr.hpp:38-70 (device conversion, K1)
+spmv_rgcsr             spmvkit/rgcsr.hpp:72-105 (device SpMV, K2)
+choose_ell_width       spmvkit/ellpack.hpp:153-166
+hybrid_split_cost      spmvkit/ellpack.hpp:145-150
+build_hybrid           spmvkit/ellpack.hpp:168-203
+spmv_hybrid            spmvkit/ellpack.hpp:205-217
+fill_report            spmvkit/fill.hpp:52-95
+measured_gflops        core/src/memsim.cpp:201-207
+=====================  =========================================================
+
+``std::invalid_argument`` maps to :class:`InvalidArgument` (a ``ValueError``),
+``std::runtime_error`` to :class:`SpmvkRuntimeError`.  x / y may be numpy
+arrays (host span semantics: H2D, SpMV, D2H, synchronous) or CUDA torch
+tensors (device-resident; launched on torch's current stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import F32, F64, HybridInfo, RgcsrInfo, lib
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class SpmvkRuntimeError(RuntimeError):
+    """std::runtime_error in the reference (size budgets, 32-bit overflow)."""
+
+
+class CudaError(RuntimeError):
+    """Device / launch failure (no CPU fallback exists)."""
+
+
+def _check(rc: int) -> None:
+    if rc == _lib.SPMVK_OK:
+        return
+    msg = _lib.last_error()
+    if rc == _lib.SPMVK_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == _lib.SPMVK_ERANGE:
+        raise SpmvkRuntimeError(msg)
+    raise CudaError(f"spmvk status {rc}: {msg}")
+
+
+def _prec(p) -> int:
+    if p in (F32, "f32", "float32", "single", np.float32):
+        return F32
+    if p in (F64, "f64", "float64", "double", np.float64, None):
+        return F64
+    raise InvalidArgument(f"unknown precision {p!r}")
+
+
+def _dtype(prec: int):
+    return np.float32 if prec == F32 else np.float64
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+# ---------------------------------------------------------------- data model
+class TripletMatrix:
+    """Canonical coordinate matrix held as CSR arrays on the host.
+
+    A canonical TripletMatrix (entries strictly increasing in (row, col)) is
+    exactly a CSR matrix whose k-th entry is the k-th sorted triplet; the
+    constructor validates like the reference's (src/triplet.cpp:22-32).
+    """
+
+    def __init__(self, num_rows: int, num_cols: int, row_ptr, col, val, validate=True):
+        self.num_rows = int(num_rows)
+        self.num_cols = int(num_cols)
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+        self.col = np.ascontiguousarray(col, dtype=np.uint32)
+        self.val = np.ascontiguousarray(val, dtype=np.float64)
+        if validate:
+            self._validate()
+
+    def _validate(self):
+        rp, n = self.row_ptr, self.num_rows
+        if rp.shape != (n + 1,) or rp[0] != 0 or rp[-1] != self.col.size or \
+                self.col.size != self.val.size or np.any(np.diff(rp.astype(np.int64)) < 0):
+            raise InvalidArgument("row pointers are not a monotone offset array ending at nnz")
+        if self.col.size and int(self.col.max()) >= self.num_cols:
+            raise InvalidArgument("entry outside the matrix")
+        if self.col.size > 1:
+            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp.astype(np.int64)))
+            same = rows[1:] == rows[:-1]
+            if np.any(same & (self.col[1:] <= self.col[:-1])):
+                raise InvalidArgument("entries not strictly increasing in (row, col)")
+
+    @classmethod
+    def from_entries(cls, num_rows: int, num_cols: int, entries: Iterable):
+        """TripletMatrix(num_rows, num_cols, {{row, col, value}, ...})."""
+        e = list(entries)
+        rows = np.array([t[0] for t in e], dtype=np.int64)
+        for t in e:
+            if t[0] >= num_rows or t[1] >= num_cols or t[0] < 0 or t[1] < 0:
+                raise InvalidArgument(f"entry ({t[0]}, {t[1]}) outside {num_rows}x{num_cols} matrix")
+        rp = np.zeros(num_rows + 1, dtype=np.int64)
+        np.add.at(rp, rows + 1, 1)
+        if len(e) > 1 and any((a[0], a[1]) >= (b[0], b[1]) for a, b in zip(e, e[1:])):
+            raise InvalidArgument("entries not strictly increasing in (row, col)")
+        return cls(num_rows, num_cols, np.cumsum(rp), [t[1] for t in e], [t[2] for t in e])
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.size)
+
+    def entries(self):
+        rows = np.repeat(np.arange(self.num_rows), np.diff(self.row_ptr.astype(np.int64)))
+        return list(zip(rows.tolist(), self.col.tolist(), self.val.tolist()))
+
+
+def canonicalize(raw: Iterable, num_rows: int, num_cols: int) -> TripletMatrix:
+    """Sorts by (row, col) and sums duplicates (src/triplet.cpp:34-49)."""
+    e = list(raw)
+    for t in e:
+        if t[0] >= num_rows or t[1] >= num_cols:
+            raise InvalidArgument(f"entry ({t[0]}, {t[1]}) outside {num_rows}x{num_cols} matrix")
+    e.sort(key=lambda t: (t[0], t[1]))  # stable, as std::sort ties do not matter after merging
+    merged = []
+    for t in e:
+        if merged and merged[-1][0] == t[0] and merged[-1][1] == t[1]:
+            merged[-1][2] += t[2]
+        else:
+            merged.append([t[0], t[1], float(t[2])])
+    return TripletMatrix.from_entries(num_rows, num_cols, merged)
+
+
+def row_lengths(m: TripletMatrix) -> np.ndarray:
+    return np.diff(m.row_ptr.astype(np.int64)).astype(np.uint64)
+
+
+# ---------------------------------------------------------------- CSR (device)
+class CsrMatrix:
+    """Device CSR (build_csr's CsrMatrix, csr.hpp:13-22) owned by a handle."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        r, c, n, p = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(lib().spmvk_csr_shape(self._h, C.byref(r), C.byref(c), C.byref(n), C.byref(p)))
+        self.num_rows, self.num_cols, self._nnz, self.val_prec = r.value, c.value, n.value, p.value
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    @classmethod
+    def stencil(cls, kind: int, n: int, stream: int = 0) -> "CsrMatrix":
+        """5-/7-/27-point stencil generated directly in HBM."""
+        h = C.c_void_p()
+        _check(lib().spmvk_csr_stencil(kind, n, stream or None, C.byref(h)))
+        return cls(h.value)
+
+    def to_host(self):
+        rp = np.empty(self.num_rows + 1, np.uint32)
+        col = np.empty(self._nnz, np.uint32)
+        val = np.empty(self._nnz, _dtype(self.val_prec))
+        _check(lib().spmvk_csr_download(self._h, _ptr(rp), _ptr(col), _ptr(val)))
+        return rp, col, val
+
+    def row_length_range(self):
+        out = (C.c_uint64 * 2)()
+        _check(lib().spmvk_csr_row_length_range(self._h, out))
+        return int(out[0]), int(out[1])
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
+            _lib._lib.spmvk_csr_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def build_csr(m: TripletMatrix, precision=F64, stream: int = 0) -> CsrMatrix:
+    """build_csr<Scalar>(m) (csr.hpp:24-39): upload + validate on the device."""
+    prec = _prec(precision)
+    val = m.val if prec == F64 else m.val.astype(np.float32)
+    h = C.c_void_p()
+    _check(lib().spmvk_csr_upload(m.num_rows, m.num_cols, m.nnz, _ptr(m.row_ptr), _ptr(m.col),
+                                  _ptr(val), prec, stream or None, C.byref(h)))
+    return CsrMatrix(h.value)
+
+
+def _as_csr(m) -> CsrMatrix:
+    if isinstance(m, CsrMatrix):
+        return m
+    if isinstance(m, TripletMatrix):
+        return build_csr(m, F64)
+    raise InvalidArgument(f"expected TripletMatrix or CsrMatrix, got {type(m).__name__}")
+
+
+# ---------------------------------------------------------------- SpMV plumbing
+def _is_torch(t) -> bool:
+    return type(t).__module__.startswith("torch")
+
+
+def _torch_stream(t) -> int:
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _device_call(fn_name_prefix: str, handle, x, y, n_rows: int, n_cols: int, prec: int,
+                 stream: Optional[int]):
+    import torch
+    dt = torch.float32 if prec == F32 else torch.float64
+    if not (x.is_cuda and x.is_contiguous()):
+        raise InvalidArgument("x must be a contiguous CUDA tensor")
+    if y is None:
+        y = torch.empty(n_rows, dtype=dt, device=x.device)
+    if x.dtype != dt or y.dtype != dt:
+        raise InvalidArgument(f"{fn_name_prefix}: handle precision differs from the x/y dtype")
+    s = stream if stream is not None else _torch_stream(x)
+    sfx = "f32" if prec == F32 else "f64"
+    _check(getattr(lib(), f"{fn_name_prefix}_{sfx}")(handle, x.data_ptr(), x.numel(),
+                                                     y.data_ptr(), y.numel(), s or None))
+    return y
+
+
+# ---------------------------------------------------------------- RgCSR
+@dataclass
+class FillReport:
+    """spmvkit::FillReport (fill.hpp:18-26)."""
+    format_name: str
+    stored_slots: int
+    nnz: int
+    artificial_zeros: int
+    fill_percent: float
+    bytes_single: int
+    bytes_double: int
+
+
+def _fill_percent(az: int, nnz: int) -> float:
+    return 0.0 if nnz == 0 else 100.0 * az / nnz
+
+
+class RgcsrMatrix:
+    """Device RgCSR (RgcsrMatrix<S>, rgcsr.hpp:19-36) owned by a handle."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self.info = RgcsrInfo()
+        _check(lib().spmvk_rgcsr_get_info(self._h, C.byref(self.info)))
+        self.num_rows = self.info.num_rows
+        self.num_cols = self.info.num_cols
+        self.group_size = self.info.group_size
+        self.precision = self.info.precision
+
+    def num_groups(self) -> int:
+        return self.info.num_groups
+
+    def rows_in_group(self, g: int) -> int:
+        return min(self.group_size, self.num_rows - g * self.group_size)
+
+    def slot_count(self) -> int:
+        return self.info.slots
+
+    def nnz(self) -> int:
+        return self.info.nnz
+
+    def to_host(self) -> dict:
+        """The four reference arrays: values, columns, group_pointers, row_lengths."""
+        i = self.info
+        out = dict(values=np.empty(i.slots, _dtype(self.precision)),
+                   columns=np.empty(i.slots, np.uint32),
+                   group_pointers=np.empty(i.num_groups + 1, np.uint32),
+                   row_lengths=np.empty(i.num_rows, np.uint32))
+        _check(lib().spmvk_rgcsr_download(self._h, _ptr(out["values"]), _ptr(out["columns"]),
+                                          _ptr(out["group_pointers"]), _ptr(out["row_lengths"])))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
+            _lib._lib.spmvk_rgcsr_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def build_rgcsr(m, group_size: int, precision=F64, stream: int = 0,
+                row_range: Optional[tuple] = None) -> RgcsrMatrix:
+    """build_rgcsr<S>(m, group_size) (rgcsr.hpp:38-70) on the device.
+
+    ``m`` is a TripletMatrix (uploaded first) or a device CsrMatrix.  Raises
+    InvalidArgument for group_size == 0 (the reference's message) and
+    SpmvkRuntimeError when the slot count overflows uint32 (the reference
+    truncates silently, rgcsr.hpp:56).  ``row_range=(r0, r1)`` builds the
+    group-aligned row slab used by the partitioner.
+    """
+    if group_size < 0:
+        raise InvalidArgument("build_rgcsr: group size must be nonzero")
+    a = _as_csr(m)
+    h = C.c_void_p()
+    if row_range is None:
+        _check(lib().spmvk_rgcsr_build(a._h, group_size, _prec(precision), stream or None,
+                                       C.byref(h)))
+    else:
+        _check(lib().spmvk_rgcsr_build_rows(a._h, row_range[0], row_range[1], group_size,
+                                            _prec(precision), stream or None, C.byref(h)))
+    return RgcsrMatrix(h.value)
+
+
+def spmv_rgcsr(a: RgcsrMatrix, x, y=None, multiply_add_count: bool = False,
+               stream: Optional[int] = None):
+    """spmv_rgcsr(a, x[, y][, &madds]) (rgcsr.hpp:75-105).
+
+    numpy x -> host span semantics (returns numpy y, plus the multiply-add
+    count when requested); CUDA tensor x -> device-resident launch on the
+    current stream (returns the y tensor)."""
+    if _is_torch(x):
+        y = _device_call("spmvk_rgcsr_spmv", a._h, x, y, a.num_rows, a.num_cols, a.precision,
+                         stream)
+        return (y, a.nnz()) if multiply_add_count else y
+    dt = _dtype(a.precision)
+    x = np.ascontiguousarray(x)
+    if x.dtype != dt:
+        raise InvalidArgument("spmv_rgcsr: handle precision differs from the x dtype")
+    if y is None:
+        y = np.empty(a.num_rows, dt)
+    madds = C.c_uint64()
+    fn = lib().spmvk_rgcsr_spmv_host_f32 if a.precision == F32 else lib().spmvk_rgcsr_spmv_host_f64
+    _check(fn(a._h, _ptr(x), x.size, _ptr(y), y.size, C.byref(madds)))
+    return (y, madds.value) if multiply_add_count else y
+
+
+# ---------------------------------------------------------------- Hybrid
+def hybrid_split_cost(row_lens, k: int) -> int:
+    """hybrid_split_cost (ellpack.hpp:145-150)."""
+    L = np.ascontiguousarray(row_lens, dtype=np.uint64)
+    return int(lib().spmvk_hybrid_split_cost(_ptr(L), L.size, k))
+
+
+def choose_ell_width(row_lens) -> int:
+    """choose_ell_width (ellpack.hpp:153-166): histogram + suffix sums."""
+    L = np.ascontiguousarray(row_lens, dtype=np.uint64)
+    return int(lib().spmvk_choose_ell_width(_ptr(L), L.size))
+
+
+class HybridMatrix:
+    """Device Hybrid ELL+COO (HybridMatrix<S>, ellpack.hpp:44-48)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self.info = HybridInfo()
+        _check(lib().spmvk_hybrid_get_info(self._h, C.byref(self.info)))
+        self.num_rows = self.info.num_rows
+        self.num_cols = self.info.num_cols
+        self.precision = self.info.precision
+
+    @property
+    def slots_per_row(self) -> int:
+        return self.info.ell_width
+
+    def coo_nnz(self) -> int:
+        return self.info.coo_nnz
+
+    def to_host(self) -> dict:
+        i, dt = self.info, _dtype(self.precision)
+        out = dict(ell_values=np.empty(i.ell_slots, dt), ell_columns=np.empty(i.ell_slots, np.uint32),
+                   coo_rows=np.empty(i.coo_nnz, np.uint32), coo_columns=np.empty(i.coo_nnz, np.uint32),
+                   coo_values=np.empty(i.coo_nnz, dt))
+        _check(lib().spmvk_hybrid_download(self._h, *(_ptr(out[k]) for k in (
+            "ell_values", "ell_columns", "coo_rows", "coo_columns", "coo_values"))))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
+            _lib._lib.spmvk_hybrid_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def build_hybrid(m, k1: Optional[int] = None, precision=F64, stream: int = 0) -> HybridMatrix:
+    """build_hybrid<S>(m, k1) (ellpack.hpp:168-203); k1=None chooses the width."""
+    a = _as_csr(m)
+    h = C.c_void_p()
+    _check(lib().spmvk_hybrid_build(a._h, -1 if k1 is None else int(k1), _prec(precision),
+                                    stream or None, C.byref(h)))
+    return HybridMatrix(h.value)
+
+
+def spmv_hybrid(h: HybridMatrix, x, y=None, stream: Optional[int] = None):
+    """spmv_hybrid(h, x, y) (ellpack.hpp:205-217)."""
+    if _is_torch(x):
+        return _device_call("spmvk_hybrid_spmv", h._h, x, y, h.num_rows, h.num_cols,
+                            h.precision, stream)
+    dt = _dtype(h.precision)
+    x = np.ascontiguousarray(x)
+    if x.dtype != dt:
+        raise InvalidArgument("spmv_hybrid: handle precision differs from the x dtype")
+    if y is None:
+        y = np.empty(h.num_rows, dt)
+    fn = lib().spmvk_hybrid_spmv_host_f32 if h.precision == F32 else lib().spmvk_hybrid_spmv_host_f64
+    _check(fn(h._h, _ptr(x), x.size, _ptr(y), y.size))
+    return y
+
+
+def spmv_csr(a: CsrMatrix, x, y=None, stream: Optional[int] = None):
+    """spmv_csr(a, x, y) (csr.hpp:41-53), device tensors only."""
+    if not _is_torch(x):
+        raise InvalidArgument("spmv_csr on the device takes CUDA tensors")
+    return _device_call("spmvk_csr_spmv", a._h, x, y, a.num_rows, a.num_cols, a.val_prec, stream)
+
+
+# ---------------------------------------------------------------- accounting
+def fill_report(a) -> FillReport:
+    """fill_report (fill.hpp:52-95) for RgCSR and Hybrid handles."""
+    i = a.info
+    if isinstance(a, RgcsrMatrix):
+        return FillReport("rgcsr", i.slots, i.nnz, i.artificial_zeros,
+                          _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
+    if isinstance(a, HybridMatrix):
+        return FillReport("hybrid", i.ell_slots + i.coo_nnz, i.nnz, i.artificial_zeros,
+                          _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
+    raise InvalidArgument(f"no fill report for {type(a).__name__}")
+
+
+def measured_gflops(nnz: int, seconds: float) -> float:
+    """2 * nnz / seconds / 1e9 (memsim.cpp:201-207)."""
+    if not seconds > 0.0:
+        raise InvalidArgument(f"measured_gflops: seconds must be positive, got {seconds}")
+    return 2.0 * nnz / seconds / 1e9

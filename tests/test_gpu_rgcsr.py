@@ -1,0 +1,205 @@
+"""GPU parity of the RgCSR path (K1 conversion, K2 SpMV) through the C-ABI.
+
+Mirrors the reference's own tests: tests/test_formats.cpp:247-350 (golden M8
+arrays, degeneracies, madds, monotone padding, fill bytes, oracle
+equivalence, float exactness) and tests/acceptance.cpp:138-173 (200-seed
+oracle equivalence).  Bar: converted arrays and y BITWISE equal to the
+reference's (stronger than the 1e-12 / 1e-5 tolerance north_star allows).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import RG_KEYS, assert_rgcsr_equal, bitwise, golden_csr, triplets
+from paper_1012_2270_b200 import spmvkit as sk
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def test_example8_golden_arrays(cuda, golden):
+    g = golden["example8"]
+    m = triplets(golden_csr(g, "m"))
+    for G in (4, 8):
+        for prec in (8, 4):
+            a = sk.build_rgcsr(m, G, prec)
+            assert_rgcsr_equal(a.to_host(), g, f"rg{G}_p{prec}_")
+            dt = np.float64 if prec == 8 else np.float32
+            y, madds = sk.spmv_rgcsr(a, np.ones(8, dt), multiply_add_count=True)
+            assert bitwise(y, g[f"rg{G}_p{prec}_y_ones"])
+            assert madds == 13  # one per stored nonzero (test_formats.cpp:267-275)
+            az, bs, bd, nnz = (int(v) for v in g[f"rg{G}_p{prec}_fill"])
+            f = sk.fill_report(a)
+            assert (f.artificial_zeros, f.bytes_single, f.bytes_double, f.nnz) == (az, bs, bd, nnz)
+    # tests/test_formats.cpp:247-256 verbatim
+    a = sk.build_rgcsr(m, 4).to_host()
+    assert a["group_pointers"].tolist() == [0, 8, 20]
+    assert a["row_lengths"].tolist() == [2, 1, 1, 1, 1, 2, 3, 2]
+    assert a["values"].tolist() == [1, 3, 4, 5, 2, 0, 0, 0, 6, 7, 9, 12, 0, 8, 10, 13, 0, 0, 11, 0]
+    assert a["columns"].tolist() == [0, 1, 2, 0, 3, 0, 0, 0, 4, 0, 1, 2, 0, 5, 4, 7, 0, 0, 6, 0]
+
+
+def test_errors_match_reference(cuda, golden):
+    m = triplets(golden_csr(golden["example8"], "m"))
+    with pytest.raises(sk.InvalidArgument, match="group size must be nonzero"):
+        sk.build_rgcsr(m, 0)
+    a = sk.build_rgcsr(m, 4)
+    with pytest.raises(sk.InvalidArgument, match="spmv_rgcsr: dimension mismatch"):
+        sk.spmv_rgcsr(a, np.ones(9))
+    with pytest.raises(sk.InvalidArgument, match="dimension mismatch"):
+        sk.spmv_rgcsr(a, dev(np.ones(8)), y=torch.empty(7, dtype=torch.float64, device="cuda"))
+    with pytest.raises(sk.InvalidArgument):
+        sk.spmv_rgcsr(a, np.ones(8, np.float32))  # precision mismatch
+    # TripletMatrix ctor validation (src/triplet.cpp:22-32), on the device
+    bad = orc.Csr(2, 2, [0, 2, 2], [1, 0], [1.0, 2.0])  # decreasing columns
+    with pytest.raises(sk.InvalidArgument, match="strictly increasing"):
+        sk.build_csr(sk.TripletMatrix(2, 2, bad.rp, bad.col, bad.val, validate=False))
+    oob = orc.Csr(2, 2, [0, 1, 1], [5], [1.0])
+    with pytest.raises(sk.InvalidArgument, match="outside"):
+        sk.build_csr(sk.TripletMatrix(2, 2, oob.rp, oob.col, oob.val, validate=False))
+
+
+@pytest.mark.parametrize("kind", ["i", "r"])
+def test_small_golden_seeds(cuda, golden, kind):
+    """random_small seeds 600-649, G = 1 + seed % 9 (test_formats.cpp:325-342)."""
+    g = golden["small"]
+    for seed in range(600, 650):
+        t = f"s{seed}_{kind}"
+        m = triplets(golden_csr(g, t))
+        G = 1 + seed % 9
+        x = g[f"{t}_x"]
+        a = sk.build_rgcsr(m, G)
+        assert_rgcsr_equal(a.to_host(), g, f"{t}_rg_")
+        assert bitwise(sk.spmv_rgcsr(a, x), g[f"{t}_rg_y"]), t
+        assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), g[f"{t}_rg_y"]), t
+        a32 = sk.build_rgcsr(m, G, 4)
+        assert_rgcsr_equal(a32.to_host(), g, f"{t}_rg32_")
+        assert bitwise(sk.spmv_rgcsr(a32, x.astype(np.float32)), g[f"{t}_rg32_y"]), t
+        if kind == "i":  # integer data: every format bitwise equal to spmv_reference
+            assert bitwise(g[f"{t}_rg_y"], g[f"{t}_ref_y"])
+
+
+def test_acceptance_200_seeds(cuda, golden):
+    """tests/acceptance.cpp:138-173: 200 random_case matrices, G = 1 + seed % 9."""
+    g = golden["acceptance"]
+    for seed in range(200):
+        m = triplets(golden_csr(g, f"a{seed}"))
+        a = sk.build_rgcsr(m, 1 + seed % 9)
+        assert_rgcsr_equal(a.to_host(), g, f"a{seed}_rg_")
+        y = sk.spmv_rgcsr(a, dev(g[f"a{seed}_xi"])).cpu().numpy()
+        assert bitwise(y, g[f"a{seed}_rg_yi"]) and bitwise(y, g[f"a{seed}_ref_yi"]), seed
+
+
+def test_padding_monotone_and_single_group_is_ell(cuda):
+    """test_formats.cpp:277-297 and acceptance.cpp:262-269."""
+    for seed in range(300, 320):
+        om = orc.random_small(seed)
+        m = triplets(om)
+        prev, first, last = 0, True, 0
+        G = 1
+        while G < 2 * om.rows:
+            a = sk.build_rgcsr(m, G)
+            z = sk.fill_report(a).artificial_zeros
+            assert (z == 0) if first else (z >= prev)
+            first, prev, last = False, z, a.slot_count()
+            G *= 2
+        ell_slots = om.rows * int(om.lens().max()) if om.nnz else 0
+        assert last == ell_slots
+        assert sk.build_rgcsr(m, om.rows + seed % 5).slot_count() == ell_slots
+
+
+@pytest.mark.parametrize("shape", ["empty_rows", "no_entries", "single_row", "identity", "dense_row"])
+def test_edge_shapes(cuda, shape):
+    if shape == "empty_rows":
+        om = orc.Csr(5, 4, [0, 0, 2, 2, 2, 3], [1, 3, 0], [2.0, -1.0, 5.0])
+    elif shape == "no_entries":
+        om = orc.Csr(3, 3, [0, 0, 0, 0], [], [])
+    elif shape == "single_row":
+        om = orc.Csr(1, 3, [0, 1], [2], [7.0])
+    elif shape == "identity":
+        om = orc.Csr(7, 7, np.arange(8), np.arange(7), np.ones(7))
+    else:  # one long row among short ones
+        n = 200
+        rp = np.concatenate([[0], n + np.arange(n)])  # row 0 dense, then one entry each
+        col = np.concatenate([np.arange(n), np.arange(1, n)])
+        om = orc.Csr(n, n, rp, col, np.arange(col.size, dtype=np.float64) - 50.5)
+    x = orc.random_vector(om.cols, 3)
+    for G in (1, 2, 3, 4, 32, 33, 256):
+        want = orc.build_rgcsr(om, G)
+        a = sk.build_rgcsr(triplets(om), G)
+        assert_rgcsr_equal(a.to_host(), want)
+        assert bitwise(sk.spmv_rgcsr(a, x), orc.spmv_rgcsr(want, x)[0])
+
+
+@pytest.mark.parametrize("G", [32, 64, 128, 256])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_config1_5pt_1024_bitwise(cuda, G, prec):
+    """Config 1 (2D 5-point 1024^2) at full size: arrays and y vs the oracle."""
+    om = orc.stencil(5, 1024)
+    a = sk.build_rgcsr(sk.CsrMatrix.stencil(5, 1024), G, prec)
+    want = orc.build_rgcsr(om, G, prec)
+    assert_rgcsr_equal(a.to_host(), want)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), orc.spmv_rgcsr(want, x)[0])
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_config2_27pt_128_bitwise(cuda, prec):
+    """Config 2 (3D 27-point 128^3, 55.7 M nnz) at full size, G = 32."""
+    om = orc.stencil(27, 128)
+    csr = sk.CsrMatrix.stencil(27, 128)
+    rp, col, val = csr.to_host()
+    assert bitwise(rp, om.rp) and bitwise(col, om.col) and bitwise(val, om.val)
+    a = sk.build_rgcsr(csr, 32, prec)
+    want = orc.build_rgcsr(om, 32, prec)
+    assert_rgcsr_equal(a.to_host(), want)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    y = sk.spmv_rgcsr(a, dev(x)).cpu().numpy()
+    assert bitwise(y, orc.spmv_rgcsr(want, x)[0])
+    if prec == 8:  # the reference's checksum on this input
+        assert float(np.cumsum(y)[-1]) == 1674.3573800651031
+
+
+def test_row_slabs_equal_global_slices(cuda):
+    """Group-aligned slabs are exactly the global arrays' slices."""
+    om = orc.stencil(27, 24)
+    csr = sk.CsrMatrix.stencil(27, 24)
+    G = 32
+    full = sk.build_rgcsr(csr, G).to_host()
+    x = orc.random_vector(om.cols, 1)
+    y_full = sk.spmv_rgcsr(sk.build_rgcsr(csr, G), x)
+    n = om.rows
+    groups = (n + G - 1) // G
+    for P in (2, 3, 4, 8):
+        cuts = [min(n, (groups * p // P) * G) for p in range(P + 1)]
+        for r0, r1 in zip(cuts, cuts[1:]):
+            s = sk.build_rgcsr(csr, G, row_range=(r0, r1))
+            h = s.to_host()
+            g0, g1 = r0 // G, (r1 + G - 1) // G
+            gp = full["group_pointers"]
+            assert bitwise(h["group_pointers"], (gp[g0:g1 + 1] - gp[g0]).astype(np.uint32))
+            assert bitwise(h["values"], full["values"][gp[g0]:gp[g1]])
+            assert bitwise(h["columns"], full["columns"][gp[g0]:gp[g1]])
+            assert bitwise(h["row_lengths"], full["row_lengths"][r0:r1])
+            assert bitwise(sk.spmv_rgcsr(s, x), y_full[r0:r1])
+
+
+def test_scaled_iteration_fused(cuda):
+    from paper_1012_2270_b200._lib import lib
+    om = orc.stencil(7, 20)
+    a = sk.build_rgcsr(sk.CsrMatrix.stencil(7, 20), 32)
+    x = dev(orc.random_vector(om.cols, 1))
+    y = torch.empty_like(x)
+    xn = torch.empty_like(x)
+    assert lib().spmvk_rgcsr_spmv_scaled_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(),
+                                             y.numel(), xn.data_ptr(), 0.0625, None) == 0
+    torch.cuda.synchronize()
+    want = orc.spmv_rgcsr(orc.build_rgcsr(om, 32), x.cpu().numpy())[0]
+    assert bitwise(y.cpu().numpy(), want)
+    assert bitwise(xn.cpu().numpy(), want * 0.0625)
