@@ -139,6 +139,11 @@ int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx
 int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
                               uint64_t ny, uint64_t* multiply_add_count);
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
+/* Tuning knob (process-wide): which K2 kernel runs — "tma" (default:
+ * bulk-async-copy shared-memory pipeline, group size <= 256), "ldg" (direct
+ * streamed loads), "ldg_pf" / "ldg8_pf" (software-pipelined loads).  All
+ * variants give bitwise identical y.  Also read from SPMVK_RGCSR_KERNEL. */
+int spmvk_set_rgcsr_kernel(const char* name);
 
 /* ------------------------------------------------------------------ Hybrid */
 typedef struct {

@@ -72,8 +72,9 @@ struct DevBuf {
   void alloc(uint64_t count) {
     release();
     n = count;
-    // one extra element keeps zero-sized arrays valid, distinct pointers
-    SPMVK_CUDA(cudaMalloc(&p, sizeof(T) * (count + 1)));
+    // 64 spare bytes: zero-sized arrays stay valid, and 16-byte-aligned bulk
+    // copies may round a range end up to 3 elements past the last one
+    SPMVK_CUDA(cudaMalloc(&p, sizeof(T) * count + 64));
   }
   void release() {
     if (p) cudaFree(p);

@@ -7,12 +7,15 @@
 // rows of a group read s CONTIGUOUS slots, so a warp of consecutive rows
 // issues fully coalesced loads with one thread per row.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <memory>
 #include <mutex>
 #include <string>
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "rgcsr_spmv.cuh"
 
 namespace spmvk {
 namespace {
@@ -76,51 +79,6 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
         }
       }
     }
-  }
-}
-
-// ------------------------------------------------------------ K2: SpMV
-// Thread per row inside its group; persistent grid-stride CTAs.  The j loop
-// keeps the reference's order: acc = ((0 + v0*x0) + v1*x1) + ..., each product
-// and sum rounded separately (no FMA), so y is bitwise spmv_rgcsr's y.
-// Matrix slots are streamed (L1 no-allocate, L2 evict-first); x is gathered
-// through the read-only path with L2 evict-last so it stays L2-resident.
-template <class T, bool kScaled>
-__global__ void __launch_bounds__(256) rgcsr_spmv_kernel(
-    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
-    const uint32_t* __restrict__ lens, const T* __restrict__ values,
-    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale) {
-  constexpr int U = sizeof(T) == 8 ? 4 : 8;
-  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-    const uint32_t t = r - g * G;
-    const uint32_t s = min(G, rows - g * G);
-    const uint32_t len = lens[r];
-    const T* __restrict__ vp = values + gp[g] + t;
-    const uint32_t* __restrict__ cp = columns + gp[g] + t;
-    T acc = T(0);
-    uint32_t j = 0;
-    for (; j + U <= len; j += U) {
-      uint32_t c[U];
-      T v[U], xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        c[u] = ld_stream(cp + (size_t)(j + u) * s, pf);
-        v[u] = ld_stream(vp + (size_t)(j + u) * s, pf);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u], pl);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
-    }
-    for (; j < len; ++j) {
-      const uint32_t c = ld_stream(cp + (size_t)j * s, pf);
-      acc = add_rn(acc, mul_rn(ld_stream(vp + (size_t)j * s, pf), ld_x(x + c, pl)));
-    }
-    y[r] = acc;
-    if (kScaled) x_next[r] = mul_rn(acc, scale);
   }
 }
 
@@ -213,15 +171,76 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
     fail(SPMVK_EINVAL, "spmv_rgcsr: handle precision differs from the entry point");
 }
 
+// K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL =
+// tma | ldg | ldg_pf | ldg8_pf; default tma (used when the group size allows).
+enum class K2 { kTma, kLdg, kLdgPf, kLdg8Pf };
+
+bool parse_k2(const std::string& v, K2* out) {
+  if (v == "tma") *out = K2::kTma;
+  else if (v == "ldg") *out = K2::kLdg;
+  else if (v == "ldg_pf") *out = K2::kLdgPf;
+  else if (v == "ldg8_pf") *out = K2::kLdg8Pf;
+  else return false;
+  return true;
+}
+
+std::atomic<int>& k2_slot() {
+  static std::atomic<int> k{[] {
+    K2 v = K2::kTma;
+    const char* e = std::getenv("SPMVK_RGCSR_KERNEL");
+    if (e) parse_k2(e, &v);
+    return static_cast<int>(v);
+  }()};
+  return k;
+}
+
+K2 k2_choice() { return static_cast<K2>(k2_slot().load(std::memory_order_relaxed)); }
+
+template <class T, bool kScaled, int NW, int NS, int CE>
+void launch_tma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
+  constexpr size_t smem = tma_smem_bytes<T, NS, CE>();
+  auto kern = rgcsr_spmv_tma<T, kScaled, NW, NS, CE>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  const uint32_t G = static_cast<uint32_t>(h->group_size);
+  const uint32_t gpt = (NW * 32) / G;
+  const uint32_t ntiles = static_cast<uint32_t>((h->groups + gpt - 1) / gpt);
+  int per_sm = 0;
+  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, smem));
+  kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), (NW + 1) * 32, smem, s>>>(
+      static_cast<uint32_t>(h->rows), G, pow2_shift(G), static_cast<uint32_t>(h->groups), gpt,
+      ntiles, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+      h->columns.p, x, y, x_next, scale);
+  SPMVK_LAUNCH("rgcsr_spmv_tma");
+}
+
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
+  const K2 k = k2_choice();
+  if (k == K2::kTma && h->group_size <= 256) {
+    if constexpr (sizeof(T) == 8)
+      launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
+    else
+      launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
+    return;
+  }
   const unsigned grid = persistent_grid((h->rows + 255) / 256, 8);
-  rgcsr_spmv_kernel<T, kScaled><<<grid, 256, 0, s>>>(
-      static_cast<uint32_t>(h->rows), static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull)),
-      pow2_shift(h->group_size), h->group_pointers.p, h->row_lengths.p,
-      reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, x_next, scale);
-  SPMVK_LAUNCH("rgcsr_spmv_kernel");
+  const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
+  const int sh = pow2_shift(h->group_size);
+  constexpr int U = sizeof(T) == 8 ? 4 : 8;
+  auto args = [&](auto kern) {
+    kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+                              h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+                              h->columns.p, x, y, x_next, scale);
+  };
+  if (k == K2::kLdgPf) args(rgcsr_spmv_ldg<T, kScaled, U, true>);
+  else if (k == K2::kLdg8Pf) args(rgcsr_spmv_ldg<T, kScaled, 8, true>);
+  else args(rgcsr_spmv_ldg<T, kScaled, U, false>);
+  SPMVK_LAUNCH("rgcsr_spmv_ldg");
 }
 
 template <class T>
@@ -335,5 +354,15 @@ int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx,
 }
 
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h) { delete h; }
+
+int spmvk_set_rgcsr_kernel(const char* name) {
+  return guarded([&] {
+    K2 k;
+    if (!name || !parse_k2(name, &k))
+      fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
+                             "' (tma | ldg | ldg_pf | ldg8_pf)");
+    k2_slot().store(static_cast<int>(k));
+  });
+}
 
 }  // extern "C"

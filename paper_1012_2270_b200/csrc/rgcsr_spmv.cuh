@@ -1,0 +1,199 @@
+// K2 RgCSR SpMV kernels (included by rgcsr.cu).
+//
+// Every variant keeps the reference's per-row order of roundings
+// (rgcsr.hpp:87-93): acc = ((0 + v0*x0) + v1*x1) + ..., product and sum
+// rounded separately, so y is bitwise spmv_rgcsr's y.  They differ only in
+// how the group-interleaved slots reach the SMs:
+//
+//  * rgcsr_spmv_ldg  — thread per row, slots streamed straight from HBM with
+//    L1-no-allocate / L2-evict-first loads, U-deep batches; with kPrefetch the
+//    next batch's loads are issued before the current batch's x gathers.
+//  * rgcsr_spmv_tma  — persistent CTAs with one producer warp that streams the
+//    CTA's contiguous slab range [gp[g0], gp[g1]) through an NS-stage shared
+//    memory ring with 1D bulk async copies (cp.async.bulk -> UBLKCP,
+//    mbarrier complete_tx), and NW consumer warps, thread per row, reading
+//    their slots from shared memory (stride s, conflict-free) and gathering x
+//    through the read-only path.  Memory-level parallelism then no longer
+//    depends on the consumers' dependent add chains.
+#pragma once
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace spmvk {
+
+template <class T, bool kScaled, int U, bool kPrefetch>
+__global__ void __launch_bounds__(256) rgcsr_spmv_ldg(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale) {
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t t = r - g * G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = lens[r];
+    const T* __restrict__ vp = values + gp[g] + t;
+    const uint32_t* __restrict__ cp = columns + gp[g] + t;
+    T acc = T(0);
+    const uint32_t full = len / U * U;
+    uint32_t cA[U];
+    T vA[U];
+    if (kPrefetch && full) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cA[u] = ld_stream(cp + (size_t)u * s, pf);
+        vA[u] = ld_stream(vp + (size_t)u * s, pf);
+      }
+    }
+    uint32_t j = 0;
+    for (; j < full; j += U) {
+      if (!kPrefetch) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cA[u] = ld_stream(cp + (size_t)(j + u) * s, pf);
+          vA[u] = ld_stream(vp + (size_t)(j + u) * s, pf);
+        }
+      }
+      uint32_t cB[U];
+      T vB[U];
+      const bool more = kPrefetch && j + U < full;
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cB[u] = ld_stream(cp + (size_t)(j + U + u) * s, pf);
+          vB[u] = ld_stream(vp + (size_t)(j + U + u) * s, pf);
+        }
+      }
+      T xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cA[u], pl);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(vA[u], xv[u]));
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cA[u] = cB[u];
+          vA[u] = vB[u];
+        }
+      }
+    }
+    for (; j < len; ++j) {
+      const uint32_t c = ld_stream(cp + (size_t)j * s, pf);
+      acc = add_rn(acc, mul_rn(ld_stream(vp + (size_t)j * s, pf), ld_x(x + c, pl)));
+    }
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+}
+
+// Shared-memory footprint of rgcsr_spmv_tma<T, NW, NS, CE>.
+template <class T, int NS, int CE>
+constexpr size_t tma_smem_bytes() {
+  return (size_t)NS * CE * (sizeof(T) + sizeof(uint32_t)) + 2 * NS * sizeof(uint64_t);
+}
+
+template <class T, bool kScaled, int NW, int NS, int CE>
+__global__ void __launch_bounds__((NW + 1) * 32) rgcsr_spmv_tma(
+    uint32_t rows, uint32_t G, int g_shift, uint32_t groups, uint32_t gpt, uint32_t ntiles,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  static_assert(CE % 4 == 0, "chunks must keep 16-byte alignment");
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* vbuf = reinterpret_cast<T*>(smem);
+  uint32_t* cbuf = reinterpret_cast<uint32_t*>(vbuf + NS * CE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + NS * CE);
+  uint64_t* empty = full + NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {  // ---------------- producer: one elected lane
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t it = 0;
+      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t g0 = tile * gpt, g1 = min(g0 + gpt, groups);
+        const uint64_t s0 = gp[g0] & ~3ull, s1 = ((uint64_t)gp[g1] + 3) & ~3ull;
+        for (uint64_t c = s0; c < s1; c += CE, ++it) {
+          const uint32_t stage = it % NS, ph = (it / NS) & 1;
+          mbar_wait(&empty[stage], ph ^ 1);
+          const uint32_t n = (uint32_t)min((uint64_t)CE, s1 - c);
+          mbar_arrive_expect_tx(&full[stage], n * (uint32_t)(sizeof(T) + sizeof(uint32_t)));
+          bulk_g2s(vbuf + stage * CE, values + c, n * (uint32_t)sizeof(T), &full[stage], pol);
+          bulk_g2s(cbuf + stage * CE, columns + c, n * 4u, &full[stage], pol);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: thread per row of the tile
+  const uint64_t pl = policy_evict_last();
+  constexpr int U = sizeof(T) == 8 ? 4 : 8;
+  uint32_t it = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t g0 = tile * gpt, g1 = min(g0 + gpt, groups);
+    const uint64_t s0 = gp[g0] & ~3ull, s1 = ((uint64_t)gp[g1] + 3) & ~3ull;
+    const uint32_t r = g0 * G + warp * 32 + lane;
+    const bool live = r < min(g1 * G, rows);
+    uint32_t len = 0, s = 1;
+    uint64_t off = 0;
+    if (live) {
+      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+      const uint32_t t = r - g * G;
+      s = min(G, rows - g * G);
+      len = lens[r];
+      off = (uint64_t)gp[g] + t;
+    }
+    uint32_t j = 0;
+    T acc = T(0);
+    for (uint64_t c = s0; c < s1; c += CE, ++it) {
+      const uint32_t stage = it % NS, ph = (it / NS) & 1;
+      mbar_wait(&full[stage], ph);
+      const uint64_t cend = min(c + CE, s1);
+      uint32_t nb = 0;
+      if (j < len && off < cend) nb = min(len - j, (uint32_t)((cend - off + s - 1) / s));
+      const T* vb = vbuf + stage * CE;
+      const uint32_t* cb = cbuf + stage * CE;
+      uint32_t i = (uint32_t)(off - c);
+      uint32_t k = 0;
+      for (; k + U <= nb; k += U) {
+        uint32_t cc[U];
+        T vv[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cc[u] = cb[i + u * s];
+          vv[u] = vb[i + u * s];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cc[u], pl);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(vv[u], xv[u]));
+        i += U * s;
+      }
+      for (; k < nb; ++k) {
+        acc = add_rn(acc, mul_rn(vb[i], ld_x(x + cb[i], pl)));
+        i += s;
+      }
+      j += nb;
+      off += (uint64_t)nb * s;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+    if (live) {
+      y[r] = acc;
+      if (kScaled) x_next[r] = mul_rn(acc, scale);
+    }
+  }
+}
+
+}  // namespace spmvk

@@ -1,0 +1,196 @@
+"""Row-slab partitioner and the iterated, distributed SpMV (north_star item 4).
+
+A is cut into P contiguous, group-aligned row slabs, one per GPU (one process
+per GPU, torch.distributed over NCCL).  Because slab boundaries are
+multiples of the group size G, each slab's RgCSR arrays are exactly the
+global build's slice (group pointers rebased) — checked in
+tests/test_gpu_rgcsr.py::test_row_slabs_equal_global_slices — so every row
+accumulates in the reference's order and the distributed y is bitwise the
+1-GPU y.  Columns stay global.
+
+Iteration (a CG-style repeated product):
+    y_k = A x_k ;  x_{k+1} = y_k * 2^-4
+The scale is fused into the SpMV epilogue (spmvk_rgcsr_spmv_scaled_f64 writes
+y and the rank's slab of x_{k+1} in one pass); the slabs are then exchanged
+with an NCCL all-gather so every rank holds the whole x_{k+1}.  All slabs
+have S = ceil(groups / P) * G rows (the last one is padded), so the
+all-gather has equal counts; padding entries of x are never referenced.
+
+The exchange is a real data dependency of the iterated product (every rank
+needs every x entry its columns touch), so this is the one place the path
+uses a collective.  A halo variant that exchanges only the column ranges a
+slab actually reads (``halo_plan``) is the scaling path for banded matrices.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+from dataclasses import dataclass
+from typing import Callable, List, Sequence
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    row_begin: int
+    row_end: int  # exclusive; real rows only
+    pad_rows: int  # S: rows every slab reserves in the gathered x
+
+    @property
+    def rows(self) -> int:
+        return self.row_end - self.row_begin
+
+
+def slab_bounds(num_rows: int, group_size: int, parts: int) -> List[Slab]:
+    """Equal, group-aligned slabs: S = ceil(groups / P) * G rows each."""
+    if group_size <= 0 or parts <= 0:
+        raise ValueError("group size and part count must be positive")
+    groups = (num_rows + group_size - 1) // group_size
+    per = (groups + parts - 1) // parts
+    S = per * group_size
+    out = []
+    for p in range(parts):
+        b = min(num_rows, p * S)
+        e = min(num_rows, (p + 1) * S)
+        out.append(Slab(p, b, e, S))
+    return out
+
+
+def weighted_slab_bounds(row_lengths: Sequence[int], group_size: int, parts: int) -> List[tuple]:
+    """Group-aligned cuts balancing stored slots (for skewed matrices such as
+    the power-law config): cut p sits at the first group boundary where the
+    running slot count reaches p/P of the total.  Returns [(r0, r1)]."""
+    lens = np.asarray(row_lengths, dtype=np.int64)
+    n = lens.size
+    G = group_size
+    groups = (n + G - 1) // G
+    pad = np.zeros(groups * G, np.int64)
+    pad[:n] = lens
+    width = pad.reshape(groups, G).max(axis=1)
+    s = np.minimum(G, n - np.arange(groups) * G)
+    slots = np.cumsum(width * s)
+    total = int(slots[-1]) if groups else 0
+    cuts = [0]
+    for p in range(1, parts):
+        g = int(np.searchsorted(slots, total * p / parts, side="left")) + 1 if total else 0
+        cuts.append(min(n, max(cuts[-1], g * G)))
+    cuts.append(n)
+    return list(zip(cuts, cuts[1:]))
+
+
+def halo_plan(slab: Slab, column_min: int, column_max: int, slabs: Sequence[Slab]):
+    """Ranks whose x slab intersects [column_min, column_max] of this slab's
+    columns and the intersecting ranges: [(rank, c0, c1)] excluding self."""
+    plan = []
+    for s in slabs:
+        if s.rank == slab.rank or s.rows == 0:
+            continue
+        c0, c1 = max(column_min, s.row_begin), min(column_max + 1, s.row_end)
+        if c0 < c1:
+            plan.append((s.rank, c0, c1))
+    return plan
+
+
+class IteratedSpmv:
+    """The distributed iteration loop, independent of where the SpMV runs.
+
+    ``slab_spmv(x_full, y_slab, x_next_slab)`` computes the rank's rows of
+    y = A x and x_next = y * scale; ``all_gather(out_full, in_slab)`` is a
+    torch.distributed all_gather_into_tensor.  Buffers are torch tensors
+    (CUDA under NCCL, CPU under gloo in the tests)."""
+
+    def __init__(self, slab: Slab, num_cols: int, world: int, slab_spmv: Callable,
+                 all_gather: Callable, like):
+        import torch
+        self.slab, self.world = slab, world
+        S = slab.pad_rows
+        self.x = torch.zeros(S * world, dtype=like.dtype, device=like.device)
+        self.x_next = torch.zeros(S, dtype=like.dtype, device=like.device)
+        self.y = torch.zeros(S, dtype=like.dtype, device=like.device)
+        self.num_cols = num_cols
+        self.slab_spmv = slab_spmv
+        self.all_gather = all_gather
+
+    def set_x(self, x_full):
+        self.x[: x_full.numel()].copy_(x_full)
+
+    def step(self):
+        """y_k = A x_k on this slab; x_{k+1} gathered from all slabs."""
+        xv = self.x[: self.num_cols]
+        self.slab_spmv(xv, self.y[: self.slab.rows], self.x_next[: self.slab.rows])
+        self.all_gather(self.x, self.x_next)
+
+
+# ---------------------------------------------------------------- bench (N > 1)
+def bench_distributed(args, metric: str, workloads: dict):
+    """bench.py leg for torchrun N > 1: strong scaling of the iterated SpMV."""
+    import torch
+    import torch.distributed as dist
+
+    from . import generators as gen
+    from . import spmvkit as sk
+    from ._lib import lib
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    assert lib().spmvk_init(local) == 0, sk._lib.last_error()
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G = 32
+    kind, a_, b_, desc = workloads[args.workload]
+    csr = sk.CsrMatrix.stencil(a_, b_) if kind == "stencil" else sk.build_csr(gen.powerlaw(b_, 7))
+    slabs = slab_bounds(csr.num_rows, G, world)
+    me = slabs[rank]
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    a = sk.build_rgcsr(csr, G, 8, stream=sp, row_range=(me.row_begin, me.row_end))
+    nnz_local = a.nnz()
+    del csr
+    L = lib()
+    x0 = torch.from_numpy(gen.random_vector(a.num_cols, 1)).cuda()
+
+    def slab_spmv(x, y, xn):
+        rc = L.spmvk_rgcsr_spmv_scaled_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(),
+                                           y.numel(), xn.data_ptr(), 0.0625, sp)
+        assert rc == 0, sk._lib.last_error()
+
+    def all_gather(out, inp):
+        with torch.cuda.stream(stream):
+            dist.all_gather_into_tensor(out, inp)
+
+    it = IteratedSpmv(me, a.num_cols, world, slab_spmv, all_gather, x0)
+    it.set_x(x0)
+    for _ in range(args.warmup):
+        it.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        it.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    tot_nnz = torch.tensor([nnz_local], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tot_nnz)
+    dist.barrier()
+    if rank == 0:
+        step_ms = ms.item() / args.steps
+        value = 2.0 * tot_nnz.item() / (step_ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": metric, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "description": desc, "format": "rgcsr",
+                       "group_size": G, "parallelism": f"row-slab x{world}, NCCL all-gather of x",
+                       "step": "slab SpMV (+fused x_next = y/16) + all_gather_into_tensor"},
+            "gpu_launches": args.steps,
+        }), flush=True)
+    dist.destroy_process_group()

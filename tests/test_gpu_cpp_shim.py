@@ -1,0 +1,21 @@
+"""The C++ drop-in (include/spmvkit_gpu.hpp) driven with the reference's own
+TripletMatrix and generators, bitwise against the reference templates
+(oracle/parity_driver.cpp, built into oracle/_ref when /root/reference was
+present at build time)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DRIVER = os.path.join(ROOT, "oracle", "_ref", "parity_driver")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.skipif(not os.path.exists(DRIVER), reason="oracle/_ref/parity_driver not built")
+def test_reference_inputs_through_cpp_shim(cuda):
+    r = subprocess.run([DRIVER], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 5

@@ -17,8 +17,20 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
+VARIANTS = ["tma", "ldg", "ldg_pf", "ldg8_pf"]
+
+
 def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.fixture(params=VARIANTS)
+def k2(request, cuda):
+    """Runs the test once per K2 kernel variant (all must be bitwise equal)."""
+    from paper_1012_2270_b200._lib import lib
+    assert lib().spmvk_set_rgcsr_kernel(request.param.encode()) == 0
+    yield request.param
+    lib().spmvk_set_rgcsr_kernel(b"tma")
 
 
 def test_example8_golden_arrays(cuda, golden):
@@ -64,7 +76,7 @@ def test_errors_match_reference(cuda, golden):
 
 
 @pytest.mark.parametrize("kind", ["i", "r"])
-def test_small_golden_seeds(cuda, golden, kind):
+def test_small_golden_seeds(cuda, golden, kind, k2):
     """random_small seeds 600-649, G = 1 + seed % 9 (test_formats.cpp:325-342)."""
     g = golden["small"]
     for seed in range(600, 650):
@@ -83,7 +95,7 @@ def test_small_golden_seeds(cuda, golden, kind):
             assert bitwise(g[f"{t}_rg_y"], g[f"{t}_ref_y"])
 
 
-def test_acceptance_200_seeds(cuda, golden):
+def test_acceptance_200_seeds(cuda, golden, k2):
     """tests/acceptance.cpp:138-173: 200 random_case matrices, G = 1 + seed % 9."""
     g = golden["acceptance"]
     for seed in range(200):
@@ -113,7 +125,7 @@ def test_padding_monotone_and_single_group_is_ell(cuda):
 
 
 @pytest.mark.parametrize("shape", ["empty_rows", "no_entries", "single_row", "identity", "dense_row"])
-def test_edge_shapes(cuda, shape):
+def test_edge_shapes(cuda, shape, k2):
     if shape == "empty_rows":
         om = orc.Csr(5, 4, [0, 0, 2, 2, 2, 3], [1, 3, 0], [2.0, -1.0, 5.0])
     elif shape == "no_entries":
@@ -137,7 +149,7 @@ def test_edge_shapes(cuda, shape):
 
 @pytest.mark.parametrize("G", [32, 64, 128, 256])
 @pytest.mark.parametrize("prec", [8, 4])
-def test_config1_5pt_1024_bitwise(cuda, G, prec):
+def test_config1_5pt_1024_bitwise(cuda, G, prec, k2):
     """Config 1 (2D 5-point 1024^2) at full size: arrays and y vs the oracle."""
     om = orc.stencil(5, 1024)
     a = sk.build_rgcsr(sk.CsrMatrix.stencil(5, 1024), G, prec)
@@ -149,7 +161,7 @@ def test_config1_5pt_1024_bitwise(cuda, G, prec):
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_config2_27pt_128_bitwise(cuda, prec):
+def test_config2_27pt_128_bitwise(cuda, prec, k2):
     """Config 2 (3D 27-point 128^3, 55.7 M nnz) at full size, G = 32."""
     om = orc.stencil(27, 128)
     csr = sk.CsrMatrix.stencil(27, 128)
@@ -166,7 +178,7 @@ def test_config2_27pt_128_bitwise(cuda, prec):
         assert float(np.cumsum(y)[-1]) == 1674.3573800651031
 
 
-def test_row_slabs_equal_global_slices(cuda):
+def test_row_slabs_equal_global_slices(cuda, k2):
     """Group-aligned slabs are exactly the global arrays' slices."""
     om = orc.stencil(27, 24)
     csr = sk.CsrMatrix.stencil(27, 24)
@@ -190,7 +202,7 @@ def test_row_slabs_equal_global_slices(cuda):
             assert bitwise(sk.spmv_rgcsr(s, x), y_full[r0:r1])
 
 
-def test_scaled_iteration_fused(cuda):
+def test_scaled_iteration_fused(cuda, k2):
     from paper_1012_2270_b200._lib import lib
     om = orc.stencil(7, 20)
     a = sk.build_rgcsr(sk.CsrMatrix.stencil(7, 20), 32)

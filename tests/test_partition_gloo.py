@@ -1,0 +1,121 @@
+"""Multi-process (gloo, world_size 2 and 3) checks of the row-slab partitioner
+and the iterated distributed SpMV loop (paper_1012_2270_b200.partition).
+The per-slab SpMV is the oracle here (CPU); on the GPU it is K2 fused with the
+x_{k+1} scale.  The distributed iterate must be bitwise the 1-process one."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as orc
+from paper_1012_2270_b200 import partition as part
+
+
+def slab_csr(m: orc.Csr, r0, r1) -> orc.Csr:
+    b, e = int(m.rp[r0]), int(m.rp[r1])
+    return orc.Csr(r1 - r0, m.cols, m.rp[r0:r1 + 1] - m.rp[r0], m.col[b:e], m.val[b:e])
+
+
+def test_slab_bounds_cover_and_align():
+    for n in (1, 31, 32, 33, 1000, 2097152):
+        for G in (1, 32, 128):
+            for P in (1, 2, 3, 4, 8):
+                sl = part.slab_bounds(n, G, P)
+                assert sl[0].row_begin == 0 and sl[-1].row_end == n
+                for a, b in zip(sl, sl[1:]):
+                    assert a.row_end == b.row_begin
+                for s in sl:
+                    assert s.row_begin % G == 0 or s.row_begin == n
+                    assert s.rows <= s.pad_rows
+
+
+def test_weighted_bounds_balance_slots():
+    m = orc.powerlaw(50_000, 7)
+    cuts = part.weighted_slab_bounds(m.lens(), 32, 4)
+    assert cuts[0][0] == 0 and cuts[-1][1] == m.rows
+    slots = []
+    for r0, r1 in cuts:
+        assert r0 % 32 == 0
+        slots.append(orc.build_rgcsr(slab_csr(m, r0, r1), 32)["values"].size)
+    assert max(slots) < 1.5 * (sum(slots) / len(slots))
+
+
+def test_slab_rgcsr_is_global_slice():
+    m = orc.stencil(27, 10)
+    G = 32
+    full = orc.build_rgcsr(m, G)
+    gp = full["group_pointers"]
+    for s in part.slab_bounds(m.rows, G, 3):
+        a = orc.build_rgcsr(slab_csr(m, s.row_begin, s.row_end), G)
+        g0, g1 = s.row_begin // G, (s.row_end + G - 1) // G
+        assert np.array_equal(a["group_pointers"], gp[g0:g1 + 1] - gp[g0])
+        assert np.array_equal(a["values"], full["values"][gp[g0]:gp[g1]])
+
+
+def test_halo_plan_of_7pt_slabs():
+    n = 16
+    rows = n ** 3
+    sl = part.slab_bounds(rows, 32, 4)
+    s = sl[1]
+    plan = part.halo_plan(s, s.row_begin - n * n, s.row_end - 1 + n * n, sl)
+    assert [p[0] for p in plan] == [0, 2]
+    assert sum(c1 - c0 for _, c0, c1 in plan) == 2 * n * n
+
+
+def _worker(rank, world, port, steps, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = orc.stencil(7, 12)
+    G = 32
+    slabs = part.slab_bounds(m.rows, G, world)
+    me = slabs[rank]
+    a = orc.build_rgcsr(slab_csr(m, me.row_begin, me.row_end), G)
+
+    def slab_spmv(x, y, xn):
+        yy = orc.spmv_rgcsr(a, x.numpy())[0]
+        y.copy_(torch.from_numpy(yy))
+        xn.copy_(torch.from_numpy(yy * 0.0625))
+
+    def all_gather(o, i):
+        dist.all_gather_into_tensor(o, i)
+
+    x0 = torch.from_numpy(orc.random_vector(m.cols, 1))
+    it = part.IteratedSpmv(me, m.cols, world, slab_spmv, all_gather, x0)
+    it.set_x(x0)
+    for _ in range(steps):
+        it.step()
+    if rank == 0:
+        out.put(it.x[: m.cols].numpy().tobytes())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_iterated_distributed_equals_single_process(world):
+    steps = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = np.frombuffer(q.get(timeout=120), np.float64)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    m = orc.stencil(7, 12)
+    full = orc.build_rgcsr(m, 32)
+    x = orc.random_vector(m.cols, 1)
+    for _ in range(steps):
+        x = orc.spmv_rgcsr(full, x)[0] * 0.0625
+    assert got.tobytes() == x.tobytes()
