@@ -171,22 +171,26 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
     fail(SPMVK_EINVAL, "spmv_rgcsr: handle precision differs from the entry point");
 }
 
-// K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL =
-// tma | ldg | ldg_pf | ldg8_pf; default tma (used when the group size allows).
-enum class K2 { kTma, kLdg, kLdgPf, kLdg8Pf };
+// K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
+// All variants give bitwise identical y; they differ in how slots are staged.
+enum class K2 { kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
 
 bool parse_k2(const std::string& v, K2* out) {
-  if (v == "tma") *out = K2::kTma;
-  else if (v == "ldg") *out = K2::kLdg;
-  else if (v == "ldg_pf") *out = K2::kLdgPf;
-  else if (v == "ldg8_pf") *out = K2::kLdg8Pf;
-  else return false;
-  return true;
+  static const std::pair<const char*, K2> names[] = {
+      {"pipe", K2::kPipe},   {"pipe_hi", K2::kPipeHi}, {"pipe8", K2::kPipe8},
+      {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
+      {"ldg8_pf", K2::kLdg8Pf}};
+  for (const auto& [n, k] : names)
+    if (v == n) {
+      *out = k;
+      return true;
+    }
+  return false;
 }
 
 std::atomic<int>& k2_slot() {
   static std::atomic<int> k{[] {
-    K2 v = K2::kTma;
+    K2 v = K2::kPipe;
     const char* e = std::getenv("SPMVK_RGCSR_KERNEL");
     if (e) parse_k2(e, &v);
     return static_cast<int>(v);
@@ -228,18 +232,26 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
     return;
   }
-  const unsigned grid = persistent_grid((h->rows + 255) / 256, 8);
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
   constexpr int U = sizeof(T) == 8 ? 4 : 8;
-  auto args = [&](auto kern) {
+  // persistent grid: exactly the resident CTAs of this variant (occupancy API)
+  auto run = [&](auto kern) {
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
     kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale);
   };
-  if (k == K2::kLdgPf) args(rgcsr_spmv_ldg<T, kScaled, U, true>);
-  else if (k == K2::kLdg8Pf) args(rgcsr_spmv_ldg<T, kScaled, 8, true>);
-  else args(rgcsr_spmv_ldg<T, kScaled, U, false>);
+  switch (k) {
+    case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
+    case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
+    case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;
+    case K2::kLdg8Pf: run(rgcsr_spmv_ldg<T, kScaled, 8, true>); break;
+    case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
+    default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
+  }
   SPMVK_LAUNCH("rgcsr_spmv_ldg");
 }
 
@@ -360,7 +372,7 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (tma | ldg | ldg_pf | ldg8_pf)");
+                             "' (pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | ldg8_pf)");
     k2_slot().store(static_cast<int>(k));
   });
 }

@@ -21,6 +21,84 @@
 
 namespace spmvk {
 
+// Row- and batch-pipelined thread-per-row kernel (the default for short and
+// medium rows).  Three latencies sit on a row's critical path — (row length,
+// group pointer) -> (slot columns, values) -> x gathers — so both levels are
+// software-pipelined: the next row's length / group pointer are loaded while
+// the current row runs, and batch b+1's slots are loaded (predicated on the
+// row length, so short rows and tails cost no extra round trip) before batch
+// b's x gathers.  Accumulation stays strictly in slot order.
+template <class T, bool kScaled, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale) {
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t len_n = 0, base_n = 0;
+  if (r < rows) {
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    len_n = lens[r];
+    base_n = gp[g];
+  }
+  while (r < rows) {
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t t = r - g * G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = len_n;
+    const T* __restrict__ vp = values + base_n + t;
+    const uint32_t* __restrict__ cp = columns + base_n + t;
+    const uint32_t rn = r + stride;
+    if (rn < rows) {
+      const uint32_t gn = g_shift >= 0 ? (rn >> g_shift) : rn / G;
+      len_n = lens[rn];
+      base_n = gp[gn];
+    }
+    uint32_t cA[U];
+    T vA[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cA[u] = 0;
+      vA[u] = T(0);
+      if ((uint32_t)u < len) {
+        cA[u] = ld_stream(cp + (size_t)u * s, pf);
+        vA[u] = ld_stream(vp + (size_t)u * s, pf);
+      }
+    }
+    T acc = T(0);
+    for (uint32_t j = 0; j < len; j += U) {
+      const uint32_t jn = j + U;
+      uint32_t cB[U];
+      T vB[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cB[u] = 0;
+        vB[u] = T(0);
+        if (jn + u < len) {
+          cB[u] = ld_stream(cp + (size_t)(jn + u) * s, pf);
+          vB[u] = ld_stream(vp + (size_t)(jn + u) * s, pf);
+        }
+      }
+      T xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j + u < len ? ld_x(x + cA[u], pl) : T(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u < len) acc = add_rn(acc, mul_rn(vA[u], xv[u]));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cA[u] = cB[u];
+        vA[u] = vB[u];
+      }
+    }
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+    r = rn;
+  }
+}
+
 template <class T, bool kScaled, int U, bool kPrefetch>
 __global__ void __launch_bounds__(256) rgcsr_spmv_ldg(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
