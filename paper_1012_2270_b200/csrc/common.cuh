@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <mutex>
 
 #include "../../include/spmvk.h"
 
@@ -184,6 +185,11 @@ struct spmvk_rgcsr {
   int prec = SPMVK_F64;
   spmvk::DevBuf<unsigned char> values;  // slots * prec bytes
   spmvk::DevBuf<uint32_t> columns, group_pointers, row_lengths;
+  // K2 launch metadata (not part of the reference arrays): the slot-balanced
+  // wave split of rgcsr_spmv_wtma for the grid it was computed for.
+  mutable std::mutex part_mu;
+  mutable spmvk::DevBuf<uint32_t> part;
+  mutable uint32_t part_W = 0;
 };
 
 struct spmvk_hybrid {

@@ -173,11 +173,12 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
-enum class K2 { kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
+enum class K2 { kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {
-      {"pipe", K2::kPipe},   {"pipe_hi", K2::kPipeHi}, {"pipe8", K2::kPipe8},
+      {"wtma", K2::kWtma},   {"wtma16", K2::kWtma16}, {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
+      {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
       {"ldg8_pf", K2::kLdg8Pf}};
   for (const auto& [n, k] : names)
@@ -190,7 +191,7 @@ bool parse_k2(const std::string& v, K2* out) {
 
 std::atomic<int>& k2_slot() {
   static std::atomic<int> k{[] {
-    K2 v = K2::kPipe;
+    K2 v = K2::kWtma;
     const char* e = std::getenv("SPMVK_RGCSR_KERNEL");
     if (e) parse_k2(e, &v);
     return static_cast<int>(v);
@@ -221,10 +222,64 @@ void launch_tma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cuda
   SPMVK_LAUNCH("rgcsr_spmv_tma");
 }
 
+// Per-warp bulk-copy streams (rgcsr_spmv_wtma), one CTA per SM.  Two shapes:
+//   wtma   : 8 warps x 4-stage ring of 512 (fp64) / 3 x 1024 (fp32) elements
+//   wtma16 : 16 warps x 3-stage ring of 256 (fp64) / 3 x 512 (fp32) elements
+// both ~192 KB of shared memory per SM in flight; x gathers in batches of 8.
+template <class T, bool kScaled, int R, int NW, int NS, int CE>
+void launch_wtma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
+  constexpr size_t smem = wtma_smem_bytes<T, NS, CE, NW>();
+  auto kern = rgcsr_spmv_wtma<T, kScaled, R, NS, CE, NW, 8>;
+  static std::once_flag once;  // per instantiation
+  std::call_once(once, [&] {
+    SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  const uint32_t G = static_cast<uint32_t>(h->group_size);
+  const uint32_t gpw = G >= 32 ? 1 : 32 / G;
+  const uint32_t nwaves = static_cast<uint32_t>((h->groups + gpw - 1) / gpw);
+  const unsigned grid = static_cast<unsigned>(sm_count());
+  const uint32_t W = grid * NW;
+  {
+    std::lock_guard<std::mutex> lk(h->part_mu);
+    if (h->part_W != W) {
+      h->part.alloc(W + 1);
+      wave_partition<<<(W + 256) / 256, 256, 0, s>>>(W, nwaves, gpw,
+                                                     static_cast<uint32_t>(h->groups),
+                                                     h->group_pointers.p, h->part.p);
+      SPMVK_LAUNCH("wave_partition");
+      h->part_W = W;
+    }
+  }
+  kern<<<grid, NW * 32, smem, s>>>(static_cast<uint32_t>(h->rows), G,
+                                   static_cast<uint32_t>(h->groups), gpw, nwaves, h->part.p,
+                                   h->group_pointers.p, h->row_lengths.p,
+                                   reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y,
+                                   x_next, scale);
+  SPMVK_LAUNCH("rgcsr_spmv_wtma");
+}
+
+template <class T, bool kScaled, int NW, int NS, int CE>
+void launch_wtma_g(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
+  const uint64_t G = h->group_size;
+  if (G <= 32) launch_wtma<T, kScaled, 1, NW, NS, CE>(h, x, y, x_next, scale, s);
+  else if (G <= 64) launch_wtma<T, kScaled, 2, NW, NS, CE>(h, x, y, x_next, scale, s);
+  else if (G <= 128) launch_wtma<T, kScaled, 4, NW, NS, CE>(h, x, y, x_next, scale, s);
+  else launch_wtma<T, kScaled, 8, NW, NS, CE>(h, x, y, x_next, scale, s);
+}
+
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
   const K2 k = k2_choice();
+  constexpr bool f64 = sizeof(T) == 8;
+  if (k == K2::kWtma && h->group_size <= 256) {
+    launch_wtma_g<T, kScaled, 8, f64 ? 4 : 3, f64 ? 512 : 1024>(h, x, y, x_next, scale, s);
+    return;
+  }
+  if (k == K2::kWtma16 && h->group_size <= 256) {
+    launch_wtma_g<T, kScaled, 16, 3, f64 ? 256 : 512>(h, x, y, x_next, scale, s);
+    return;
+  }
   if (k == K2::kTma && h->group_size <= 256) {
     if constexpr (sizeof(T) == 8)
       launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
@@ -372,7 +427,7 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | ldg8_pf)");
+                             "' (wtma | wtma16 | pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | ldg8_pf)");
     k2_slot().store(static_cast<int>(k));
   });
 }

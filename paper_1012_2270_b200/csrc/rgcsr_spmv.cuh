@@ -165,6 +165,210 @@ __global__ void __launch_bounds__(256) rgcsr_spmv_ldg(
   }
 }
 
+// ---------------------------------------------------------------------------
+// rgcsr_spmv_wtma — per-warp bulk-copy streams (the B200-native default).
+//
+// Every warp owns a contiguous range of "waves" (a wave is the rows one warp
+// covers at once: one group when G >= 32, lane l then holding rows
+// t = l + 32 i, i < R; floor(32/G) groups when G < 32), balanced across warps
+// by slot count with a binary search over the group pointers.  Because the
+// groups of a range are contiguous in memory, the warp's slots form ONE
+// contiguous element range [gp[first], gp[last]); lane 0 streams it through a
+// private NS-stage shared-memory ring of CE-element chunks with 1D bulk async
+// copies (cp.async.bulk -> UBLKCP, mbarrier complete_tx), refilling a stage
+// as soon as the warp has consumed it.  No CTA-wide barrier exists: each warp
+// is its own producer/consumer, so bytes in flight (NS * CE * (S + 4) per
+// warp) no longer depend on registers, row length or the add chains.  Lanes
+// read their slots from shared memory at stride s (conflict-free), gather x
+// through the read-only path in batches, and add in slot order (bitwise the
+// reference).  The next wave's row lengths / group pointers are prefetched.
+template <class T, int NS, int CE, int NW>
+constexpr size_t wtma_smem_bytes() {
+  return (size_t)NW * NS * CE * (sizeof(T) + sizeof(uint32_t)) + (size_t)NW * NS * 8;
+}
+
+// part[i] = first wave of warp i (part[W] = nwaves): slot-balanced split, the
+// smallest wave whose first slot is >= total * i / W.  Computed once per
+// (handle, grid) and cached.
+__global__ void wave_partition(uint32_t W, uint32_t nwaves, uint32_t gpw, uint32_t groups,
+                               const uint32_t* __restrict__ gp, uint32_t* __restrict__ part) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > W) return;
+  const uint64_t total = gp[groups];
+  if (i == 0 || i == W || total == 0) {
+    part[i] = (i == 0) ? 0 : nwaves;
+    return;
+  }
+  const uint64_t slot = total * i / W;
+  uint32_t lo = 0, hi = nwaves;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (gp[min((uint64_t)mid * gpw, (uint64_t)groups)] < slot) lo = mid + 1; else hi = mid;
+  }
+  part[i] = lo;
+}
+
+template <class T, bool kScaled, int R, int NS, int CE, int NW, int U>
+__global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
+    uint32_t rows, uint32_t G, uint32_t groups, uint32_t gpw, uint32_t nwaves,
+    const uint32_t* __restrict__ part,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  static_assert(CE % 4 == 0, "chunks must keep 16-byte alignment");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* vbuf = reinterpret_cast<T*>(smem) + (size_t)warp * NS * CE;
+  uint32_t* cbuf = reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(smem) + (size_t)NW * NS * CE) +
+                   (size_t)warp * NS * CE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint32_t*>(
+                       reinterpret_cast<T*>(smem) + (size_t)NW * NS * CE) + (size_t)NW * NS * CE) +
+                   warp * NS;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+
+  // ---- this warp's wave range (slot-balanced, precomputed by wave_partition)
+  const uint32_t wg = blockIdx.x * NW + warp;
+  auto wave_start = [&](uint32_t w) -> uint64_t {
+    return gp[min((uint64_t)w * gpw, (uint64_t)groups)];
+  };
+  const uint32_t w0 = part[wg], w1 = part[wg + 1];
+  if (w0 >= w1) return;
+
+  const uint64_t s0 = wave_start(w0) & ~3ull;
+  const uint64_t s1 = (wave_start(w1) + 3) & ~3ull;
+  const uint32_t nchunks = (uint32_t)((s1 - s0 + CE - 1) / CE);
+
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](uint32_t k) {
+    const uint32_t stage = k % NS;
+    const uint64_t c = s0 + (uint64_t)k * CE;
+    const uint32_t n = (uint32_t)min((uint64_t)CE, s1 - c);
+    mbar_arrive_expect_tx(&full[stage], n * (uint32_t)(sizeof(T) + sizeof(uint32_t)));
+    bulk_g2s(vbuf + stage * CE, values + c, n * (uint32_t)sizeof(T), &full[stage], pf);
+    bulk_g2s(cbuf + stage * CE, columns + c, n * 4u, &full[stage], pf);
+  };
+  if (lane == 0)
+    for (uint32_t k = 0; k < nchunks && k < (uint32_t)NS; ++k) issue(k);
+
+  // ---- per-lane row state of the current wave
+  const uint32_t wave_rows = G >= 32 ? G : gpw * G;
+  uint32_t row[R], rem[R], s[R];
+  uint64_t off[R];
+  T acc[R];
+  uint32_t nlen[R], nbase[R];  // prefetched metadata of the next wave
+  auto row_of = [&](uint32_t w, int i) -> uint32_t {
+    const uint32_t lr = lane + 32u * i;
+    return lr < wave_rows ? w * wave_rows + lr : 0xffffffffu;
+  };
+  auto group_of = [&](uint32_t r) -> uint32_t { return r / G; };
+  auto fetch_meta = [&](uint32_t w) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint32_t r = row_of(w, i);
+      nlen[i] = 0;
+      nbase[i] = 0;
+      if (w < w1 && r < rows) {
+        nlen[i] = lens[r];
+        nbase[i] = gp[group_of(r)];
+      }
+    }
+  };
+  uint32_t w = w0;
+  auto start_wave = [&]() {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      row[i] = row_of(w, i);
+      const bool live = row[i] < rows;
+      const uint32_t g = live ? group_of(row[i]) : 0;
+      s[i] = live ? min(G, rows - g * G) : 1;
+      rem[i] = nlen[i];
+      off[i] = (uint64_t)nbase[i] + (live ? row[i] - g * G : 0);
+      acc[i] = T(0);
+    }
+    fetch_meta(w + 1);
+  };
+  auto finish_wave = [&]() {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (row[i] < rows) {
+        y[row[i]] = acc[i];
+        if (kScaled) x_next[row[i]] = mul_rn(acc[i], scale);
+      }
+    ++w;
+  };
+  fetch_meta(w0);
+  start_wave();
+  uint64_t wave_end = wave_start(w + 1);
+
+  for (uint32_t k = 0; k < nchunks; ++k) {
+    const uint32_t stage = k % NS;
+    mbar_wait(&full[stage], (k / NS) & 1);
+    const uint64_t cbeg = s0 + (uint64_t)k * CE, cend = min(cbeg + CE, s1);
+    const T* vb = vbuf + stage * CE;
+    const uint32_t* cb = cbuf + stage * CE;
+    for (;;) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        uint32_t nb = 0;
+        if (rem[i] && off[i] < cend)
+          nb = min(rem[i], (uint32_t)((cend - off[i] + s[i] - 1) / s[i]));
+        uint32_t idx = (uint32_t)(off[i] - cbeg);
+        const uint32_t si = s[i];
+        uint32_t q = 0;
+        for (; q + U <= nb; q += U) {
+          uint32_t cc[U];
+          T vv[U], xv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            cc[u] = cb[idx + u * si];
+            vv[u] = vb[idx + u * si];
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cc[u], pl);
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[i] = add_rn(acc[i], mul_rn(vv[u], xv[u]));
+          idx += U * si;
+        }
+        if (q < nb) {  // tail: gather all remaining x first, then add in order
+          uint32_t cc[U];
+          T vv[U], xv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool ok = q + u < nb;
+            cc[u] = ok ? cb[idx + u * si] : 0;
+            vv[u] = ok ? vb[idx + u * si] : T(0);
+            xv[u] = ok ? ld_x(x + cc[u], pl) : T(0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (q + u < nb) acc[i] = add_rn(acc[i], mul_rn(vv[u], xv[u]));
+        }
+        rem[i] -= nb;
+        off[i] += (uint64_t)nb * si;
+      }
+      if (w >= w1 || wave_end > cend) break;
+      finish_wave();  // every slot of this wave lies in chunks <= k
+      if (w >= w1) break;
+      start_wave();
+      wave_end = wave_start(w + 1);
+    }
+    __syncwarp();
+    if (lane == 0 && k + NS < nchunks) {
+      // consumed stage -> async-proxy overwrite: order the generic reads first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + NS);
+    }
+  }
+  while (w < w1) {  // waves whose slots all precede the last chunk end (or are empty)
+    finish_wave();
+    if (w < w1) start_wave();
+  }
+}
+
 // Shared-memory footprint of rgcsr_spmv_tma<T, NW, NS, CE>.
 template <class T, int NS, int CE>
 constexpr size_t tma_smem_bytes() {

@@ -17,7 +17,7 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = ["pipe", "pipe_hi", "pipe8", "tma", "ldg", "ldg_pf", "ldg8_pf"]
+VARIANTS = ["wtma", "wtma16", "pipe", "pipe_hi", "pipe8", "tma", "ldg", "ldg_pf", "ldg8_pf"]
 
 
 def dev(x):
@@ -30,7 +30,7 @@ def k2(request, cuda):
     from paper_1012_2270_b200._lib import lib
     assert lib().spmvk_set_rgcsr_kernel(request.param.encode()) == 0
     yield request.param
-    lib().spmvk_set_rgcsr_kernel(b"pipe")
+    lib().spmvk_set_rgcsr_kernel(b"wtma")
 
 
 def test_example8_golden_arrays(cuda, golden):
