@@ -139,10 +139,13 @@ int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx
 int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
                               uint64_t ny, uint64_t* multiply_add_count);
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
-/* Tuning knob (process-wide): which K2 kernel runs — "tma" (default:
- * bulk-async-copy shared-memory pipeline, group size <= 256), "ldg" (direct
- * streamed loads), "ldg_pf" / "ldg8_pf" (software-pipelined loads).  All
- * variants give bitwise identical y.  Also read from SPMVK_RGCSR_KERNEL. */
+/* Tuning knob (process-wide): which K2 kernel runs — "auto" (default: picked
+ * from the precision and mean row length), "ldg_pf" / "ldg8_pf" / "ldg"
+ * (thread per row, software-pipelined streamed loads), "pipe" / "pipe_hi" /
+ * "pipe8" (thread per row with row-metadata prefetch and predicated batches),
+ * "tma" (CTA-wide bulk-async-copy shared-memory ring), "wtma" / "wtma16"
+ * (per-warp bulk-async-copy streams).  All variants give bitwise identical
+ * y.  Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
 
 /* ------------------------------------------------------------------ Hybrid */
@@ -151,8 +154,9 @@ typedef struct {
   uint64_t ell_width;        /* K1 = EllpackMatrix::slots_per_row */
   uint64_t ell_slots;        /* num_rows * K1 */
   uint64_t coo_nnz;
-  uint64_t nnz;
-  uint64_t artificial_zeros; /* FillReport (fill.hpp:67-72) */
+  uint64_t nnz;              /* stored entries of the source matrix (multiply-adds) */
+  uint64_t fill_nnz;         /* FillReport::nnz: ell_nnz recount + coo (fill.hpp:67-72) */
+  uint64_t artificial_zeros; /* FillReport: slots - fill_nnz */
   uint64_t bytes_single, bytes_double;
   int precision;
 } spmvk_hybrid_info;

@@ -95,6 +95,10 @@ def small():
             h = r.hybrid()
             hy_arrays(f"{tag}_hy", h, d)
             d[f"{tag}_hy_y"] = r.hybrid_spmv(h, x)
+            d[f"{tag}_hy_fill"] = np.array([h["artificial_zeros"], h["bytes_single"],
+                                            h["bytes_double"]], np.uint64)
+            d[f"{tag}_rg_fill"] = np.array([a["artificial_zeros"], a["bytes_single"],
+                                            a["bytes_double"], a["nnz"]], np.uint64)
             d[f"{tag}_csr_y"] = r.csr_spmv(x)
             d[f"{tag}_ref_y"] = r.spmv_reference(x)
     np.savez_compressed(os.path.join(OUT, "small.npz"), **d)

@@ -32,7 +32,7 @@ class RgcsrInfo(C.Structure):
 
 class HybridInfo(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
-        "num_rows", "num_cols", "ell_width", "ell_slots", "coo_nnz", "nnz",
+        "num_rows", "num_cols", "ell_width", "ell_slots", "coo_nnz", "nnz", "fill_nnz",
         "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int)]
 
 

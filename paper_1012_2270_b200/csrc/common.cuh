@@ -194,6 +194,7 @@ struct spmvk_rgcsr {
 
 struct spmvk_hybrid {
   uint64_t rows = 0, cols = 0, k1 = 0, coo = 0, nnz = 0;
+  uint64_t fill_nnz = 0;  // FillReport nnz: ell_nnz recount + coo (fill.hpp:67-72)
   int prec = SPMVK_F64;
   spmvk::DevBuf<unsigned char> ell_values, coo_values;
   spmvk::DevBuf<uint32_t> ell_columns, coo_rows, coo_columns;

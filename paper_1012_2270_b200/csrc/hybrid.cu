@@ -156,6 +156,34 @@ __global__ void coo_tile_bounds(uint64_t ntiles, uint64_t rows, uint64_t n,
   }
 }
 
+// FillReport's ELL nnz (fill.hpp:61-65 -> ell_nnz, ellpack.hpp:55-78): the
+// reference recounts real slots from the layout — the first non-increasing
+// column starts the pad region, and a lone stored zero at column 0 counts as
+// empty — so a stored zero can change fill_report.  Same recount, thread per row.
+template <class T>
+__global__ void ell_nnz_recount(uint64_t rows, uint32_t k1, const T* __restrict__ ev,
+                                const uint32_t* __restrict__ ec, unsigned long long* out) {
+  unsigned long long total = 0;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t len = 0, prev = 0;
+    for (uint32_t slot = 0; slot < k1; ++slot) {
+      const uint64_t idx = (uint64_t)slot * rows + r;
+      const uint32_t c = ec[idx];
+      if (slot > 0 && c <= prev) break;
+      if (slot == 0 && c == 0 && ev[idx] == T(0)) {
+        const bool real_successor = k1 > 1 && ec[rows + r] > 0;
+        if (!real_successor) break;
+      }
+      ++len;
+      prev = c;
+    }
+    total += len;
+  }
+  for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
+}
+
 // ------------------------------------------------------------ K4/K5: SpMV
 // One CTA-tile of 256 rows: (1) thread per row walks its K1 ELL slots (pads
 // included, as spmv_ellpack does); (2) the tile's COO range is staged in
@@ -250,7 +278,18 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
         ntiles, a->rows, coo, h->coo_rows.p, h->tile_ptr.p);
     SPMVK_LAUNCH("coo_tile_bounds");
   }
+  DevBuf<unsigned long long> cnt(1);
+  SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+  if (h->k1 && a->rows) {
+    ell_nnz_recount<T><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
+                                            reinterpret_cast<const T*>(h->ell_values.p),
+                                            h->ell_columns.p, cnt.p);
+    SPMVK_LAUNCH("ell_nnz_recount");
+  }
+  unsigned long long ell_nnz = 0;
+  SPMVK_CUDA(cudaMemcpyAsync(&ell_nnz, cnt.p, sizeof(ell_nnz), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
+  h->fill_nnz = ell_nnz + coo;
 }
 
 spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
@@ -361,8 +400,9 @@ int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info) {
     info->ell_slots = h->rows * h->k1;
     info->coo_nnz = h->coo;
     info->nnz = h->nnz;
+    info->fill_nnz = h->fill_nnz;
     const uint64_t slots = info->ell_slots + h->coo;
-    info->artificial_zeros = slots - h->nnz;
+    info->artificial_zeros = slots - h->fill_nnz;
     // fill.hpp:67-72: index words = ell slots + 2 * coo
     const uint64_t words = info->ell_slots + 2 * h->coo;
     info->bytes_single = slots * 4 + words * 4;

@@ -173,11 +173,23 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
-enum class K2 { kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
+enum class K2 { kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
+
+// "auto" (default): the variant that measured fastest for the row-length
+// regime on B200 (profiles/r01_k2_sweep.md): long rows (mean > 12 slots)
+// stream best with the software-pipelined 4/8-deep loads at full occupancy
+// (ldg_pf); short rows need the row-level metadata prefetch with more warps
+// per SM (pipe_hi for fp64, pipe for fp32).
+K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
+  const double mean = h->rows ? double(h->nnz) / double(h->rows) : 0.0;
+  if (mean > 12.0) return K2::kLdgPf;
+  return f64 ? K2::kPipeHi : K2::kPipe;
+}
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {
-      {"wtma", K2::kWtma},   {"wtma16", K2::kWtma16}, {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
+      {"auto", K2::kAuto},   {"wtma", K2::kWtma},   {"wtma16", K2::kWtma16},
+      {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
       {"ldg8_pf", K2::kLdg8Pf}};
@@ -191,7 +203,7 @@ bool parse_k2(const std::string& v, K2* out) {
 
 std::atomic<int>& k2_slot() {
   static std::atomic<int> k{[] {
-    K2 v = K2::kWtma;
+    K2 v = K2::kAuto;
     const char* e = std::getenv("SPMVK_RGCSR_KERNEL");
     if (e) parse_k2(e, &v);
     return static_cast<int>(v);
@@ -270,8 +282,9 @@ void launch_wtma_g(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, c
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
-  const K2 k = k2_choice();
   constexpr bool f64 = sizeof(T) == 8;
+  K2 k = k2_choice();
+  if (k == K2::kAuto) k = auto_k2(h, f64);
   if (k == K2::kWtma && h->group_size <= 256) {
     launch_wtma_g<T, kScaled, 8, f64 ? 4 : 3, f64 ? 512 : 1024>(h, x, y, x_next, scale, s);
     return;
@@ -427,7 +440,8 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (wtma | wtma16 | pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | ldg8_pf)");
+                             "' (auto | wtma | wtma16 | pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | "
+                             "ldg8_pf)");
     k2_slot().store(static_cast<int>(k));
   });
 }

@@ -260,12 +260,14 @@ __global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
   uint64_t off[R];
   T acc[R];
   uint32_t nlen[R], nbase[R];  // prefetched metadata of the next wave
+  uint64_t nend = 0, wave_end = 0;
   auto row_of = [&](uint32_t w, int i) -> uint32_t {
     const uint32_t lr = lane + 32u * i;
     return lr < wave_rows ? w * wave_rows + lr : 0xffffffffu;
   };
   auto group_of = [&](uint32_t r) -> uint32_t { return r / G; };
   auto fetch_meta = [&](uint32_t w) {
+    nend = w < w1 ? wave_start(w + 1) : 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const uint32_t r = row_of(w, i);
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
       off[i] = (uint64_t)nbase[i] + (live ? row[i] - g * G : 0);
       acc[i] = T(0);
     }
+    wave_end = nend;
     fetch_meta(w + 1);
   };
   auto finish_wave = [&]() {
@@ -302,7 +305,6 @@ __global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
   };
   fetch_meta(w0);
   start_wave();
-  uint64_t wave_end = wave_start(w + 1);
 
   for (uint32_t k = 0; k < nchunks; ++k) {
     const uint32_t stage = k % NS;
@@ -314,8 +316,8 @@ __global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         uint32_t nb = 0;
-        if (rem[i] && off[i] < cend)
-          nb = min(rem[i], (uint32_t)((cend - off[i] + s[i] - 1) / s[i]));
+        if (rem[i] && off[i] < cend)  // off >= cbeg, so the distance fits 32 bits
+          nb = min(rem[i], ((uint32_t)(cend - off[i]) + s[i] - 1) / s[i]);
         uint32_t idx = (uint32_t)(off[i] - cbeg);
         const uint32_t si = s[i];
         uint32_t q = 0;
@@ -354,7 +356,6 @@ __global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
       finish_wave();  // every slot of this wave lies in chunks <= k
       if (w >= w1) break;
       start_wave();
-      wave_end = wave_start(w + 1);
     }
     __syncwarp();
     if (lane == 0 && k + NS < nchunks) {

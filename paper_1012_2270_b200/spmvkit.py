@@ -424,8 +424,10 @@ def fill_report(a) -> FillReport:
         return FillReport("rgcsr", i.slots, i.nnz, i.artificial_zeros,
                           _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
     if isinstance(a, HybridMatrix):
-        return FillReport("hybrid", i.ell_slots + i.coo_nnz, i.nnz, i.artificial_zeros,
-                          _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
+        # the reference recounts ELL nnz from the layout (ell_nnz, ellpack.hpp:55-78)
+        return FillReport("hybrid", i.ell_slots + i.coo_nnz, i.fill_nnz, i.artificial_zeros,
+                          _fill_percent(i.artificial_zeros, i.fill_nnz), i.bytes_single,
+                          i.bytes_double)
     raise InvalidArgument(f"no fill report for {type(a).__name__}")
 
 

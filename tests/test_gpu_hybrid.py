@@ -49,6 +49,9 @@ def test_small_golden_seeds(cuda, golden, kind):
         assert h.slots_per_row == int(g[f"{t}_hy_k1"][0])
         assert_hybrid_equal(h.to_host(), g, f"{t}_hy_")
         x = g[f"{t}_x"]
+        f = sk.fill_report(h)  # includes the reference's ell_nnz recount of stored zeros
+        assert [f.artificial_zeros, f.bytes_single, f.bytes_double] == \
+            [int(v) for v in g[f"{t}_hy_fill"]], t
         assert bitwise(sk.spmv_hybrid(h, x), g[f"{t}_hy_y"]), t
         assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), g[f"{t}_hy_y"]), t
 

@@ -17,7 +17,7 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = ["wtma", "wtma16", "pipe", "pipe_hi", "pipe8", "tma", "ldg", "ldg_pf", "ldg8_pf"]
+VARIANTS = ["auto", "wtma", "wtma16", "pipe", "pipe_hi", "pipe8", "tma", "ldg", "ldg_pf", "ldg8_pf"]
 
 
 def dev(x):
@@ -30,7 +30,7 @@ def k2(request, cuda):
     from paper_1012_2270_b200._lib import lib
     assert lib().spmvk_set_rgcsr_kernel(request.param.encode()) == 0
     yield request.param
-    lib().spmvk_set_rgcsr_kernel(b"wtma")
+    lib().spmvk_set_rgcsr_kernel(b"auto")
 
 
 def test_example8_golden_arrays(cuda, golden):
@@ -86,6 +86,9 @@ def test_small_golden_seeds(cuda, golden, kind, k2):
         x = g[f"{t}_x"]
         a = sk.build_rgcsr(m, G)
         assert_rgcsr_equal(a.to_host(), g, f"{t}_rg_")
+        f = sk.fill_report(a)
+        assert [f.artificial_zeros, f.bytes_single, f.bytes_double, f.nnz] == \
+            [int(v) for v in g[f"{t}_rg_fill"]], t
         assert bitwise(sk.spmv_rgcsr(a, x), g[f"{t}_rg_y"]), t
         assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), g[f"{t}_rg_y"]), t
         a32 = sk.build_rgcsr(m, G, 4)

@@ -66,7 +66,7 @@ def test_halo_plan_of_7pt_slabs():
     assert sum(c1 - c0 for _, c0, c1 in plan) == 2 * n * n
 
 
-def _worker(rank, world, port, steps, out):
+def _worker(rank, world, port, steps, out, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m = orc.stencil(7, 12)
@@ -84,12 +84,31 @@ def _worker(rank, world, port, steps, out):
         dist.all_gather_into_tensor(o, i)
 
     x0 = torch.from_numpy(orc.random_vector(m.cols, 1))
-    it = part.IteratedSpmv(me, m.cols, world, slab_spmv, all_gather, x0)
+    if mode == "allgather":
+        it = part.IteratedSpmv(me, m.cols, world, slab_spmv, all_gather, x0)
+    else:
+        sc = slab_csr(m, me.row_begin, me.row_end)
+        mine = (int(sc.col.min()), int(sc.col.max())) if sc.nnz else (1, 0)
+        ranges = [None] * world
+        dist.all_gather_object(ranges, mine)
+        it = part.HaloIteratedSpmv(me, slabs, ranges, m.cols, slab_spmv, part.torch_p2p, x0)
+        # every entry the slab reads must be covered by its own rows + halos
+        covered = set(range(me.row_begin, me.row_end))
+        for _, c0, c1 in it.recv:
+            covered |= set(range(c0, c1))
+        assert set(np.unique(a["columns"][a["values"] != 0]).tolist()) <= covered
     it.set_x(x0)
     for _ in range(steps):
         it.step()
+    x_now = it.x[: m.cols] if mode == "allgather" else it.x_current
+    # gather full x on rank 0 to compare (halo ranks hold only their rows fresh)
+    xs = [None] * world
+    dist.all_gather_object(xs, (me.row_begin, me.row_end, x_now[me.row_begin:me.row_end].numpy()))
     if rank == 0:
-        out.put(it.x[: m.cols].numpy().tobytes())
+        full = np.empty(m.cols)
+        for r0, r1, v in xs:
+            full[r0:r1] = v
+        out.put(full.tobytes())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -100,13 +119,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("mode", ["allgather", "halo"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_iterated_distributed_equals_single_process(world):
+def test_iterated_distributed_equals_single_process(world, mode):
     steps = 5
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q, mode))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = np.frombuffer(q.get(timeout=120), np.float64)
