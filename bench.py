@@ -233,7 +233,7 @@ def run_ours(args):
     from paper_1012_2270_b200._lib import lib
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or args.distributed:
         from paper_1012_2270_b200 import partition
         return partition.bench_distributed(args, METRIC, WORKLOADS)
 
@@ -359,6 +359,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="27pt-128", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-reps", type=int, default=10)
+    ap.add_argument("--distributed", action="store_true",
+                    help="use the row-slab + NCCL path even at world size 1 (under torchrun)")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+                    help="x exchange of the distributed iterated SpMV")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -85,6 +85,11 @@ int spmvk_csr_download(const spmvk_csr* a, uint32_t* row_ptr, uint32_t* col, voi
 /* Row-length statistics (src/triplet.cpp:51-69 row_lengths / matrix_stats):
  * out[0]=max out[1]=min (rows>0). */
 int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2);
+/* Smallest / largest column index over rows [row_begin, row_end): the x range
+ * a row slab reads (out2[0] > out2[1] for a slab without entries).  Used by
+ * the halo exchange of the distributed product. */
+int spmvk_csr_column_range(const spmvk_csr* a, uint64_t row_begin, uint64_t row_end,
+                           uint64_t* out2);
 /* spmv_csr (spmvkit/csr.hpp:41-53): thread-per-row, same accumulation order. */
 int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
                        void* stream);

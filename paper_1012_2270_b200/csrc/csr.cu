@@ -133,6 +133,25 @@ __global__ void row_len_range(uint64_t rows, const uint32_t* __restrict__ rp,
   }
 }
 
+// ------------------------------------------------------------ column range
+// min / max column index over entries [b, e) (the x range a row slab reads).
+__global__ void col_range(uint64_t b, uint64_t e, const uint32_t* __restrict__ col,
+                          unsigned* out /* [0]=min [1]=max */) {
+  unsigned mn = 0xffffffffu, mx = 0;
+  for (uint64_t k = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned c = col[k];
+    mn = min(mn, c);
+    mx = max(mx, c);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
+}
+
 // ------------------------------------------------------------ spmv_csr
 // Thread per row, entries in column order, separately rounded multiply/add:
 // bitwise the reference's spmv_csr (csr.hpp:45-51).
@@ -321,6 +340,29 @@ int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2) {
     row_length_range(a, 0, a->rows, &mx, &mn, nullptr);
     out2[0] = mx;
     out2[1] = mn;
+  });
+}
+
+int spmvk_csr_column_range(const spmvk_csr* a, uint64_t row_begin, uint64_t row_end,
+                           uint64_t* out2) {
+  return guarded([&] {
+    if (!a || !out2) fail(SPMVK_EINVAL, "null argument");
+    if (row_begin > row_end || row_end > a->rows) fail(SPMVK_EINVAL, "row range outside the matrix");
+    uint32_t b = 0, e = 0;
+    SPMVK_CUDA(cudaMemcpy(&b, a->row_ptr.p + row_begin, 4, cudaMemcpyDeviceToHost));
+    SPMVK_CUDA(cudaMemcpy(&e, a->row_ptr.p + row_end, 4, cudaMemcpyDeviceToHost));
+    DevBuf<unsigned> d(2);
+    unsigned init[2] = {0xffffffffu, 0};
+    SPMVK_CUDA(cudaMemcpy(d.p, init, sizeof(init), cudaMemcpyHostToDevice));
+    if (e > b) {
+      col_range<<<persistent_grid((e - b + 255) / 256, 8), 256>>>(b, e, a->col.p, d.p);
+      SPMVK_LAUNCH("col_range");
+    }
+    unsigned h[2];
+    SPMVK_CUDA(cudaMemcpy(h, d.p, sizeof(h), cudaMemcpyDeviceToHost));
+    // an empty slab reads nothing: min > max
+    out2[0] = e > b ? h[0] : 1;
+    out2[1] = e > b ? h[1] : 0;
   });
 }
 

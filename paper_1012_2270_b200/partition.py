@@ -215,6 +215,15 @@ def bench_distributed(args, metric: str, workloads: dict):
     sp = stream.cuda_stream
     a = sk.build_rgcsr(csr, G, 8, stream=sp, row_range=(me.row_begin, me.row_end))
     nnz_local = a.nnz()
+    exchange = getattr(args, "exchange", "allgather")
+    if exchange == "halo":
+        import ctypes as C
+        cr = (C.c_uint64 * 2)()
+        sk._check(lib().spmvk_csr_column_range(csr._h, me.row_begin, me.row_end, cr))
+        mine = torch.tensor([int(cr[0]), int(cr[1])], dtype=torch.int64, device="cuda")
+        allr = torch.empty(2 * world, dtype=torch.int64, device="cuda")
+        dist.all_gather_into_tensor(allr, mine)
+        ranges = [tuple(allr[2 * r: 2 * r + 2].tolist()) for r in range(world)]
     del csr
     L = lib()
     x0 = torch.from_numpy(gen.random_vector(a.num_cols, 1)).cuda()
@@ -228,7 +237,14 @@ def bench_distributed(args, metric: str, workloads: dict):
         with torch.cuda.stream(stream):
             dist.all_gather_into_tensor(out, inp)
 
-    it = IteratedSpmv(me, a.num_cols, world, slab_spmv, all_gather, x0)
+    def p2p(ops):
+        with torch.cuda.stream(stream):
+            torch_p2p(ops)
+
+    if exchange == "halo":
+        it = HaloIteratedSpmv(me, slabs, ranges, a.num_cols, slab_spmv, p2p, x0)
+    else:
+        it = IteratedSpmv(me, a.num_cols, world, slab_spmv, all_gather, x0)
     it.set_x(x0)
     for _ in range(args.warmup):
         it.step()
@@ -245,18 +261,29 @@ def bench_distributed(args, metric: str, workloads: dict):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     tot_nnz = torch.tensor([nnz_local], device="cuda", dtype=torch.float64)
     dist.all_reduce(tot_nnz)
+    # checksum of this rank's rows of the final iterate (bitwise across P: the
+    # slab arrays are global slices and every row keeps the reference's order)
+    xf = it.x[: a.num_cols] if exchange == "allgather" else it.x_current
+    # order-independent bit checksum: wrapping int64 sum of the raw bits
+    part_sum = xf[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
+    sums = torch.empty(world, dtype=torch.int64, device="cuda")
+    dist.all_gather_into_tensor(sums, part_sum)
     dist.barrier()
     if rank == 0:
         step_ms = ms.item() / args.steps
         value = 2.0 * tot_nnz.item() / (step_ms * 1e-3) / 1e9
+        halo = it.halo_entries() if exchange == "halo" else None
         print(json.dumps({
             "metric": metric, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.workload, "description": desc, "format": "rgcsr",
-                       "group_size": G, "parallelism": f"row-slab x{world}, NCCL all-gather of x",
-                       "step": "slab SpMV (+fused x_next = y/16) + all_gather_into_tensor"},
+                       "group_size": G,
+                       "parallelism": f"row-slab x{world}, NCCL {exchange} of x",
+                       "step": f"slab SpMV (+fused x_next = y/16) + {exchange} exchange",
+                       "halo_entries_rank0": halo},
             "gpu_launches": args.steps,
+            "x_bits_checksum": int(sums.sum().item()),
         }), flush=True)
     dist.destroy_process_group()
