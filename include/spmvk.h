@@ -90,6 +90,14 @@ int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2);
  * the halo exchange of the distributed product. */
 int spmvk_csr_column_range(const spmvk_csr* a, uint64_t row_begin, uint64_t row_end,
                            uint64_t* out2);
+/* descending_row_permutation (src/reorder.cpp:35-42), on the device: map[i] =
+ * old row of new row i, rows by decreasing length, ties by index (stable). */
+int spmvk_csr_descending_permutation(const spmvk_csr* a, uint32_t* map);
+/* apply_permutation(m, descending_row_permutation(m), RowsOnly)
+ * (src/reorder.cpp:44-61): a new CSR whose row i is old row map[i]; `map`
+ * (HOST, rows entries, may be NULL) receives the permutation. */
+int spmvk_csr_permute_rows_descending(const spmvk_csr* a, void* stream, spmvk_csr** out,
+                                      uint32_t* map);
 /* spmv_csr (spmvkit/csr.hpp:41-53): thread-per-row, same accumulation order. */
 int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
                        void* stream);

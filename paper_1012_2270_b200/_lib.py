@@ -48,6 +48,8 @@ SIGNATURES = {
     "spmvk_csr_download": (cint, [vp, vp, vp, vp]),
     "spmvk_csr_row_length_range": (cint, [vp, u64p]),
     "spmvk_csr_column_range": (cint, [vp, u64, u64, u64p]),
+    "spmvk_csr_descending_permutation": (cint, [vp, vp]),
+    "spmvk_csr_permute_rows_descending": (cint, [vp, vp, C.POINTER(vp), vp]),
     "spmvk_csr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
     "spmvk_csr_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),
     "spmvk_csr_destroy": (None, [vp]),

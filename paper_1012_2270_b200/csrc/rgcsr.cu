@@ -173,7 +173,9 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
-enum class K2 { kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf };
+enum class K2 {
+  kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf, kLdg32, kLdgPf6
+};
 
 // "auto" (default): the variant that measured fastest for the row-length
 // regime on B200 (profiles/r01_k2_sweep.md): long rows (mean > 12 slots)
@@ -192,7 +194,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
-      {"ldg8_pf", K2::kLdg8Pf}};
+      {"ldg8_pf", K2::kLdg8Pf}, {"ldg32", K2::kLdg32}, {"ldg_pf6", K2::kLdgPf6}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -318,6 +320,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;
     case K2::kLdg8Pf: run(rgcsr_spmv_ldg<T, kScaled, 8, true>); break;
     case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
+    case K2::kLdg32: run(rgcsr_spmv_ldg<T, kScaled, U, false, 8>); break;
+    case K2::kLdgPf6: run(rgcsr_spmv_ldg<T, kScaled, U, true, 6>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
   }
   SPMVK_LAUNCH("rgcsr_spmv_ldg");

@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
   }
 }
 
-template <class T, bool kScaled, int U, bool kPrefetch>
-__global__ void __launch_bounds__(256) rgcsr_spmv_ldg(
+template <class T, bool kScaled, int U, bool kPrefetch, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_ldg(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,

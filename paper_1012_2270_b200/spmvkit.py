@@ -189,6 +189,26 @@ class CsrMatrix:
             self._h = C.c_void_p()
 
 
+def descending_row_permutation(m) -> np.ndarray:
+    """descending_row_permutation(m) (src/reorder.cpp:35-42) on the device:
+    map[new] = old, rows by decreasing length, ties by original index."""
+    a = _as_csr(m)
+    out = np.empty(a.num_rows, np.uint32)
+    _check(lib().spmvk_csr_descending_permutation(a._h, _ptr(out)))
+    return out
+
+
+def apply_descending_permutation(m, stream: int = 0):
+    """apply_permutation(m, descending_row_permutation(m), RowsOnly)
+    (src/reorder.cpp:44-61) on the device.  Returns (CsrMatrix, map); row i of
+    the result is row map[i] of m, so spmv(result, x)[i] == spmv(m, x)[map[i]]."""
+    a = _as_csr(m)
+    out = np.empty(a.num_rows, np.uint32)
+    h = C.c_void_p()
+    _check(lib().spmvk_csr_permute_rows_descending(a._h, stream or None, C.byref(h), _ptr(out)))
+    return CsrMatrix(h.value), out
+
+
 def build_csr(m: TripletMatrix, precision=F64, stream: int = 0) -> CsrMatrix:
     """build_csr<Scalar>(m) (csr.hpp:24-39): upload + validate on the device."""
     prec = _prec(precision)

@@ -27,7 +27,9 @@ from paper_1012_2270_b200._lib import lib  # noqa: E402
 
 
 def flush_l2(buf):
-    buf.add_(1.0)
+    """Evicts L2 by READING 512 MB (a write-based flush would leave dirty lines
+    whose write-back lands inside the next timed kernel)."""
+    return buf.sum()
 
 
 def main():
