@@ -123,6 +123,26 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+// Register-lean forms (no policy operand) for occupancy-bound kernels.
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T ld_x(const T* p) {
+  return __ldg(p);
+}
 // Gathered vector x: read-only path, L1-allocating.
 __device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
   double v;
@@ -190,7 +210,15 @@ struct spmvk_rgcsr {
   mutable std::mutex part_mu;
   mutable spmvk::DevBuf<uint32_t> part;
   mutable uint32_t part_W = 0;
+  // Rows longer than kLongRow (ascending ids): K2's thread-per-row kernels
+  // skip them and a warp-per-row kernel handles them (power-law tails).
+  spmvk::DevBuf<uint32_t> long_rows;
+  uint64_t n_long = 0;
 };
+
+namespace spmvk {
+constexpr uint32_t kLongRow = 128;
+}
 
 struct spmvk_hybrid {
   uint64_t rows = 0, cols = 0, k1 = 0, coo = 0, nnz = 0;

@@ -243,7 +243,20 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
             const uint32_t mid = (lo + hi) >> 1;
             if (prow[mid] < r) lo = mid + 1; else hi = mid;
           }
-          for (uint32_t i = lo; i < n && prow[i] == r; ++i) acc = add_rn(acc, prod[i]);
+          uint32_t end = lo, top = n;  // first staged entry with row > r
+          while (end < top) {
+            const uint32_t mid = (end + top) >> 1;
+            if (prow[mid] <= r) end = mid + 1; else top = mid;
+          }
+          uint32_t i = lo;
+          for (; i + 8 <= end; i += 8) {  // 8 independent LDS in flight, adds in order
+            T p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = prod[i + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+          }
+          for (; i < end; ++i) acc = add_rn(acc, prod[i]);
         }
         __syncthreads();
       }

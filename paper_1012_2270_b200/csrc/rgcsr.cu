@@ -40,6 +40,20 @@ __global__ void narrow_pointers(uint64_t groups, const uint64_t* __restrict__ gp
     gp[g] = (uint32_t)(g == groups ? total : gp64[g]);
 }
 
+__global__ void long_row_flags(uint64_t rows, const uint32_t* __restrict__ lens,
+                               uint64_t* __restrict__ flag) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    flag[r] = lens[r] > kLongRow ? 1 : 0;
+}
+
+__global__ void long_row_scatter(uint64_t rows, const uint32_t* __restrict__ lens,
+                                 const uint64_t* __restrict__ pos, uint32_t* __restrict__ out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    if (lens[r] > kLongRow) out[pos[r]] = (uint32_t)r;
+}
+
 // ------------------------------------------------------------ K1: scatter
 // One warp per group.  Lane t owns local row t (+32 per chunk) and walks its
 // slots j = 0..K_g-1; for a fixed j the warp writes 32 contiguous slots, and
@@ -137,6 +151,17 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
     SPMVK_CUDA(cudaMemcpy(&e, a->row_ptr.p + r1, 4, cudaMemcpyDeviceToHost));
     h->nnz = e - b;
   }
+  if (h->rows) {  // long-row list (ascending): flag, scan, scatter
+    DevBuf<uint64_t> pos(h->rows);
+    long_row_flags<<<rgrid, 256, 0, s>>>(h->rows, h->row_lengths.p, pos.p);
+    SPMVK_LAUNCH("long_row_flags");
+    h->n_long = exclusive_scan_u64(pos.p, h->rows, s);
+    h->long_rows.alloc(h->n_long);
+    if (h->n_long) {
+      long_row_scatter<<<rgrid, 256, 0, s>>>(h->rows, h->row_lengths.p, pos.p, h->long_rows.p);
+      SPMVK_LAUNCH("long_row_scatter");
+    }
+  }
   h->values.alloc(total * static_cast<uint64_t>(prec));
   h->columns.alloc(total);
   if (h->groups) {
@@ -174,7 +199,8 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
-  kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf, kLdg32, kLdgPf6
+  kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf, kLdg32, kLdgPf6,
+  kLite, kLite6, kLite8
 };
 
 // "auto" (default): the variant that measured fastest for the row-length
@@ -194,7 +220,8 @@ bool parse_k2(const std::string& v, K2* out) {
       {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
-      {"ldg8_pf", K2::kLdg8Pf}, {"ldg32", K2::kLdg32}, {"ldg_pf6", K2::kLdgPf6}};
+      {"ldg8_pf", K2::kLdg8Pf}, {"ldg32", K2::kLdg32}, {"ldg_pf6", K2::kLdgPf6},
+      {"lite", K2::kLite},     {"lite6", K2::kLite6}, {"lite8", K2::kLite8}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -305,6 +332,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
   constexpr int U = sizeof(T) == 8 ? 4 : 8;
+  // rows longer than kLongRow go to the warp-per-row kernel (launched second,
+  // same stream; the two kernels write disjoint rows of y)
+  const uint32_t long_cut = h->n_long ? kLongRow : 0xffffffffu;
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -312,7 +342,15 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
     kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
-                              h->columns.p, x, y, x_next, scale);
+                              h->columns.p, x, y, x_next, scale, long_cut);
+    SPMVK_LAUNCH("rgcsr_spmv (thread per row)");
+    if (h->n_long) {
+      rgcsr_spmv_long<T, kScaled><<<persistent_grid((h->n_long + 7) / 8, 8), 256, 0, s>>>(
+          static_cast<uint32_t>(h->n_long), h->long_rows.p, static_cast<uint32_t>(h->rows), G,
+          sh, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+          h->columns.p, x, y, x_next, scale);
+      SPMVK_LAUNCH("rgcsr_spmv_long");
+    }
   };
   switch (k) {
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
@@ -322,9 +360,11 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
     case K2::kLdg32: run(rgcsr_spmv_ldg<T, kScaled, U, false, 8>); break;
     case K2::kLdgPf6: run(rgcsr_spmv_ldg<T, kScaled, U, true, 6>); break;
+    case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
+    case K2::kLite6: run(rgcsr_spmv_lite<T, kScaled, 4, 6>); break;
+    case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
   }
-  SPMVK_LAUNCH("rgcsr_spmv_ldg");
 }
 
 template <class T>

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale) {
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
       const uint32_t gn = g_shift >= 0 ? (rn >> g_shift) : rn / G;
       len_n = lens[rn];
       base_n = gp[gn];
+    }
+    if (len > long_cut) {  // handled by rgcsr_spmv_long
+      r = rn;
+      continue;
     }
     uint32_t cA[U];
     T vA[U];
@@ -99,18 +103,82 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
   }
 }
 
+// Lean thread-per-row kernel built for occupancy: a CTA handles 256-row
+// tiles (CTA-stride), each thread walks its row in U-deep predicated batches
+// with 32-bit strided pointers (no prefetch buffers), so it fits the register
+// budget of MINB resident CTAs per SM.  Full occupancy (64 warps / SM) gives
+// the memory system the most independent requests; a predicated last batch
+// avoids serialised single-slot round trips on short rows and tails.
+template <class T, bool kScaled, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  const uint32_t ntiles = (rows + 255) / 256;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r = tile * 256 + threadIdx.x;
+    if (r >= rows) continue;
+    const uint32_t len = lens[r];
+    if (len > long_cut) continue;  // handled by rgcsr_spmv_long
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t off = gp[g] + (r - g * G);
+    const T* __restrict__ vp = values + off;
+    const uint32_t* __restrict__ cp = columns + off;
+    T acc = T(0);
+    uint32_t j = 0;
+    for (; j + U <= len; j += U) {  // full batches: U slot pairs, then U x gathers
+      uint32_t c[U];
+      T v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = ld_stream(cp + u * s);
+        v[u] = ld_stream(vp + u * s);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+      cp += U * s;
+      vp += U * s;
+    }
+    if (j < len) {  // predicated last batch
+      uint32_t c[U];
+      T v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u) {
+        c[u] = 0;
+        v[u] = T(0);
+        if (j + u < len) {
+          c[u] = ld_stream(cp + u * s);
+          v[u] = ld_stream(vp + u * s);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u) xv[u] = j + u < len ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u)
+        if (j + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    }
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+}
+
 template <class T, bool kScaled, int U, bool kPrefetch, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_ldg(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale) {
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
     const uint32_t t = r - g * G;
     const uint32_t s = min(G, rows - g * G);
     const uint32_t len = lens[r];
+    if (len > long_cut) continue;  // handled by rgcsr_spmv_long
     const T* __restrict__ vp = values + gp[g] + t;
     const uint32_t* __restrict__ cp = columns + gp[g] + t;
     T acc = T(0);
@@ -166,7 +234,73 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_ldg(
 }
 
 // ---------------------------------------------------------------------------
-// rgcsr_spmv_wtma — per-warp bulk-copy streams (the B200-native default).
+// rgcsr_spmv_long — the rows longer than kLongRow (power-law tails), one warp
+// per row.  A thread-per-row kernel would serialise a 4096-slot row in one
+// thread for ~1000 dependent round trips; here the warp loads 256 slots of the
+// row at a time (8 per lane, all in flight), forms the products in parallel,
+// stages them in shared memory, and one lane adds them in slot order — the
+// reference's rounding sequence, so y stays bitwise.
+template <class T, bool kScaled>
+__global__ void __launch_bounds__(256) rgcsr_spmv_long(
+    uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,
+    int g_shift, const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  constexpr int K = 8, W = 32 * K;
+  __shared__ T prod[8][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  for (uint32_t i = blockIdx.x * 8 + warp; i < nlong; i += gridDim.x * 8) {
+    const uint32_t r = long_rows[i];
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t t = r - g * G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = lens[r];
+    const T* __restrict__ vp = values + gp[g] + t;
+    const uint32_t* __restrict__ cp = columns + gp[g] + t;
+    T acc = T(0);
+    for (uint32_t j0 = 0; j0 < len; j0 += W) {
+      uint32_t c[K];
+      T v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t j = j0 + lane + 32 * k;
+        c[k] = 0;
+        v[k] = T(0);
+        if (j < len) {
+          c[k] = ld_stream(cp + (size_t)j * s, pf);
+          v[k] = ld_stream(vp + (size_t)j * s, pf);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t j = j0 + lane + 32 * k;
+        if (j < len) prod[warp][lane + 32 * k] = mul_rn(v[k], ld_x(x + c[k], pl));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t n = min((uint32_t)W, len - j0);
+        uint32_t q = 0;
+        for (; q + 8 <= n; q += 8) {
+          T p[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p[u] = prod[warp][q + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+        }
+        for (; q < n; ++q) acc = add_rn(acc, prod[warp][q]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      y[r] = acc;
+      if (kScaled) x_next[r] = mul_rn(acc, scale);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// rgcsr_spmv_wtma — per-warp bulk-copy streams (experimental variant).
 //
 // Every warp owns a contiguous range of "waves" (a wave is the rows one warp
 // covers at once: one group when G >= 32, lane l then holding rows
