@@ -42,7 +42,8 @@ typedef enum {
   SPMVK_ERANGE = 2, /* std::runtime_error (size budget / 32-bit overflow) */
   SPMVK_ECUDA = 3,  /* CUDA runtime / launch failure */
   SPMVK_ENCCL = 4,  /* collective failure (distributed path) */
-  SPMVK_ENOMEM = 5  /* device allocation failure */
+  SPMVK_ENOMEM = 5, /* device allocation failure */
+  SPMVK_EPARSE = 6  /* Matrix Market syntax error (MatrixMarketError, a std::runtime_error) */
 } spmvk_status;
 
 /* Storage precision: the reference's Scalar template argument
@@ -85,6 +86,17 @@ int spmvk_csr_download(const spmvk_csr* a, uint32_t* row_ptr, uint32_t* col, voi
 /* Row-length statistics (src/triplet.cpp:51-69 row_lengths / matrix_stats):
  * out[0]=max out[1]=min (rows>0). */
 int spmvk_csr_row_length_range(const spmvk_csr* a, uint64_t* out2);
+/* Matrix Market ingest (parse_matrix_market / load_matrix_market,
+ * src/matrix_market.cpp:61-148): same accepted banner, messages and 1-based
+ * line numbers ("line N: ..." in spmvk_last_error(), N also in *error_line,
+ * SPMVK_EPARSE), canonicalised like spmvkit::canonicalize (sorted, duplicate
+ * coordinates summed in the reference's order), then uploaded and validated
+ * like spmvk_csr_upload.  Entry lines are parsed with `threads` host threads
+ * (0 = all).  A file that cannot be opened gives SPMVK_ERANGE. */
+int spmvk_mm_parse(const char* text, uint64_t len, int threads, int val_prec, void* stream,
+                   spmvk_csr** out, uint64_t* error_line);
+int spmvk_mm_load(const char* path, int threads, int val_prec, void* stream, spmvk_csr** out,
+                  uint64_t* error_line);
 /* Smallest / largest column index over rows [row_begin, row_end): the x range
  * a row slab reads (out2[0] > out2[1] for a slab without entries).  Used by
  * the halo exchange of the distributed product. */

@@ -349,6 +349,8 @@ def R():
             "ref_slabs_build": (ci, [vp, ci, u64, i64, ci, ci, pp]),
             "ref_slabs_spmv": (ci, [vp, vp, vp]),
             "ref_slabs_free": (None, [vp]),
+            "ref_mm_parse": (ci, [C.c_char_p, u64, pp, C.POINTER(C.c_uint64)]),
+            "ref_mm_write": (u64, [vp, C.c_char_p, u64]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -401,6 +403,22 @@ class RefMatrix:
 
     def descending(self):
         return RefMatrix._make("ref_tm_descending", self.h)
+
+    @classmethod
+    def mm_parse(cls, text: bytes):
+        """parse_matrix_market; returns (RefMatrix or None, error line, message)."""
+        h = C.c_void_p()
+        line = C.c_uint64()
+        rc = R().ref_mm_parse(text, len(text), C.byref(h), C.byref(line))
+        if rc:
+            return None, line.value, R().ref_last_error().decode()
+        return cls(h.value), 0, ""
+
+    def mm_write(self) -> bytes:
+        n = R().ref_mm_write(self.h, None, 0)
+        buf = C.create_string_buffer(n)
+        R().ref_mm_write(self.h, buf, n)
+        return buf.raw[:n]
 
     def descending_map(self):
         out = np.empty(self.rows, np.uint32)

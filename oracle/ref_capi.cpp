@@ -21,6 +21,7 @@
 #include <cstring>
 #include <memory>
 #include <random>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -196,6 +197,34 @@ void ref_tm_export(const void* h, uint32_t* row_ptr, uint32_t* col, double* val)
 }
 
 void ref_tm_free(void* h) { delete static_cast<RefMatrix*>(h); }
+
+// parse_matrix_market (src/matrix_market.cpp:61-138) on an in-memory text;
+// returns 3 with *line set on MatrixMarketError.
+int ref_mm_parse(const char* text, uint64_t len, void** out, uint64_t* line) {
+  *line = 0;
+  try {
+    std::istringstream in(std::string(text, len));
+    *out = new RefMatrix{parse_matrix_market(in)};
+    return 0;
+  } catch (const MatrixMarketError& e) {
+    g_err = e.what();
+    *line = e.line();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// write_matrix_market (src/matrix_market.cpp:150-158) into a caller buffer;
+// returns the byte count (call with buf NULL to size).
+uint64_t ref_mm_write(const void* h, char* buf, uint64_t cap) {
+  std::ostringstream out;
+  write_matrix_market(out, static_cast<const RefMatrix*>(h)->m);
+  const std::string s = out.str();
+  if (buf) std::memcpy(buf, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
 
 int ref_spmv_reference(const void* h, const double* x, uint64_t nx, double* y) {
   return guard([&] {

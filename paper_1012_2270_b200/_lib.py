@@ -13,7 +13,8 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspmvk.so")
 
-SPMVK_OK, SPMVK_EINVAL, SPMVK_ERANGE, SPMVK_ECUDA, SPMVK_ENCCL, SPMVK_ENOMEM = range(6)
+SPMVK_OK, SPMVK_EINVAL, SPMVK_ERANGE, SPMVK_ECUDA, SPMVK_ENCCL, SPMVK_ENOMEM, SPMVK_EPARSE = \
+    range(7)
 F32, F64 = 4, 8
 
 u32p = C.POINTER(C.c_uint32)
@@ -48,6 +49,8 @@ SIGNATURES = {
     "spmvk_csr_download": (cint, [vp, vp, vp, vp]),
     "spmvk_csr_row_length_range": (cint, [vp, u64p]),
     "spmvk_csr_column_range": (cint, [vp, u64, u64, u64p]),
+    "spmvk_mm_parse": (cint, [C.c_char_p, u64, cint, cint, vp, C.POINTER(vp), u64p]),
+    "spmvk_mm_load": (cint, [C.c_char_p, cint, cint, vp, C.POINTER(vp), u64p]),
     "spmvk_csr_descending_permutation": (cint, [vp, vp]),
     "spmvk_csr_permute_rows_descending": (cint, [vp, vp, C.POINTER(vp), vp]),
     "spmvk_csr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),

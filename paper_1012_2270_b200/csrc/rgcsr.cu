@@ -203,16 +203,12 @@ enum class K2 {
   kLite, kLite6, kLite8
 };
 
-// "auto" (default): the variant that measured fastest for the row-length
-// regime on B200 (profiles/r01_k2_sweep.md): long rows (mean > 12 slots)
-// stream best with the software-pipelined 4/8-deep loads at full occupancy
-// (ldg_pf); short rows need the row-level metadata prefetch with more warps
-// per SM (pipe_hi for fp64, pipe for fp32).
-K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
-  const double mean = h->rows ? double(h->nnz) / double(h->rows) : 0.0;
-  if (mean > 12.0) return K2::kLdgPf;
-  return f64 ? K2::kPipeHi : K2::kPipe;
-}
+// "auto" (default): the variant that measured fastest on B200 across the
+// stencil shapes (profiles/r01_k2_sweep.md): the register-lean tile kernel —
+// 8-deep batches at 40 warps / SM for fp64 (lite8), 4-deep at full occupancy
+// (64 warps / SM) for fp32 (lite).  Occupancy beats deeper per-thread
+// pipelines: every variant with prefetch buffers lost to it.
+K2 auto_k2(const spmvk_rgcsr*, bool f64) { return f64 ? K2::kLite8 : K2::kLite; }
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {

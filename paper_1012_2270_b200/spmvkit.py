@@ -189,6 +189,42 @@ class CsrMatrix:
             self._h = C.c_void_p()
 
 
+class MatrixMarketError(RuntimeError):
+    """spmvkit::MatrixMarketError (matrix_market.hpp:14-23): message "line N: ..."
+    and the 1-based line number in ``.line``."""
+
+    def __init__(self, message: str, line: int):
+        super().__init__(message)
+        self.line = line
+
+
+def _mm_check(rc: int, line: C.c_uint64) -> None:
+    if rc == _lib.SPMVK_EPARSE:
+        raise MatrixMarketError(_lib.last_error(), line.value)
+    _check(rc)
+
+
+def parse_matrix_market(text, precision=F64, threads: int = 0, stream: int = 0) -> CsrMatrix:
+    """parse_matrix_market (src/matrix_market.cpp:61-138) straight to a device
+    CSR: same accepted language, messages and line numbers; canonicalised."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    line = C.c_uint64()
+    _mm_check(lib().spmvk_mm_parse(data, len(data), threads, _prec(precision), stream or None,
+                                   C.byref(h), C.byref(line)), line)
+    return CsrMatrix(h.value)
+
+
+def load_matrix_market(path, precision=F64, threads: int = 0, stream: int = 0) -> CsrMatrix:
+    """load_matrix_market (src/matrix_market.cpp:140-148); parse errors carry
+    the path prefix like the reference's rethrow."""
+    h = C.c_void_p()
+    line = C.c_uint64()
+    _mm_check(lib().spmvk_mm_load(str(path).encode(), threads, _prec(precision), stream or None,
+                                  C.byref(h), C.byref(line)), line)
+    return CsrMatrix(h.value)
+
+
 def descending_row_permutation(m) -> np.ndarray:
     """descending_row_permutation(m) (src/reorder.cpp:35-42) on the device:
     map[new] = old, rows by decreasing length, ties by original index."""
