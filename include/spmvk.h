@@ -214,6 +214,18 @@ int spmvk_hybrid_spmv_host_f32(const spmvk_hybrid* h, const float* x, uint64_t n
                                uint64_t ny);
 void spmvk_hybrid_destroy(spmvk_hybrid* h);
 
+/* ------------------------------------------------------------------ CG
+ * Unpreconditioned conjugate gradients for an SPD fp64 RgCSR matrix, fully
+ * device-resident (scalars never leave HBM; the host reads the residual every
+ * `check_every` iterations).  b, x are DEVICE vectors of n; x holds the initial
+ * guess and receives the solution.  Stops when ||r|| <= tol * ||b|| or after
+ * max_iter iterations.  Dots are deterministic (fixed-grid partials). */
+int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_t n, double tol,
+                       uint64_t max_iter, uint64_t check_every, uint64_t* iters,
+                       double* rel_residual, void* stream);
+/* out_dev[0] = a . b (deterministic), device pointers. */
+int spmvk_dot_f64(const double* a, const double* b, uint64_t n, double* out_dev, void* stream);
+
 /* ------------------------------------------------------------------ host generators
  * Seeded, platform-independent generators (std::mt19937_64 draws, the
  * reference's unit_real convention src/synthetic.cpp:7-9).  Two-pass: pass

@@ -78,6 +78,9 @@ SIGNATURES = {
     "spmvk_hybrid_spmv_host_f64": (cint, [vp, vp, u64, vp, u64]),
     "spmvk_hybrid_spmv_host_f32": (cint, [vp, vp, u64, vp, u64]),
     "spmvk_hybrid_destroy": (None, [vp]),
+    "spmvk_cg_solve_f64": (cint, [vp, vp, vp, u64, C.c_double, u64, u64, u64p,
+                                  C.POINTER(C.c_double), vp]),
+    "spmvk_dot_f64": (cint, [vp, vp, u64, vp, vp]),
     "spmvk_gen_random_vector": (None, [u64, u64, vp]),
     "spmvk_gen_stencil": (u64, [cint, u64, vp, vp, vp]),
     "spmvk_gen_powerlaw": (u64, [u64, u64, vp, vp, vp]),

@@ -472,6 +472,24 @@ def spmv_csr(a: CsrMatrix, x, y=None, stream: Optional[int] = None):
     return _device_call("spmvk_csr_spmv", a._h, x, y, a.num_rows, a.num_cols, a.val_prec, stream)
 
 
+# ---------------------------------------------------------------- CG (§8f-4)
+def cg(a: RgcsrMatrix, b, x0=None, tol: float = 1e-10, max_iter: int = 1000,
+       check_every: int = 10, stream: Optional[int] = None):
+    """Conjugate gradients on the device for an SPD fp64 RgCSR matrix (the
+    paper's motivating workload; not in the reference).  b (and x0) are CUDA
+    float64 tensors.  Returns (x, iterations, relative residual)."""
+    import torch
+    if a.precision != F64:
+        raise InvalidArgument("cg: fp64 RgCSR required")
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    it = C.c_uint64()
+    res = C.c_double()
+    s = stream if stream is not None else _torch_stream(b)
+    _check(lib().spmvk_cg_solve_f64(a._h, b.data_ptr(), x.data_ptr(), b.numel(), tol, max_iter,
+                                    check_every, C.byref(it), C.byref(res), s or None))
+    return x, it.value, res.value
+
+
 # ---------------------------------------------------------------- accounting
 def fill_report(a) -> FillReport:
     """fill_report (fill.hpp:52-95) for RgCSR and Hybrid handles."""

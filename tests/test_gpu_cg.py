@@ -1,0 +1,44 @@
+"""CG around the RgCSR SpMV (not in the reference): converges
+on SPD stencil systems and matches a direct sparse solve (scipy, test-only)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import triplets
+from paper_1012_2270_b200 import spmvkit as sk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind,n", [(5, 64), (7, 24), (27, 16)])
+def test_cg_solves_stencil_systems(cuda, kind, n):
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    om = orc.stencil(kind, n)
+    a = sk.build_rgcsr(triplets(om), 32)
+    bh = orc.random_vector(om.rows, 3)
+    b = torch.from_numpy(bh).cuda()
+    x, iters, rel = sk.cg(a, b, tol=1e-10, max_iter=5000)
+    assert rel <= 1e-10 and 0 < iters < 5000
+    xh = x.cpu().numpy()
+    # true residual with the reference-order SpMV
+    r = bh - orc.spmv_rgcsr(orc.build_rgcsr(om, 32), xh)[0]
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(bh)
+    A = sp.csr_matrix((om.val, om.col.astype(np.int64), om.rp.astype(np.int64)),
+                      shape=(om.rows, om.cols))
+    xs = spl.spsolve(A.tocsc(), bh)
+    assert np.linalg.norm(xh - xs) <= 1e-7 * np.linalg.norm(xs)
+
+
+def test_dot_is_deterministic(cuda):
+    from paper_1012_2270_b200._lib import lib
+    v = torch.from_numpy(orc.random_vector(1_000_003, 5)).cuda()
+    w = torch.from_numpy(orc.random_vector(1_000_003, 6)).cuda()
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
+    for i in range(4):
+        assert lib().spmvk_dot_f64(v.data_ptr(), w.data_ptr(), v.numel(),
+                                   out[i:].data_ptr(), None) == 0
+    o = out.cpu().numpy()
+    assert len(set(o.tobytes()[k:k + 8] for k in range(0, 32, 8))) == 1
+    assert abs(o[0] - float(np.dot(v.cpu().numpy(), w.cpu().numpy()))) < 1e-9 * abs(o[0]) + 1e-9
