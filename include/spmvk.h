@@ -172,6 +172,10 @@ void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
  * (per-warp bulk-async-copy streams).  All variants give bitwise identical
  * y.  Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
+/* Tuning knob (process-wide, read at build): rows with more than `cut` slots
+ * (default 128) are handled by a warp-per-row kernel instead of one thread
+ * (power-law tails).  Does not change y. */
+int spmvk_set_long_row_cut(uint32_t cut);
 
 /* ------------------------------------------------------------------ Hybrid */
 typedef struct {

@@ -210,10 +210,11 @@ struct spmvk_rgcsr {
   mutable std::mutex part_mu;
   mutable spmvk::DevBuf<uint32_t> part;
   mutable uint32_t part_W = 0;
-  // Rows longer than kLongRow (ascending ids): K2's thread-per-row kernels
+  // Rows longer than long_cut (ascending ids): K2's thread-per-row kernels
   // skip them and a warp-per-row kernel handles them (power-law tails).
   spmvk::DevBuf<uint32_t> long_rows;
   uint64_t n_long = 0;
+  uint32_t long_cut = 128;
 };
 
 namespace spmvk {

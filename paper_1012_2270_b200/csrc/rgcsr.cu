@@ -40,18 +40,24 @@ __global__ void narrow_pointers(uint64_t groups, const uint64_t* __restrict__ gp
     gp[g] = (uint32_t)(g == groups ? total : gp64[g]);
 }
 
-__global__ void long_row_flags(uint64_t rows, const uint32_t* __restrict__ lens,
+__global__ void long_row_flags(uint64_t rows, uint32_t cut, const uint32_t* __restrict__ lens,
                                uint64_t* __restrict__ flag) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x)
-    flag[r] = lens[r] > kLongRow ? 1 : 0;
+    flag[r] = lens[r] > cut ? 1 : 0;
 }
 
-__global__ void long_row_scatter(uint64_t rows, const uint32_t* __restrict__ lens,
+__global__ void long_row_scatter(uint64_t rows, uint32_t cut, const uint32_t* __restrict__ lens,
                                  const uint64_t* __restrict__ pos, uint32_t* __restrict__ out) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x)
-    if (lens[r] > kLongRow) out[pos[r]] = (uint32_t)r;
+    if (lens[r] > cut) out[pos[r]] = (uint32_t)r;
+}
+
+// Rows longer than this go to the warp-per-row kernel (spmvk_set_long_row_cut).
+std::atomic<uint32_t>& long_cut_slot() {
+  static std::atomic<uint32_t> v{kLongRow};
+  return v;
 }
 
 // ------------------------------------------------------------ K1: scatter
@@ -153,12 +159,14 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
   }
   if (h->rows) {  // long-row list (ascending): flag, scan, scatter
     DevBuf<uint64_t> pos(h->rows);
-    long_row_flags<<<rgrid, 256, 0, s>>>(h->rows, h->row_lengths.p, pos.p);
+    h->long_cut = long_cut_slot().load();
+    long_row_flags<<<rgrid, 256, 0, s>>>(h->rows, h->long_cut, h->row_lengths.p, pos.p);
     SPMVK_LAUNCH("long_row_flags");
     h->n_long = exclusive_scan_u64(pos.p, h->rows, s);
     h->long_rows.alloc(h->n_long);
     if (h->n_long) {
-      long_row_scatter<<<rgrid, 256, 0, s>>>(h->rows, h->row_lengths.p, pos.p, h->long_rows.p);
+      long_row_scatter<<<rgrid, 256, 0, s>>>(h->rows, h->long_cut, h->row_lengths.p, pos.p,
+                                             h->long_rows.p);
       SPMVK_LAUNCH("long_row_scatter");
     }
   }
@@ -328,9 +336,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
   constexpr int U = sizeof(T) == 8 ? 4 : 8;
-  // rows longer than kLongRow go to the warp-per-row kernel (launched second,
+  // rows longer than h->long_cut go to the warp-per-row kernel (launched second,
   // same stream; the two kernels write disjoint rows of y)
-  const uint32_t long_cut = h->n_long ? kLongRow : 0xffffffffu;
+  const uint32_t long_cut = h->n_long ? h->long_cut : 0xffffffffu;
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -474,6 +482,13 @@ int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx,
 }
 
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h) { delete h; }
+
+int spmvk_set_long_row_cut(uint32_t cut) {
+  return guarded([&] {
+    if (cut == 0) fail(SPMVK_EINVAL, "long-row cut must be positive");
+    long_cut_slot().store(cut);
+  });
+}
 
 int spmvk_set_rgcsr_kernel(const char* name) {
   return guarded([&] {
