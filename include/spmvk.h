@@ -229,6 +229,14 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
                        double* rel_residual, void* stream);
 /* out_dev[0] = a . b (deterministic), device pointers. */
 int spmvk_dot_f64(const double* a, const double* b, uint64_t n, double* out_dev, void* stream);
+/* CG building blocks for the row-slab distributed solver (device pointers,
+ * n = slab rows; dots are the slab's partials, all-reduced by the caller):
+ * update: alpha = *rr / *pap; x += alpha p; r -= alpha q; *rr_new = r . r.
+ * direction: p = r + (*rr_new / *rr) p; then *rr = *rr_new. */
+int spmvk_cg_update_f64(uint64_t n, const double* rr, const double* pap, const double* p,
+                        const double* q, double* x, double* r, double* rr_new, void* stream);
+int spmvk_cg_direction_f64(uint64_t n, const double* r, double* p, double* rr,
+                           const double* rr_new, void* stream);
 
 /* ------------------------------------------------------------------ host generators
  * Seeded, platform-independent generators (std::mt19937_64 draws, the

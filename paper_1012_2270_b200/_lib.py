@@ -82,6 +82,8 @@ SIGNATURES = {
     "spmvk_cg_solve_f64": (cint, [vp, vp, vp, u64, C.c_double, u64, u64, u64p,
                                   C.POINTER(C.c_double), vp]),
     "spmvk_dot_f64": (cint, [vp, vp, u64, vp, vp]),
+    "spmvk_cg_update_f64": (cint, [u64, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvk_cg_direction_f64": (cint, [u64, vp, vp, vp, vp, vp]),
     "spmvk_gen_random_vector": (None, [u64, u64, vp]),
     "spmvk_gen_stencil": (u64, [cint, u64, vp, vp, vp]),
     "spmvk_gen_powerlaw": (u64, [u64, u64, vp, vp, vp]),

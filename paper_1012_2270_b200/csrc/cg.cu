@@ -111,6 +111,14 @@ __global__ void __launch_bounds__(kDotThreads) cg_init(uint64_t n, const double*
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// Per-thread partials buffer of the fixed-grid dots (stream-ordered reuse:
+// calls issued from one host thread must share one stream).
+DevBuf<double>& dot_scratch() {
+  static thread_local DevBuf<double> part;
+  if (part.n < (uint64_t)kDotBlocks) part.alloc(kDotBlocks);
+  return part;
+}
+
 }  // namespace
 }  // namespace spmvk
 
@@ -121,12 +129,34 @@ extern "C" {
 int spmvk_dot_f64(const double* a, const double* b, uint64_t n, double* out_dev, void* stream) {
   return guarded([&] {
     cudaStream_t s = as_stream(stream);
-    DevBuf<double> part(kDotBlocks);
+    DevBuf<double>& part = dot_scratch();
     dot_partials<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, part.p);
     SPMVK_LAUNCH("dot_partials");
     dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, out_dev);
     SPMVK_LAUNCH("dot_finish");
-    SPMVK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int spmvk_cg_update_f64(uint64_t n, const double* rr, const double* pap, const double* p,
+                        const double* q, double* x, double* r, double* rr_new, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    DevBuf<double>& part = dot_scratch();
+    cg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, rr, pap, p, q, x, r, part.p);
+    SPMVK_LAUNCH("cg_update");
+    dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, rr_new);
+    SPMVK_LAUNCH("dot_finish");
+  });
+}
+
+int spmvk_cg_direction_f64(uint64_t n, const double* r, double* p, double* rr,
+                           const double* rr_new, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    cg_direction<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, p, rr, rr_new);
+    SPMVK_LAUNCH("cg_direction");
+    copy_scalar<<<1, 1, 0, s>>>(rr_new, rr);
+    SPMVK_LAUNCH("copy_scalar");
   });
 }
 

@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 #include <mutex>
+#include <vector>
 
 #include "../../include/spmvk.h"
 
@@ -215,6 +216,9 @@ struct spmvk_rgcsr {
   spmvk::DevBuf<uint32_t> long_rows;
   uint64_t n_long = 0;
   uint32_t long_cut = 128;
+  // Pipelined host-span SpMV: x column range [min, max] of each row chunk.
+  mutable std::vector<unsigned> chunk_cols;
+  mutable uint32_t chunk_rows = 0;
 };
 
 namespace spmvk {

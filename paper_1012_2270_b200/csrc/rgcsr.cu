@@ -371,12 +371,125 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   }
 }
 
+bool pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Pipelined host-span SpMV: x goes up in kPipeChunks pieces on one copy
+// stream, each 1/kPipeChunks of the rows runs as soon as the x range it reads
+// (precomputed per chunk from its first / last slot columns) has landed, and
+// its y slice goes down on a second copy stream while later chunks compute.
+// The PCIe transfers in both directions and the SpMV overlap; y is bitwise the
+// one-launch result (same kernel, same per-row order).  Needs pinned host x/y.
+constexpr int kPipeChunks = 16;
+
+struct PipeStage {
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+  cudaEvent_t ex[kPipeChunks], ey[kPipeChunks];
+  bool ready = false;
+  void ensure() {
+    if (ready) return;
+    for (auto& st : s) SPMVK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (int i = 0; i < kPipeChunks; ++i) {
+      SPMVK_CUDA(cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming));
+      SPMVK_CUDA(cudaEventCreateWithFlags(&ey[i], cudaEventDisableTiming));
+    }
+    ready = true;
+  }
+  ~PipeStage() {
+    if (!ready) return;
+    for (int i = 0; i < kPipeChunks; ++i) {
+      cudaEventDestroy(ex[i]);
+      cudaEventDestroy(ey[i]);
+    }
+    for (auto st : s) cudaStreamDestroy(st);
+  }
+};
+
+PipeStage& pipe_stage() {
+  static thread_local PipeStage p;
+  return p;
+}
+
+template <class T>
+bool spmv_host_pipelined(const spmvk_rgcsr* h, const T* x, T* y, HostStage& st) {
+  const uint64_t rows = h->rows, cols = h->cols;
+  if (h->n_long || rows < (1u << 16) || cols < (1u << 16) || !pinned(x) || !pinned(y))
+    return false;
+  const uint32_t chunk_rows =
+      static_cast<uint32_t>(((rows + kPipeChunks - 1) / kPipeChunks + 255) / 256 * 256);
+  const uint32_t nchunks = static_cast<uint32_t>((rows + chunk_rows - 1) / chunk_rows);
+  {
+    std::lock_guard<std::mutex> lk(h->part_mu);
+    if (h->chunk_rows != chunk_rows) {
+      DevBuf<unsigned> d(2 * nchunks);
+      std::vector<unsigned> init(2 * nchunks);
+      for (uint32_t k = 0; k < nchunks; ++k) init[2 * k] = 0xffffffffu, init[2 * k + 1] = 0;
+      SPMVK_CUDA(cudaMemcpy(d.p, init.data(), 8 * nchunks, cudaMemcpyHostToDevice));
+      chunk_column_ranges<<<persistent_grid((rows + 255) / 256, 8), 256>>>(
+          static_cast<uint32_t>(rows), static_cast<uint32_t>(h->group_size), chunk_rows,
+          h->group_pointers.p, h->row_lengths.p, h->columns.p, d.p);
+      SPMVK_LAUNCH("chunk_column_ranges");
+      h->chunk_cols.resize(2 * nchunks);
+      SPMVK_CUDA(cudaMemcpy(h->chunk_cols.data(), d.p, 8 * nchunks, cudaMemcpyDeviceToHost));
+      h->chunk_rows = chunk_rows;
+    }
+  }
+  PipeStage& ps = pipe_stage();
+  ps.ensure();
+  const uint64_t xchunk = (cols + kPipeChunks - 1) / kPipeChunks;
+  T* dx = reinterpret_cast<T*>(st.x.p);
+  T* dy = reinterpret_cast<T*>(st.y.p);
+  for (int c = 0; c < kPipeChunks; ++c) {
+    const uint64_t b = c * xchunk, e = std::min<uint64_t>(cols, b + xchunk);
+    if (b < e)
+      SPMVK_CUDA(cudaMemcpyAsync(dx + b, x + b, (e - b) * sizeof(T), cudaMemcpyHostToDevice,
+                                 ps.s[0]));
+    SPMVK_CUDA(cudaEventRecord(ps.ex[c], ps.s[0]));
+  }
+  const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
+  const int sh = pow2_shift(h->group_size);
+  constexpr bool f64 = sizeof(T) == 8;
+  auto kern = f64 ? rgcsr_spmv_lite_range<T, 8, 5> : rgcsr_spmv_lite_range<T, 4, 8>;
+  int per_sm = 0;
+  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  for (uint32_t k = 0; k < nchunks; ++k) {
+    const unsigned cmax = h->chunk_cols[2 * k + 1];
+    const int need = h->chunk_cols[2 * k] > cmax ? 0 : static_cast<int>(cmax / xchunk);
+    SPMVK_CUDA(cudaStreamWaitEvent(ps.s[1], ps.ex[std::min(need, kPipeChunks - 1)], 0));
+    const uint32_t t0 = k * (chunk_rows / 256);
+    const uint32_t t1 = std::min<uint32_t>(static_cast<uint32_t>((rows + 255) / 256),
+                                           t0 + chunk_rows / 256);
+    kern<<<persistent_grid(t1 - t0, per_sm > 0 ? per_sm : 1), 256, 0, ps.s[1]>>>(
+        t0, t1, static_cast<uint32_t>(rows), G, sh, h->group_pointers.p, h->row_lengths.p,
+        reinterpret_cast<const T*>(h->values.p), h->columns.p, dx, dy);
+    SPMVK_LAUNCH("rgcsr_spmv_lite_range");
+    SPMVK_CUDA(cudaEventRecord(ps.ey[k], ps.s[1]));
+    SPMVK_CUDA(cudaStreamWaitEvent(ps.s[2], ps.ey[k], 0));
+    const uint64_t r0 = static_cast<uint64_t>(k) * chunk_rows;
+    const uint64_t r1 = std::min<uint64_t>(rows, r0 + chunk_rows);
+    SPMVK_CUDA(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost,
+                               ps.s[2]));
+  }
+  SPMVK_CUDA(cudaStreamSynchronize(ps.s[2]));
+  return true;
+}
+
 template <class T>
 void spmv_host(const spmvk_rgcsr* h, const T* x, uint64_t nx, T* y, uint64_t ny,
                uint64_t* madds) {
   check_spmv_args<T>(h, nx, ny);
   HostStage& st = host_stage();
   st.reserve(nx * sizeof(T), ny * sizeof(T));
+  if (spmv_host_pipelined<T>(h, x, y, st)) {
+    if (madds) *madds = h->nnz;
+    return;
+  }
   if (nx) SPMVK_CUDA(cudaMemcpyAsync(st.x.p, x, nx * sizeof(T), cudaMemcpyHostToDevice, st.stream));
   launch_spmv<T, false>(h, reinterpret_cast<const T*>(st.x.p), reinterpret_cast<T*>(st.y.p),
                         nullptr, T(0), st.stream);

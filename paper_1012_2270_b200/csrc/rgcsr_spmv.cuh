@@ -109,14 +109,13 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
 // budget of MINB resident CTAs per SM.  Full occupancy (64 warps / SM) gives
 // the memory system the most independent requests; a predicated last batch
 // avoids serialised single-slot round trips on short rows and tails.
-template <class T, bool kScaled, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
-    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
-    const uint32_t* __restrict__ lens, const T* __restrict__ values,
-    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  const uint32_t ntiles = (rows + 255) / 256;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+template <class T, bool kScaled, int U>
+__device__ __forceinline__ void lite_tiles(
+    uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     const uint32_t r = tile * 256 + threadIdx.x;
     if (r >= rows) continue;
     const uint32_t len = lens[r];
@@ -163,6 +162,46 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     }
     y[r] = acc;
     if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+}
+
+template <class T, bool kScaled, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  lite_tiles<T, kScaled, U>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns,
+                            x, y, x_next, scale, long_cut);
+}
+
+// Same kernel over the 256-row tiles [tile_begin, tile_end) only: the unit of
+// the pipelined host-span SpMV (H2D of x, row chunks and D2H of y overlap).
+template <class T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite_range(
+    uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y) {
+  lite_tiles<T, false, U>(tile_begin, tile_end, rows, G, g_shift, gp, lens, values, columns, x, y,
+                          nullptr, T(0), 0xffffffffu);
+}
+
+// Per row chunk of `chunk_rows` rows: the smallest first-slot column and the
+// largest last-slot column (columns increase along a row), i.e. the x range
+// the chunk reads.  out[2k] = min, out[2k+1] = max (min > max if empty).
+__global__ void chunk_column_ranges(uint32_t rows, uint32_t G, uint32_t chunk_rows,
+                                    const uint32_t* __restrict__ gp,
+                                    const uint32_t* __restrict__ lens,
+                                    const uint32_t* __restrict__ columns,
+                                    unsigned* __restrict__ out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t len = lens[r];
+    if (!len) continue;
+    const uint32_t g = r / G, s = min(G, rows - g * G), base = gp[g] + (r - g * G);
+    const uint32_t k = r / chunk_rows;
+    atomicMin(out + 2 * k, columns[base]);
+    atomicMax(out + 2 * k + 1, columns[base + (len - 1) * s]);
   }
 }
 

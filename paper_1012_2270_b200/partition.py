@@ -181,6 +181,80 @@ class HaloIteratedSpmv:
         self.cur = 1 - self.cur
 
 
+def distributed_cg(slab: Slab, world: int, num_cols: int, b, ops, all_gather, all_reduce,
+                   tol: float = 1e-10, max_iter: int = 1000, check_every: int = 10):
+    """Conjugate gradients over row slabs (SURVEY §8f-4 on top of the §8e
+    partition): every rank owns its rows of A, x, r, p; p is all-gathered
+    before each SpMV and the two dot products per iteration are all-reduced
+    scalars that never leave the device.
+
+    ``ops`` supplies the slab-local kernels (``spmv(p_full, q)``,
+    ``dot(a, b, out)``, ``update(rr, pap, p, q, x, r, rr_new)``,
+    ``direction(r, p, rr, rr_new)`` — GpuCgOps wraps the C-ABI; the gloo
+    tests pass a numpy stand-in).  Returns (x_slab, iterations, rel_residual)."""
+    import torch
+    n = slab.rows
+    S = slab.pad_rows
+    dev, dt = b.device, b.dtype
+    x = torch.zeros(max(n, 1), dtype=dt, device=dev)
+    r = b.clone() if n else torch.zeros(1, dtype=dt, device=dev)
+    p_local = torch.zeros(S, dtype=dt, device=dev)
+    p_local[:n] = r[:n]
+    p_full = torch.zeros(S * world, dtype=dt, device=dev)
+    q = torch.zeros(max(n, 1), dtype=dt, device=dev)
+    sc = torch.zeros(4, dtype=dt, device=dev)  # rr, pap, rr_new, bb
+    rr, pap, rrn, bb = (sc[i:i + 1] for i in range(4))
+    ops.dot(b[:n], b[:n], bb)
+    ops.dot(r[:n], r[:n], rr)
+    all_reduce(sc[0:1])
+    all_reduce(sc[3:4])
+    bnorm = float(bb.item()) ** 0.5
+    res = (float(rr.item()) ** 0.5) / (bnorm or 1.0)
+    k = 0
+    while k < max_iter and res > tol:
+        all_gather(p_full, p_local)
+        ops.spmv(p_full[:num_cols], q[:n])
+        ops.dot(p_local[:n], q[:n], pap)
+        all_reduce(pap)
+        ops.update(rr, pap, p_local[:n], q[:n], x[:n], r[:n], rrn)
+        all_reduce(rrn)
+        ops.direction(r[:n], p_local[:n], rr, rrn)
+        k += 1
+        if k % check_every == 0 or k == max_iter:
+            res = (float(rr.item()) ** 0.5) / (bnorm or 1.0)
+    return x[:n], k, res
+
+
+class GpuCgOps:
+    """distributed_cg's slab kernels through the C-ABI (fp64, one stream)."""
+
+    def __init__(self, a, stream: int):
+        from ._lib import lib
+        from . import spmvkit as sk
+        self.a, self.s, self.L, self.sk = a, stream or None, lib(), sk
+
+    def _ok(self, rc):
+        if rc:
+            self.sk._check(rc)
+
+    def spmv(self, p_full, q):
+        self._ok(self.L.spmvk_rgcsr_spmv_f64(self.a._h, p_full.data_ptr(), p_full.numel(),
+                                             q.data_ptr(), q.numel(), self.s))
+
+    def dot(self, a, b, out):
+        self._ok(self.L.spmvk_dot_f64(a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),
+                                      self.s))
+
+    def update(self, rr, pap, p, q, x, r, rrn):
+        self._ok(self.L.spmvk_cg_update_f64(p.numel(), rr.data_ptr(), pap.data_ptr(),
+                                            p.data_ptr(), q.data_ptr(), x.data_ptr(),
+                                            r.data_ptr(), rrn.data_ptr(), self.s))
+
+    def direction(self, r, p, rr, rrn):
+        self._ok(self.L.spmvk_cg_direction_f64(r.numel(), r.data_ptr(), p.data_ptr(),
+                                               rr.data_ptr(), rrn.data_ptr(), self.s))
+
+
 def torch_p2p(ops):
     """p2p callable for HaloIteratedSpmv over torch.distributed."""
     import torch.distributed as dist

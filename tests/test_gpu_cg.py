@@ -42,3 +42,29 @@ def test_dot_is_deterministic(cuda):
     o = out.cpu().numpy()
     assert len(set(o.tobytes()[k:k + 8] for k in range(0, 32, 8))) == 1
     assert abs(o[0] - float(np.dot(v.cpu().numpy(), w.cpu().numpy()))) < 1e-9 * abs(o[0]) + 1e-9
+
+
+def test_distributed_cg_world1_nccl_matches_single_gpu_solver(cuda, tmp_path):
+    """partition.distributed_cg over NCCL at world size 1 runs the same kernels
+    in the same order as spmvk_cg_solve_f64: after K iterations x is bitwise equal."""
+    import torch.distributed as dist
+    from paper_1012_2270_b200 import partition as part
+    om = orc.stencil(7, 32)
+    a = sk.build_rgcsr(triplets(om), 32)
+    b = torch.from_numpy(orc.random_vector(om.rows, 3)).cuda()
+    x1, it1, _ = sk.cg(a, b, tol=0.0, max_iter=25, check_every=1000)
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        s = torch.cuda.current_stream().cuda_stream
+        slab = part.slab_bounds(om.rows, 32, 1)[0]
+        x2, it2, _ = part.distributed_cg(
+            slab, 1, om.cols, b, part.GpuCgOps(a, s),
+            lambda o, i: dist.all_gather_into_tensor(o, i), lambda t: dist.all_reduce(t),
+            tol=0.0, max_iter=25, check_every=1000)
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    assert it1 == it2 == 25
+    assert torch.equal(x1.view(torch.int64), x2.view(torch.int64))

@@ -218,3 +218,21 @@ def test_scaled_iteration_fused(cuda, k2):
     want = orc.spmv_rgcsr(orc.build_rgcsr(om, 32), x.cpu().numpy())[0]
     assert bitwise(y.cpu().numpy(), want)
     assert bitwise(xn.cpu().numpy(), want * 0.0625)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("kind,n", [(27, 64), (7, 96), (5, 512)])
+def test_pipelined_host_span_equals_device(cuda, prec, kind, n):
+    """Pinned host x/y take the pipelined path (chunked H2D / SpMV / D2H on
+    three streams); pageable memory takes the single-launch path.  Both must be
+    bitwise the device-resident y."""
+    dt = np.float64 if prec == 8 else np.float32
+    a = sk.build_rgcsr(sk.CsrMatrix.stencil(kind, n), 32, prec)
+    xh = orc.random_vector(a.num_cols, 2).astype(dt)
+    want = sk.spmv_rgcsr(a, dev(xh)).cpu().numpy()
+    xp = torch.from_numpy(xh).pin_memory()
+    yp = torch.empty(a.num_rows, dtype=xp.dtype).pin_memory()
+    for _ in range(2):
+        sk.spmv_rgcsr(a, xp.numpy(), yp.numpy())
+        assert bitwise(yp.numpy(), want)
+    assert bitwise(sk.spmv_rgcsr(a, xh), want)

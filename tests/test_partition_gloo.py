@@ -140,3 +140,71 @@ def test_iterated_distributed_equals_single_process(world, mode):
     for _ in range(steps):
         x = orc.spmv_rgcsr(full, x)[0] * 0.0625
     assert got.tobytes() == x.tobytes()
+
+
+class NumpyCgOps:
+    """CPU stand-in for the slab kernels of partition.distributed_cg."""
+
+    def __init__(self, a):
+        self.a = a
+
+    def spmv(self, p_full, q):
+        q.copy_(torch.from_numpy(orc.spmv_rgcsr(self.a, p_full.numpy())[0]))
+
+    def dot(self, a, b, out):
+        out.fill_(float(np.dot(a.numpy(), b.numpy())))
+
+    def update(self, rr, pap, p, q, x, r, rrn):
+        alpha = float(rr) / float(pap)
+        x += alpha * p
+        r -= alpha * q
+        rrn.fill_(float(torch.dot(r, r)))
+
+    def direction(self, r, p, rr, rrn):
+        p.copy_(r + (float(rrn) / float(rr)) * p)
+        rr.copy_(rrn)
+
+
+def _cg_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = orc.stencil(7, 10)
+    slabs = part.slab_bounds(m.rows, 32, world)
+    me = slabs[rank]
+    a = orc.build_rgcsr(slab_csr(m, me.row_begin, me.row_end), 32)
+    b = torch.from_numpy(orc.random_vector(m.rows, 4)[me.row_begin:me.row_end].copy())
+    x, iters, res = part.distributed_cg(
+        me, world, m.cols, b, NumpyCgOps(a),
+        lambda o, i: dist.all_gather_into_tensor(o, i), lambda t: dist.all_reduce(t),
+        tol=1e-11, max_iter=500, check_every=1)
+    xs = [None] * world
+    dist.all_gather_object(xs, (me.row_begin, x.numpy(), iters, res))
+    if rank == 0:
+        full = np.empty(m.rows)
+        for r0, v, _, _ in xs:
+            full[r0:r0 + v.size] = v
+        out.put((full.tobytes(), iters, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_cg_solves(world):
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    xb, iters, res = q.get(timeout=180)
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    x = np.frombuffer(xb, np.float64)
+    m = orc.stencil(7, 10)
+    A = sp.csr_matrix((m.val, m.col.astype(np.int64), m.rp.astype(np.int64)), shape=(m.rows, m.cols))
+    bh = orc.random_vector(m.rows, 4)
+    assert res <= 1e-11 and iters < 500
+    assert np.linalg.norm(x - spl.spsolve(A.tocsc(), bh)) <= 1e-8 * np.linalg.norm(x)
