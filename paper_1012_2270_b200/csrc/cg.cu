@@ -189,23 +189,65 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
     double res = bnorm > 0 ? std::sqrt(h[0]) / bnorm : std::sqrt(h[0]);
     uint64_t k = 0;
     if (check_every == 0) check_every = 10;
-    while (k < max_iter && res > tol) {
-      if (spmvk_rgcsr_spmv_f64(a, p.p, n, q.p, n, s) != SPMVK_OK)
+    auto iteration = [&](cudaStream_t st) {
+      if (spmvk_rgcsr_spmv_f64(a, p.p, n, q.p, n, st) != SPMVK_OK)
         fail(SPMVK_ECUDA, std::string("cg spmv: ") + spmvk_last_error());
-      dot_partials<<<grid, kDotThreads, 0, s>>>(n, p.p, q.p, part.p);
-      dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, pap);
-      cg_update<<<grid, kDotThreads, 0, s>>>(n, rr, pap, p.p, q.p, x, r.p, part.p);
-      dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, rrn);
-      cg_direction<<<grid, kDotThreads, 0, s>>>(n, r.p, p.p, rr, rrn);
-      copy_scalar<<<1, 1, 0, s>>>(rrn, rr);
+      dot_partials<<<grid, kDotThreads, 0, st>>>(n, p.p, q.p, part.p);
+      dot_finish<<<1, kDotThreads, 0, st>>>(part.p, kDotBlocks, pap);
+      cg_update<<<grid, kDotThreads, 0, st>>>(n, rr, pap, p.p, q.p, x, r.p, part.p);
+      dot_finish<<<1, kDotThreads, 0, st>>>(part.p, kDotBlocks, rrn);
+      cg_direction<<<grid, kDotThreads, 0, st>>>(n, r.p, p.p, rr, rrn);
+      copy_scalar<<<1, 1, 0, st>>>(rrn, rr);
       SPMVK_LAUNCH("cg iteration");
-      ++k;
-      if (k % check_every == 0 || k == max_iter) {
-        SPMVK_CUDA(cudaMemcpyAsync(h, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
-        SPMVK_CUDA(cudaStreamSynchronize(s));
-        res = bnorm > 0 ? std::sqrt(h[0]) / bnorm : std::sqrt(h[0]);
+    };
+    auto read_res = [&](cudaStream_t st) {
+      SPMVK_CUDA(cudaMemcpyAsync(h, rr, sizeof(double), cudaMemcpyDeviceToHost, st));
+      SPMVK_CUDA(cudaStreamSynchronize(st));
+      res = bnorm > 0 ? std::sqrt(h[0]) / bnorm : std::sqrt(h[0]);
+    };
+    // check_every iterations are captured once as a CUDA graph (7 launches
+    // each) on a private stream ordered after the caller's, then replayed:
+    // same kernels, same order, so x is bitwise the eager loop's.
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    SPMVK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    SPMVK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SPMVK_CUDA(cudaEventRecord(ev, s));
+    SPMVK_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+    try {
+      if (check_every >= 2 && max_iter >= check_every && res > tol) {
+        SPMVK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (uint64_t i = 0; i < check_every; ++i) iteration(cs);
+        SPMVK_CUDA(cudaStreamEndCapture(cs, &graph));
+        SPMVK_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        while (k + check_every <= max_iter && res > tol) {
+          SPMVK_CUDA(cudaGraphLaunch(exec, cs));
+          k += check_every;
+          read_res(cs);
+        }
       }
+      while (k < max_iter && res > tol) {
+        iteration(cs);
+        ++k;
+        if (k % check_every == 0 || k == max_iter) read_res(cs);
+      }
+      SPMVK_CUDA(cudaEventRecord(ev, cs));
+      SPMVK_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      SPMVK_CUDA(cudaStreamSynchronize(cs));
+    } catch (...) {
+      cudaStreamEndCapture(cs, &graph);
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      cudaEventDestroy(ev);
+      cudaStreamDestroy(cs);
+      throw;
     }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(cs);
     SPMVK_CUDA(cudaStreamSynchronize(s));
     if (iters) *iters = k;
     if (rel_residual) *rel_residual = res;
