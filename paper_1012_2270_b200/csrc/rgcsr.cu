@@ -216,7 +216,13 @@ enum class K2 {
 // 8-deep batches at 40 warps / SM for fp64 (lite8), 4-deep at full occupancy
 // (64 warps / SM) for fp32 (lite).  Occupancy beats deeper per-thread
 // pipelines: every variant with prefetch buffers lost to it.
-K2 auto_k2(const spmvk_rgcsr*, bool f64) { return f64 ? K2::kLite8 : K2::kLite; }
+// Irregular matrices (rows beyond the long-row cut, e.g. the power-law
+// config) favour the row-prefetching `pipe` kernel in fp32
+// (profiles/r01_powerlaw.md: 1,070 vs 1,353 us).
+K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
+  if (f64) return K2::kLite8;
+  return h->n_long ? K2::kPipe : K2::kLite;
+}
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {
