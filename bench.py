@@ -13,9 +13,11 @@ ride along in ``variants``.
                   [--workload 27pt-128|5pt-1024|powerlaw-8M|7pt-512]
 
 N > 1 (torchrun, one rank per GPU): the matrix is cut into group-aligned row
-slabs (paper_1012_2270_b200.partition), each step is one slab SpMV plus the
-NCCL all-gather of the next x (x_{k+1} = y_k * 2^-4, fused into the SpMV
-epilogue), timed as the max over ranks; scaling "strong" (fixed matrix).
+slabs (paper_1012_2270_b200.partition), each step is one slab SpMV (with the
+next x = y_k * 2^-4 fused into its epilogue) plus the NCCL exchange of x —
+`--exchange halo` (default: only the column ranges each slab reads,
+point-to-point) or `allgather` (the whole vector) — timed as the max over
+ranks; scaling "strong" (fixed matrix).
 
 ``--impl reference`` times the reference's own CPU spmv_rgcsr (oracle/_ref:
 the unmodified reference compiled in place; the plain-C port when _ref is not
@@ -235,7 +237,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.distributed:
         from paper_1012_2270_b200 import partition
-        return partition.bench_distributed(args, METRIC, WORKLOADS)
+        return partition.bench_distributed(args, METRIC, WORKLOADS, ClockSampler, peaks(), rg_bytes)
 
     torch.cuda.set_device(0)
     assert lib().spmvk_init(0) == 0, sk._lib.last_error()
@@ -361,7 +363,7 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=10)
     ap.add_argument("--distributed", action="store_true",
                     help="use the row-slab + NCCL path even at world size 1 (under torchrun)")
-    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+    ap.add_argument("--exchange", default="halo", choices=["allgather", "halo"],
                     help="x exchange of the distributed iterated SpMV")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -265,8 +265,11 @@ def torch_p2p(ops):
 
 
 # ---------------------------------------------------------------- bench (N > 1)
-def bench_distributed(args, metric: str, workloads: dict):
-    """bench.py leg for torchrun N > 1: strong scaling of the iterated SpMV."""
+def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=None,
+                      rg_bytes=None):
+    """bench.py leg for torchrun N > 1: strong scaling of the iterated SpMV.
+    ``clock_cls`` / ``peaks`` / ``rg_bytes`` are bench.py's NVML clock sampler,
+    measured HBM peak and algorithmic-bytes function."""
     import torch
     import torch.distributed as dist
 
@@ -325,16 +328,57 @@ def bench_distributed(args, metric: str, workloads: dict):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    clocks = clock_cls(local) if clock_cls else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.__enter__()
     e0.record(stream)
     for _ in range(args.steps):
         it.step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if clocks:
+        clocks.__exit__(None, None, None)
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     tot_nnz = torch.tensor([nnz_local], device="cuda", dtype=torch.float64)
     dist.all_reduce(tot_nnz)
+
+    # kernel-only time of this rank's slab SpMV (roofline of the dominant kernel)
+    xs = (it.x[: a.num_cols] if exchange == "allgather" else it.x_current).clone()
+    ys = torch.empty(max(a.num_rows, 1), dtype=torch.float64, device="cuda")
+    xn = torch.empty_like(ys)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(min(args.steps, 200))]
+    for s_, e_ in kev:
+        s_.record(stream)
+        slab_spmv(xs, ys[: a.num_rows], xn[: a.num_rows])
+        e_.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = torch.tensor([sum(s_.elapsed_time(e_) for s_, e_ in kev) / len(kev)], device="cuda")
+    dist.all_reduce(kern_ms, op=dist.ReduceOp.MAX)
+    slab_bytes = (rg_bytes(a.info, 8) if rg_bytes else 0)
+
+    # e2e: every step each rank uploads its x slab from pinned host memory,
+    # runs the exchange + slab SpMV, and downloads its y slab
+    xh = torch.from_numpy(gen.random_vector(a.num_cols, 1)[me.row_begin:me.row_end].copy())
+    xh = xh.pin_memory()
+    yh = torch.empty(max(a.num_rows, 1), dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(stream):
+            cur = it.x if exchange == "allgather" else it.x[it.cur]
+            cur[me.row_begin:me.row_end].copy_(xh, non_blocking=True)
+        it.step()
+        with torch.cuda.stream(stream):
+            yh[: a.num_rows].copy_(it.y[: a.num_rows], non_blocking=True)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     # checksum of this rank's rows of the final iterate (bitwise across P: the
     # slab arrays are global slices and every row keeps the reference's order)
     xf = it.x[: a.num_cols] if exchange == "allgather" else it.x_current
@@ -347,6 +391,9 @@ def bench_distributed(args, metric: str, workloads: dict):
         step_ms = ms.item() / args.steps
         value = 2.0 * tot_nnz.item() / (step_ms * 1e-3) / 1e9
         halo = it.halo_entries() if exchange == "halo" else None
+        k_s = kern_ms.item() * 1e-3
+        achieved = slab_bytes / k_s / 1e9 if slab_bytes else None
+        peak, peak_kind = peaks if peaks else (None, None)
         print(json.dumps({
             "metric": metric, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -356,7 +403,19 @@ def bench_distributed(args, metric: str, workloads: dict):
                        "group_size": G,
                        "parallelism": f"row-slab x{world}, NCCL {exchange} of x",
                        "step": f"slab SpMV (+fused x_next = y/16) + {exchange} exchange",
-                       "halo_entries_rank0": halo},
+                       "halo_entries_rank0": halo,
+                       "l2": "per-rank slab streamed from HBM each step (no flush)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved and peak else None,
+                         "peak_kind": peak_kind, "bytes_per_launch": slab_bytes,
+                         "kernel_us": k_s * 1e6, "scope": "rank-0 slab SpMV, max over ranks",
+                         "traffic": None},
+            "e2e": {"value": 2.0 * tot_nnz.item() / e2e_s.item() / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": 8 * me.rows * world,
+                    "d2h_bytes_per_step": 8 * me.rows * world,
+                    "ms_per_step": e2e_s.item() * 1e3,
+                    "path": "per rank: pinned H2D of the x slab, exchange + slab SpMV, D2H of y"},
+            "clocks": clocks.summary() if clocks else None,
             "gpu_launches": args.steps,
             "x_bits_checksum": int(sums.sum().item()),
         }), flush=True)
