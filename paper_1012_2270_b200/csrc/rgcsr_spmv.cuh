@@ -109,13 +109,42 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
 // budget of MINB resident CTAs per SM.  Full occupancy (64 warps / SM) gives
 // the memory system the most independent requests; a predicated last batch
 // avoids serialised single-slot round trips on short rows and tails.
-template <class T, bool kScaled, int U>
+// Bulk L2 prefetch (cp.async.bulk.prefetch -> the TMA unit) of the contiguous
+// slot range of 256-row tile `tile`: its groups' slabs [gp[g0], gp[g1]).
+template <class T>
+__device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint32_t G,
+                                              uint32_t groups, const uint32_t* __restrict__ gp,
+                                              const T* __restrict__ values,
+                                              const uint32_t* __restrict__ columns) {
+  const uint32_t r0 = tile * 256;
+  if (r0 >= rows) return;
+  const uint32_t g0 = r0 / G, g1 = min(groups, (min(rows, r0 + 256) + G - 1) / G);
+  const uint64_t s0 = gp[g0], s1 = gp[g1];
+  if (s1 <= s0) return;
+  const uint64_t vb = (s0 * sizeof(T)) & ~15ull, ve = (s1 * sizeof(T) + 15) & ~15ull;
+  const uint64_t cb = (s0 * 4) & ~15ull, ce = (s1 * 4 + 15) & ~15ull;
+  const char* vbase = reinterpret_cast<const char*>(values);
+  const char* cbase = reinterpret_cast<const char*>(columns);
+  for (uint64_t o = vb; o < ve; o += 65536)
+    bulk_prefetch_l2(vbase + o, (uint32_t)min((uint64_t)65536, ve - o));
+  for (uint64_t o = cb; o < ce; o += 65536)
+    bulk_prefetch_l2(cbase + o, (uint32_t)min((uint64_t)65536, ce - o));
+}
+
+template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
 __device__ __forceinline__ void lite_tiles(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
     T* __restrict__ y, T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  if (kPrefetchL2 && threadIdx.x == 0) {
+    const uint32_t groups = (rows + G - 1) / G;
+    if (tile_begin + blockIdx.x < tile_end)
+      prefetch_tile<T>(tile_begin + blockIdx.x, rows, G, groups, gp, values, columns);
+  }
   for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
+    if (kPrefetchL2 && threadIdx.x == 0 && tile + gridDim.x < tile_end)
+      prefetch_tile<T>(tile + gridDim.x, rows, G, (rows + G - 1) / G, gp, values, columns);
     const uint32_t r = tile * 256 + threadIdx.x;
     if (r >= rows) continue;
     const uint32_t len = lens[r];
@@ -165,14 +194,14 @@ __device__ __forceinline__ void lite_tiles(
   }
 }
 
-template <class T, bool kScaled, int U, int MINB>
+template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles<T, kScaled, U>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns,
-                            x, y, x_next, scale, long_cut);
+  lite_tiles<T, kScaled, U, kPrefetchL2>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens,
+                                         values, columns, x, y, x_next, scale, long_cut);
 }
 
 // Same kernel over the 256-row tiles [tile_begin, tile_end) only: the unit of
