@@ -208,7 +208,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
   kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf, kLdg32, kLdgPf6,
-  kLite, kLite6, kLite8, kLite8Pf, kLitePf, kLite8Mp, kLiteMp
+  kLite, kLite6, kLite8, kLite8Pf, kLitePf
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -232,8 +232,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
       {"ldg8_pf", K2::kLdg8Pf}, {"ldg32", K2::kLdg32}, {"ldg_pf6", K2::kLdgPf6},
       {"lite", K2::kLite},     {"lite6", K2::kLite6}, {"lite8", K2::kLite8},
-      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf},
-      {"lite8_mp", K2::kLite8Mp},   {"lite_mp", K2::kLiteMp}};
+      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -377,8 +376,6 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
-    case K2::kLite8Mp: run(rgcsr_spmv_lite<T, kScaled, 8, 5, false, true>); break;
-    case K2::kLiteMp: run(rgcsr_spmv_lite<T, kScaled, 4, 8, false, true>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
   }
 }

@@ -131,7 +131,7 @@ __device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint
     bulk_prefetch_l2(cbase + o, (uint32_t)min((uint64_t)65536, ce - o));
 }
 
-template <class T, bool kScaled, int U, bool kPrefetchL2 = false, bool kMetaPf = false>
+template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
 __device__ __forceinline__ void lite_tiles(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
@@ -142,39 +142,16 @@ __device__ __forceinline__ void lite_tiles(
     if (tile_begin + blockIdx.x < tile_end)
       prefetch_tile<T>(tile_begin + blockIdx.x, rows, G, groups, gp, values, columns);
   }
-  // kMetaPf: the next tile's (row length, slot offset) are loaded while the
-  // current row runs, taking one dependent round trip off each row.
-  auto meta = [&](uint32_t t, uint32_t& l, uint32_t& o) {
-    const uint32_t rr = t * 256 + threadIdx.x;
-    l = 0;
-    o = 0;
-    if (t < tile_end && rr < rows) {
-      const uint32_t gg = g_shift >= 0 ? (rr >> g_shift) : rr / G;
-      l = lens[rr];
-      o = gp[gg] + (rr - gg * G);
-    }
-  };
-  uint32_t len_n = 0, off_n = 0;
-  if (kMetaPf) meta(tile_begin + blockIdx.x, len_n, off_n);
   for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     if (kPrefetchL2 && threadIdx.x == 0 && tile + gridDim.x < tile_end)
       prefetch_tile<T>(tile + gridDim.x, rows, G, (rows + G - 1) / G, gp, values, columns);
     const uint32_t r = tile * 256 + threadIdx.x;
-    uint32_t len, off;
-    if (kMetaPf) {
-      len = len_n;
-      off = off_n;
-      meta(tile + gridDim.x, len_n, off_n);
-      if (r >= rows) continue;
-    } else {
-      if (r >= rows) continue;
-      len = lens[r];
-      const uint32_t g0 = g_shift >= 0 ? (r >> g_shift) : r / G;
-      off = gp[g0] + (r - g0 * G);
-    }
+    if (r >= rows) continue;
+    const uint32_t len = lens[r];
     if (len > long_cut) continue;  // handled by rgcsr_spmv_long
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
     const uint32_t s = min(G, rows - g * G);
+    const uint32_t off = gp[g] + (r - g * G);
     const T* __restrict__ vp = values + off;
     const uint32_t* __restrict__ cp = columns + off;
     T acc = T(0);
@@ -217,15 +194,14 @@ __device__ __forceinline__ void lite_tiles(
   }
 }
 
-template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false, bool kMetaPf = false>
+template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles<T, kScaled, U, kPrefetchL2, kMetaPf>(0, (rows + 255) / 256, rows, G, g_shift, gp,
-                                                  lens, values, columns, x, y, x_next, scale,
-                                                  long_cut);
+  lite_tiles<T, kScaled, U, kPrefetchL2>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens,
+                                         values, columns, x, y, x_next, scale, long_cut);
 }
 
 // Same kernel over the 256-row tiles [tile_begin, tile_end) only: the unit of
