@@ -103,14 +103,9 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
   }
 }
 
-// Lean thread-per-row kernel built for occupancy: a CTA handles 256-row
-// tiles (CTA-stride), each thread walks its row in U-deep predicated batches
-// with 32-bit strided pointers (no prefetch buffers), so it fits the register
-// budget of MINB resident CTAs per SM.  Full occupancy (64 warps / SM) gives
-// the memory system the most independent requests; a predicated last batch
-// avoids serialised single-slot round trips on short rows and tails.
 // Bulk L2 prefetch (cp.async.bulk.prefetch -> the TMA unit) of the contiguous
 // slot range of 256-row tile `tile`: its groups' slabs [gp[g0], gp[g1]).
+// Used by the lite*_l2pf variants (measured slower; kept for the record).
 template <class T>
 __device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint32_t G,
                                               uint32_t groups, const uint32_t* __restrict__ gp,
@@ -131,6 +126,13 @@ __device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint
     bulk_prefetch_l2(cbase + o, (uint32_t)min((uint64_t)65536, ce - o));
 }
 
+// Lean thread-per-row kernel built for occupancy (the default K2): a CTA
+// handles 256-row tiles (CTA-stride), each thread walks its row in U-deep
+// batches with 32-bit strided pointers (no prefetch buffers, no cache-policy
+// registers), so it fits the register budget of MINB resident CTAs per SM.
+// Occupancy (40-64 warps / SM) gives the memory system the most independent
+// requests; a predicated last batch avoids serialised single-slot round trips
+// on short rows and tails.
 template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
 __device__ __forceinline__ void lite_tiles(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
