@@ -3,8 +3,12 @@
 // Every variant keeps the reference's per-row order of roundings
 // (rgcsr.hpp:87-93): acc = ((0 + v0*x0) + v1*x1) + ..., product and sum
 // rounded separately, so y is bitwise spmv_rgcsr's y.  They differ only in
-// how the group-interleaved slots reach the SMs:
+// how the group-interleaved slots reach the SMs (measured comparison in
+// DESIGN.md §3 and profiles/r01_k2_sweep*.md):
 //
+//  * rgcsr_spmv_lite — the default: register-lean thread per row at high
+//    occupancy (below); rgcsr_spmv_long takes the rows past the long-row cut.
+//  * rgcsr_spmv_pipe — row- and batch-pipelined thread per row.
 //  * rgcsr_spmv_ldg  — thread per row, slots streamed straight from HBM with
 //    L1-no-allocate / L2-evict-first loads, U-deep batches; with kPrefetch the
 //    next batch's loads are issued before the current batch's x gathers.
