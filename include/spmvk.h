@@ -145,6 +145,9 @@ int spmvk_rgcsr_get_info(const spmvk_rgcsr* h, spmvk_rgcsr_info* info);
  * slots / slots / num_groups+1 / num_rows elements (any may be NULL). */
 int spmvk_rgcsr_download(const spmvk_rgcsr* h, void* values, uint32_t* columns,
                          uint32_t* group_pointers, uint32_t* row_lengths);
+/* to_triplets(RgcsrMatrix) (spmvkit/rgcsr.hpp:107-123): the real slots of
+ * every row back to a canonical device CSR (values widened to double). */
+int spmvk_rgcsr_to_csr(const spmvk_rgcsr* h, void* stream, spmvk_csr** out);
 /* spmv_rgcsr(a, x, y) (spmvkit/rgcsr.hpp:75-97): y = A x with x, y in HBM.
  * EINVAL "spmv_rgcsr: dimension mismatch" unless nx == num_cols and
  * ny == num_rows, or if the handle's precision differs from the entry point. */
@@ -206,6 +209,10 @@ int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info);
  * rows/columns/values (coo_nnz); any pointer may be NULL. */
 int spmvk_hybrid_download(const spmvk_hybrid* h, void* ell_values, uint32_t* ell_columns,
                           uint32_t* coo_rows, uint32_t* coo_columns, void* coo_values);
+/* to_triplets(HybridMatrix) (spmvkit/ellpack.hpp:219-240): ELL rows through
+ * the ell_row_length recount (:55-78) plus the COO overflow, as a canonical
+ * device CSR (double values). */
+int spmvk_hybrid_to_csr(const spmvk_hybrid* h, void* stream, spmvk_csr** out);
 /* spmv_hybrid (spmvkit/ellpack.hpp:205-210) = spmv_ellpack (:110-123) then
  * spmv_coo (:132-141), fused in one kernel; y is bitwise the reference's. */
 int spmvk_hybrid_spmv_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,

@@ -60,6 +60,8 @@ SIGNATURES = {
     "spmvk_rgcsr_build_rows": (cint, [vp, u64, u64, u64, cint, vp, C.POINTER(vp)]),
     "spmvk_rgcsr_get_info": (cint, [vp, C.POINTER(RgcsrInfo)]),
     "spmvk_rgcsr_download": (cint, [vp, vp, vp, vp, vp]),
+    "spmvk_rgcsr_to_csr": (cint, [vp, vp, C.POINTER(vp)]),
+    "spmvk_hybrid_to_csr": (cint, [vp, vp, C.POINTER(vp)]),
     "spmvk_rgcsr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
     "spmvk_rgcsr_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),
     "spmvk_rgcsr_spmv_scaled_f64": (cint, [vp, vp, u64, vp, u64, vp, C.c_double, vp]),

@@ -217,6 +217,10 @@ void csr_spmv(const spmvk_csr* a, const T* x, uint64_t nx, T* y, uint64_t ny, cu
 
 }  // namespace
 
+spmvk_csr* new_csr(uint64_t rows, uint64_t cols, uint64_t nnz, int val_prec) {
+  return make_csr(rows, cols, nnz, val_prec);
+}
+
 // row lengths -> uint32 (used by rgcsr / hybrid builders)
 __global__ void csr_row_lengths(uint64_t r0, uint64_t rows, const uint32_t* __restrict__ rp,
                                 uint32_t* __restrict__ lens) {

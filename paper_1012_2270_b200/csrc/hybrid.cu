@@ -184,6 +184,101 @@ __global__ void ell_nnz_recount(uint64_t rows, uint32_t k1, const T* __restrict_
   if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
 }
 
+// ------------------------------------------------------------ to_triplets
+// ellpack.hpp:219-240: ELL rows through the ell_row_length recount, then the
+// COO overflow; per row the ELL columns precede the COO ones, so the result is
+// already canonical (the reference re-sorts).
+template <class T>
+__device__ __forceinline__ uint32_t ell_len_of(uint64_t rows, uint32_t k1, const T* ev,
+                                               const uint32_t* ec, uint64_t r) {
+  uint32_t len = 0, prev = 0;
+  for (uint32_t slot = 0; slot < k1; ++slot) {
+    const uint64_t idx = (uint64_t)slot * rows + r;
+    const uint32_t c = ec[idx];
+    if (slot > 0 && c <= prev) break;
+    if (slot == 0 && c == 0 && ev[idx] == T(0)) {
+      const bool real_successor = k1 > 1 && ec[rows + r] > 0;
+      if (!real_successor) break;
+    }
+    ++len;
+    prev = c;
+  }
+  return len;
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t* a, uint64_t n, uint32_t v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <class T>
+__global__ void hybrid_row_counts(uint64_t rows, uint32_t k1, const T* __restrict__ ev,
+                                  const uint32_t* __restrict__ ec, uint64_t coo,
+                                  const uint32_t* __restrict__ cr, uint64_t* __restrict__ cnt) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lb = lower_bound_u32(cr, coo, (uint32_t)r);
+    const uint64_t ub = lower_bound_u32(cr, coo, (uint32_t)r + 1);
+    cnt[r] = ell_len_of(rows, k1, ev, ec, r) + (ub - lb);
+  }
+}
+
+template <class T>
+__global__ void hybrid_gather_rows(uint64_t rows, uint32_t k1, uint64_t nnz,
+                                   const T* __restrict__ ev, const uint32_t* __restrict__ ec,
+                                   uint64_t coo, const uint32_t* __restrict__ cr,
+                                   const uint32_t* __restrict__ cc, const T* __restrict__ cv,
+                                   const uint64_t* __restrict__ off, uint32_t* __restrict__ rp,
+                                   uint32_t* __restrict__ col, double* __restrict__ val) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t o = off[r];
+    rp[r] = (uint32_t)o;
+    if (r + 1 == rows) rp[rows] = (uint32_t)nnz;
+    const uint32_t n = ell_len_of(rows, k1, ev, ec, r);
+    for (uint32_t j = 0; j < n; ++j, ++o) {
+      col[o] = ec[(uint64_t)j * rows + r];
+      val[o] = static_cast<double>(ev[(uint64_t)j * rows + r]);
+    }
+    const uint64_t lb = lower_bound_u32(cr, coo, (uint32_t)r);
+    for (uint64_t i = lb; i < coo && cr[i] == r; ++i, ++o) {
+      col[o] = cc[i];
+      val[o] = static_cast<double>(cv[i]);
+    }
+  }
+}
+
+template <class T>
+spmvk_csr* hybrid_to_csr(const spmvk_hybrid* h, cudaStream_t s) {
+  const unsigned grid = persistent_grid((h->rows + 255) / 256, 8);
+  DevBuf<uint64_t> off(h->rows);
+  const T* ev = reinterpret_cast<const T*>(h->ell_values.p);
+  const T* cv = reinterpret_cast<const T*>(h->coo_values.p);
+  uint64_t total = 0;
+  if (h->rows) {
+    hybrid_row_counts<T><<<grid, 256, 0, s>>>(h->rows, static_cast<uint32_t>(h->k1), ev,
+                                              h->ell_columns.p, h->coo, h->coo_rows.p, off.p);
+    SPMVK_LAUNCH("hybrid_row_counts");
+    total = exclusive_scan_u64(off.p, h->rows, s);
+  }
+  std::unique_ptr<spmvk_csr> c(new_csr(h->rows, h->cols, total, SPMVK_F64));
+  if (h->rows) {
+    hybrid_gather_rows<T><<<grid, 256, 0, s>>>(h->rows, static_cast<uint32_t>(h->k1), total, ev,
+                                               h->ell_columns.p, h->coo, h->coo_rows.p,
+                                               h->coo_columns.p, cv, off.p, c->row_ptr.p,
+                                               c->col.p, reinterpret_cast<double*>(c->val.p));
+    SPMVK_LAUNCH("hybrid_gather_rows");
+  } else {
+    SPMVK_CUDA(cudaMemsetAsync(c->row_ptr.p, 0, 4, s));
+  }
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  return c.release();
+}
+
 // ------------------------------------------------------------ K4/K5: SpMV
 // One CTA-tile of 256 rows: (1) thread per row walks its K1 ELL slots (pads
 // included, as spmv_ellpack does); (2) the tile's COO range is staged in
@@ -421,6 +516,14 @@ int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info) {
     info->bytes_single = slots * 4 + words * 4;
     info->bytes_double = slots * 8 + words * 4;
     info->precision = h->prec;
+  });
+}
+
+int spmvk_hybrid_to_csr(const spmvk_hybrid* h, void* stream, spmvk_csr** out) {
+  return guarded([&] {
+    if (!h || !out) fail(SPMVK_EINVAL, "null argument");
+    *out = h->prec == SPMVK_F64 ? hybrid_to_csr<double>(h, as_stream(stream))
+                                : hybrid_to_csr<float>(h, as_stream(stream));
   });
 }
 

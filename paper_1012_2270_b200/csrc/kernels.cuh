@@ -8,6 +8,9 @@ namespace spmvk {
 __global__ void csr_row_lengths(uint64_t r0, uint64_t rows, const uint32_t* __restrict__ rp,
                                 uint32_t* __restrict__ lens);
 
+// An empty device CSR handle with arrays allocated (row_ptr rows+1, nnz entries).
+spmvk_csr* new_csr(uint64_t rows, uint64_t cols, uint64_t nnz, int val_prec);
+
 // max / min row length over rows [r0, r1) (synchronous)
 void row_length_range(const spmvk_csr* a, uint64_t r0, uint64_t r1, unsigned* mx, unsigned* mn,
                       cudaStream_t s);

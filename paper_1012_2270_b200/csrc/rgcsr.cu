@@ -54,6 +54,36 @@ __global__ void long_row_scatter(uint64_t rows, uint32_t cut, const uint32_t* __
     if (lens[r] > cut) out[pos[r]] = (uint32_t)r;
 }
 
+// ------------------------------------------------------------ to_triplets
+// rgcsr.hpp:107-123: every row's real slots, in slot order, back to entries
+// (values widened to double).  Thread per row into a scanned CSR.
+__global__ void lens_u64(uint64_t rows, const uint32_t* __restrict__ lens,
+                         uint64_t* __restrict__ out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    out[r] = lens[r];
+}
+
+template <class T>
+__global__ void rgcsr_gather_rows(uint64_t rows, uint64_t G, uint64_t nnz,
+                                  const uint32_t* __restrict__ gp,
+                                  const uint32_t* __restrict__ lens, const T* __restrict__ values,
+                                  const uint32_t* __restrict__ columns,
+                                  const uint64_t* __restrict__ off, uint32_t* __restrict__ rp,
+                                  uint32_t* __restrict__ col, double* __restrict__ val) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = r / G, s = min(G, rows - g * G);
+    const uint64_t base = gp[g] + (r - g * G), o = off[r];
+    rp[r] = (uint32_t)o;
+    if (r + 1 == rows) rp[rows] = (uint32_t)nnz;
+    for (uint32_t j = 0; j < lens[r]; ++j) {
+      col[o + j] = columns[base + j * s];
+      val[o + j] = static_cast<double>(values[base + j * s]);
+    }
+  }
+}
+
 // Rows longer than this go to the warp-per-row kernel (spmvk_set_long_row_cut).
 std::atomic<uint32_t>& long_cut_slot() {
   static std::atomic<uint32_t> v{kLongRow};
@@ -547,6 +577,36 @@ int spmvk_rgcsr_get_info(const spmvk_rgcsr* h, spmvk_rgcsr_info* info) {
     info->bytes_single = h->slots * 4 + words * 4;
     info->bytes_double = h->slots * 8 + words * 4;
     info->precision = h->prec;
+  });
+}
+
+int spmvk_rgcsr_to_csr(const spmvk_rgcsr* h, void* stream, spmvk_csr** out) {
+  return guarded([&] {
+    if (!h || !out) fail(SPMVK_EINVAL, "null argument");
+    cudaStream_t s = as_stream(stream);
+    std::unique_ptr<spmvk_csr> c(new_csr(h->rows, h->cols, h->nnz, SPMVK_F64));
+    if (h->rows) {
+      DevBuf<uint64_t> off(h->rows);
+      const unsigned grid = persistent_grid((h->rows + 255) / 256, 8);
+      lens_u64<<<grid, 256, 0, s>>>(h->rows, h->row_lengths.p, off.p);
+      SPMVK_LAUNCH("lens_u64");
+      exclusive_scan_u64(off.p, h->rows, s);
+      if (h->prec == SPMVK_F64)
+        rgcsr_gather_rows<double><<<grid, 256, 0, s>>>(
+            h->rows, h->group_size, h->nnz, h->group_pointers.p, h->row_lengths.p,
+            reinterpret_cast<const double*>(h->values.p), h->columns.p, off.p, c->row_ptr.p,
+            c->col.p, reinterpret_cast<double*>(c->val.p));
+      else
+        rgcsr_gather_rows<float><<<grid, 256, 0, s>>>(
+            h->rows, h->group_size, h->nnz, h->group_pointers.p, h->row_lengths.p,
+            reinterpret_cast<const float*>(h->values.p), h->columns.p, off.p, c->row_ptr.p,
+            c->col.p, reinterpret_cast<double*>(c->val.p));
+      SPMVK_LAUNCH("rgcsr_gather_rows");
+    } else {
+      SPMVK_CUDA(cudaMemsetAsync(c->row_ptr.p, 0, 4, s));
+    }
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    *out = c.release();
   });
 }
 

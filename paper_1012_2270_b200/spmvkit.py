@@ -490,6 +490,20 @@ def cg(a: RgcsrMatrix, b, x0=None, tol: float = 1e-10, max_iter: int = 1000,
     return x, it.value, res.value
 
 
+def to_triplets(a) -> TripletMatrix:
+    """to_triplets for RgCSR (rgcsr.hpp:107-123), Hybrid (ellpack.hpp:219-240)
+    and device CSR (csr.hpp:62-72): the canonical host TripletMatrix."""
+    if isinstance(a, CsrMatrix):
+        c = a
+    else:
+        h = C.c_void_p()
+        fn = lib().spmvk_rgcsr_to_csr if isinstance(a, RgcsrMatrix) else lib().spmvk_hybrid_to_csr
+        _check(fn(a._h, None, C.byref(h)))
+        c = CsrMatrix(h.value)
+    rp, col, val = c.to_host()
+    return TripletMatrix(c.num_rows, c.num_cols, rp, col, val.astype(np.float64))
+
+
 # ---------------------------------------------------------------- accounting
 def fill_report(a) -> FillReport:
     """fill_report (fill.hpp:52-95) for RgCSR and Hybrid handles."""

@@ -111,3 +111,34 @@ def test_csr_spmv_bitwise(cuda, golden):
         a = sk.build_csr(triplets(golden_csr(g, t)))
         y = sk.spmv_csr(a, dev(g[f"{t}_x"])).cpu().numpy()
         assert bitwise(y, g[f"{t}_csr_y"]), t
+
+
+def _same(a: sk.TripletMatrix, m: orc.Csr) -> bool:
+    return (a.num_rows, a.num_cols) == (m.rows, m.cols) and bitwise(a.row_ptr, m.rp) and \
+        bitwise(a.col, m.col) and bitwise(a.val, m.val)
+
+
+def test_round_trip_through_every_format(cuda):
+    """tests/test_formats.cpp:314-323 (seeds 500-529, nonzero values) and the
+    Hybrid partition check :184-192 (seeds 200-229): to_triplets(build_*(m)) == m."""
+    for seed in list(range(500, 530)) + list(range(200, 230)):
+        om = orc.random_small(seed, allow_zero=False)
+        m = triplets(om)
+        assert _same(sk.to_triplets(sk.build_csr(m)), om)
+        assert _same(sk.to_triplets(sk.build_rgcsr(m, 1 + seed % 16)), om), seed
+        assert _same(sk.to_triplets(sk.build_rgcsr(m, 1 + seed % 16, 4)), om), seed
+        h = sk.build_hybrid(m)
+        assert h.info.fill_nnz == om.nnz  # ell_nnz + coo == nnz without stored zeros
+        assert _same(sk.to_triplets(h), om), seed
+
+
+def test_hybrid_to_triplets_drops_lone_stored_zero_like_reference(cuda):
+    """ellpack.hpp:50-54: a row whose only entry is a stored zero at column 0
+    is indistinguishable from an empty row — the reference loses it too."""
+    om = orc.Csr(3, 3, [0, 1, 2, 3], [0, 0, 2], [0.0, 5.0, 1.0])
+    t = sk.to_triplets(sk.build_hybrid(triplets(om)))
+    assert t.entries() == [(1, 0, 5.0), (2, 2, 1.0)]
+    if orc.ref_available():
+        r = orc.RefMatrix.from_csr(om)
+        h = r.hybrid()
+        assert h["artificial_zeros"] == sk.fill_report(sk.build_hybrid(triplets(om))).artificial_zeros
