@@ -167,13 +167,14 @@ int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx
 int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
                               uint64_t ny, uint64_t* multiply_add_count);
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
-/* Tuning knob (process-wide): which K2 kernel runs — "auto" (default: picked
- * from the precision and mean row length), "ldg_pf" / "ldg8_pf" / "ldg"
- * (thread per row, software-pipelined streamed loads), "pipe" / "pipe_hi" /
- * "pipe8" (thread per row with row-metadata prefetch and predicated batches),
- * "tma" (CTA-wide bulk-async-copy shared-memory ring), "wtma" / "wtma16"
- * (per-warp bulk-async-copy streams).  All variants give bitwise identical
- * y.  Also read from SPMVK_RGCSR_KERNEL. */
+/* Tuning knob (process-wide): which K2 kernel runs — "auto" (default: lite8
+ * for fp64, lite — or pipe for irregular matrices — for fp32), "lite" /
+ * "lite8" (register-lean thread per row at high occupancy), "lite_l2pf" /
+ * "lite8_l2pf" (+ bulk L2 prefetch of the next tile), "pipe" / "pipe_hi" /
+ * "pipe8" (row-metadata prefetch, predicated batches), "ldg" / "ldg_pf"
+ * (first kernels), "tma" (CTA-wide bulk-async-copy ring), "wtma" (per-warp
+ * bulk-async-copy streams).  All give bitwise identical y; the measured
+ * comparison is in DESIGN.md §3.  Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
 /* Tuning knob (process-wide, read at build): rows with more than `cut` slots
  * (default 128) are handled by a warp-per-row kernel instead of one thread

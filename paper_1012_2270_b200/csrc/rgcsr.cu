@@ -237,8 +237,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
-  kAuto, kWtma, kWtma16, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLdg8Pf, kLdg32, kLdgPf6,
-  kLite, kLite6, kLite8, kLite8Pf, kLitePf
+  kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -256,12 +255,11 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {
-      {"auto", K2::kAuto},   {"wtma", K2::kWtma},   {"wtma16", K2::kWtma16},
+      {"auto", K2::kAuto},   {"wtma", K2::kWtma},
       {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
-      {"ldg8_pf", K2::kLdg8Pf}, {"ldg32", K2::kLdg32}, {"ldg_pf6", K2::kLdgPf6},
-      {"lite", K2::kLite},     {"lite6", K2::kLite6}, {"lite8", K2::kLite8},
+      {"lite", K2::kLite},     {"lite8", K2::kLite8},
       {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}};
   for (const auto& [n, k] : names)
     if (v == n) {
@@ -304,10 +302,9 @@ void launch_tma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cuda
   SPMVK_LAUNCH("rgcsr_spmv_tma");
 }
 
-// Per-warp bulk-copy streams (rgcsr_spmv_wtma), one CTA per SM.  Two shapes:
-//   wtma   : 8 warps x 4-stage ring of 512 (fp64) / 3 x 1024 (fp32) elements
-//   wtma16 : 16 warps x 3-stage ring of 256 (fp64) / 3 x 512 (fp32) elements
-// both ~192 KB of shared memory per SM in flight; x gathers in batches of 8.
+// Per-warp bulk-copy streams (rgcsr_spmv_wtma), one CTA per SM: 8 warps x a
+// 4-stage ring of 512 (fp64) / 3 x 1024 (fp32) elements, ~192 KB of shared
+// memory per SM in flight; x gathers in batches of 8.
 template <class T, bool kScaled, int R, int NW, int NS, int CE>
 void launch_wtma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   constexpr size_t smem = wtma_smem_bytes<T, NS, CE, NW>();
@@ -359,10 +356,6 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     launch_wtma_g<T, kScaled, 8, f64 ? 4 : 3, f64 ? 512 : 1024>(h, x, y, x_next, scale, s);
     return;
   }
-  if (k == K2::kWtma16 && h->group_size <= 256) {
-    launch_wtma_g<T, kScaled, 16, 3, f64 ? 256 : 512>(h, x, y, x_next, scale, s);
-    return;
-  }
   if (k == K2::kTma && h->group_size <= 256) {
     if constexpr (sizeof(T) == 8)
       launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
@@ -397,12 +390,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
     case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
     case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;
-    case K2::kLdg8Pf: run(rgcsr_spmv_ldg<T, kScaled, 8, true>); break;
     case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
-    case K2::kLdg32: run(rgcsr_spmv_ldg<T, kScaled, U, false, 8>); break;
-    case K2::kLdgPf6: run(rgcsr_spmv_ldg<T, kScaled, U, true, 6>); break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
-    case K2::kLite6: run(rgcsr_spmv_lite<T, kScaled, 4, 6>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
@@ -677,8 +666,8 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (auto | wtma | wtma16 | pipe | pipe_hi | pipe8 | tma | ldg | ldg_pf | "
-                             "ldg8_pf)");
+                             "' (auto | lite | lite8 | lite_l2pf | lite8_l2pf | pipe | pipe_hi | "
+                             "pipe8 | ldg | ldg_pf | tma | wtma)");
     k2_slot().store(static_cast<int>(k));
   });
 }

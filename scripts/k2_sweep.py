@@ -21,7 +21,7 @@ from paper_1012_2270_b200._lib import lib  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--variants", default="auto,wtma,wtma16,pipe,pipe_hi,pipe8,tma,ldg_pf")
+    ap.add_argument("--variants", default="auto,lite,lite8,pipe,pipe_hi,tma,wtma,ldg_pf")
     ap.add_argument("--cases", default="27:128:32,27:128:128,5:1024:32,7:256:32,7:512:32")
     args = ap.parse_args()
     torch.cuda.set_device(0)

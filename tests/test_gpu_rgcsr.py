@@ -17,7 +17,8 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = ["auto", "lite", "lite6", "lite8", "lite8_l2pf", "lite_l2pf", "ldg32", "ldg_pf6", "wtma", "wtma16", "pipe", "pipe_hi", "pipe8", "tma", "ldg", "ldg_pf", "ldg8_pf"]
+VARIANTS = ["auto", "lite", "lite8", "lite8_l2pf", "lite_l2pf", "pipe", "pipe_hi", "pipe8",
+            "ldg", "ldg_pf", "tma", "wtma"]
 
 
 def dev(x):
