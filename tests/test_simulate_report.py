@@ -1,0 +1,37 @@
+"""scripts/simulate.py attribution of ncu per-instruction sectors to the
+reference `simulate` report's arrays (values / columns / x / output), CPU only."""
+import os
+import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "scripts"))
+import simulate  # noqa: E402
+
+HDR = ["Address", "Source", "Access Operation", "Access Size", "L2 Theoretical Sectors Global",
+       "L2 Theoretical Sectors Global Ideal"]
+
+
+def rows(*ins):
+    return [["Kernel Name", "k"], HDR] + [["0x0", s, op, str(sz), str(sec), str(ideal)]
+                                          for s, op, sz, sec, ideal in ins]
+
+
+def test_fp64_attribution():
+    r = rows(("LDG.E.CONSTANT R2, [R2.64]", "Load", 32, 10, 10),          # row length
+             ("LDG.E.NA.CONSTANT R3, [R4.64]", "Load", 32, 40, 40),       # column
+             ("LDG.E.NA.64.CONSTANT R6, [R6.64]", "Load", 64, 80, 80),    # value
+             ("LDG.E.64.CONSTANT R8, [R8.64]", "Load", 64, 90, 80),       # x gather
+             ("STG.E.64 [R10.64], R12", "Store", 64, 8, 8),               # y
+             ("IADD3 R1, R1, 1", "-", 0, 0, 0))
+    t = simulate.classify(r, 8)
+    assert t["columns"] == [40, 40] and t["values"] == [80, 80] and t["x"] == [90, 80]
+    assert t["output"] == [8, 8] and t["metadata"] == [10, 10]
+
+
+def test_fp32_splits_identical_slot_streams():
+    r = rows(("LDG.E.NA.CONSTANT R3, [R4.64]", "Load", 32, 50, 40),
+             ("LDG.E.NA.CONSTANT R5, [R6.64]", "Load", 32, 50, 40),
+             ("LDG.E.CONSTANT R7, [R8.64]", "Load", 32, 33, 30))
+    t = simulate.classify(r, 4, meta_sectors=3)
+    assert t["values"] == [50, 40] and t["columns"] == [50, 40]
+    assert t["x"] == [30, 27] and t["metadata"] == [3, 3]
