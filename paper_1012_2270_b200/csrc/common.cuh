@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -216,9 +217,15 @@ struct spmvk_rgcsr {
   spmvk::DevBuf<uint32_t> long_rows;
   uint64_t n_long = 0;
   uint32_t long_cut = 128;
-  // Pipelined host-span SpMV: x column range [min, max] of each row chunk.
-  mutable std::vector<unsigned> chunk_cols;
-  mutable uint32_t chunk_rows = 0;
+  // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile.
+  mutable std::vector<unsigned> tile_cols;
+  // Process-unique id: keys the host-span pipeline's captured CUDA graph
+  // (a recycled handle address must not replay a graph of freed arrays).
+  const uint64_t serial = next_serial();
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+  }
 };
 
 namespace spmvk {

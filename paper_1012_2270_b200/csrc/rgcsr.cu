@@ -399,26 +399,65 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   }
 }
 
-bool pinned(const void* p) {
+bool pinned(const void* p, void** mapped = nullptr) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  if (mapped) *mapped = a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
   return a.type == cudaMemoryTypeHost;
 }
 
-// Pipelined host-span SpMV: x goes up in kPipeChunks pieces on one copy
-// stream, each 1/kPipeChunks of the rows runs as soon as the x range it reads
-// (precomputed per chunk from its first / last slot columns) has landed, and
-// its y slice goes down on a second copy stream while later chunks compute.
-// The PCIe transfers in both directions and the SpMV overlap; y is bitwise the
-// one-launch result (same kernel, same per-row order).  Needs pinned host x/y.
-constexpr int kPipeChunks = 16;
+// Pipelined host-span SpMV.  x goes up in pieces on one copy stream; each
+// row chunk runs as soon as the x prefix it reads (from per-256-row-tile
+// column ranges, computed once per matrix) has landed, and stores its y slice
+// straight into the mapped pinned host buffer, so the x upload, the SpMV and
+// the y download overlap.  y is bitwise the one-launch result (same kernel,
+// same per-row order).  Needs pinned host x/y.  The stream operations are
+// captured ONCE into a CUDA graph per (matrix, x, y, staging buffers) and
+// replayed with one cudaGraphLaunch: issued one by one they cost ~4 us of host
+// time each and left the copy engine idle.  Chunk sizes ramp 1:2:4..4:2:1 so
+// the pipeline fill (first x piece) and drain (last y slice over PCIe) are
+// short while the middle pieces are large enough (~4 MB of x) to keep
+// per-copy overhead and copy/store interference low (profiles/r01_e2e_pipeline.md).
+constexpr int kPipeChunks = 64;  // upper bound on the chunk count
+
+// Row-chunk boundaries in 256-row tiles.  SPMVK_PIPE_CHUNKS=n forces n equal
+// chunks (scripts/e2e_sweep.py).
+std::vector<uint32_t> pipe_plan(uint32_t tiles, uint64_t x_bytes) {
+  static const int forced = [] {
+    const char* e = std::getenv("SPMVK_PIPE_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  std::vector<uint32_t> w;
+  if (forced > 0) {
+    w.assign(std::min(forced, kPipeChunks), 1);
+  } else {
+    const int mid = static_cast<int>(std::clamp<uint64_t>(x_bytes >> 22, 1, 12));
+    w = {1, 2};
+    w.insert(w.end(), mid, 4);
+    w.push_back(2);
+    w.push_back(1);
+  }
+  uint64_t total = 0;
+  for (auto v : w) total += v;
+  std::vector<uint32_t> b{0};
+  uint64_t acc = 0;
+  for (auto v : w) {
+    acc += v;
+    const auto e = static_cast<uint32_t>(acc * tiles / total);
+    if (e > b.back()) b.push_back(e);
+  }
+  b.back() = tiles;
+  return b;
+}
 
 struct PipeStage {
   cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
-  cudaEvent_t ex[kPipeChunks], ey[kPipeChunks];
+  cudaEvent_t ex[kPipeChunks], ey[kPipeChunks], fork, join[2];
+  cudaGraphExec_t exec = nullptr;
+  uint64_t key[7] = {};  // matrix serial, x, y, dx, dy, mapped y, sizeof(T)
   bool ready = false;
   void ensure() {
     if (ready) return;
@@ -427,14 +466,19 @@ struct PipeStage {
       SPMVK_CUDA(cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming));
       SPMVK_CUDA(cudaEventCreateWithFlags(&ey[i], cudaEventDisableTiming));
     }
+    SPMVK_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (auto& e : join) SPMVK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ready = true;
   }
   ~PipeStage() {
     if (!ready) return;
+    if (exec) cudaGraphExecDestroy(exec);
     for (int i = 0; i < kPipeChunks; ++i) {
       cudaEventDestroy(ex[i]);
       cudaEventDestroy(ey[i]);
     }
+    cudaEventDestroy(fork);
+    for (auto e : join) cudaEventDestroy(e);
     for (auto st : s) cudaStreamDestroy(st);
   }
 };
@@ -444,41 +488,33 @@ PipeStage& pipe_stage() {
   return p;
 }
 
+// Enqueue the pipeline on ps.s[0..2] (s[0] is the capture origin).  x chunk
+// c ends where row chunk c's largest column does (prefix max), so row chunk c
+// waits for exactly x chunks 0..c.  y: when the pinned buffer is mapped into
+// the device address space (UVA: cudaHostAlloc / torch pin_memory), the SpMV
+// chunks store straight into it over PCIe -- no D2H copies, and the copy
+// engine only carries x (two directions of 1 MB copies on two engines
+// interfere, profiles/r01_e2e_pipeline.md); otherwise y slices go down on s[2].
 template <class T>
-bool spmv_host_pipelined(const spmvk_rgcsr* h, const T* x, T* y, HostStage& st) {
+void enqueue_pipeline(const spmvk_rgcsr* h, const T* x, T* y, T* y_mapped, T* dx, T* dy,
+                      PipeStage& ps, const std::vector<uint32_t>& plan) {
   const uint64_t rows = h->rows, cols = h->cols;
-  if (h->n_long || rows < (1u << 16) || cols < (1u << 16) || !pinned(x) || !pinned(y))
-    return false;
-  const uint32_t chunk_rows =
-      static_cast<uint32_t>(((rows + kPipeChunks - 1) / kPipeChunks + 255) / 256 * 256);
-  const uint32_t nchunks = static_cast<uint32_t>((rows + chunk_rows - 1) / chunk_rows);
-  {
-    std::lock_guard<std::mutex> lk(h->part_mu);
-    if (h->chunk_rows != chunk_rows) {
-      DevBuf<unsigned> d(2 * nchunks);
-      std::vector<unsigned> init(2 * nchunks);
-      for (uint32_t k = 0; k < nchunks; ++k) init[2 * k] = 0xffffffffu, init[2 * k + 1] = 0;
-      SPMVK_CUDA(cudaMemcpy(d.p, init.data(), 8 * nchunks, cudaMemcpyHostToDevice));
-      chunk_column_ranges<<<persistent_grid((rows + 255) / 256, 8), 256>>>(
-          static_cast<uint32_t>(rows), static_cast<uint32_t>(h->group_size), chunk_rows,
-          h->group_pointers.p, h->row_lengths.p, h->columns.p, d.p);
-      SPMVK_LAUNCH("chunk_column_ranges");
-      h->chunk_cols.resize(2 * nchunks);
-      SPMVK_CUDA(cudaMemcpy(h->chunk_cols.data(), d.p, 8 * nchunks, cudaMemcpyDeviceToHost));
-      h->chunk_rows = chunk_rows;
-    }
-  }
-  PipeStage& ps = pipe_stage();
-  ps.ensure();
-  const uint64_t xchunk = (cols + kPipeChunks - 1) / kPipeChunks;
-  T* dx = reinterpret_cast<T*>(st.x.p);
-  T* dy = reinterpret_cast<T*>(st.y.p);
-  for (int c = 0; c < kPipeChunks; ++c) {
-    const uint64_t b = c * xchunk, e = std::min<uint64_t>(cols, b + xchunk);
-    if (b < e)
-      SPMVK_CUDA(cudaMemcpyAsync(dx + b, x + b, (e - b) * sizeof(T), cudaMemcpyHostToDevice,
+  const auto nchunks = static_cast<uint32_t>(plan.size() - 1);
+  SPMVK_CUDA(cudaEventRecord(ps.fork, ps.s[0]));
+  SPMVK_CUDA(cudaStreamWaitEvent(ps.s[1], ps.fork, 0));
+  SPMVK_CUDA(cudaStreamWaitEvent(ps.s[2], ps.fork, 0));
+  uint64_t xb = 0;
+  for (uint32_t k = 0; k < nchunks; ++k) {
+    uint64_t e = xb;  // one past the largest column of row chunk k (prefix max)
+    for (uint32_t t = plan[k]; t < plan[k + 1]; ++t)
+      if (h->tile_cols[2 * t] <= h->tile_cols[2 * t + 1])
+        e = std::max<uint64_t>(e, uint64_t(h->tile_cols[2 * t + 1]) + 1);
+    if (k + 1 == nchunks) e = cols;
+    if (xb < e)
+      SPMVK_CUDA(cudaMemcpyAsync(dx + xb, x + xb, (e - xb) * sizeof(T), cudaMemcpyHostToDevice,
                                  ps.s[0]));
-    SPMVK_CUDA(cudaEventRecord(ps.ex[c], ps.s[0]));
+    SPMVK_CUDA(cudaEventRecord(ps.ex[k], ps.s[0]));
+    xb = e;
   }
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
@@ -486,25 +522,85 @@ bool spmv_host_pipelined(const spmvk_rgcsr* h, const T* x, T* y, HostStage& st) 
   auto kern = f64 ? rgcsr_spmv_lite_range<T, 8, 5> : rgcsr_spmv_lite_range<T, 4, 8>;
   int per_sm = 0;
   SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  T* yk = y_mapped ? y_mapped : dy;
   for (uint32_t k = 0; k < nchunks; ++k) {
-    const unsigned cmax = h->chunk_cols[2 * k + 1];
-    const int need = h->chunk_cols[2 * k] > cmax ? 0 : static_cast<int>(cmax / xchunk);
-    SPMVK_CUDA(cudaStreamWaitEvent(ps.s[1], ps.ex[std::min(need, kPipeChunks - 1)], 0));
-    const uint32_t t0 = k * (chunk_rows / 256);
-    const uint32_t t1 = std::min<uint32_t>(static_cast<uint32_t>((rows + 255) / 256),
-                                           t0 + chunk_rows / 256);
+    SPMVK_CUDA(cudaStreamWaitEvent(ps.s[1], ps.ex[k], 0));
+    const uint32_t t0 = plan[k], t1 = plan[k + 1];
     kern<<<persistent_grid(t1 - t0, per_sm > 0 ? per_sm : 1), 256, 0, ps.s[1]>>>(
         t0, t1, static_cast<uint32_t>(rows), G, sh, h->group_pointers.p, h->row_lengths.p,
-        reinterpret_cast<const T*>(h->values.p), h->columns.p, dx, dy);
+        reinterpret_cast<const T*>(h->values.p), h->columns.p, dx, yk);
     SPMVK_LAUNCH("rgcsr_spmv_lite_range");
+    if (y_mapped) continue;
     SPMVK_CUDA(cudaEventRecord(ps.ey[k], ps.s[1]));
     SPMVK_CUDA(cudaStreamWaitEvent(ps.s[2], ps.ey[k], 0));
-    const uint64_t r0 = static_cast<uint64_t>(k) * chunk_rows;
-    const uint64_t r1 = std::min<uint64_t>(rows, r0 + chunk_rows);
+    const uint64_t r0 = uint64_t(t0) * 256, r1 = std::min<uint64_t>(rows, uint64_t(t1) * 256);
     SPMVK_CUDA(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * sizeof(T), cudaMemcpyDeviceToHost,
                                ps.s[2]));
   }
-  SPMVK_CUDA(cudaStreamSynchronize(ps.s[2]));
+  SPMVK_CUDA(cudaEventRecord(ps.join[0], ps.s[1]));
+  SPMVK_CUDA(cudaEventRecord(ps.join[1], ps.s[2]));
+  SPMVK_CUDA(cudaStreamWaitEvent(ps.s[0], ps.join[0], 0));
+  SPMVK_CUDA(cudaStreamWaitEvent(ps.s[0], ps.join[1], 0));
+}
+
+template <class T>
+bool spmv_host_pipelined(const spmvk_rgcsr* h, const T* x, T* y, HostStage& st) {
+  const uint64_t rows = h->rows, cols = h->cols;
+  void* ym = nullptr;
+  if (h->n_long || rows < (1u << 16) || cols < (1u << 16) || !pinned(x) || !pinned(y, &ym))
+    return false;
+  static const bool use_mapped = [] {
+    const char* e = std::getenv("SPMVK_PIPE_MAPPED_Y");
+    return !e || std::atoi(e) != 0;
+  }();
+  T* y_mapped = use_mapped ? static_cast<T*>(ym) : nullptr;
+  const uint32_t tiles = static_cast<uint32_t>((rows + 255) / 256);
+  {
+    std::lock_guard<std::mutex> lk(h->part_mu);
+    if (h->tile_cols.empty()) {
+      DevBuf<unsigned> d(2 * uint64_t(tiles));
+      std::vector<unsigned> init(2 * uint64_t(tiles));
+      for (uint32_t k = 0; k < tiles; ++k) init[2 * k] = 0xffffffffu, init[2 * k + 1] = 0;
+      SPMVK_CUDA(cudaMemcpy(d.p, init.data(), 8ull * tiles, cudaMemcpyHostToDevice));
+      chunk_column_ranges<<<persistent_grid(tiles, 8), 256>>>(
+          static_cast<uint32_t>(rows), static_cast<uint32_t>(h->group_size), 256,
+          h->group_pointers.p, h->row_lengths.p, h->columns.p, d.p);
+      SPMVK_LAUNCH("chunk_column_ranges");
+      h->tile_cols.resize(2 * uint64_t(tiles));
+      SPMVK_CUDA(cudaMemcpy(h->tile_cols.data(), d.p, 8ull * tiles, cudaMemcpyDeviceToHost));
+    }
+  }
+  const std::vector<uint32_t> plan = pipe_plan(tiles, cols * sizeof(T));
+  PipeStage& ps = pipe_stage();
+  ps.ensure();
+  T* dx = reinterpret_cast<T*>(st.x.p);
+  T* dy = reinterpret_cast<T*>(st.y.p);
+  const uint64_t key[7] = {h->serial, reinterpret_cast<uint64_t>(x),
+                           reinterpret_cast<uint64_t>(y), reinterpret_cast<uint64_t>(dx),
+                           reinterpret_cast<uint64_t>(dy), reinterpret_cast<uint64_t>(y_mapped),
+                           sizeof(T)};
+  if (!ps.exec || !std::equal(key, key + 7, ps.key)) {
+    if (ps.exec) {
+      SPMVK_CUDA(cudaGraphExecDestroy(ps.exec));
+      ps.exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    SPMVK_CUDA(cudaStreamBeginCapture(ps.s[0], cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_pipeline<T>(h, x, y, y_mapped, dx, dy, ps, plan);
+    } catch (...) {
+      cudaStreamEndCapture(ps.s[0], &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    SPMVK_CUDA(cudaStreamEndCapture(ps.s[0], &g));
+    const cudaError_t e = cudaGraphInstantiate(&ps.exec, g, 0);
+    cudaGraphDestroy(g);
+    SPMVK_CUDA(e);
+    std::copy(key, key + 7, ps.key);
+  }
+  SPMVK_CUDA(cudaGraphLaunch(ps.exec, ps.s[0]));
+  SPMVK_CUDA(cudaStreamSynchronize(ps.s[0]));
   return true;
 }
 

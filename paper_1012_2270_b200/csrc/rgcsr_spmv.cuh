@@ -230,13 +230,29 @@ __global__ void chunk_column_ranges(uint32_t rows, uint32_t G, uint32_t chunk_ro
                                     const uint32_t* __restrict__ lens,
                                     const uint32_t* __restrict__ columns,
                                     unsigned* __restrict__ out) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    const uint32_t len = lens[r];
-    if (!len) continue;
-    const uint32_t g = r / G, s = min(G, rows - g * G), base = gp[g] + (r - g * G);
+  // warp-uniform trip count so the warp reductions see all 32 lanes
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; w < rows;
+       w += gridDim.x * blockDim.x) {
+    const uint32_t r = w + (threadIdx.x & 31);
+    unsigned lo = 0xffffffffu, hi = 0;
+    const uint32_t len = r < rows ? lens[r] : 0;
+    if (len) {
+      const uint32_t g = r / G, s = min(G, rows - g * G), base = gp[g] + (r - g * G);
+      lo = columns[base];
+      hi = columns[base + (len - 1) * s];
+    }
     const uint32_t k = r / chunk_rows;
-    atomicMin(out + 2 * k, columns[base]);
-    atomicMax(out + 2 * k + 1, columns[base + (len - 1) * s]);
+    if ((w / chunk_rows) == ((w + 31) / chunk_rows)) {  // warp inside one chunk
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(out + 2 * k, lo);
+        atomicMax(out + 2 * k + 1, hi);
+      }
+    } else if (len) {
+      atomicMin(out + 2 * k, lo);
+      atomicMax(out + 2 * k + 1, hi);
+    }
   }
 }
 

@@ -237,3 +237,58 @@ def test_pipelined_host_span_equals_device(cuda, prec, kind, n):
         sk.spmv_rgcsr(a, xp.numpy(), yp.numpy())
         assert bitwise(yp.numpy(), want)
     assert bitwise(sk.spmv_rgcsr(a, xh), want)
+    # the pipeline is a captured CUDA graph keyed on (matrix, x, y): switching
+    # buffers, inputs or matrices must re-capture, never replay a stale graph
+    xh2 = orc.random_vector(a.num_cols, 3).astype(dt)
+    want2 = sk.spmv_rgcsr(a, dev(xh2)).cpu().numpy()
+    xp2 = torch.from_numpy(xh2).pin_memory()
+    yp2 = torch.empty_like(yp).pin_memory()
+    for _ in range(2):
+        sk.spmv_rgcsr(a, xp2.numpy(), yp2.numpy())
+        assert bitwise(yp2.numpy(), want2)
+        sk.spmv_rgcsr(a, xp.numpy(), yp.numpy())
+        assert bitwise(yp.numpy(), want)
+    xp.copy_(xp2)  # same buffers, new contents: the replay reads them afresh
+    sk.spmv_rgcsr(a, xp.numpy(), yp.numpy())
+    assert bitwise(yp.numpy(), want2)
+    del a
+    b = sk.build_rgcsr(sk.CsrMatrix.stencil(kind, n), 64, prec)
+    sk.spmv_rgcsr(b, xp.numpy(), yp.numpy())
+    assert bitwise(yp.numpy(), sk.spmv_rgcsr(b, dev(xh2)).cpu().numpy())
+
+
+@pytest.mark.parametrize("env", [{"SPMVK_PIPE_MAPPED_Y": "0"},
+                                 {"SPMVK_PIPE_CHUNKS": "7"},
+                                 {"SPMVK_PIPE_CHUNKS": "1", "SPMVK_PIPE_MAPPED_Y": "0"}])
+def test_pipelined_host_span_configurations(env):
+    """The pipeline's other shapes (y through D2H copies instead of mapped
+    stores, forced equal chunk counts) -- read once per process, so each runs
+    in a child -- stay bitwise the device-resident y."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch
+import oracle as orc
+from paper_1012_2270_b200 import generators as gen, spmvkit as sk
+mats = [sk.CsrMatrix.stencil(27, 48), sk.CsrMatrix.stencil(5, 400),
+        sk.build_csr(gen.random_rows(90000, 70000, 6, 3)),  # x chunk 0 = all of x
+        sk.build_csr(gen.banded(200000, 40, 4))]
+for prec, dt in ((8, np.float64), (4, np.float32)):
+    for kind, m in enumerate(mats):
+        if prec == 4:
+            m = sk.build_csr(sk.TripletMatrix(m.num_rows, m.num_cols, *m.to_host()), 4)
+        a = sk.build_rgcsr(m, 32, prec)
+        xh = orc.random_vector(a.num_cols, 5).astype(dt)
+        want = sk.spmv_rgcsr(a, torch.from_numpy(xh).cuda()).cpu().numpy()
+        xp = torch.from_numpy(xh).pin_memory()
+        yp = torch.empty(a.num_rows, dtype=xp.dtype).pin_memory()
+        for _ in range(2):
+            sk.spmv_rgcsr(a, xp.numpy(), yp.numpy())
+            assert yp.numpy().tobytes() == want.tobytes(), (prec, kind)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, PYTHONPATH=root, **env), timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
