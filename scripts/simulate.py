@@ -64,8 +64,7 @@ def child(a):
         h, fn, az = csr, sk.spmv_csr, 0
     dt = torch.float64 if prec == 8 else torch.float32
     x = torch.from_numpy(gen.random_vector(csr.num_cols, a.seed)).cuda().to(dt)
-    for _ in range(2):
-        fn(h, x)
+    fn(h, x)  # ONE SpMV: every kernel it launches is profiled (ncu flushes caches)
     torch.cuda.synchronize()
     with open(a.meta, "w") as f:
         json.dump({"nnz": csr.nnz(), "artificial_zeros": az, "rows": csr.num_rows}, f)
@@ -81,12 +80,23 @@ def load(a, sk, gen):
 
 
 def classify(rows, sv, meta_sectors=0):
-    h = rows[1]
-    ix = {k: h.index(k) for k in ("Source", "Access Operation", "Access Size",
-                                  "L2 Theoretical Sectors Global",
-                                  "L2 Theoretical Sectors Global Ideal")}
+    """Sum per-instruction sectors over every profiled kernel's section of the
+    `--page source --csv` output (each section: a "Kernel Name" row, a header
+    row, then one row per SASS instruction)."""
     out = {k: [0, 0] for k in ("values", "columns", "x", "output", "metadata", "na32")}
-    for r in rows[2:]:
+    ix, i = None, 0
+    while i < len(rows):
+        r = rows[i]
+        i += 1
+        if r and r[0] == "Kernel Name":
+            h = rows[i]
+            i += 1
+            ix = {k: h.index(k) for k in ("Source", "Access Operation", "Access Size",
+                                          "L2 Theoretical Sectors Global",
+                                          "L2 Theoretical Sectors Global Ideal")}
+            continue
+        if ix is None or len(r) <= max(ix.values()):
+            continue
         op = r[ix["Access Operation"]]
         if op not in ("Load", "Store"):
             continue
@@ -148,7 +158,7 @@ def main():
                         "--metrics", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum,"
                         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum",
                         "--clock-control", "none", "-k", f"regex:{KERNELS[a.format]}",
-                        "-s", "1", "-c", "1", "-o", rep] + argv, check=True,
+                        "-o", rep] + argv, check=True,
                        stdout=subprocess.DEVNULL)
         src = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "source", "--csv",
                               "--print-source", "sass"], capture_output=True, text=True,
@@ -161,11 +171,14 @@ def main():
         meta_sec = (m["rows"] * 4 + 31) // 32 + (m["rows"] + 31) // 32
     tx = classify(list(csv.reader(io.StringIO(src))), sv, meta_sec)
     rr = list(csv.reader(io.StringIO(raw)))
-    hdr, vals = rr[0], rr[2]
-    hits = int(float(vals[hdr.index("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum")]
-                     .replace(",", "")))
-    miss_all = int(float(vals[hdr.index(
-        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum")].replace(",", "")))
+    hdr = rr[0]
+
+    def total_of(metric):  # summed over the profiled kernels (one raw row each)
+        j = hdr.index(metric)
+        return sum(int(float(v[j].replace(",", ""))) for v in rr[2:] if len(v) > j and v[j])
+    hits = total_of("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum")
+    miss_all = total_of("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum")
+    kernels = [v[hdr.index("Kernel Name")] for v in rr[2:] if len(v) > 1]
     total = sum(v[0] for v in tx.values())
     ideal = sum(v[1] for v in tx.values())
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -180,7 +193,7 @@ def main():
            "metadata_sectors": tx["metadata"][0],
            "units": "32-byte L2 sectors per launch (ncu SourceCounters), B200; "
                     "cache = L1 global-load lookup hits of the x gathers",
-           "all_load_lookup_misses": miss_all}
+           "all_load_lookup_misses": miss_all, "kernels": kernels}
     if a.format == "rgcsr":
         doc["group_size"] = a.group_size
     text = json.dumps(doc, indent=2)

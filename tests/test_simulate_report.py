@@ -35,3 +35,11 @@ def test_fp32_splits_identical_slot_streams():
     t = simulate.classify(r, 4, meta_sectors=3)
     assert t["values"] == [50, 40] and t["columns"] == [50, 40]
     assert t["x"] == [30, 27] and t["metadata"] == [3, 3]
+
+
+def test_sums_every_kernel_section():
+    a = rows(("LDG.E.NA.64.CONSTANT R6, [R6.64]", "Load", 64, 80, 80))
+    b = rows(("LDG.E.NA.64.CONSTANT R6, [R6.64]", "Load", 64, 8, 4),
+             ("STG.E.64 [R10.64], R12", "Store", 64, 2, 2))
+    t = simulate.classify(a + b, 8)
+    assert t["values"] == [88, 84] and t["output"] == [2, 2]
