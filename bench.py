@@ -13,11 +13,13 @@ ride along in ``variants``.
                   [--workload 27pt-128|5pt-1024|powerlaw-8M|7pt-512]
 
 N > 1 (torchrun, one rank per GPU): the matrix is cut into group-aligned row
-slabs (paper_1012_2270_b200.partition), each step is one slab SpMV (with the
-next x = y_k * 2^-4 fused into its epilogue) plus the NCCL exchange of x —
-`--exchange halo` (default: only the column ranges each slab reads,
-point-to-point) or `allgather` (the whole vector) — timed as the max over
-ranks; scaling "strong" (fixed matrix).
+slabs (paper_1012_2270_b200.partition), each step is one slab SpMV with the
+next x = y_k * 2^-4 computed in its epilogue, plus the exchange of x —
+`--exchange fused` (default: the epilogue itself stores each x row into the
+exchange window of every peer whose slab reads it, over NVLink, then a device
+flag barrier; csrc/dist.cu), `halo` (NCCL point-to-point of only the column
+ranges each slab reads) or `allgather` (NCCL, the whole vector) — timed as the
+max over ranks; scaling "strong" (fixed matrix).
 
 ``--impl reference`` times the reference's own CPU spmv_rgcsr (oracle/_ref:
 the unmodified reference compiled in place; the plain-C port when _ref is not
@@ -363,8 +365,10 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=10)
     ap.add_argument("--distributed", action="store_true",
                     help="use the row-slab + NCCL path even at world size 1 (under torchrun)")
-    ap.add_argument("--exchange", default="halo", choices=["allgather", "halo"],
-                    help="x exchange of the distributed iterated SpMV")
+    ap.add_argument("--exchange", default="fused", choices=["allgather", "halo", "fused"],
+                    help="x exchange of the distributed iterated SpMV: NCCL all-gather, NCCL "
+                         "halo send/recv, or fused (SpMV epilogue stores into peer windows "
+                         "over NVLink + device barrier)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -53,6 +53,8 @@ typedef enum { SPMVK_F32 = 4, SPMVK_F64 = 8 } spmvk_precision;
 typedef struct spmvk_csr spmvk_csr;
 typedef struct spmvk_rgcsr spmvk_rgcsr;
 typedef struct spmvk_hybrid spmvk_hybrid;
+typedef struct spmvk_window spmvk_window;
+typedef struct spmvk_dist spmvk_dist;
 
 /* Thread-local message of the last failing call on this thread. */
 const char* spmvk_last_error(void);
@@ -245,6 +247,50 @@ int spmvk_cg_update_f64(uint64_t n, const double* rr, const double* pap, const d
                         const double* q, double* x, double* r, double* rr_new, void* stream);
 int spmvk_cg_direction_f64(uint64_t n, const double* r, double* p, double* rr,
                            const double* rr_new, void* stream);
+
+/* ------------------------------------------------------------------ fused multi-GPU step
+ * SURVEY §8e (the reference has no multi-GPU path; §8b lists spmvk_dist_*):
+ * row slabs, x_{k+1} = (A x_k)_slab * scale, with the x exchange fused into
+ * the SpMV's row epilogue as stores into the peers' exchange windows over
+ * NVLink (no separate collective), and one device-side flag barrier per step.
+ *
+ * Window: two x buffers of n entries (double-buffered) + flags, in this
+ * device's HBM, zero-initialised.  Export it with spmvk_window_ipc_handle
+ * (64 bytes, cudaIpcMemHandle_t) and exchange the handles out of band (MPI,
+ * torch.distributed, a file); every rank then calls spmvk_dist_open with the
+ * handles of all ranks in rank order (its own entry is ignored).  Ranks that
+ * live in ONE process (one process driving several GPUs, or tests sharing a
+ * device) use spmvk_dist_open_local with the window pointers instead.
+ * At most 8 ranks (one NVLink domain node).  Destroy a window only after
+ * every peer has destroyed the dist handle that opened it. */
+int spmvk_window_create(uint64_t n, int prec, spmvk_window** out);
+int spmvk_window_ipc_handle(const spmvk_window* w, unsigned char* handle_out);
+/* Device pointer of x buffer 0 or 1 (write the starting x into the buffer
+ * spmvk_dist_current names before the first step). */
+int spmvk_window_x(const spmvk_window* w, int buffer, void** out);
+void spmvk_window_destroy(spmvk_window* w);
+int spmvk_dist_open(const spmvk_window* own, int rank, int world, const unsigned char* handles,
+                    spmvk_dist** out);
+int spmvk_dist_open_local(const spmvk_window* const* windows, int rank, int world,
+                          spmvk_dist** out);
+/* This rank's slab = global rows [row_begin, row_end) (its RgCSR holds
+ * exactly those rows, global columns).  receive_ranges[2q], [2q+1]: global
+ * rows [lo, hi) that rank q must receive every step -- its own slab for
+ * itself, and for peers either everything (all-gather) or the rows their
+ * slab reads (halo, partition.halo_plan).  Only the part inside this rank's
+ * slab is sent. */
+int spmvk_dist_set_rows(spmvk_dist* d, uint64_t row_begin, uint64_t row_end,
+                        const uint64_t* receive_ranges);
+/* One step: y = A_slab x[cur] (slab-local y, device), x_next = y * scale
+ * stored into x[1-cur] of every window whose receive range covers the row,
+ * then (barrier != 0) the device barrier; cur flips.  barrier = 0 is for
+ * ranks stepped one after another by one host thread on one device. */
+int spmvk_dist_step_f64(spmvk_dist* d, const spmvk_rgcsr* slab, double scale, double* y,
+                        int barrier, void* stream);
+int spmvk_dist_step_f32(spmvk_dist* d, const spmvk_rgcsr* slab, float scale, float* y,
+                        int barrier, void* stream);
+int spmvk_dist_current(const spmvk_dist* d, int* buffer);
+void spmvk_dist_destroy(spmvk_dist* d);
 
 /* ------------------------------------------------------------------ host generators
  * Seeded, platform-independent generators (std::mt19937_64 draws, the

@@ -86,6 +86,17 @@ SIGNATURES = {
     "spmvk_dot_f64": (cint, [vp, vp, u64, vp, vp]),
     "spmvk_cg_update_f64": (cint, [u64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvk_cg_direction_f64": (cint, [u64, vp, vp, vp, vp, vp]),
+    "spmvk_window_create": (cint, [u64, cint, C.POINTER(vp)]),
+    "spmvk_window_ipc_handle": (cint, [vp, vp]),
+    "spmvk_window_x": (cint, [vp, cint, C.POINTER(vp)]),
+    "spmvk_window_destroy": (None, [vp]),
+    "spmvk_dist_open": (cint, [vp, cint, cint, vp, C.POINTER(vp)]),
+    "spmvk_dist_open_local": (cint, [C.POINTER(vp), cint, cint, C.POINTER(vp)]),
+    "spmvk_dist_set_rows": (cint, [vp, u64, u64, vp]),
+    "spmvk_dist_step_f64": (cint, [vp, vp, C.c_double, vp, cint, vp]),
+    "spmvk_dist_step_f32": (cint, [vp, vp, C.c_float, vp, cint, vp]),
+    "spmvk_dist_current": (cint, [vp, C.POINTER(cint)]),
+    "spmvk_dist_destroy": (None, [vp]),
     "spmvk_gen_random_vector": (None, [u64, u64, vp]),
     "spmvk_gen_stencil": (u64, [cint, u64, vp, vp, vp]),
     "spmvk_gen_powerlaw": (u64, [u64, u64, vp, vp, vp]),

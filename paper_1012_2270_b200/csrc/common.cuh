@@ -165,6 +165,14 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
 // Grid of `per_sm` CTAs per SM, capped by the work.
+// log2(G) when G is a power of two (the kernels then shift instead of divide), else -1.
+inline int pow2_shift(uint64_t G) {
+  if (G == 0 || (G & (G - 1))) return -1;
+  int s = 0;
+  while ((1ull << s) < G) ++s;
+  return s;
+}
+
 inline unsigned persistent_grid(uint64_t work_ctas, int per_sm) {
   const uint64_t cap = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(per_sm);
   const uint64_t g = work_ctas < cap ? work_ctas : cap;

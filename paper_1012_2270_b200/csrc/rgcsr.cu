@@ -132,13 +132,6 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
   }
 }
 
-int pow2_shift(uint64_t G) {
-  if (G == 0 || (G & (G - 1))) return -1;
-  int s = 0;
-  while ((1ull << s) < G) ++s;
-  return s;
-}
-
 spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int prec,
                    cudaStream_t s) {
   if (!a) fail(SPMVK_EINVAL, "null CSR handle");

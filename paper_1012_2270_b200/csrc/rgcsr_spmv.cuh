@@ -137,12 +137,51 @@ __device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint
 // Occupancy (40-64 warps / SM) gives the memory system the most independent
 // requests; a predicated last batch avoids serialised single-slot round trips
 // on short rows and tails.
-template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
-__device__ __forceinline__ void lite_tiles(
+// Row epilogues: what a finished row does with its sum.  StoreEpi is the
+// plain / iterated form (y, and x_next = y * scale); PeerEpi (the fused
+// distributed step, dist.cu) also stores x_next into every peer window whose
+// receive range covers the row -- over NVLink when the peer is another GPU.
+template <class T, bool kScaled>
+struct StoreEpi {
+  T* __restrict__ y;
+  T* __restrict__ x_next;
+  T scale;
+  __device__ __forceinline__ void operator()(uint32_t r, T acc) const {
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+};
+
+constexpr int kMaxPeers = 8;
+template <class T>
+struct PeerSet {
+  T* dst[kMaxPeers];             // x_next buffer of each destination window
+  uint32_t lo[kMaxPeers], hi[kMaxPeers];  // global rows [lo, hi) it receives
+  int n;
+};
+
+template <class T>
+struct PeerEpi {
+  T* __restrict__ y;
+  T scale;
+  uint32_t row0;  // global index of the slab's first row
+  PeerSet<T> ps;
+  __device__ __forceinline__ void operator()(uint32_t r, T acc) const {
+    y[r] = acc;
+    const T xs = mul_rn(acc, scale);
+    const uint32_t gr = row0 + r;
+#pragma unroll
+    for (int i = 0; i < kMaxPeers; ++i)
+      if (i < ps.n && gr >= ps.lo[i] && gr < ps.hi[i]) ps.dst[i][gr] = xs;
+  }
+};
+
+template <class T, int U, bool kPrefetchL2, class Epi>
+__device__ __forceinline__ void lite_tiles_epi(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
-    T* __restrict__ y, T* __restrict__ x_next, T scale, uint32_t long_cut) {
+    uint32_t long_cut, const Epi& epi) {
   if (kPrefetchL2 && threadIdx.x == 0) {
     const uint32_t groups = (rows + G - 1) / G;
     if (tile_begin + blockIdx.x < tile_end)
@@ -195,9 +234,18 @@ __device__ __forceinline__ void lite_tiles(
       for (int u = 0; u < U - 1; ++u)
         if (j + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
     }
-    y[r] = acc;
-    if (kScaled) x_next[r] = mul_rn(acc, scale);
+    epi(r, acc);
   }
+}
+
+template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
+__device__ __forceinline__ void lite_tiles(
+    uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  lite_tiles_epi<T, U, kPrefetchL2>(tile_begin, tile_end, rows, G, g_shift, gp, lens, values,
+                                    columns, x, long_cut, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
 template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false>
@@ -225,7 +273,7 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite_range(
 // Per row chunk of `chunk_rows` rows: the smallest first-slot column and the
 // largest last-slot column (columns increase along a row), i.e. the x range
 // the chunk reads.  out[2k] = min, out[2k+1] = max (min > max if empty).
-__global__ void chunk_column_ranges(uint32_t rows, uint32_t G, uint32_t chunk_rows,
+static __global__ void chunk_column_ranges(uint32_t rows, uint32_t G, uint32_t chunk_rows,
                                     const uint32_t* __restrict__ gp,
                                     const uint32_t* __restrict__ lens,
                                     const uint32_t* __restrict__ columns,
@@ -330,12 +378,12 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_ldg(
 // row at a time (8 per lane, all in flight), forms the products in parallel,
 // stages them in shared memory, and one lane adds them in slot order — the
 // reference's rounding sequence, so y stays bitwise.
-template <class T, bool kScaled>
-__global__ void __launch_bounds__(256) rgcsr_spmv_long(
+template <class T, class Epi>
+__device__ __forceinline__ void long_rows_epi(
     uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,
     int g_shift, const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
-    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+    const Epi& epi) {
   constexpr int K = 8, W = 32 * K;
   __shared__ T prod[8][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -382,11 +430,18 @@ __global__ void __launch_bounds__(256) rgcsr_spmv_long(
       }
       __syncwarp();
     }
-    if (lane == 0) {
-      y[r] = acc;
-      if (kScaled) x_next[r] = mul_rn(acc, scale);
-    }
+    if (lane == 0) epi(r, acc);
   }
+}
+
+template <class T, bool kScaled>
+__global__ void __launch_bounds__(256) rgcsr_spmv_long(
+    uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,
+    int g_shift, const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  long_rows_epi<T>(nlong, long_rows, rows, G, g_shift, gp, lens, values, columns, x,
+                   StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
 // ---------------------------------------------------------------------------
@@ -414,7 +469,7 @@ constexpr size_t wtma_smem_bytes() {
 // part[i] = first wave of warp i (part[W] = nwaves): slot-balanced split, the
 // smallest wave whose first slot is >= total * i / W.  Computed once per
 // (handle, grid) and cached.
-__global__ void wave_partition(uint32_t W, uint32_t nwaves, uint32_t gpw, uint32_t groups,
+static __global__ void wave_partition(uint32_t W, uint32_t nwaves, uint32_t gpw, uint32_t groups,
                                const uint32_t* __restrict__ gp, uint32_t* __restrict__ part) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > W) return;

@@ -264,6 +264,162 @@ def torch_p2p(ops):
         r.wait()
 
 
+# ---------------------------------------------------------------- fused peer-memory step
+def fused_receive_ranges(slabs: Sequence[Slab], ranges, mode: str) -> List[tuple]:
+    """Global rows [lo, hi) each rank's window must receive every step of the
+    fused path (spmvk_dist_set_rows): the whole x for "allgather"; for "halo"
+    the span of its own slab and the columns its slab reads (``ranges[q]`` =
+    (cmin, cmax), cmin > cmax for a slab without entries)."""
+    n = max((s.row_end for s in slabs), default=0)
+    out = []
+    for s in slabs:
+        if mode == "allgather":
+            out.append((0, n))
+            continue
+        cmin, cmax = ranges[s.rank]
+        lo, hi = s.row_begin, s.row_end
+        if cmin <= cmax:
+            lo, hi = min(lo, cmin), max(hi, cmax + 1)
+        out.append((lo, hi) if lo < hi else (0, 0))
+    return out
+
+
+def simulate_fused_routing(slabs, receive, slab_matvec, x0, steps: int):
+    """CPU model of the fused step's data movement (for the gloo-free unit
+    tests): every rank owns two window buffers; step k reads its window's
+    x[cur] and stores its slab of x_{k+1} into x[1-cur] of every window whose
+    receive range covers the row.  ``slab_matvec(rank, x) -> x_next slab``.
+    Returns the windows' current buffers."""
+    n = max(x0.size, max(s.row_end for s in slabs))
+    win = [[np.zeros(n, x0.dtype), np.zeros(n, x0.dtype)] for _ in slabs]
+    for w in win:
+        w[0][: x0.size] = x0
+    cur = 0
+    for _ in range(steps):
+        for s in slabs:
+            xn = slab_matvec(s.rank, win[s.rank][cur])
+            for q, (lo, hi) in enumerate(receive):
+                a, b = max(lo, s.row_begin), min(hi, s.row_end)
+                if a < b:
+                    win[q][1 - cur][a:b] = xn[a - s.row_begin: b - s.row_begin]
+        cur = 1 - cur
+    return [w[cur] for w in win]
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 2, "strides": None}
+
+
+class ExchangeWindow:
+    """This rank's exchange window (spmvk_window): two x buffers + flags."""
+
+    def __init__(self, n: int, prec: int = 8):
+        import ctypes as C
+
+        import torch
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        self._L, self.n, self.prec = lib(), n, prec
+        h = C.c_void_p()
+        sk._check(self._L.spmvk_window_create(n, prec, C.byref(h)))
+        self._h = h
+        self.x = []
+        for b in range(2):
+            p = C.c_void_p()
+            sk._check(self._L.spmvk_window_x(h, b, C.byref(p)))
+            self.x.append(torch.as_tensor(_DevArray(p.value, n, "<f8" if prec == 8 else "<f4"),
+                                          device="cuda"))
+
+    def ipc_handle(self) -> bytes:
+        import ctypes as C
+
+        from . import spmvkit as sk
+        buf = (C.c_ubyte * 64)()
+        sk._check(self._L.spmvk_window_ipc_handle(self._h, buf))
+        return bytes(buf)
+
+    def close(self):
+        if self._h:
+            self.x = []
+            self._L.spmvk_window_destroy(self._h)
+            self._h = None
+
+
+class FusedIteratedSpmv:
+    """Iterated SpMV with the x exchange fused into the SpMV (spmvk_dist_*):
+    the kernel's row epilogue stores x_{k+1} into every window whose receive
+    range covers the row (peer windows over NVLink), then a device flag
+    barrier ends the step.  ``handles`` = the 64-byte IPC handles of every
+    rank's window in rank order (gathered by the caller), or ``local_windows``
+    = the ExchangeWindow of every rank when all ranks live in this process
+    (then ``barrier`` is usually False and the caller steps ranks in turn)."""
+
+    def __init__(self, slab: Slab, receive: Sequence[tuple], a, window: ExchangeWindow,
+                 world: int, stream: int, handles=None, local_windows=None, barrier=True,
+                 scale: float = 0.0625):
+        import ctypes as C
+
+        import torch
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        self._L, self.slab, self.a, self.window, self.stream = lib(), slab, a, window, stream
+        self.world, self.scale, self.barrier = world, scale, bool(barrier)
+        self.num_cols = a.num_cols
+        d = C.c_void_p()
+        if local_windows is not None:
+            arr = (C.c_void_p * world)(*[w._h.value for w in local_windows])
+            sk._check(self._L.spmvk_dist_open_local(arr, slab.rank, world, C.byref(d)))
+        else:
+            blob = b"".join(handles) if handles else None
+            sk._check(self._L.spmvk_dist_open(window._h, slab.rank, world, blob, C.byref(d)))
+        self._d = d
+        rr = (C.c_uint64 * (2 * world))(*[v for lo_hi in receive for v in lo_hi])
+        sk._check(self._L.spmvk_dist_set_rows(d, slab.row_begin, slab.row_end, rr))
+        dt = torch.float64 if window.prec == 8 else torch.float32
+        self.y = torch.zeros(max(slab.rows, 1), dtype=dt, device="cuda")
+        self._step = self._L.spmvk_dist_step_f64 if window.prec == 8 else \
+            self._L.spmvk_dist_step_f32
+        lo, hi = receive[slab.rank]  # entries received from peers per step
+        self.halo = max(0, min(hi, slab.row_begin) - lo) + max(0, hi - max(lo, slab.row_end))
+
+    @property
+    def cur(self) -> int:
+        import ctypes as C
+        c = C.c_int()
+        self._L.spmvk_dist_current(self._d, C.byref(c))
+        return c.value
+
+    @property
+    def x(self):  # the two window buffers (HaloIteratedSpmv's x[cur] convention)
+        return self.window.x
+
+    @property
+    def x_current(self):
+        return self.window.x[self.cur][: self.num_cols]
+
+    def set_x(self, x_full):
+        self.window.x[self.cur][: x_full.numel()].copy_(x_full)
+
+    def halo_entries(self) -> int:
+        return self.halo
+
+    def step(self):
+        from . import spmvkit as sk
+        sk._check(self._step(self._d, self.a._h, self.scale, self.y.data_ptr(),
+                             1 if self.barrier else 0, self.stream))
+
+    def close(self):
+        if self._d:
+            self._L.spmvk_dist_destroy(self._d)
+            self._d = None
+
+
 # ---------------------------------------------------------------- bench (N > 1)
 def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=None,
                       rg_bytes=None):
@@ -293,7 +449,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     a = sk.build_rgcsr(csr, G, 8, stream=sp, row_range=(me.row_begin, me.row_end))
     nnz_local = a.nnz()
     exchange = getattr(args, "exchange", "allgather")
-    if exchange == "halo":
+    if exchange in ("halo", "fused"):
         import ctypes as C
         cr = (C.c_uint64 * 2)()
         sk._check(lib().spmvk_csr_column_range(csr._h, me.row_begin, me.row_end, cr))
@@ -318,11 +474,43 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
         with torch.cuda.stream(stream):
             torch_p2p(ops)
 
-    if exchange == "halo":
+    fallback = None
+    if exchange == "fused":
+        # peer windows need CUDA IPC + P2P between the GPUs; if any rank cannot
+        # map them, every rank switches to the NCCL halo exchange (recorded)
+        win = it = None
+        try:
+            win = ExchangeWindow(max(a.num_cols, slabs[-1].row_end), 8)
+            handles = [None] * world
+            dist.all_gather_object(handles, win.ipc_handle())
+            recv = fused_receive_ranges(slabs, ranges, "halo")
+            it = FusedIteratedSpmv(me, recv, a, win, world, sp, handles=handles,
+                                   barrier=world > 1)
+            ok, why = 1, ""
+        except Exception as e:  # noqa: BLE001 -- reported, then the NCCL path runs
+            ok, why = 0, f"rank {rank}: {e}"
+        flag = torch.tensor([ok], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item():
+            reasons = [None] * world
+            dist.all_gather_object(reasons, why)
+            fallback = "; ".join(r for r in reasons if r) or "a peer could not map windows"
+            if it is not None:
+                it.close()
+            dist.barrier()
+            if win is not None:
+                win.close()
+            exchange = "halo"
+    if exchange == "fused":
+        pass
+    elif exchange == "halo":
         it = HaloIteratedSpmv(me, slabs, ranges, a.num_cols, slab_spmv, p2p, x0)
     else:
         it = IteratedSpmv(me, a.num_cols, world, slab_spmv, all_gather, x0)
-    it.set_x(x0)
+    with torch.cuda.stream(stream):
+        it.set_x(x0)
+    stream.synchronize()
+    dist.barrier()
     for _ in range(args.warmup):
         it.step()
     torch.cuda.synchronize()
@@ -390,7 +578,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     if rank == 0:
         step_ms = ms.item() / args.steps
         value = 2.0 * tot_nnz.item() / (step_ms * 1e-3) / 1e9
-        halo = it.halo_entries() if exchange == "halo" else None
+        halo = it.halo_entries() if exchange in ("halo", "fused") else None
         k_s = kern_ms.item() * 1e-3
         achieved = slab_bytes / k_s / 1e9 if slab_bytes else None
         peak, peak_kind = peaks if peaks else (None, None)
@@ -401,9 +589,16 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             "data": "synthetic",
             "config": {"workload": args.workload, "description": desc, "format": "rgcsr",
                        "group_size": G,
-                       "parallelism": f"row-slab x{world}, NCCL {exchange} of x",
-                       "step": f"slab SpMV (+fused x_next = y/16) + {exchange} exchange",
+                       "parallelism": (f"row-slab x{world}, halo of x stored into peer windows "
+                                       "by the SpMV epilogue (NVLink P2P) + device flag barrier"
+                                       if exchange == "fused" else
+                                       f"row-slab x{world}, NCCL {exchange} of x"),
+                       "step": (f"fused slab SpMV + peer-window x_next stores"
+                                f"{' + flag barrier' if world > 1 else ''}"
+                                if exchange == "fused" else
+                                f"slab SpMV (+fused x_next = y/16) + {exchange} exchange"),
                        "halo_entries_rank0": halo,
+                       "exchange_fallback": fallback,
                        "l2": "per-rank slab streamed from HBM each step (no flush)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved and peak else None,
@@ -416,7 +611,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
                     "ms_per_step": e2e_s.item() * 1e3,
                     "path": "per rank: pinned H2D of the x slab, exchange + slab SpMV, D2H of y"},
             "clocks": clocks.summary() if clocks else None,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if exchange == "fused" and world > 1 else 1),
             "x_bits_checksum": int(sums.sum().item()),
         }), flush=True)
     dist.destroy_process_group()
