@@ -230,7 +230,8 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
-  kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf
+  kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
+  kLite8Full
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -243,7 +244,12 @@ enum class K2 {
 // (profiles/r01_powerlaw.md: 1,070 vs 1,353 us).
 K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
   if (f64) return K2::kLite8;
-  return h->n_long ? K2::kPipe : K2::kLite;
+  if (h->n_long) return K2::kPipe;
+  // fp32, short rows (<= ~12 slots): one 8-deep batch per row at full
+  // occupancy (32 registers, no spills) keeps more slot bytes in flight
+  // (7-pt 256^3: 193 vs 201 us; 5-pt 1024^2: 14.6 vs 16.7 us); longer rows
+  // (27-pt: 88 vs 78 us) prefer 4-deep batches (profiles/r01_k2_sweep3.md)
+  return h->slots <= 12 * h->rows ? K2::kLite8Full : K2::kLite;
 }
 
 bool parse_k2(const std::string& v, K2* out) {
@@ -253,7 +259,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
       {"lite", K2::kLite},     {"lite8", K2::kLite8},
-      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}};
+      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -386,6 +392,7 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
+    case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
     case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
