@@ -138,25 +138,30 @@ def host_csr(workload):
 
 
 # ---------------------------------------------------------------- timing helpers
+# Read-only streaming bandwidth measured on B200 (float4 lanes, full occupancy;
+# scripts/probes/ld_width.cu, profiles/r01_ld_width.md).
+READ_STREAM_GBS = 7164.4
+
+
 def time_launches(fn, stream, steps, warmup):
-    """Warm up, then time `steps` launches with per-launch CUDA events on
-    `stream` (barrier+sync both sides).  Returns (total_ms, [per-launch ms])."""
+    """Warm up, then time `steps` back-to-back launches with CUDA events on
+    `stream` around the whole region (synchronize on both sides).  Events
+    between launches would add their own gaps (~3 us per launch on the 27-pt
+    headline), so the per-launch duration is the region time / steps.
+    Returns (total_ms, per-launch ms)."""
     import torch
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         t0.record(stream)
-        for s, e in ev:
-            s.record(stream)
+        for _ in range(steps):
             fn()
-            e.record(stream)
         t1.record(stream)
     torch.cuda.synchronize()
-    return t0.elapsed_time(t1), [s.elapsed_time(e) for s, e in ev]
+    total = t0.elapsed_time(t1)
+    return total, total / steps
 
 
 def rg_bytes(info, sv):
@@ -269,9 +274,8 @@ def run_ours(args):
     clocks = ClockSampler(0)
     torch.cuda.synchronize()
     with clocks:
-        total_ms, per = time_launches(step, stream, args.steps, args.warmup)
+        total_ms, kern_ms = time_launches(step, stream, args.steps, args.warmup)
     ms = total_ms / args.steps
-    kern_ms = statistics.mean(per)
     B = rg_bytes(a.info, 8)
     achieved = B / (kern_ms * 1e-3) / 1e9
     value = 2.0 * nnz / (ms * 1e-3) / 1e9
@@ -316,7 +320,7 @@ def run_ours(args):
         tconv = time.perf_counter() - tt
         _, pv = time_launches(lambda: fn(h._h, xv.data_ptr(), h.num_cols, yv.data_ptr(),
                                          h.num_rows, sp), stream, args.steps, args.warmup)
-        km = statistics.mean(pv)
+        km = pv
         variants[label] = {"gflops": 2.0 * nnz / (km * 1e-3) / 1e9, "kernel_us": km * 1e3,
                            "bytes": Bv, "achieved_gbs": Bv / (km * 1e-3) / 1e9,
                            "frac_of_peak": Bv / (km * 1e-3) / 1e9 / peak,
@@ -340,7 +344,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "bytes_per_launch": B, "kernel_us": kern_ms * 1e3,
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     # the peak above is a copy (half writes); SpMV traffic is ~98 % reads
+                     "read_stream_peak": READ_STREAM_GBS,
+                     "frac_read_stream": achieved / READ_STREAM_GBS},
         "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,

@@ -317,10 +317,24 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
 #pragma unroll
         for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
       }
-      for (; j < k1; ++j) {
-        const size_t idx = (size_t)j * rows + r;
-        const uint32_t c = ld_stream(ec + idx, pf);
-        acc = add_rn(acc, mul_rn(ld_stream(ev + idx, pf), ld_x(x + c, pl)));
+      if (j < k1) {  // tail of < U slots: one predicated batch, loads in flight together
+        uint32_t c[U - 1];
+        T v[U - 1], xv[U - 1];
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u) {
+          c[u] = 0;
+          v[u] = T(0);
+          if (j + u < k1) {
+            const size_t idx = (size_t)(j + u) * rows + r;
+            c[u] = ld_stream(ec + idx, pf);
+            v[u] = ld_stream(ev + idx, pf);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u) xv[u] = j + u < k1 ? ld_x(x + c[u], pl) : T(0);
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u)
+          if (j + u < k1) acc = add_rn(acc, mul_rn(v[u], xv[u]));
       }
     }
     if (tile_ptr) {

@@ -231,7 +231,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
   kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
-  kLite8Full
+  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -259,7 +259,9 @@ bool parse_k2(const std::string& v, K2* out) {
       {"pipe8", K2::kPipe8},
       {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
       {"lite", K2::kLite},     {"lite8", K2::kLite8},
-      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full}};
+      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full},
+      {"lite_mpf", K2::kLiteMpf}, {"lite8_mpf", K2::kLite8Mpf},
+      {"lite8_full_mpf", K2::kLite8FullMpf}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -393,6 +395,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
+    case K2::kLiteMpf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, false, true>); break;
+    case K2::kLite8Mpf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, false, true>); break;
+    case K2::kLite8FullMpf: run(rgcsr_spmv_lite<T, kScaled, 8, 8, false, true>); break;
     case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;

@@ -176,7 +176,10 @@ struct PeerEpi {
   }
 };
 
-template <class T, int U, bool kPrefetchL2, class Epi>
+// kMetaPf: the row length and group pointer of the thread's NEXT tile row are
+// loaded while the current row runs, taking that dependent DRAM round trip
+// (length -> slots) off every row but the first.
+template <class T, int U, bool kPrefetchL2, class Epi, bool kMetaPf = false>
 __device__ __forceinline__ void lite_tiles_epi(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
@@ -187,16 +190,35 @@ __device__ __forceinline__ void lite_tiles_epi(
     if (tile_begin + blockIdx.x < tile_end)
       prefetch_tile<T>(tile_begin + blockIdx.x, rows, G, groups, gp, values, columns);
   }
+  uint32_t len_n = 0, base_n = 0;
+  if (kMetaPf) {
+    const uint32_t r0 = (tile_begin + blockIdx.x) * 256 + threadIdx.x;
+    if (tile_begin + blockIdx.x < tile_end && r0 < rows) {
+      len_n = lens[r0];
+      base_n = gp[g_shift >= 0 ? (r0 >> g_shift) : r0 / G];
+    }
+  }
   for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     if (kPrefetchL2 && threadIdx.x == 0 && tile + gridDim.x < tile_end)
       prefetch_tile<T>(tile + gridDim.x, rows, G, (rows + G - 1) / G, gp, values, columns);
     const uint32_t r = tile * 256 + threadIdx.x;
+    uint32_t len, base;
+    if (kMetaPf) {
+      len = len_n;
+      base = base_n;
+      const uint32_t rn = r + gridDim.x * 256;
+      if (tile + gridDim.x < tile_end && rn < rows) {
+        len_n = lens[rn];
+        base_n = gp[g_shift >= 0 ? (rn >> g_shift) : rn / G];
+      }
+    }
     if (r >= rows) continue;
-    const uint32_t len = lens[r];
+    if (!kMetaPf) len = lens[r];
     if (len > long_cut) continue;  // handled by rgcsr_spmv_long
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
     const uint32_t s = min(G, rows - g * G);
-    const uint32_t off = gp[g] + (r - g * G);
+    if (!kMetaPf) base = gp[g];
+    const uint32_t off = base + (r - g * G);
     const T* __restrict__ vp = values + off;
     const uint32_t* __restrict__ cp = columns + off;
     T acc = T(0);
@@ -248,14 +270,15 @@ __device__ __forceinline__ void lite_tiles(
                                     columns, x, long_cut, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
-template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false>
+template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false, bool kMetaPf = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles<T, kScaled, U, kPrefetchL2>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens,
-                                         values, columns, x, y, x_next, scale, long_cut);
+  lite_tiles_epi<T, U, kPrefetchL2, StoreEpi<T, kScaled>, kMetaPf>(
+      0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns, x, long_cut,
+      StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
 // Same kernel over the 256-row tiles [tile_begin, tile_end) only: the unit of
