@@ -286,7 +286,7 @@ spmvk_csr* hybrid_to_csr(const spmvk_hybrid* h, cudaStream_t s) {
 // then adds its own products sequentially in column order.  Per row this is
 // exactly the reference's sequence of roundings: ELL slots 0..K1-1, then the
 // row's COO entries in array order -> y bitwise equal to spmv_hybrid.
-template <class T>
+template <class T, int U>
 __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
@@ -294,7 +294,6 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
     T* __restrict__ y) {
   __shared__ T prod[kCooTile];
   __shared__ uint32_t prow[kCooTile];
-  constexpr int U = sizeof(T) == 8 ? 4 : 8;
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   const uint32_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -455,7 +454,10 @@ template <class T>
 void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s) {
   if (h->rows == 0) return;
   const uint64_t ntiles = (h->rows + kRowsPerTile - 1) / kRowsPerTile;
-  hybrid_spmv_kernel<T><<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
+  // 4-deep slot batches at full occupancy (32 registers) for both precisions:
+  // fp32 8-deep measured 2-9 % slower (27-pt 79.3 vs 77.5 us, 7-pt 512^3
+  // 1550 vs 1410 us; scripts/ab_formats.py, profiles/r01_k2_sweep3.md)
+  hybrid_spmv_kernel<T, 4><<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
       static_cast<uint32_t>(h->rows), static_cast<uint32_t>(h->k1),
       reinterpret_cast<const T*>(h->ell_values.p), h->ell_columns.p,
       h->coo ? h->tile_ptr.p : nullptr, h->coo_rows.p, h->coo_columns.p,
