@@ -348,6 +348,7 @@ def R():
             "ref_run_spmv_bench": (ci, [vp, ci, i64, ci, u64, vp]),
             "ref_slabs_build": (ci, [vp, ci, u64, i64, ci, ci, pp]),
             "ref_slabs_spmv": (ci, [vp, vp, vp]),
+            "ref_slabs_spmv_serial": (ci, [vp, vp, vp]),
             "ref_slabs_free": (None, [vp]),
             "ref_mm_parse": (ci, [C.c_char_p, u64, pp, C.POINTER(C.c_uint64)]),
             "ref_mm_write": (u64, [vp, C.c_char_p, u64]),

@@ -488,6 +488,26 @@ int ref_slabs_spmv(const void* h, const void* x, void* y) {
   });
 }
 
+// The same slabs run one after another on the calling thread: the reference's
+// single-core SpMV over all rows (its per-row work and order are unchanged).
+int ref_slabs_spmv_serial(const void* h, const void* x, void* y) {
+  return guard([&] {
+    const auto* s = static_cast<const RefSlabs*>(h);
+    for (std::size_t t = 0; t + 1 < s->row_begin.size(); ++t) {
+      const std::size_t r0 = s->row_begin[t], r1 = s->row_begin[t + 1];
+      if (s->prec == 4) {
+        std::span<const float> xs(static_cast<const float*>(x), s->cols);
+        std::span<float> ys(static_cast<float*>(y) + r0, r1 - r0);
+        if (s->fmt == 1) spmv_rgcsr(s->rf[t], xs, ys); else spmv_hybrid(s->hf[t], xs, ys);
+      } else {
+        std::span<const double> xs(static_cast<const double*>(x), s->cols);
+        std::span<double> ys(static_cast<double*>(y) + r0, r1 - r0);
+        if (s->fmt == 1) spmv_rgcsr(s->rd[t], xs, ys); else spmv_hybrid(s->hd[t], xs, ys);
+      }
+    }
+  });
+}
+
 void ref_slabs_free(void* h) { delete static_cast<RefSlabs*>(h); }
 
 }  // extern "C"
