@@ -12,7 +12,9 @@ ride along in ``variants``.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload 27pt-128|5pt-1024|powerlaw-8M|7pt-512]
 
-N > 1 (torchrun, one rank per GPU): the matrix is cut into group-aligned row
+N > 1 (torchrun, one rank per GPU): the workload defaults to BASELINE
+configs[4] (7-point 512^3, the iterated product the north star asks to scale
+near-linearly; strong scaling: the matrix is fixed), cut into group-aligned row
 slabs (paper_1012_2270_b200.partition), each step is one slab SpMV with the
 next x = y_k * 2^-4 computed in its epilogue, plus the exchange of x —
 `--exchange fused` (default: the epilogue itself stores each x row into the
@@ -201,7 +203,10 @@ def cpu_reference(workload, sample_reps, threads=None, fmt="rgcsr", G=32, prec=8
         a = orc.build_rgcsr(m, G, prec)
         run = lambda: orc.spmv_rgcsr(a, x)  # noqa: E731
         kind, used, cleanup = "port", 1, (lambda: None)
+    t = time.perf_counter()
     run()
+    # bounded sample: at most ~20 s of CPU SpMVs (config 5 is ~0.3 s per SpMV)
+    sample_reps = max(3, min(sample_reps, int(20.0 / max(time.perf_counter() - t, 1e-6))))
     times = []
     for _ in range(sample_reps):
         t = time.perf_counter()
@@ -368,7 +373,9 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="27pt-128", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: 27pt-128 (configs[1]) on one GPU; 7pt-512 (configs[4], the "
+                         "iterated, row-slab sharded config) under torchrun with N > 1")
     ap.add_argument("--cpu-reps", type=int, default=10)
     ap.add_argument("--distributed", action="store_true",
                     help="use the row-slab + NCCL path even at world size 1 (under torchrun)")
@@ -377,6 +384,9 @@ def main():
                          "halo send/recv, or fused (SpMV epilogue stores into peer windows "
                          "over NVLink + device barrier)")
     args = ap.parse_args()
+    if args.workload is None:
+        multi = int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1
+        args.workload = "7pt-512" if multi else "27pt-128"
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
