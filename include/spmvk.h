@@ -275,10 +275,11 @@ int spmvk_dist_open_local(const spmvk_window* const* windows, int rank, int worl
                           spmvk_dist** out);
 /* This rank's slab = global rows [row_begin, row_end) (its RgCSR holds
  * exactly those rows, global columns).  receive_ranges[2q], [2q+1]: global
- * rows [lo, hi) that rank q must receive every step -- its own slab for
- * itself, and for peers either everything (all-gather) or the rows their
- * slab reads (halo, partition.halo_plan).  Only the part inside this rank's
- * slab is sent. */
+ * rows [lo, hi) that rank q must receive every step: for peers either
+ * everything (all-gather) or the rows their slab reads (halo,
+ * partition.fused_receive_ranges).  Only the part inside this rank's slab is
+ * sent; the rank's own rows always go to its own window (its own entry is
+ * not consulted). */
 int spmvk_dist_set_rows(spmvk_dist* d, uint64_t row_begin, uint64_t row_end,
                         const uint64_t* receive_ranges);
 /* One step: y = A_slab x[cur] (slab-local y, device), x_next = y * scale

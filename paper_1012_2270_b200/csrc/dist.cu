@@ -150,16 +150,26 @@ void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, 
   epi.y = y;
   epi.scale = scale;
   epi.row0 = static_cast<uint32_t>(d->row_begin);
+  epi.self = reinterpret_cast<T*>(d->base[d->rank] + (1 - cur) * xb);
+  // interior: the slab rows no peer receives (halo plans put the peers'
+  // ranges at the slab edges); rows there take the single self store
+  uint64_t ilo = d->row_begin, ihi = d->row_end;
   int n = 0;
   for (int q = 0; q < d->world; ++q) {
+    if (q == d->rank) continue;
     const uint64_t lo = std::max(d->lo[q], d->row_begin), hi = std::min(d->hi[q], d->row_end);
     if (lo >= hi) continue;
     epi.ps.dst[n] = reinterpret_cast<T*>(d->base[q] + (1 - cur) * xb);
     epi.ps.lo[n] = static_cast<uint32_t>(lo);
     epi.ps.hi[n] = static_cast<uint32_t>(hi);
     ++n;
+    if (lo <= ilo) ilo = std::max(ilo, hi);
+    else if (hi >= ihi) ihi = std::min(ihi, lo);
+    else ihi = ilo;  // a range strictly inside the slab: no fast path
   }
   epi.ps.n = n;
+  epi.int_lo = static_cast<uint32_t>(ilo);
+  epi.int_hi = static_cast<uint32_t>(std::max(ilo, ihi));
   if (a->rows) {
     const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(a->group_size, 0xffffffffull));
     const int sh = pow2_shift(a->group_size);

@@ -163,22 +163,23 @@ struct PeerSet {
 template <class T>
 struct PeerEpi {
   T* __restrict__ y;
+  T* __restrict__ self;  // this rank's x_next buffer (every own row goes there)
   T scale;
-  uint32_t row0;  // global index of the slab's first row
-  PeerSet<T> ps;
+  uint32_t row0;           // global index of the slab's first row
+  uint32_t int_lo, int_hi;  // global rows no peer receives: self store only
+  PeerSet<T> ps;            // peers (not self) and the rows each receives
   __device__ __forceinline__ void operator()(uint32_t r, T acc) const {
     y[r] = acc;
     const T xs = mul_rn(acc, scale);
     const uint32_t gr = row0 + r;
+    self[gr] = xs;
+    if (gr >= int_lo && gr < int_hi) return;
 #pragma unroll
     for (int i = 0; i < kMaxPeers; ++i)
       if (i < ps.n && gr >= ps.lo[i] && gr < ps.hi[i]) ps.dst[i][gr] = xs;
   }
 };
 
-// kMetaPf: the row length and group pointer of the thread's NEXT tile row are
-// loaded while the current row runs, taking that dependent DRAM round trip
-// (length -> slots) off every row but the first.
 template <class T, int U, bool kPrefetchL2, class Epi, bool kMetaPf = false>
 __device__ __forceinline__ void lite_tiles_epi(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
