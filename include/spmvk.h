@@ -194,6 +194,7 @@ typedef struct {
   uint64_t artificial_zeros; /* FillReport: slots - fill_nnz */
   uint64_t bytes_single, bytes_double;
   int precision;
+  int ellpack;               /* 1: built by spmvk_ellpack_build (FillReport "ellpack") */
 } spmvk_hybrid_info;
 
 /* hybrid_split_cost / choose_ell_width (spmvkit/ellpack.hpp:143-166) over the
@@ -207,6 +208,13 @@ uint64_t spmvk_hybrid_split_cost(const uint64_t* lens, uint64_t n, uint64_t k);
  * std::nullopt (choose_ell_width).  EINVAL if k1 > max row length. */
 int spmvk_hybrid_build(const spmvk_csr* a, int64_t k1, int prec, void* stream,
                        spmvk_hybrid** out);
+/* build_ellpack<S>(m, slot_budget) (spmvkit/ellpack.hpp:84-107): a Hybrid
+ * handle with K1 = the maximum row length and no COO part, flagged ellpack
+ * (its FillReport is fill_report(EllpackMatrix): index words = slots).
+ * ERANGE "build_ellpack: R rows x width K exceeds the slot budget of B" when
+ * rows > slot_budget / K (the reference's default budget is 2^31). */
+int spmvk_ellpack_build(const spmvk_csr* a, uint64_t slot_budget, int prec, void* stream,
+                        spmvk_hybrid** out);
 int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info);
 /* EllpackMatrix values/columns (slot-major, rows*K1) + CooArrays
  * rows/columns/values (coo_nnz); any pointer may be NULL. */
@@ -222,6 +230,30 @@ int spmvk_hybrid_spmv_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, d
                           uint64_t ny, void* stream);
 int spmvk_hybrid_spmv_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
                           uint64_t ny, void* stream);
+/* spmv_ellpack(h.ell, x, y) (ellpack.hpp:110-123): y = the ELL part only,
+ * every slot walked (pads add 0 * x[0]); EINVAL "spmv_ellpack: dimension
+ * mismatch" unless nx == cols and ny == rows. */
+int spmvk_hybrid_spmv_ell_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, void* stream);
+int spmvk_hybrid_spmv_ell_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, void* stream);
+/* spmv_coo(h.coo, x, y) (ellpack.hpp:132-141): y[row] += v * x[col] for the
+ * COO part in array order (accumulates into the caller's y); EINVAL
+ * "spmv_coo: entry outside x/y dimensions" if an entry's row >= ny or
+ * column >= nx. */
+int spmvk_hybrid_spmv_coo_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, void* stream);
+int spmvk_hybrid_spmv_coo_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, void* stream);
+/* The same two parts on host spans (x, y in host memory; synchronous). */
+int spmvk_hybrid_spmv_ell_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx,
+                                   double* y, uint64_t ny);
+int spmvk_hybrid_spmv_ell_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                                   uint64_t ny);
+int spmvk_hybrid_spmv_coo_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx,
+                                   double* y, uint64_t ny);
+int spmvk_hybrid_spmv_coo_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                                   uint64_t ny);
 int spmvk_hybrid_spmv_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
                                uint64_t ny);
 int spmvk_hybrid_spmv_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,

@@ -16,6 +16,9 @@
 //   spmv_rgcsr(a, x, y, &madds)         rgcsr.hpp:75-77 (+ vector overload :99-105)
 //   build_hybrid<S>(m, k1)              ellpack.hpp:170-172
 //   spmv_hybrid(h, x, y)                ellpack.hpp:206-210
+//   build_ellpack<S>(m, budget)         ellpack.hpp:84-107
+//   spmv_ellpack(h, x, y)               ellpack.hpp:110-130
+//   spmv_coo(h, x, y)                   ellpack.hpp:132-141
 //   choose_ell_width(lens)              ellpack.hpp:153
 //   hybrid_split_cost(lens, k)          ellpack.hpp:145
 // The span overloads take HOST memory (H2D / D2H inside, synchronous).  For
@@ -207,14 +210,14 @@ class HybridMatrix {
 
   template <class S, class T>
   friend HybridMatrix<S> build_hybrid(const T&, std::optional<std::size_t>);
+  template <class S, class T>
+  friend HybridMatrix<S> build_ellpack(const T&, std::size_t);
+  template <class S>
+  friend HybridMatrix<S> adopt_hybrid(spmvk_hybrid*);
 };
 
-template <class Scalar = double, class Triplets>
-HybridMatrix<Scalar> build_hybrid(const Triplets& m, std::optional<std::size_t> k1 = std::nullopt) {
-  auto csr = detail::upload(m);
-  spmvk_hybrid* h = nullptr;
-  detail::check(spmvk_hybrid_build(csr.get(), k1 ? static_cast<std::int64_t>(*k1) : -1,
-                                   detail::prec<Scalar>(), nullptr, &h));
+template <class Scalar>
+HybridMatrix<Scalar> adopt_hybrid(spmvk_hybrid* h) {
   HybridMatrix<Scalar> a;
   a.h_ = std::shared_ptr<spmvk_hybrid>(h, typename HybridMatrix<Scalar>::Del{});
   detail::check(spmvk_hybrid_get_info(h, &a.info_));
@@ -222,6 +225,28 @@ HybridMatrix<Scalar> build_hybrid(const Triplets& m, std::optional<std::size_t> 
   a.num_cols = a.info_.num_cols;
   a.slots_per_row = a.info_.ell_width;
   return a;
+}
+
+inline constexpr std::size_t kDefaultEllSlotBudget = std::size_t{1} << 31;
+
+// build_ellpack<S>(m, slot_budget) (ellpack.hpp:84-107): the ELL-only Hybrid;
+// throws std::runtime_error past the slot budget, like the reference.
+template <class Scalar = double, class Triplets>
+HybridMatrix<Scalar> build_ellpack(const Triplets& m,
+                                   std::size_t slot_budget = kDefaultEllSlotBudget) {
+  auto csr = detail::upload(m);
+  spmvk_hybrid* h = nullptr;
+  detail::check(spmvk_ellpack_build(csr.get(), slot_budget, detail::prec<Scalar>(), nullptr, &h));
+  return adopt_hybrid<Scalar>(h);
+}
+
+template <class Scalar = double, class Triplets>
+HybridMatrix<Scalar> build_hybrid(const Triplets& m, std::optional<std::size_t> k1 = std::nullopt) {
+  auto csr = detail::upload(m);
+  spmvk_hybrid* h = nullptr;
+  detail::check(spmvk_hybrid_build(csr.get(), k1 ? static_cast<std::int64_t>(*k1) : -1,
+                                   detail::prec<Scalar>(), nullptr, &h));
+  return adopt_hybrid<Scalar>(h);
 }
 
 template <class Scalar>
@@ -237,6 +262,37 @@ std::vector<Scalar> spmv_hybrid(const HybridMatrix<Scalar>& h, const std::vector
   std::vector<Scalar> y(h.num_rows);
   spmv_hybrid(h, std::span<const Scalar>(x), std::span<Scalar>(y));
   return y;
+}
+
+// spmv_ellpack(h.ell, x, y) (ellpack.hpp:110-130): the ELL part of a Hybrid
+// (all of an ELLPACK); every slot walked, as the reference.
+template <class Scalar>
+void spmv_ellpack(const HybridMatrix<Scalar>& h, std::span<const Scalar> x, std::span<Scalar> y) {
+  if constexpr (std::is_same_v<Scalar, double>)
+    detail::check(spmvk_hybrid_spmv_ell_host_f64(h.handle(), x.data(), x.size(), y.data(),
+                                                 y.size()));
+  else
+    detail::check(spmvk_hybrid_spmv_ell_host_f32(h.handle(), x.data(), x.size(), y.data(),
+                                                 y.size()));
+}
+
+template <class Scalar>
+std::vector<Scalar> spmv_ellpack(const HybridMatrix<Scalar>& h, const std::vector<Scalar>& x) {
+  std::vector<Scalar> y(h.num_rows);
+  spmv_ellpack(h, std::span<const Scalar>(x), std::span<Scalar>(y));
+  return y;
+}
+
+// spmv_coo(h.coo, x, y) (ellpack.hpp:132-141): y[row] += v * x[col] over the
+// COO part in array order; std::invalid_argument for entries outside x / y.
+template <class Scalar>
+void spmv_coo(const HybridMatrix<Scalar>& h, std::span<const Scalar> x, std::span<Scalar> y) {
+  if constexpr (std::is_same_v<Scalar, double>)
+    detail::check(spmvk_hybrid_spmv_coo_host_f64(h.handle(), x.data(), x.size(), y.data(),
+                                                 y.size()));
+  else
+    detail::check(spmvk_hybrid_spmv_coo_host_f32(h.handle(), x.data(), x.size(), y.data(),
+                                                 y.size()));
 }
 
 }  // namespace spmvkit::gpu

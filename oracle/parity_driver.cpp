@@ -95,6 +95,32 @@ std::string hybrid_case(const TripletMatrix& m, std::optional<std::size_t> k1, s
   return {};
 }
 
+// build_ellpack / spmv_ellpack / spmv_coo through the shim vs the reference
+// (ellpack.hpp:84-141): arrays, the ELL and COO parts separately (the COO
+// part accumulating into a nonzero y), and the slot-budget error.
+template <class S>
+std::string ellpack_case(const TripletMatrix& m, std::uint64_t xseed) {
+  const auto ref = build_ellpack<S>(m);
+  const auto dev = gpu::build_ellpack<S>(m);
+  if (dev.slots_per_row != ref.slots_per_row) return "ELLPACK width differs";
+  const auto h = dev.to_host();
+  if (!same_bits(h.ell_values, ref.values) || !same_u32(h.ell_columns, ref.columns))
+    return "ELLPACK arrays differ";
+  const auto xd = random_vector(m.num_cols(), xseed);
+  const std::vector<S> x(xd.begin(), xd.end());
+  if (!same_bits(gpu::spmv_ellpack(dev, x), spmv_ellpack(ref, x))) return "spmv_ellpack differs";
+  if (m.nnz() == 0) return {};
+  const auto hr = build_hybrid<S>(m, std::size_t{1});
+  const auto hd = gpu::build_hybrid<S>(m, std::size_t{1});
+  if (!same_bits(gpu::spmv_ellpack(hd, x), spmv_ellpack(hr.ell, x))) return "h.ell part differs";
+  std::vector<S> y1(m.num_rows()), y2(m.num_rows());
+  for (std::size_t i = 0; i < y1.size(); ++i) y1[i] = y2[i] = static_cast<S>(0.25 * i - 3.0);
+  spmv_coo(hr.coo, std::span<const S>(x), std::span<S>(y1));
+  gpu::spmv_coo(hd, std::span<const S>(x), std::span<S>(y2));
+  if (!same_bits(y1, y2)) return "spmv_coo differs";
+  return {};
+}
+
 }  // namespace
 
 int main() {
@@ -129,6 +155,20 @@ int main() {
       if (!w.empty()) return w;
     }
     return hybrid_case<double>(m, std::nullopt, 1);
+  });
+  criterion("ellpack + separate ELL / COO parts fp64/fp32: 100 random_case matrices", [] {
+    for (std::uint64_t s = 0; s < 100; ++s) {
+      const auto m = random_case(s, 64);
+      auto w = ellpack_case<double>(m, s);
+      if (w.empty()) w = ellpack_case<float>(m, s + 1);
+      if (!w.empty()) return w + " at seed " + std::to_string(s);
+    }
+    try {  // test_formats.cpp:82-85
+      gpu::build_ellpack<double>(banded_matrix(100, 2, 1), 0);
+    } catch (const std::runtime_error&) {
+      return std::string();
+    }
+    return std::string("no throw past the slot budget");
   });
   criterion("errors: G == 0 and dimension mismatch throw std::invalid_argument", [] {
     const auto m = random_case(3, 64);

@@ -28,13 +28,15 @@ cint = C.c_int
 class RgcsrInfo(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "num_rows", "num_cols", "group_size", "num_groups", "slots", "nnz",
-        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int)]
+        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int),
+                                                                ("ellpack", C.c_int)]
 
 
 class HybridInfo(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "num_rows", "num_cols", "ell_width", "ell_slots", "coo_nnz", "nnz", "fill_nnz",
-        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int)]
+        "artificial_zeros", "bytes_single", "bytes_double")] + [("precision", C.c_int),
+                                                                ("ellpack", C.c_int)]
 
 
 # name -> (restype, argtypes); every symbol include/spmvk.h declares.
@@ -86,6 +88,15 @@ SIGNATURES = {
     "spmvk_dot_f64": (cint, [vp, vp, u64, vp, vp]),
     "spmvk_cg_update_f64": (cint, [u64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvk_cg_direction_f64": (cint, [u64, vp, vp, vp, vp, vp]),
+    "spmvk_ellpack_build": (cint, [vp, u64, cint, vp, C.POINTER(vp)]),
+    "spmvk_hybrid_spmv_ell_f64": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_ell_f32": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_coo_f64": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_coo_f32": (cint, [vp, vp, u64, vp, u64, vp]),
+    "spmvk_hybrid_spmv_ell_host_f64": (cint, [vp, vp, u64, vp, u64]),
+    "spmvk_hybrid_spmv_ell_host_f32": (cint, [vp, vp, u64, vp, u64]),
+    "spmvk_hybrid_spmv_coo_host_f64": (cint, [vp, vp, u64, vp, u64]),
+    "spmvk_hybrid_spmv_coo_host_f32": (cint, [vp, vp, u64, vp, u64]),
     "spmvk_window_create": (cint, [u64, cint, C.POINTER(vp)]),
     "spmvk_window_ipc_handle": (cint, [vp, vp]),
     "spmvk_window_x": (cint, [vp, cint, C.POINTER(vp)]),

@@ -244,6 +244,8 @@ struct spmvk_hybrid {
   uint64_t rows = 0, cols = 0, k1 = 0, coo = 0, nnz = 0;
   uint64_t fill_nnz = 0;  // FillReport nnz: ell_nnz recount + coo (fill.hpp:67-72)
   int prec = SPMVK_F64;
+  bool ellpack = false;  // built by build_ellpack: fill_report names it "ellpack"
+  uint64_t coo_max_row = 0, coo_max_col = 0;  // spmv_coo's bounds check (ellpack.hpp:135)
   spmvk::DevBuf<unsigned char> ell_values, coo_values;
   spmvk::DevBuf<uint32_t> ell_columns, coo_rows, coo_columns;
   // tile_ptr[t]: first COO entry of row tile t (256 rows); kernel metadata,

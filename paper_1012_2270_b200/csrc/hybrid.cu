@@ -156,6 +156,15 @@ __global__ void coo_tile_bounds(uint64_t ntiles, uint64_t rows, uint64_t n,
   }
 }
 
+__global__ void coo_max_column(uint64_t n, const uint32_t* __restrict__ cc, unsigned* out) {
+  unsigned m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, cc[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // FillReport's ELL nnz (fill.hpp:61-65 -> ell_nnz, ellpack.hpp:55-78): the
 // reference recounts real slots from the layout — the first non-increasing
 // column starts the pad region, and a lone stored zero at column 0 counts as
@@ -286,7 +295,7 @@ spmvk_csr* hybrid_to_csr(const spmvk_hybrid* h, cudaStream_t s) {
 // then adds its own products sequentially in column order.  Per row this is
 // exactly the reference's sequence of roundings: ELL slots 0..K1-1, then the
 // row's COO entries in array order -> y bitwise equal to spmv_hybrid.
-template <class T, int U>
+template <class T, int U, bool kAccum = false>
 __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
@@ -300,6 +309,7 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
     const uint32_t r = tile * kRowsPerTile + threadIdx.x;
     const bool live = r < rows;
     T acc = T(0);
+    if (kAccum && live) acc = y[r];  // spmv_coo: y += COO x (ellpack.hpp:132-141)
     if (live) {
       uint32_t j = 0;
       for (; j + U <= k1; j += U) {
@@ -439,6 +449,19 @@ spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
   if (prec == SPMVK_F64) fill<double, double>(h.get(), a, s);
   else if (a->val_prec == SPMVK_F64) fill<float, double>(h.get(), a, s);
   else fill<float, float>(h.get(), a, s);
+  if (h->coo) {  // bounds of the COO part, for spmv_coo's check
+    DevBuf<unsigned> mc(1);
+    SPMVK_CUDA(cudaMemsetAsync(mc.p, 0, 4, s));
+    coo_max_column<<<persistent_grid((h->coo + 255) / 256, 4), 256, 0, s>>>(
+        h->coo, h->coo_columns.p, mc.p);
+    SPMVK_LAUNCH("coo_max_column");
+    uint32_t mr = 0, mcol = 0;
+    SPMVK_CUDA(cudaMemcpyAsync(&mr, h->coo_rows.p + h->coo - 1, 4, cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaMemcpyAsync(&mcol, mc.p, 4, cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    h->coo_max_row = mr;  // COO is sorted by row
+    h->coo_max_col = mcol;
+  }
   return h.release();
 }
 
@@ -450,17 +473,26 @@ void check_args(const spmvk_hybrid* h, uint64_t nx, uint64_t ny) {
     fail(SPMVK_EINVAL, "spmv_hybrid: handle precision differs from the entry point");
 }
 
+// part: kBoth = spmv_hybrid, kEll = spmv_ellpack(h.ell), kCoo = spmv_coo(h.coo)
+// (accumulating into y, rows limited to the caller's y length).
+enum class Part { kBoth, kEll, kCoo };
+
 template <class T>
-void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s) {
-  if (h->rows == 0) return;
-  const uint64_t ntiles = (h->rows + kRowsPerTile - 1) / kRowsPerTile;
+void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part = Part::kBoth,
+            uint64_t rows_limit = ~0ull) {
+  const uint64_t rows = std::min<uint64_t>(h->rows, rows_limit);
+  if (rows == 0) return;
+  if (part == Part::kCoo && !h->coo) return;
+  const uint64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
+  const uint32_t k1 = part == Part::kCoo ? 0u : static_cast<uint32_t>(h->k1);
+  const uint32_t* tp = part != Part::kEll && h->coo ? h->tile_ptr.p : nullptr;
   // 4-deep slot batches at full occupancy (32 registers) for both precisions:
   // fp32 8-deep measured 2-9 % slower (27-pt 79.3 vs 77.5 us, 7-pt 512^3
   // 1550 vs 1410 us; scripts/ab_formats.py, profiles/r01_k2_sweep3.md)
-  hybrid_spmv_kernel<T, 4><<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
-      static_cast<uint32_t>(h->rows), static_cast<uint32_t>(h->k1),
-      reinterpret_cast<const T*>(h->ell_values.p), h->ell_columns.p,
-      h->coo ? h->tile_ptr.p : nullptr, h->coo_rows.p, h->coo_columns.p,
+  auto kern = part == Part::kCoo ? hybrid_spmv_kernel<T, 4, true> : hybrid_spmv_kernel<T, 4>;
+  kern<<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
+      static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
+      h->ell_columns.p, tp, h->coo_rows.p, h->coo_columns.p,
       reinterpret_cast<const T*>(h->coo_values.p), x, y);
   SPMVK_LAUNCH("hybrid_spmv_kernel");
 }
@@ -472,6 +504,38 @@ void spmv_host(const spmvk_hybrid* h, const T* x, uint64_t nx, T* y, uint64_t ny
   st.reserve(nx * sizeof(T), ny * sizeof(T));
   if (nx) SPMVK_CUDA(cudaMemcpyAsync(st.x.p, x, nx * sizeof(T), cudaMemcpyHostToDevice, st.stream));
   launch<T>(h, reinterpret_cast<const T*>(st.x.p), reinterpret_cast<T*>(st.y.p), st.stream);
+  if (ny) SPMVK_CUDA(cudaMemcpyAsync(y, st.y.p, ny * sizeof(T), cudaMemcpyDeviceToHost, st.stream));
+  SPMVK_CUDA(cudaStreamSynchronize(st.stream));
+}
+
+template <class T>
+void spmv_part(const spmvk_hybrid* h, const T* x, uint64_t nx, T* y, uint64_t ny, Part part,
+               cudaStream_t s) {
+  if (!h) fail(SPMVK_EINVAL, "null Hybrid handle");
+  if (h->prec != static_cast<int>(sizeof(T)))
+    fail(SPMVK_EINVAL, "spmv_hybrid: handle precision differs from the entry point");
+  if (part == Part::kEll) {
+    if (nx != h->cols || ny != h->rows) fail(SPMVK_EINVAL, "spmv_ellpack: dimension mismatch");
+    launch<T>(h, x, y, s, Part::kEll);
+    return;
+  }
+  if (h->coo && (h->coo_max_row >= ny || h->coo_max_col >= nx))
+    fail(SPMVK_EINVAL, "spmv_coo: entry outside x/y dimensions");
+  launch<T>(h, x, y, s, Part::kCoo, ny);
+}
+
+// Host spans: x (and, for the accumulating COO part, y) staged through the
+// per-thread device buffers.
+template <class T>
+void spmv_part_host(const spmvk_hybrid* h, const T* x, uint64_t nx, T* y, uint64_t ny,
+                    Part part) {
+  HostStage& st = host_stage();
+  st.reserve(nx * sizeof(T), ny * sizeof(T));
+  if (nx) SPMVK_CUDA(cudaMemcpyAsync(st.x.p, x, nx * sizeof(T), cudaMemcpyHostToDevice, st.stream));
+  if (part == Part::kCoo && ny)
+    SPMVK_CUDA(cudaMemcpyAsync(st.y.p, y, ny * sizeof(T), cudaMemcpyHostToDevice, st.stream));
+  spmv_part<T>(h, reinterpret_cast<const T*>(st.x.p), nx, reinterpret_cast<T*>(st.y.p), ny, part,
+               st.stream);
   if (ny) SPMVK_CUDA(cudaMemcpyAsync(y, st.y.p, ny * sizeof(T), cudaMemcpyDeviceToHost, st.stream));
   SPMVK_CUDA(cudaStreamSynchronize(st.stream));
 }
@@ -515,6 +579,24 @@ int spmvk_hybrid_build(const spmvk_csr* a, int64_t k1, int prec, void* stream,
   });
 }
 
+int spmvk_ellpack_build(const spmvk_csr* a, uint64_t slot_budget, int prec, void* stream,
+                        spmvk_hybrid** out) {
+  return guarded([&] {
+    require_device();
+    if (!out || !a) fail(SPMVK_EINVAL, "null argument");
+    unsigned mx = 0, mn = 0;
+    row_length_range(a, 0, a->rows, &mx, &mn, as_stream(stream));
+    const uint64_t k = mx;
+    if (k != 0 && a->rows > slot_budget / k)  // ellpack.hpp:88-93
+      fail(SPMVK_ERANGE, "build_ellpack: " + std::to_string(a->rows) + " rows x width " +
+                             std::to_string(k) + " exceeds the slot budget of " +
+                             std::to_string(slot_budget));
+    spmvk_hybrid* h = build(a, static_cast<int64_t>(k), prec, as_stream(stream));
+    h->ellpack = true;
+    *out = h;
+  });
+}
+
 int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info) {
   return guarded([&] {
     if (!h || !info) fail(SPMVK_EINVAL, "null argument");
@@ -532,6 +614,7 @@ int spmvk_hybrid_get_info(const spmvk_hybrid* h, spmvk_hybrid_info* info) {
     info->bytes_single = slots * 4 + words * 4;
     info->bytes_double = slots * 8 + words * 4;
     info->precision = h->prec;
+    info->ellpack = h->ellpack ? 1 : 0;
   });
 }
 
@@ -585,6 +668,46 @@ int spmvk_hybrid_spmv_host_f64(const spmvk_hybrid* h, const double* x, uint64_t 
 int spmvk_hybrid_spmv_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
                                uint64_t ny) {
   return guarded([&] { spmv_host<float>(h, x, nx, y, ny); });
+}
+
+int spmvk_hybrid_spmv_ell_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, void* stream) {
+  return guarded([&] { spmv_part<double>(h, x, nx, y, ny, Part::kEll, as_stream(stream)); });
+}
+
+int spmvk_hybrid_spmv_ell_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, void* stream) {
+  return guarded([&] { spmv_part<float>(h, x, nx, y, ny, Part::kEll, as_stream(stream)); });
+}
+
+int spmvk_hybrid_spmv_coo_f64(const spmvk_hybrid* h, const double* x, uint64_t nx, double* y,
+                              uint64_t ny, void* stream) {
+  return guarded([&] { spmv_part<double>(h, x, nx, y, ny, Part::kCoo, as_stream(stream)); });
+}
+
+int spmvk_hybrid_spmv_coo_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                              uint64_t ny, void* stream) {
+  return guarded([&] { spmv_part<float>(h, x, nx, y, ny, Part::kCoo, as_stream(stream)); });
+}
+
+int spmvk_hybrid_spmv_ell_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx,
+                                   double* y, uint64_t ny) {
+  return guarded([&] { spmv_part_host<double>(h, x, nx, y, ny, Part::kEll); });
+}
+
+int spmvk_hybrid_spmv_ell_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                                   uint64_t ny) {
+  return guarded([&] { spmv_part_host<float>(h, x, nx, y, ny, Part::kEll); });
+}
+
+int spmvk_hybrid_spmv_coo_host_f64(const spmvk_hybrid* h, const double* x, uint64_t nx,
+                                   double* y, uint64_t ny) {
+  return guarded([&] { spmv_part_host<double>(h, x, nx, y, ny, Part::kCoo); });
+}
+
+int spmvk_hybrid_spmv_coo_host_f32(const spmvk_hybrid* h, const float* x, uint64_t nx, float* y,
+                                   uint64_t ny) {
+  return guarded([&] { spmv_part_host<float>(h, x, nx, y, ny, Part::kCoo); });
 }
 
 void spmvk_hybrid_destroy(spmvk_hybrid* h) { delete h; }

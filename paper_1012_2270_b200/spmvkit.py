@@ -449,6 +449,54 @@ def build_hybrid(m, k1: Optional[int] = None, precision=F64, stream: int = 0) ->
     return HybridMatrix(h.value)
 
 
+K_DEFAULT_ELL_SLOT_BUDGET = 1 << 31  # kDefaultEllSlotBudget (ellpack.hpp:80)
+
+
+def build_ellpack(m, slot_budget: int = K_DEFAULT_ELL_SLOT_BUDGET, precision=F64,
+                  stream: int = 0) -> HybridMatrix:
+    """build_ellpack<S>(m, slot_budget) (ellpack.hpp:84-107): ELLPACK of width
+    K = max row length (a Hybrid handle without COO, fill_report "ellpack").
+    Raises SpmvkRuntimeError (std::runtime_error) past the slot budget."""
+    a = _as_csr(m)
+    h = C.c_void_p()
+    _check(lib().spmvk_ellpack_build(a._h, int(slot_budget), _prec(precision), stream or None,
+                                     C.byref(h)))
+    return HybridMatrix(h.value)
+
+
+def _hybrid_part(fn: str, h: HybridMatrix, x, y, stream, need_y: bool):
+    if _is_torch(x):
+        if need_y and y is None:
+            raise InvalidArgument(f"{fn}: y is required (it accumulates)")
+        return _device_call(f"spmvk_hybrid_{fn}", h._h, x, y, h.num_rows, h.num_cols,
+                            h.precision, stream)
+    dt = _dtype(h.precision)
+    x = np.ascontiguousarray(x)
+    if x.dtype != dt:
+        raise InvalidArgument(f"{fn}: handle precision differs from the x dtype")
+    if y is None:
+        if need_y:
+            raise InvalidArgument(f"{fn}: y is required (it accumulates)")
+        y = np.empty(h.num_rows, dt)
+    if not (isinstance(y, np.ndarray) and y.dtype == dt and y.flags.c_contiguous):
+        raise InvalidArgument(f"{fn}: y must be a contiguous array of the handle precision")
+    sfx = "f32" if h.precision == F32 else "f64"
+    _check(getattr(lib(), f"spmvk_hybrid_{fn}_host_{sfx}")(h._h, _ptr(x), x.size, _ptr(y),
+                                                           y.size))
+    return y
+
+
+def spmv_ellpack(h: HybridMatrix, x, y=None, stream: Optional[int] = None):
+    """spmv_ellpack(h.ell, x, y) (ellpack.hpp:110-130): the ELL part only."""
+    return _hybrid_part("spmv_ell", h, x, y, stream, need_y=False)
+
+
+def spmv_coo(h: HybridMatrix, x, y, stream: Optional[int] = None):
+    """spmv_coo(h.coo, x, y) (ellpack.hpp:132-141): y[row] += v * x[col] over
+    the COO part in array order, in place."""
+    return _hybrid_part("spmv_coo", h, x, y, stream, need_y=True)
+
+
 def spmv_hybrid(h: HybridMatrix, x, y=None, stream: Optional[int] = None):
     """spmv_hybrid(h, x, y) (ellpack.hpp:205-217)."""
     if _is_torch(x):
@@ -511,6 +559,11 @@ def fill_report(a) -> FillReport:
     if isinstance(a, RgcsrMatrix):
         return FillReport("rgcsr", i.slots, i.nnz, i.artificial_zeros,
                           _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
+    if isinstance(a, HybridMatrix) and i.ellpack:
+        # fill_report(EllpackMatrix) (fill.hpp:61-64): nnz = ell_nnz recount, words = slots
+        az = i.ell_slots - i.fill_nnz
+        return FillReport("ellpack", i.ell_slots, i.fill_nnz, az, _fill_percent(az, i.fill_nnz),
+                          i.ell_slots * 8, i.ell_slots * 12)
     if isinstance(a, HybridMatrix):
         # the reference recounts ELL nnz from the layout (ell_nnz, ellpack.hpp:55-78)
         return FillReport("hybrid", i.ell_slots + i.coo_nnz, i.fill_nnz, i.artificial_zeros,

@@ -18,4 +18,4 @@ def test_reference_inputs_through_cpp_shim(cuda):
     r = subprocess.run([DRIVER], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 5
+    assert r.stdout.count("PASS") == 6 and "FAIL" not in r.stdout

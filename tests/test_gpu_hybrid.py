@@ -130,6 +130,7 @@ def test_round_trip_through_every_format(cuda):
         h = sk.build_hybrid(m)
         assert h.info.fill_nnz == om.nnz  # ell_nnz + coo == nnz without stored zeros
         assert _same(sk.to_triplets(h), om), seed
+        assert _same(sk.to_triplets(sk.build_ellpack(m)), om), seed
 
 
 def test_hybrid_to_triplets_drops_lone_stored_zero_like_reference(cuda):
@@ -142,3 +143,86 @@ def test_hybrid_to_triplets_drops_lone_stored_zero_like_reference(cuda):
         r = orc.RefMatrix.from_csr(om)
         h = r.hybrid()
         assert h["artificial_zeros"] == sk.fill_report(sk.build_hybrid(triplets(om))).artificial_zeros
+
+
+# ------------------------------------------------ ELLPACK and the separate parts
+ONES_Y = [3, 3, 4, 5, 6, 15, 30, 25]  # kExampleOnesResult (test_matrix_core.cpp:88-91)
+
+
+def test_ellpack_example_and_shapes(cuda, golden):
+    """tests/test_formats.cpp:60-94 (build_ellpack, fill, budget, spmv_ellpack)."""
+    m = triplets(golden_csr(golden["example8"], "m"))
+    a = sk.build_ellpack(m)
+    assert a.slots_per_row == 3 and a.info.ell_slots == 24 and a.coo_nnz() == 0
+    f = sk.fill_report(a)
+    assert (f.format_name, f.artificial_zeros, f.stored_slots, f.nnz) == ("ellpack", 11, 24, 13)
+    assert (f.bytes_single, f.bytes_double) == (24 * 8, 24 * 12)  # index words = slots
+    assert a.to_host()["ell_values"].tolist() == [1, 3, 4, 5, 6, 7, 9, 12,
+                                                  2, 0, 0, 0, 0, 8, 10, 13,
+                                                  0, 0, 0, 0, 0, 0, 11, 0]
+    ident = sk.canonicalize([(i, i, 1.0) for i in range(5)], 5, 5)
+    assert sk.fill_report(sk.build_ellpack(ident)).artificial_zeros == 0
+    skew = sk.canonicalize([(0, 0, 1.0), (0, 1, 1.0), (0, 2, 1.0), (0, 3, 1.0), (1, 1, 2.0),
+                            (2, 2, 3.0), (3, 0, 4.0)], 4, 4)
+    b = sk.build_ellpack(skew)
+    assert (b.slots_per_row, b.info.ell_slots, sk.fill_report(b).artificial_zeros) == (4, 16, 9)
+    with pytest.raises(sk.SpmvkRuntimeError, match="exceeds the slot budget of 16"):
+        sk.build_ellpack(m, 16)
+    sk.build_ellpack(m, 24)
+    assert sk.spmv_ellpack(a, np.ones(8)).tolist() == ONES_Y
+    assert sk.spmv_ellpack(a, np.zeros(8)).tolist() == [0.0] * 8
+    one = sk.canonicalize([(0, 2, 7.0)], 1, 3)
+    assert sk.spmv_ellpack(sk.build_ellpack(one), np.array([0, 0, 5.0])).tolist() == [35.0]
+    t = sk.to_triplets(a)  # test_formats.cpp:318
+    assert t.row_ptr.tolist() == m.row_ptr.tolist() and t.col.tolist() == m.col.tolist()
+    assert t.val.tolist() == m.val.tolist()
+    with pytest.raises(sk.InvalidArgument, match="spmv_ellpack: dimension mismatch"):
+        sk.spmv_ellpack(a, np.ones(9))
+
+
+def test_spmv_coo_accumulates(cuda, golden):
+    """tests/test_formats.cpp:96-122: the COO part adds into y in array order."""
+    single = sk.build_hybrid(sk.canonicalize([(0, 0, 2.0)], 1, 1), 0)  # all entries in COO
+    y = np.array([1.0])
+    sk.spmv_coo(single, np.array([3.0]), y)
+    assert y.tolist() == [7.0]
+    empty = sk.build_hybrid(sk.canonicalize([(0, 0, 2.0)], 1, 1), 1)  # COO part empty
+    sk.spmv_coo(empty, np.array([3.0]), y)
+    assert y.tolist() == [7.0]
+    m = triplets(golden_csr(golden["example8"], "m"))
+    h = sk.build_hybrid(m, 0)
+    y = np.zeros(8)
+    sk.spmv_coo(h, np.ones(8), y)
+    assert y.tolist() == ONES_Y
+    yd = torch.zeros(8, dtype=torch.float64, device="cuda")
+    sk.spmv_coo(h, dev(np.ones(8)), yd)
+    assert yd.cpu().numpy().tolist() == ONES_Y
+    with pytest.raises(sk.InvalidArgument, match="spmv_coo: entry outside x/y dimensions"):
+        sk.spmv_coo(h, np.ones(8), np.zeros(7))
+    with pytest.raises(sk.InvalidArgument, match="spmv_coo: entry outside x/y dimensions"):
+        sk.spmv_coo(h, np.ones(7), np.zeros(8))
+    longer = np.full(10, 5.0)  # rows past the matrix are left alone
+    sk.spmv_coo(h, np.ones(8), longer)
+    assert longer.tolist() == [v + 5.0 for v in ONES_Y] + [5.0, 5.0]
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_parts_compose_to_spmv_hybrid(cuda, golden, prec):
+    """spmv_ellpack(h.ell) then spmv_coo(h.coo) is spmv_hybrid (ellpack.hpp:
+    205-210), bitwise, host and device, on the 200 acceptance matrices."""
+    g = golden["acceptance"]
+    dt = np.float64 if prec == 8 else np.float32
+    for seed in range(0, 200, 3):
+        m = triplets(golden_csr(g, f"a{seed}"))
+        if len(m.col) == 0:
+            continue
+        x = g[f"a{seed}_xi"].astype(dt)
+        for k1 in (None, 1):
+            h = sk.build_hybrid(m, k1, prec)
+            want = sk.spmv_hybrid(h, x)
+            y = sk.spmv_ellpack(h, x)
+            sk.spmv_coo(h, x, y)
+            assert bitwise(y, want), (seed, k1)
+            yd = sk.spmv_ellpack(h, dev(x))
+            sk.spmv_coo(h, dev(x), yd)
+            assert bitwise(yd.cpu().numpy(), want), (seed, k1)
