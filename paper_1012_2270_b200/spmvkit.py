@@ -554,11 +554,15 @@ def to_triplets(a) -> TripletMatrix:
 
 # ---------------------------------------------------------------- accounting
 def fill_report(a) -> FillReport:
-    """fill_report (fill.hpp:52-95) for RgCSR and Hybrid handles."""
-    i = a.info
+    """fill_report (fill.hpp:52-95) for CSR, RgCSR, ELLPACK and Hybrid handles."""
+    i = getattr(a, "info", None)
     if isinstance(a, RgcsrMatrix):
         return FillReport("rgcsr", i.slots, i.nnz, i.artificial_zeros,
                           _fill_percent(i.artificial_zeros, i.nnz), i.bytes_single, i.bytes_double)
+    if isinstance(a, CsrMatrix):  # fill_report(CsrMatrix) (fill.hpp:52-55)
+        n = a.nnz()
+        words = n + a.num_rows + 1
+        return FillReport("csr", n, n, 0, 0.0, n * 4 + words * 4, n * 8 + words * 4)
     if isinstance(a, HybridMatrix) and i.ellpack:
         # fill_report(EllpackMatrix) (fill.hpp:61-64): nnz = ell_nnz recount, words = slots
         az = i.ell_slots - i.fill_nnz
@@ -577,3 +581,113 @@ def measured_gflops(nnz: int, seconds: float) -> float:
     if not seconds > 0.0:
         raise InvalidArgument(f"measured_gflops: seconds must be positive, got {seconds}")
     return 2.0 * nnz / seconds / 1e9
+
+
+# ---------------------------------------------------------------- bench harness
+class ChecksumError(RuntimeError):
+    """spmvkit::ChecksumError (bench.hpp:33-37): a format disagrees with the oracle."""
+
+
+FORMAT_KINDS = ("csr", "ellpack", "coo", "hybrid", "bcsr", "rgcsr")  # format_kind.hpp
+
+
+@dataclass
+class BenchOptions:
+    """spmvkit::BenchOptions (bench.hpp:39-44)."""
+    repetitions: int = 20
+    x_ones: bool = False
+    seed: int = 1
+    target_rep_seconds: float = 2e-4
+
+
+@dataclass
+class BenchRecord:
+    """spmvkit::BenchRecord (bench.hpp:16-29)."""
+    matrix_name: str
+    format_name: str
+    group_size: Optional[int]
+    precision: str
+    repetitions: int
+    nnz: int
+    median_seconds: float
+    gflops: float
+    fill_percent: float
+    artificial_zeros: int
+    bytes: int
+    checksum: float
+
+
+def run_spmv_bench(m: TripletMatrix, matrix_name: str, kind: str, group_size: Optional[int] = None,
+                   precision=F64, options: Optional[BenchOptions] = None) -> BenchRecord:
+    """run_spmv_bench (src/bench.cpp:47-138) on the B200: builds the format on
+    the device, gates the y checksum against spmv_reference on the
+    storage-quantized inputs (the fp64 device CSR SpMV: same sorted-entry
+    accumulation; tolerance 1e-10 fp64 / 1e-5 fp32 relative), then reports the
+    median of `repetitions` device-timed repetitions, each a calibrated
+    inner loop of at least `target_rep_seconds` (CUDA events; A, x and y stay
+    resident in HBM -- the device analogue of the reference's host arrays)."""
+    import torch
+    o = options or BenchOptions()
+    prec = _prec(precision)
+    if kind not in FORMAT_KINDS:
+        raise InvalidArgument(f"unknown format {kind!r}")
+    if kind == "coo":
+        raise InvalidArgument("run_spmv_bench: coo is benchmarked as part of hybrid")
+    if kind == "bcsr":
+        raise InvalidArgument("run_spmv_bench: bcsr is not on the B200 path")
+    dt_np = np.float32 if prec == F32 else np.float64
+    dt = torch.float32 if prec == F32 else torch.float64
+    if o.x_ones:
+        xd = np.ones(m.num_cols)
+    else:
+        xd = np.empty(m.num_cols)
+        lib().spmvk_gen_random_vector(m.num_cols, o.seed, _ptr(xd))
+    x = torch.from_numpy(xd.astype(dt_np)).cuda()
+    y = torch.zeros(m.num_rows, dtype=dt, device="cuda")
+    # oracle inputs: values and x quantized to the storage precision, in fp64
+    q = TripletMatrix(m.num_rows, m.num_cols, m.row_ptr, m.col,
+                      m.val.astype(dt_np).astype(np.float64), validate=False)
+    y_ref = spmv_csr(build_csr(q, F64), x.double())
+    if kind == "csr":
+        a = build_csr(m, prec)
+        fn = lambda: spmv_csr(a, x, y)  # noqa: E731
+    elif kind == "ellpack":
+        a = build_ellpack(m, precision=prec)
+        fn = lambda: spmv_ellpack(a, x, y)  # noqa: E731
+    elif kind == "hybrid":
+        a = build_hybrid(m, group_size, prec)
+        fn = lambda: spmv_hybrid(a, x, y)  # noqa: E731
+    else:
+        a = build_rgcsr(m, group_size if group_size is not None else 32, prec)
+        fn = lambda: spmv_rgcsr(a, x, y)  # noqa: E731
+    fill = fill_report(a)
+    fn()
+    # sequential sums in row order, as the reference's loops (bench.cpp:106-109)
+    checksum = float(np.cumsum(y.double().cpu().numpy())[-1]) if m.num_rows else 0.0
+    checksum_ref = float(np.cumsum(y_ref.cpu().numpy())[-1]) if m.num_rows else 0.0
+    tol = 1e-10 if prec == F64 else 1e-5
+    if abs(checksum - checksum_ref) > tol * max(1.0, abs(checksum_ref)):
+        raise ChecksumError(f"{kind} checksum {checksum:.6f} disagrees with oracle "
+                            f"{checksum_ref:.6f} on {matrix_name}")
+
+    def time_once(inner: int) -> float:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(inner):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / inner
+
+    inner = 1
+    probe = time_once(inner)
+    while probe * inner < o.target_rep_seconds and inner < (1 << 20):
+        inner *= 8
+        probe = time_once(inner)
+    times = sorted(time_once(inner) for _ in range(max(o.repetitions, 1)))
+    med = times[len(times) // 2]
+    return BenchRecord(matrix_name, kind, (group_size if group_size is not None else 32)
+                       if kind == "rgcsr" else None, "double" if prec == F64 else "single",
+                       o.repetitions, m.nnz, med, measured_gflops(m.nnz, med),
+                       fill.fill_percent, fill.artificial_zeros,
+                       fill.bytes_double if prec == F64 else fill.bytes_single, checksum)
