@@ -576,6 +576,29 @@ def fill_report(a) -> FillReport:
     raise InvalidArgument(f"no fill report for {type(a).__name__}")
 
 
+B200_COPY_GBS = 6545.3  # MEASURED_PEAKS.json hbm_gbs on this pool's B200s
+
+
+@dataclass
+class PeakEstimate:
+    """spmvkit::PeakEstimate (memsim.hpp:92-99)."""
+    precision: str
+    cached_x: bool
+    bytes_per_nnz: int
+    gflops: float
+
+
+def peak_performance(precision=F64, cached_x: bool = True,
+                     bandwidth_gb_s: float = B200_COPY_GBS, index_bytes: int = 4) -> PeakEstimate:
+    """peak_performance (memsim.cpp:192-199): 2 * BW / (index + S * (cached ? 1 : 2))
+    flops per byte-bound SpMV, for the B200's measured bandwidth by default
+    (the reference's AccessModel defaults to a GTX 280, 141.7 GB/s)."""
+    sv = _prec(precision)
+    bpn = index_bytes + sv * (1 if cached_x else 2)
+    return PeakEstimate("double" if sv == F64 else "single", bool(cached_x), bpn,
+                        2.0 * bandwidth_gb_s / bpn)
+
+
 def measured_gflops(nnz: int, seconds: float) -> float:
     """2 * nnz / seconds / 1e9 (memsim.cpp:201-207)."""
     if not seconds > 0.0:

@@ -88,3 +88,14 @@ def test_triplet_matrix_validation():
     assert sk.measured_gflops(1000000, 1e-3) == 2.0  # acceptance.cpp:299
     with pytest.raises(sk.InvalidArgument):
         sk.measured_gflops(1, 0.0)
+
+
+def test_peak_performance_table():
+    """tests/test_memsim.cpp:182-202 at the reference model's 141 GB/s, and the
+    B200 default (measured copy bandwidth)."""
+    for prec, cached, gf, bpn in ((4, False, 23.5, 12), (8, False, 14.1, 20),
+                                  (4, True, 35.25, 8), (8, True, 23.5, 12)):
+        p = sk.peak_performance(prec, cached, bandwidth_gb_s=141.0)
+        assert (p.gflops, p.bytes_per_nnz) == (gf, bpn)
+    assert sk.peak_performance(8, False, 282.0).gflops == 2 * sk.peak_performance(8, False, 141.0).gflops
+    assert sk.peak_performance(8, True).gflops == 2 * 6545.3 / 12
