@@ -139,7 +139,7 @@ dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + os.environ["POR
                         rank=rank, world_size=world)
 torch.cuda.set_device(0)
 assert lib().spmvk_init(0) == 0
-mode, steps, G = os.environ["MODE"], 12, 32
+mode, steps, G = os.environ["MODE"], int(os.environ.get("STEPS", "12")), 32
 csr = sk.CsrMatrix.stencil(7, 24)
 x0 = torch.from_numpy(gen.random_vector(csr.num_cols, 1)).cuda()
 want_x, _ = reference_iterates(csr, G, 8, x0, steps)
@@ -174,13 +174,15 @@ def free_port():
         return str(s.getsockname()[1])
 
 
-@pytest.mark.parametrize("mode,world", [("halo", 2), ("allgather", 2), ("halo", 3)])
-def test_two_processes_ipc_barrier(cuda, mode, world):
+@pytest.mark.parametrize("mode,world,steps", [("halo", 2, 12), ("allgather", 2, 12),
+                                              ("halo", 3, 12), ("allgather", 4, 12),
+                                              ("halo", 3, 150)])
+def test_two_processes_ipc_barrier(cuda, mode, world, steps):
     port = free_port()
     procs = [subprocess.Popen([sys.executable, "-c", CHILD], cwd=ROOT, stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True,
                               env=dict(os.environ, ROOT=ROOT, RANK=str(r), WORLD_SIZE=str(world),
-                                       PORT=port, MODE=mode))
+                                       PORT=port, MODE=mode, STEPS=str(steps)))
              for r in range(world)]
     outs = []
     try:
