@@ -99,6 +99,14 @@ int spmvk_mm_parse(const char* text, uint64_t len, int threads, int val_prec, vo
                    spmvk_csr** out, uint64_t* error_line);
 int spmvk_mm_load(const char* path, int threads, int val_prec, void* stream, spmvk_csr** out,
                   uint64_t* error_line);
+/* write_matrix_market / save_matrix_market (src/matrix_market.cpp:150-164):
+ * the reference's text byte for byte ("%.17g" values, 1-based indices, rows
+ * in order), formatted by `threads` host threads (0 = all).  mm_write puts
+ * the length in *len and, when buf is non-NULL, the text in buf (ERANGE if
+ * cap is too small); mm_save writes the file (ERANGE "cannot open ... for
+ * writing"). */
+int spmvk_mm_write(const spmvk_csr* a, int threads, char* buf, uint64_t cap, uint64_t* len);
+int spmvk_mm_save(const spmvk_csr* a, const char* path, int threads);
 /* Smallest / largest column index over rows [row_begin, row_end): the x range
  * a row slab reads (out2[0] > out2[1] for a slab without entries).  Used by
  * the halo exchange of the distributed product. */

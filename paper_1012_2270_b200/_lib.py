@@ -53,6 +53,8 @@ SIGNATURES = {
     "spmvk_csr_column_range": (cint, [vp, u64, u64, u64p]),
     "spmvk_mm_parse": (cint, [C.c_char_p, u64, cint, cint, vp, C.POINTER(vp), u64p]),
     "spmvk_mm_load": (cint, [C.c_char_p, cint, cint, vp, C.POINTER(vp), u64p]),
+    "spmvk_mm_write": (cint, [vp, cint, vp, u64, u64p]),
+    "spmvk_mm_save": (cint, [vp, C.c_char_p, cint]),
     "spmvk_csr_descending_permutation": (cint, [vp, vp]),
     "spmvk_csr_permute_rows_descending": (cint, [vp, vp, C.POINTER(vp), vp]),
     "spmvk_csr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <stdexcept>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -279,9 +280,102 @@ int run_parse(const char* text, uint64_t len, int threads, void* stream, int val
                           SPMVK_F64, stream, out);
 }
 
+// write_matrix_market (src/matrix_market.cpp:150-158): banner, "rows cols
+// nnz", then 1-based "row col %.17g" per entry in (row, col) order.  Rows are
+// formatted by `threads` host threads into per-thread strings, concatenated.
+std::string format_mm(const spmvk_csr* a, int threads) {
+  uint64_t rows = 0, cols = 0, nnz = 0;
+  int prec = 0;
+  if (spmvk_csr_shape(a, &rows, &cols, &nnz, &prec) != SPMVK_OK)
+    throw std::runtime_error(spmvk_last_error());
+  std::vector<uint32_t> rp(rows + 1), col(nnz);
+  std::vector<double> val(nnz);
+  if (prec == SPMVK_F32) {
+    std::vector<float> v32(nnz);
+    if (spmvk_csr_download(a, rp.data(), col.data(), v32.data()) != SPMVK_OK)
+      throw std::runtime_error(spmvk_last_error());
+    for (uint64_t i = 0; i < nnz; ++i) val[i] = v32[i];
+  } else if (spmvk_csr_download(a, rp.data(), col.data(), val.data()) != SPMVK_OK) {
+    throw std::runtime_error(spmvk_last_error());
+  }
+  std::string head = "%%MatrixMarket matrix coordinate real general\n" + std::to_string(rows) +
+                     ' ' + std::to_string(cols) + ' ' + std::to_string(nnz) + '\n';
+  const int T = std::max(1, std::min<int>(threads, static_cast<int>((rows + 4095) / 4096)));
+  std::vector<std::string> part(T);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t) {
+    pool.emplace_back([&, t] {
+      const uint64_t r0 = rows * t / T, r1 = rows * (t + 1) / T;
+      std::string& o = part[t];
+      o.reserve((rp[r1] - rp[r0]) * 32);
+      char buf[96];
+      for (uint64_t r = r0; r < r1; ++r)
+        for (uint32_t k = rp[r]; k < rp[r + 1]; ++k) {
+          const int n = std::snprintf(buf, sizeof buf, "%llu %llu %.17g\n",
+                                      static_cast<unsigned long long>(r + 1),
+                                      static_cast<unsigned long long>(col[k]) + 1, val[k]);
+          o.append(buf, static_cast<size_t>(n));
+        }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (const auto& p : part) head += p;
+  return head;
+}
+
 }  // namespace
 
 extern "C" {
+
+int spmvk_mm_write(const spmvk_csr* a, int threads, char* buf, uint64_t cap, uint64_t* len) {
+  if (!a || !len) {
+    spmvk::set_last_error("null argument");
+    return SPMVK_EINVAL;
+  }
+  try {
+    const std::string text =
+        format_mm(a, threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency()));
+    *len = text.size();
+    if (!buf) return SPMVK_OK;
+    if (cap < text.size()) {
+      spmvk::set_last_error("write_matrix_market: buffer of " + std::to_string(cap) +
+                            " bytes, need " + std::to_string(text.size()));
+      return SPMVK_ERANGE;
+    }
+    std::memcpy(buf, text.data(), text.size());
+    return SPMVK_OK;
+  } catch (const std::bad_alloc&) {
+    spmvk::set_last_error("host allocation failed");
+    return SPMVK_ENOMEM;
+  } catch (const std::exception& e) {
+    spmvk::set_last_error(e.what());
+    return SPMVK_ECUDA;
+  }
+}
+
+int spmvk_mm_save(const spmvk_csr* a, const char* path, int threads) {
+  if (!a || !path) {
+    spmvk::set_last_error("null argument");
+    return SPMVK_EINVAL;
+  }
+  try {
+    const std::string text =
+        format_mm(a, threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency()));
+    std::ofstream out(path, std::ios::binary);
+    if (!out) {  // save_matrix_market (:160-164)
+      spmvk::set_last_error(std::string("cannot open ") + path + " for writing");
+      return SPMVK_ERANGE;
+    }
+    out.write(text.data(), static_cast<std::streamsize>(text.size()));
+    return out ? SPMVK_OK : SPMVK_ERANGE;
+  } catch (const std::bad_alloc&) {
+    spmvk::set_last_error("host allocation failed");
+    return SPMVK_ENOMEM;
+  } catch (const std::exception& e) {
+    spmvk::set_last_error(e.what());
+    return SPMVK_ECUDA;
+  }
+}
 
 int spmvk_mm_parse(const char* text, uint64_t len, int threads, int val_prec, void* stream,
                    spmvk_csr** out, uint64_t* error_line) {

@@ -225,6 +225,46 @@ def load_matrix_market(path, precision=F64, threads: int = 0, stream: int = 0) -
     return CsrMatrix(h.value)
 
 
+def write_matrix_market(a, threads: int = 0) -> str:
+    """write_matrix_market (src/matrix_market.cpp:150-158) of a CSR handle (or
+    anything build_csr accepts): the reference's text byte for byte."""
+    a = _as_csr(a)
+    n = C.c_uint64()
+    _check(lib().spmvk_mm_write(a._h, threads, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().spmvk_mm_write(a._h, threads, buf, n.value, C.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def save_matrix_market(path, a, threads: int = 0) -> None:
+    """save_matrix_market (src/matrix_market.cpp:160-164)."""
+    a = _as_csr(a)
+    _check(lib().spmvk_mm_save(a._h, str(path).encode(), threads))
+
+
+@dataclass
+class MatrixStats:
+    """spmvkit::MatrixStats (triplet.hpp:54-61)."""
+    num_rows: int
+    nnz: int
+    row_len_max: int
+    row_len_mean: float
+    row_len_min: int
+    density_percent: float
+
+
+def matrix_stats(m) -> MatrixStats:
+    """matrix_stats (src/triplet.cpp:57-69); row-length extremes from the device."""
+    a = _as_csr(m)
+    if a.num_rows == 0:
+        raise InvalidArgument("matrix_stats: matrix has zero rows")
+    mx, mn = a.row_length_range()
+    nnz = a.nnz()
+    cells = float(a.num_rows) * float(a.num_cols)
+    return MatrixStats(a.num_rows, nnz, mx, nnz / a.num_rows, mn,
+                       100.0 * nnz / cells if cells > 0 else 0.0)
+
+
 def descending_row_permutation(m) -> np.ndarray:
     """descending_row_permutation(m) (src/reorder.cpp:35-42) on the device:
     map[new] = old, rows by decreasing length, ties by original index."""

@@ -136,3 +136,41 @@ def test_reference_examples_and_writer_round_trip(cuda, tmp_path):
         sk.load_matrix_market(str(p))
     assert e.value.line == 3 and str(e.value).startswith(str(p) + ": line 3: ")
     torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+def test_writer_matches_reference_bytes(cuda, tmp_path):
+    """write_matrix_market / save_matrix_market (src/matrix_market.cpp:150-164):
+    identical bytes to the reference writer, any thread count; parse round trip."""
+    for seed in range(20, 40):
+        r = orc.RefMatrix.random_small(seed, True, seed % 2 == 0)
+        want = r.mm_write()
+        w = r.to_csr()
+        a = sk.build_csr(sk.TripletMatrix(w.rows, w.cols, w.rp, w.col, w.val))
+        for threads in (1, 3, 0):
+            assert sk.write_matrix_market(a, threads).encode() == want, (seed, threads)
+        p = tmp_path / f"w{seed}.mtx"
+        sk.save_matrix_market(p, a)
+        assert p.read_bytes() == want
+        rp, col, val = sk.load_matrix_market(p).to_host()
+        assert bitwise(rp, w.rp) and bitwise(col, w.col) and bitwise(val, w.val)
+    big = sk.CsrMatrix.stencil(7, 40)  # 64k rows: several formatting threads
+    text = sk.write_matrix_market(big, 8)
+    assert text == sk.write_matrix_market(big, 1)
+    rp, col, val = sk.parse_matrix_market(text).to_host()
+    rp2, col2, val2 = big.to_host()
+    assert bitwise(rp, rp2) and bitwise(col, col2) and bitwise(val, val2)
+    with pytest.raises(sk.SpmvkRuntimeError, match="for writing"):
+        sk.save_matrix_market(tmp_path / "no" / "such" / "dir.mtx", big)
+
+
+@pytest.mark.gpu
+def test_matrix_stats(cuda):
+    """matrix_stats (src/triplet.cpp:57-69)."""
+    m = sk.canonicalize([(0, 0, 1.0), (0, 2, 2.0), (2, 1, 3.0)], 4, 5)
+    s = sk.matrix_stats(m)
+    assert (s.num_rows, s.nnz, s.row_len_max, s.row_len_min) == (4, 3, 2, 0)
+    assert s.row_len_mean == 0.75 and s.density_percent == 100.0 * 3 / 20
+    with pytest.raises(sk.InvalidArgument, match="matrix has zero rows"):
+        sk.matrix_stats(sk.canonicalize([], 0, 3))
