@@ -120,6 +120,24 @@ int spmvk_csr_descending_permutation(const spmvk_csr* a, uint32_t* map);
  * (HOST, rows entries, may be NULL) receives the permutation. */
 int spmvk_csr_permute_rows_descending(const spmvk_csr* a, void* stream, spmvk_csr** out,
                                       uint32_t* map);
+/* apply_permutation(m, Permutation(map), mode) (src/reorder.cpp:12-21,44-61)
+ * for any HOST map[new] = old of n entries: row i of the result is old row
+ * map[i]; symmetric != 0 also relabels columns (new = inverse[old]) and
+ * re-sorts each row, as the reference's canonicalize.  EINVAL with the
+ * reference's messages: "permutation is not a bijection on 0..n-1",
+ * "apply_permutation: permutation length L does not match R rows",
+ * "apply_permutation: symmetric mode needs a square matrix". */
+int spmvk_csr_permute(const spmvk_csr* a, const uint32_t* map, uint64_t n, int symmetric,
+                      void* stream, spmvk_csr** out);
+/* Vectors under a permutation (DEVICE map and vectors): out[i] = in[map[i]]
+ * (into the permuted numbering, e.g. x for a symmetric permutation), or with
+ * inverse != 0 out[map[i]] = in[i] (y of a permuted matrix back to the
+ * original row order; the reference's check `yp[i] == y[p[i]]`,
+ * tests/test_reorder.cpp:123-133). */
+int spmvk_permute_vector_f64(const uint32_t* map_dev, uint64_t n, const double* in, double* out,
+                             int inverse, void* stream);
+int spmvk_permute_vector_f32(const uint32_t* map_dev, uint64_t n, const float* in, float* out,
+                             int inverse, void* stream);
 /* spmv_csr (spmvkit/csr.hpp:41-53): thread-per-row, same accumulation order. */
 int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
                        void* stream);

@@ -56,6 +56,9 @@ SIGNATURES = {
     "spmvk_mm_write": (cint, [vp, cint, vp, u64, u64p]),
     "spmvk_mm_save": (cint, [vp, C.c_char_p, cint]),
     "spmvk_csr_descending_permutation": (cint, [vp, vp]),
+    "spmvk_csr_permute": (cint, [vp, vp, u64, cint, vp, C.POINTER(vp)]),
+    "spmvk_permute_vector_f64": (cint, [vp, u64, vp, vp, cint, vp]),
+    "spmvk_permute_vector_f32": (cint, [vp, u64, vp, vp, cint, vp]),
     "spmvk_csr_permute_rows_descending": (cint, [vp, vp, C.POINTER(vp), vp]),
     "spmvk_csr_spmv_f64": (cint, [vp, vp, u64, vp, u64, vp]),
     "spmvk_csr_spmv_f32": (cint, [vp, vp, u64, vp, u64, vp]),

@@ -12,6 +12,9 @@
 // the reference's std::stable_sort order); the permuted CSR is built by a
 // row-length gather, an exclusive scan and a warp-per-row entry copy.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <vector>
 
 #include <memory>
 #include <string>
@@ -40,12 +43,14 @@ __global__ void permuted_lengths(uint64_t rows, const uint32_t* __restrict__ map
   }
 }
 
+// inv != nullptr: symmetric mode, columns relabelled new = inv[old] (the
+// row's entries are then re-sorted by a segmented sort).
 template <class V>
 __global__ void permuted_copy(uint64_t rows, uint64_t nnz, const uint32_t* __restrict__ map,
                               const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
                               const V* __restrict__ val, const uint64_t* __restrict__ off,
                               uint32_t* __restrict__ rp2, uint32_t* __restrict__ col2,
-                              V* __restrict__ val2) {
+                              V* __restrict__ val2, const uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < rows;
@@ -57,9 +62,96 @@ __global__ void permuted_copy(uint64_t rows, uint64_t nnz, const uint32_t* __res
       if (i + 1 == rows) rp2[rows] = (uint32_t)nnz;
     }
     for (uint32_t k = lane; k < n; k += 32) {
-      col2[d + k] = col[b + k];
+      const uint32_t c = col[b + k];
+      col2[d + k] = inv ? inv[c] : c;
       val2[d + k] = val[b + k];
     }
+  }
+}
+
+__global__ void invert_map(uint64_t n, const uint32_t* __restrict__ map, uint32_t* __restrict__ inv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    inv[map[i]] = (uint32_t)i;
+}
+
+template <class V>
+__global__ void permute_vector(uint64_t n, const uint32_t* __restrict__ map, const V* __restrict__ in,
+                               V* __restrict__ out, int inverse) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (inverse) out[map[i]] = in[i];
+    else out[i] = in[map[i]];
+  }
+}
+
+// apply_permutation(m, p, mode) (src/reorder.cpp:44-61) with a DEVICE map
+// (map[new] = old): row i of the result is old row map[i]; in symmetric
+// mode columns become inv[col] and each row is re-sorted by column (the
+// reference's canonicalize; a bijection creates no duplicates).
+spmvk_csr* permute_csr(const spmvk_csr* a, const uint32_t* d_map, bool symmetric,
+                       cudaStream_t s) {
+  auto b = std::make_unique<spmvk_csr>();
+  b->rows = a->rows;
+  b->cols = a->cols;
+  b->nnz = a->nnz;
+  b->val_prec = a->val_prec;
+  b->row_ptr.alloc(a->rows + 1);
+  b->col.alloc(a->nnz);
+  b->val.alloc(a->nnz * static_cast<uint64_t>(a->val_prec));
+  if (a->rows == 0) {
+    SPMVK_CUDA(cudaMemsetAsync(b->row_ptr.p, 0, 4, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    return b.release();
+  }
+  DevBuf<uint32_t> inv(symmetric ? a->rows : 0);
+  if (symmetric) {
+    invert_map<<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(a->rows, d_map, inv.p);
+    SPMVK_LAUNCH("invert_map");
+  }
+  DevBuf<uint64_t> off(a->rows);
+  const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
+  permuted_lengths<<<grid, 256, 0, s>>>(a->rows, d_map, a->row_ptr.p, off.p);
+  SPMVK_LAUNCH("permuted_lengths");
+  exclusive_scan_u64(off.p, a->rows, s);
+  const unsigned wgrid = persistent_grid((a->rows + 7) / 8, 8);
+  // symmetric: copy into scratch, then segmented-sort into b
+  DevBuf<uint32_t> col_t(symmetric ? a->nnz : 0);
+  DevBuf<unsigned char> val_t(symmetric ? a->nnz * static_cast<uint64_t>(a->val_prec) : 0);
+  uint32_t* col_dst = symmetric ? col_t.p : b->col.p;
+  unsigned char* val_dst = symmetric ? val_t.p : b->val.p;
+  auto run = [&](auto tag) {
+    using V = decltype(tag);
+    permuted_copy<V><<<wgrid, 256, 0, s>>>(
+        a->rows, a->nnz, d_map, a->row_ptr.p, a->col.p, reinterpret_cast<const V*>(a->val.p),
+        off.p, b->row_ptr.p, col_dst, reinterpret_cast<V*>(val_dst),
+        symmetric ? inv.p : nullptr);
+    SPMVK_LAUNCH("permuted_copy");
+    if (!symmetric || a->nnz == 0) return;
+    if (a->nnz > 0x7fffffffull) fail(SPMVK_ERANGE, "apply_permutation: nnz exceeds 2^31 - 1");
+    size_t tmp_bytes = 0;
+    const int nnz = static_cast<int>(a->nnz), rows = static_cast<int>(a->rows);
+    SPMVK_CUDA(cub::DeviceSegmentedSort::SortPairs(
+        nullptr, tmp_bytes, col_t.p, b->col.p, reinterpret_cast<const V*>(val_t.p),
+        reinterpret_cast<V*>(b->val.p), nnz, rows, b->row_ptr.p, b->row_ptr.p + 1, s));
+    DevBuf<unsigned char> tmp(tmp_bytes);
+    SPMVK_CUDA(cub::DeviceSegmentedSort::SortPairs(
+        tmp.p, tmp_bytes, col_t.p, b->col.p, reinterpret_cast<const V*>(val_t.p),
+        reinterpret_cast<V*>(b->val.p), nnz, rows, b->row_ptr.p, b->row_ptr.p + 1, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));  // tmp / scratch die with this scope
+  };
+  if (a->val_prec == SPMVK_F64) run(double{});
+  else run(float{});
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  return b.release();
+}
+
+void check_bijection(const uint32_t* map, uint64_t n) {  // Permutation ctor (reorder.cpp:12-21)
+  std::vector<char> seen(n, 0);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (map[i] >= n || seen[map[i]])
+      fail(SPMVK_EINVAL, "permutation is not a bijection on 0.." + std::to_string(n ? n - 1 : 0));
+    seen[map[i]] = 1;
   }
 }
 
@@ -105,42 +197,57 @@ int spmvk_csr_permute_rows_descending(const spmvk_csr* a, void* stream, spmvk_cs
     require_device();
     if (!a || !out) fail(SPMVK_EINVAL, "null argument");
     cudaStream_t s = as_stream(stream);
-    auto b = std::make_unique<spmvk_csr>();
-    b->rows = a->rows;
-    b->cols = a->cols;
-    b->nnz = a->nnz;
-    b->val_prec = a->val_prec;
-    b->row_ptr.alloc(a->rows + 1);
-    b->col.alloc(a->nnz);
-    b->val.alloc(a->nnz * static_cast<uint64_t>(a->val_prec));
-    if (a->rows == 0) {
-      SPMVK_CUDA(cudaMemsetAsync(b->row_ptr.p, 0, 4, s));
-      SPMVK_CUDA(cudaStreamSynchronize(s));
-      *out = b.release();
-      return;
-    }
     DevBuf<uint32_t> d_map(a->rows);
-    descending_map(a, d_map.p, s);
-    DevBuf<uint64_t> off(a->rows);
-    const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
-    permuted_lengths<<<grid, 256, 0, s>>>(a->rows, d_map.p, a->row_ptr.p, off.p);
-    SPMVK_LAUNCH("permuted_lengths");
-    exclusive_scan_u64(off.p, a->rows, s);
-    const unsigned wgrid = persistent_grid((a->rows + 7) / 8, 8);
-    if (a->val_prec == SPMVK_F64)
-      permuted_copy<double><<<wgrid, 256, 0, s>>>(
-          a->rows, a->nnz, d_map.p, a->row_ptr.p, a->col.p,
-          reinterpret_cast<const double*>(a->val.p), off.p, b->row_ptr.p, b->col.p,
-          reinterpret_cast<double*>(b->val.p));
-    else
-      permuted_copy<float><<<wgrid, 256, 0, s>>>(
-          a->rows, a->nnz, d_map.p, a->row_ptr.p, a->col.p,
-          reinterpret_cast<const float*>(a->val.p), off.p, b->row_ptr.p, b->col.p,
-          reinterpret_cast<float*>(b->val.p));
-    SPMVK_LAUNCH("permuted_copy");
-    if (map) SPMVK_CUDA(cudaMemcpyAsync(map, d_map.p, 4 * a->rows, cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaStreamSynchronize(s));
-    *out = b.release();
+    if (a->rows) descending_map(a, d_map.p, s);
+    spmvk_csr* b = permute_csr(a, d_map.p, false, s);
+    if (map && a->rows) {
+      const cudaError_t e = cudaMemcpy(map, d_map.p, 4 * a->rows, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        spmvk_csr_destroy(b);
+        SPMVK_CUDA(e);
+      }
+    }
+    *out = b;
+  });
+}
+
+int spmvk_csr_permute(const spmvk_csr* a, const uint32_t* map, uint64_t n, int symmetric,
+                      void* stream, spmvk_csr** out) {
+  return guarded([&] {
+    require_device();
+    if (!a || !out || (!map && n)) fail(SPMVK_EINVAL, "null argument");
+    check_bijection(map, n);
+    if (n != a->rows)
+      fail(SPMVK_EINVAL, "apply_permutation: permutation length " + std::to_string(n) +
+                             " does not match " + std::to_string(a->rows) + " rows");
+    if (symmetric && a->rows != a->cols)
+      fail(SPMVK_EINVAL, "apply_permutation: symmetric mode needs a square matrix");
+    cudaStream_t s = as_stream(stream);
+    DevBuf<uint32_t> d_map(n);
+    if (n) SPMVK_CUDA(cudaMemcpyAsync(d_map.p, map, 4 * n, cudaMemcpyHostToDevice, s));
+    *out = permute_csr(a, d_map.p, symmetric != 0, s);
+  });
+}
+
+int spmvk_permute_vector_f64(const uint32_t* map_dev, uint64_t n, const double* in, double* out,
+                             int inverse, void* stream) {
+  return guarded([&] {
+    if (n && (!map_dev || !in || !out)) fail(SPMVK_EINVAL, "null argument");
+    if (!n) return;
+    permute_vector<double><<<persistent_grid((n + 255) / 256, 8), 256, 0, as_stream(stream)>>>(
+        n, map_dev, in, out, inverse);
+    SPMVK_LAUNCH("permute_vector");
+  });
+}
+
+int spmvk_permute_vector_f32(const uint32_t* map_dev, uint64_t n, const float* in, float* out,
+                             int inverse, void* stream) {
+  return guarded([&] {
+    if (n && (!map_dev || !in || !out)) fail(SPMVK_EINVAL, "null argument");
+    if (!n) return;
+    permute_vector<float><<<persistent_grid((n + 255) / 256, 8), 256, 0, as_stream(stream)>>>(
+        n, map_dev, in, out, inverse);
+    SPMVK_LAUNCH("permute_vector");
   });
 }
 

@@ -285,6 +285,116 @@ def apply_descending_permutation(m, stream: int = 0):
     return CsrMatrix(h.value), out
 
 
+class Permutation:
+    """spmvkit::Permutation (reorder.hpp, src/reorder.cpp:12-33): a bijection
+    map[new] = old on 0..n-1, validated on construction."""
+
+    def __init__(self, mapping):
+        self._map = np.ascontiguousarray(mapping, dtype=np.int64)
+        n = self._map.size
+        ok = bool(((self._map >= 0) & (self._map < n)).all()) if n else True
+        if not ok or (n and np.bincount(self._map, minlength=n).max() > 1):
+            raise InvalidArgument(f"permutation is not a bijection on 0..{n - 1 if n else 0}")
+        self._map = self._map.astype(np.uint32)
+        self._dev = None
+
+    @classmethod
+    def identity(cls, n: int) -> "Permutation":
+        return cls(np.arange(n, dtype=np.uint32))
+
+    def map(self) -> np.ndarray:
+        return self._map
+
+    def size(self) -> int:
+        return int(self._map.size)
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def __getitem__(self, i):
+        return self._map[i]
+
+    def inverse(self) -> np.ndarray:
+        inv = np.empty_like(self._map)
+        inv[self._map] = np.arange(self._map.size, dtype=np.uint32)
+        return inv
+
+    def device_map(self):
+        """The map as a CUDA uint32 buffer (cached)."""
+        if self._dev is None:
+            import torch
+            self._dev = torch.from_numpy(self._map.view(np.int32)).cuda()
+        return self._dev
+
+
+def parse_permutation(text: str) -> Permutation:
+    """parse_permutation (src/reorder.cpp:63-85): one 0-based index per line,
+    blank lines skipped, the reference's messages."""
+    out = []
+    for no, line in enumerate(text.split("\n"), 1):
+        if line.endswith("\r"):
+            line = line[:-1]
+        if not line.strip(" \t"):
+            continue
+        s = line.lstrip(" \t\n\v\f\r")
+        j = 1 if s[:1] in "+-" else 0
+        while j < len(s) and s[j].isdigit():
+            j += 1
+        if j == 0 or not s[:j].lstrip("+-"):
+            raise InvalidArgument(f"permutation line {no}: expected an index, got '{line}'")
+        v = int(s[:j])
+        if v < 0 or s[j:].strip(" \t"):
+            raise InvalidArgument(
+                f"permutation line {no}: expected a single 0-based index, got '{line}'")
+        out.append(v)
+    return Permutation(np.array(out, dtype=np.int64))
+
+
+def load_permutation(path) -> Permutation:
+    """load_permutation (src/reorder.cpp:87-91)."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        raise SpmvkRuntimeError(f"cannot open {path}") from None
+    return parse_permutation(text)
+
+
+def apply_permutation(m, p, mode: str = "rows_only", stream: int = 0) -> CsrMatrix:
+    """apply_permutation(m, p, RowsOnly | Symmetric) (src/reorder.cpp:44-61) on
+    the device: row i of the result is row p[i] of m; "symmetric" also
+    relabels the columns (square matrices) and re-sorts each row."""
+    if mode not in ("rows_only", "symmetric"):
+        raise InvalidArgument(f"unknown permutation mode {mode!r}")
+    p = p if isinstance(p, Permutation) else Permutation(p)
+    a = _as_csr(m)
+    h = C.c_void_p()
+    mp = p.map()
+    _check(lib().spmvk_csr_permute(a._h, _ptr(mp) if mp.size else None, mp.size,
+                                   1 if mode == "symmetric" else 0, stream or None, C.byref(h)))
+    return CsrMatrix(h.value)
+
+
+def permute_vector(p: Permutation, v, inverse: bool = False, stream: Optional[int] = None):
+    """out[i] = v[p[i]] (into the permuted numbering), or with inverse=True
+    out[p[i]] = v[i] (a permuted matrix's y back to the original row order).
+    CUDA tensors in and out."""
+    import torch
+    if not (_is_torch(v) and v.is_cuda and v.is_contiguous()):
+        raise InvalidArgument("permute_vector takes a contiguous CUDA tensor")
+    if v.numel() != p.size():
+        raise InvalidArgument("permute_vector: vector length differs from the permutation")
+    out = torch.empty_like(v)
+    fn = {torch.float64: lib().spmvk_permute_vector_f64,
+          torch.float32: lib().spmvk_permute_vector_f32}.get(v.dtype)
+    if fn is None:
+        raise InvalidArgument("permute_vector: float32 or float64 vectors")
+    s = stream if stream is not None else _torch_stream(v)
+    _check(fn(p.device_map().data_ptr() if p.size() else None, p.size(), v.data_ptr(),
+              out.data_ptr(), 1 if inverse else 0, s or None))
+    return out
+
+
 def build_csr(m: TripletMatrix, precision=F64, stream: int = 0) -> CsrMatrix:
     """build_csr<Scalar>(m) (csr.hpp:24-39): upload + validate on the device."""
     prec = _prec(precision)
