@@ -231,7 +231,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
   kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
-  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf
+  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf, kVec2, kVec4
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -243,6 +243,10 @@ enum class K2 {
 // config) favour the row-prefetching `pipe` kernel in fp32
 // (profiles/r01_powerlaw.md: 1,070 vs 1,353 us).
 K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
+  // <= 5.5 slots per row (5-point class): two / four rows per thread with
+  // 128-bit value loads win (5-pt 4096^2: fp64 220 vs 232 us, fp32 152 vs
+  // 163 us); from 7 slots on they lose (profiles/r01_k2_sweep3.md)
+  if (!h->n_long && 2 * h->slots <= 11 * h->rows) return K2::kVec2;
   if (f64) return K2::kLite8;
   if (h->n_long) return K2::kPipe;
   // fp32, short rows (<= ~12 slots): one 8-deep batch per row at full
@@ -261,7 +265,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"lite", K2::kLite},     {"lite8", K2::kLite8},
       {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full},
       {"lite_mpf", K2::kLiteMpf}, {"lite8_mpf", K2::kLite8Mpf},
-      {"lite8_full_mpf", K2::kLite8FullMpf}};
+      {"lite8_full_mpf", K2::kLite8FullMpf}, {"vec2", K2::kVec2}, {"vec4", K2::kVec4}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -387,6 +391,25 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       SPMVK_LAUNCH("rgcsr_spmv_long");
     }
   };
+  // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
+  auto run_vec = [&](auto kern) {
+    constexpr uint64_t R = sizeof(T) == 8 ? 2 : 4;
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const unsigned grid = persistent_grid((h->rows + 256 * R - 1) / (256 * R),
+                                          per_sm > 0 ? per_sm : 1);
+    kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+                              h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+                              h->columns.p, x, y, x_next, scale, long_cut);
+    SPMVK_LAUNCH("rgcsr_spmv_vec");
+    if (h->n_long) {
+      rgcsr_spmv_long<T, kScaled><<<persistent_grid((h->n_long + 7) / 8, 8), 256, 0, s>>>(
+          static_cast<uint32_t>(h->n_long), h->long_rows.p, static_cast<uint32_t>(h->rows), G,
+          sh, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+          h->columns.p, x, y, x_next, scale);
+      SPMVK_LAUNCH("rgcsr_spmv_long");
+    }
+  };
   switch (k) {
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
     case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
@@ -398,6 +421,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLiteMpf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, false, true>); break;
     case K2::kLite8Mpf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, false, true>); break;
     case K2::kLite8FullMpf: run(rgcsr_spmv_lite<T, kScaled, 8, 8, false, true>); break;
+    case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
+    case K2::kVec4: run_vec(rgcsr_spmv_vec<T, kScaled, 4, 4>); break;
     case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;

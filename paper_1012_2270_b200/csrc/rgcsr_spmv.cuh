@@ -282,6 +282,153 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
       StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
+// ---------------------------------------------------------------------------
+// rgcsr_spmv_vec -- 128-bit vectorised slot loads (north_star subsystem 2).
+//
+// A thread owns R consecutive rows of one group (fp64: R = 2, one 16-byte
+// double2 value load and one 8-byte uint2 column load per slot; fp32: R = 4,
+// float4 + uint4, 16 bytes each).  Rows t..t+R-1 of a group are adjacent in
+// every slot (entry j of row t at gp[g] + t + j*s), so when s % R == 0 (every
+// full group for G % R == 0; then gp[g] and t are multiples of R too) the R
+// rows' slot j is one aligned vector.  The pair / quad walks max(len) slots;
+// each row accumulates only its own first len slots, in slot order, so y is
+// bitwise the thread-per-row result.  Misaligned vectors (s % R != 0 or
+// gp[g] % R != 0: odd G, a short last group) and vectors holding a long row
+// take the scalar per-row path.
+template <class T, int R>
+struct VecOf;
+template <>
+struct VecOf<double, 2> {
+  using V = double2;
+  using C = uint2;
+  __device__ static double get(const double2& v, int i) { return i ? v.y : v.x; }
+  __device__ static uint32_t col(const uint2& c, int i) { return i ? c.y : c.x; }
+};
+template <>
+struct VecOf<float, 4> {
+  using V = float4;
+  using C = uint4;
+  __device__ static float get(const float4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  __device__ static uint32_t col(const uint4& c, int i) {
+    return i == 0 ? c.x : i == 1 ? c.y : i == 2 ? c.z : c.w;
+  }
+};
+
+template <class T, int U>
+__device__ __forceinline__ T scalar_row(const T* __restrict__ vp, const uint32_t* __restrict__ cp,
+                                        uint32_t s, uint32_t len, const T* __restrict__ x) {
+  T acc = T(0);
+  uint32_t j = 0;
+  for (; j + U <= len; j += U) {
+    uint32_t c[U];
+    T v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = ld_stream(cp + u * s);
+      v[u] = ld_stream(vp + u * s);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    cp += U * s;
+    vp += U * s;
+  }
+  for (; j < len; ++j, cp += s, vp += s) acc = add_rn(acc, mul_rn(ld_stream(vp), ld_x(x + *cp)));
+  return acc;
+}
+
+template <class T, int R, int U, class Epi>
+__device__ __forceinline__ void vec_tiles(uint32_t rows, uint32_t G, int g_shift,
+                                          const uint32_t* __restrict__ gp,
+                                          const uint32_t* __restrict__ lens,
+                                          const T* __restrict__ values,
+                                          const uint32_t* __restrict__ columns,
+                                          const T* __restrict__ x, uint32_t long_cut,
+                                          const Epi& epi) {
+  using W = VecOf<T, R>;
+  using V = typename W::V;
+  using Cv = typename W::C;
+  constexpr uint32_t kTile = 256 * R;
+  const uint32_t tiles = (rows + kTile - 1) / kTile;
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint32_t r0 = tile * kTile + threadIdx.x * R;
+    if (r0 >= rows) continue;
+    const uint32_t g = g_shift >= 0 ? (r0 >> g_shift) : r0 / G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t t = r0 - g * G;
+    const uint32_t base = gp[g] + t;
+    uint32_t len[R], n = 0;
+    bool any_long = false;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      len[i] = r0 + i < rows ? lens[r0 + i] : 0;
+      any_long |= len[i] > long_cut;
+      n = max(n, len[i]);
+    }
+    // vector path: the R rows' slots are aligned R-vectors (s, t and gp[g]
+    // multiples of R -- gp[g] is not when an odd G precedes an even last group)
+    if (s % R != 0 || base % R != 0 || t + R > s || any_long) {  // scalar per-row path
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint32_t r = r0 + i;
+        if (r >= rows || len[i] > long_cut) continue;
+        const uint32_t gi = g_shift >= 0 ? (r >> g_shift) : r / G;
+        const uint32_t si = min(G, rows - gi * G);
+        const uint32_t off = gp[gi] + (r - gi * G);
+        epi(r, scalar_row<T, 4>(values + off, columns + off, si, len[i], x));
+      }
+      continue;
+    }
+    const V* __restrict__ vp = reinterpret_cast<const V*>(values + base);
+    const Cv* __restrict__ cp = reinterpret_cast<const Cv*>(columns + base);
+    const uint32_t sv = s / R;  // slot stride in vectors
+    T acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = T(0);
+    uint32_t j = 0;
+    for (; j + U <= n; j += U) {
+      V v[U];
+      Cv c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = ld_stream_v(cp + u * sv);
+        v[u] = ld_stream_v(vp + u * sv);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+          if (j + u < len[i])
+            acc[i] = add_rn(acc[i], mul_rn(W::get(v[u], i), ld_x(x + W::col(c[u], i))));
+      cp += U * sv;
+      vp += U * sv;
+    }
+    for (; j < n; ++j, cp += sv, vp += sv) {
+      const Cv c = ld_stream_v(cp);
+      const V v = ld_stream_v(vp);
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (j < len[i]) acc[i] = add_rn(acc[i], mul_rn(W::get(v, i), ld_x(x + W::col(c, i))));
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) epi(r0 + i, acc[i]);
+  }
+}
+
+template <class T, bool kScaled, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_vec(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  constexpr int R = sizeof(T) == 8 ? 2 : 4;
+  vec_tiles<T, R, U>(rows, G, g_shift, gp, lens, values, columns, x, long_cut,
+                     StoreEpi<T, kScaled>{y, x_next, scale});
+}
+
 // Same kernel over the 256-row tiles [tile_begin, tile_end) only: the unit of
 // the pipelined host-span SpMV (H2D of x, row chunks and D2H of y overlap).
 template <class T, int U, int MINB>

@@ -17,7 +17,7 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = ["auto", "lite", "lite8", "lite8_full", "lite8_l2pf", "lite_l2pf", "pipe", "pipe_hi", "pipe8",
+VARIANTS = ["auto", "lite", "lite8", "lite8_full", "lite8_l2pf", "lite_l2pf", "vec2", "vec4", "pipe", "pipe_hi", "pipe8",
             "ldg", "ldg_pf", "tma", "wtma"]
 
 
