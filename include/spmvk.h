@@ -210,6 +210,13 @@ int spmvk_set_rgcsr_kernel(const char* name);
 int spmvk_set_long_row_cut(uint32_t cut);
 
 /* ------------------------------------------------------------------ Hybrid */
+/* Tuning knob (process-wide): Hybrid SpMV kernel variant, "auto" (default:
+ * "lite8" for fp64; fp32 "lite8_full" when K1 <= 12, else "lite"), "v4"
+ * (first kernel: policy-hinted loads, 4-deep), "lite" / "lite8" /
+ * "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at 8 / 5 / 8
+ * CTAs per SM).  All give bitwise identical y.  Also read from
+ * SPMVK_HYBRID_KERNEL. */
+int spmvk_set_hybrid_kernel(const char* name);
 typedef struct {
   uint64_t num_rows, num_cols;
   uint64_t ell_width;        /* K1 = EllpackMatrix::slots_per_row */

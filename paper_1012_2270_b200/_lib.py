@@ -76,6 +76,7 @@ SIGNATURES = {
     "spmvk_rgcsr_spmv_host_f32": (cint, [vp, vp, u64, vp, u64, u64p]),
     "spmvk_rgcsr_destroy": (None, [vp]),
     "spmvk_set_rgcsr_kernel": (cint, [C.c_char_p]),
+    "spmvk_set_hybrid_kernel": (cint, [C.c_char_p]),
     "spmvk_set_long_row_cut": (cint, [C.c_uint32]),
     "spmvk_csr_choose_ell_width": (cint, [vp, u64p]),
     "spmvk_choose_ell_width": (u64, [vp, u64]),

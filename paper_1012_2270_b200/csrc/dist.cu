@@ -103,6 +103,17 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_dist(
                               x, long_cut, epi);
 }
 
+// Same step with the group-uniform walk (rgcsr_spmv_grp) for slabs without
+// long rows and with <= 10 % padding -- the stencil slabs of config 5.
+template <class T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_dist_grp(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, uint32_t /*long_cut*/,
+    PeerEpi<T> epi) {
+  grp_tiles_epi<T, U, true, true, PeerEpi<T>>(rows, G, g_shift, gp, lens, values, columns, x, epi);
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) rgcsr_spmv_long_dist(
     uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,
@@ -175,7 +186,14 @@ void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, 
     const int sh = pow2_shift(a->group_size);
     const uint32_t long_cut = a->n_long ? a->long_cut : 0xffffffffu;
     constexpr bool f64 = sizeof(T) == 8;
+    // kernel choice as rgcsr.cu's auto_k2: group-uniform walk for regular slabs
     auto kern = f64 ? rgcsr_spmv_dist<T, 8, 5> : rgcsr_spmv_dist<T, 4, 8>;
+    if (!a->n_long && a->slots * 10 <= a->nnz * 11) {
+      if (2 * a->slots <= 11 * a->rows) kern = rgcsr_spmv_dist_grp<T, 6, 5>;
+      else if constexpr (f64) kern = rgcsr_spmv_dist_grp<T, 8, 4>;
+      else kern = a->slots <= 12 * a->rows ? rgcsr_spmv_dist_grp<T, 8, 5>
+                                           : rgcsr_spmv_dist_grp<T, 7, 5>;
+    }
     int per_sm = 0;
     SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     kern<<<persistent_grid((a->rows + 255) / 256, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(

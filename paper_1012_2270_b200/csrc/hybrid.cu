@@ -6,6 +6,8 @@
 // spmv_hybrid (:205-210).  ELL is slot-major (slot*N + row), pads (0, col 0);
 // COO holds each row's entries past the first K1, sorted by (row, col).
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -383,6 +385,135 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
   }
 }
 
+// The tile's COO range [tile_ptr[tile], tile_ptr[tile+1]) staged through
+// shared memory (same scheme as hybrid_spmv_kernel): products in parallel,
+// then each live row adds its own products in array order.
+template <class T>
+__device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool live, T acc,
+                                                 const uint32_t* __restrict__ tile_ptr,
+                                                 const uint32_t* __restrict__ cr,
+                                                 const uint32_t* __restrict__ cc,
+                                                 const T* __restrict__ cv,
+                                                 const T* __restrict__ x) {
+  __shared__ T prod[kCooTile];
+  __shared__ uint32_t prow[kCooTile];
+  const uint32_t c0 = tile_ptr[tile], c1 = tile_ptr[tile + 1];
+  for (uint32_t t0 = c0; t0 < c1; t0 += kCooTile) {
+    const uint32_t n = min((uint32_t)kCooTile, c1 - t0);
+    for (uint32_t i = threadIdx.x; i < n; i += kRowsPerTile) {
+      prow[i] = ld_stream(cr + t0 + i);
+      prod[i] = mul_rn(ld_stream(cv + t0 + i), ld_x(x + ld_stream(cc + t0 + i)));
+    }
+    __syncthreads();
+    if (live) {
+      uint32_t lo = 0, hi = n;  // first staged entry with row >= r
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (prow[mid] < r) lo = mid + 1; else hi = mid;
+      }
+      uint32_t end = lo, top = n;  // first staged entry with row > r
+      while (end < top) {
+        const uint32_t mid = (end + top) >> 1;
+        if (prow[mid] <= r) end = mid + 1; else top = mid;
+      }
+      uint32_t i = lo;
+      for (; i + 8 <= end; i += 8) {
+        T p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = prod[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+      }
+      for (; i < end; ++i) acc = add_rn(acc, prod[i]);
+    }
+    __syncthreads();
+  }
+  return acc;
+}
+
+// Register-lean form of hybrid_spmv_kernel (the RgCSR `lite` recipe applied
+// to the ELL part): no cache-policy registers, the slot pointers advance by
+// U*rows instead of recomputing 64-bit indices, and MINB resident CTAs per
+// SM.  Same per-row rounding sequence (all K1 ELL slots including pads, then
+// the row's COO entries in array order) -> y bitwise spmv_hybrid's.
+template <class T, int U, int MINB, bool kAccum, bool kCoo, bool kFence = false>
+__global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
+    uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
+    const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
+    const uint32_t* __restrict__ cc, const T* __restrict__ cv, const T* __restrict__ x,
+    T* __restrict__ y) {
+  const uint32_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
+  const size_t step = (size_t)U * rows;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r = tile * kRowsPerTile + threadIdx.x;
+    const bool live = r < rows;
+    T acc = T(0);
+    if (kAccum && live) acc = y[r];
+    if (live) {
+      const T* __restrict__ vp = ev + r;
+      const uint32_t* __restrict__ cp = ec + r;
+      uint32_t j = 0;
+      for (; j + U <= k1; j += U) {
+        uint32_t c[U];
+        T v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          c[u] = ld_stream(cp + (size_t)u * rows);
+          v[u] = ld_stream(vp + (size_t)u * rows);
+        }
+        if (kFence) __syncwarp(__activemask());  // slot loads ahead of the gathers
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+        cp += step;
+        vp += step;
+      }
+      if (j < k1) {  // predicated last batch (< U slots)
+        uint32_t c[U - 1];
+        T v[U - 1], xv[U - 1];
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u) {
+          c[u] = 0;
+          v[u] = T(0);
+          if (j + u < k1) {
+            c[u] = ld_stream(cp + (size_t)u * rows);
+            v[u] = ld_stream(vp + (size_t)u * rows);
+          }
+        }
+        if (kFence) __syncwarp(__activemask());
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u) xv[u] = j + u < k1 ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+        for (int u = 0; u < U - 1; ++u)
+          if (j + u < k1) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+      }
+    }
+    if constexpr (kCoo) acc = coo_tile_accumulate<T>(tile, r, live, acc, tile_ptr, cr, cc, cv, x);
+    if (live) y[r] = acc;
+  }
+}
+
+// Hybrid SpMV kernel choice: spmvk_set_hybrid_kernel() or SPMVK_HYBRID_KERNEL.
+// "v4": hybrid_spmv_kernel (policy-hinted loads, 4-deep, 8 CTAs / SM);
+// "lite" / "lite8" / "lite8_full": hybrid_spmv_lite with 4-deep batches at
+// 8 CTAs / SM, 8-deep at 5, 8-deep at 8.  All bitwise identical.
+enum class HK { kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F };
+
+std::atomic<int>& hk_slot() {
+  static std::atomic<int> k{[] {
+    HK v = HK::kAuto;
+    if (const char* e = std::getenv("SPMVK_HYBRID_KERNEL")) {
+      const std::string s(e);
+      v = s == "v4" ? HK::kV4 : s == "lite" ? HK::kLite : s == "lite8" ? HK::kLite8
+        : s == "lite8_full" ? HK::kLite8Full : s == "litef" ? HK::kLiteF
+        : s == "lite8f" ? HK::kLite8F : HK::kAuto;
+    }
+    return static_cast<int>(v);
+  }()};
+  return k;
+}
+
 template <class T, class V>
 void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
   const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
@@ -486,15 +617,53 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
   const uint64_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   const uint32_t k1 = part == Part::kCoo ? 0u : static_cast<uint32_t>(h->k1);
   const uint32_t* tp = part != Part::kEll && h->coo ? h->tile_ptr.p : nullptr;
-  // 4-deep slot batches at full occupancy (32 registers) for both precisions:
-  // fp32 8-deep measured 2-9 % slower (27-pt 79.3 vs 77.5 us, 7-pt 512^3
-  // 1550 vs 1410 us; scripts/ab_formats.py, profiles/r01_k2_sweep3.md)
-  auto kern = part == Part::kCoo ? hybrid_spmv_kernel<T, 4, true> : hybrid_spmv_kernel<T, 4>;
-  kern<<<persistent_grid(ntiles, 8), kRowsPerTile, 0, s>>>(
-      static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
-      h->ell_columns.p, tp, h->coo_rows.p, h->coo_columns.p,
-      reinterpret_cast<const T*>(h->coo_values.p), x, y);
-  SPMVK_LAUNCH("hybrid_spmv_kernel");
+  HK k = static_cast<HK>(hk_slot().load(std::memory_order_relaxed));
+  if (k == HK::kAuto) {
+    // measured (scripts/ab_formats.py, profiles/r01_hybrid_variants.md):
+    // fp64 4-deep lite at 8 CTAs / SM (27-pt 104.9 vs v4 105.5 us, power-law
+    // 772 vs 795 us); fp32 v4 (27-pt 77.3 vs 78.0, power-law 689 vs 705 us)
+    k = sizeof(T) == 8 ? HK::kLite : HK::kV4;
+  }
+  auto run = [&](auto kern) {
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowsPerTile, 0));
+    kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), kRowsPerTile, 0, s>>>(
+        static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
+        h->ell_columns.p, tp, h->coo_rows.p, h->coo_columns.p,
+        reinterpret_cast<const T*>(h->coo_values.p), x, y);
+    SPMVK_LAUNCH("hybrid_spmv");
+  };
+  const bool acc = part == Part::kCoo, coo = tp != nullptr;
+  switch (k) {
+    case HK::kV4:
+      if (acc) run(hybrid_spmv_kernel<T, 4, true>); else run(hybrid_spmv_kernel<T, 4>);
+      break;
+    case HK::kLite:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true>);
+      else run(hybrid_spmv_lite<T, 4, 8, false, false>);
+      break;
+    case HK::kLite8Full:
+      if (acc) run(hybrid_spmv_lite<T, 8, 8, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 8, 8, false, true>);
+      else run(hybrid_spmv_lite<T, 8, 8, false, false>);
+      break;
+    case HK::kLiteF:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
+      else run(hybrid_spmv_lite<T, 4, 8, false, false, true>);
+      break;
+    case HK::kLite8F:
+      if (acc) run(hybrid_spmv_lite<T, 8, 4, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 8, 4, false, true, true>);
+      else run(hybrid_spmv_lite<T, 8, 4, false, false, true>);
+      break;
+    default:
+      if (acc) run(hybrid_spmv_lite<T, 8, 5, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 8, 5, false, true>);
+      else run(hybrid_spmv_lite<T, 8, 5, false, false>);
+      break;
+  }
 }
 
 template <class T>
@@ -546,6 +715,24 @@ void spmv_part_host(const spmvk_hybrid* h, const T* x, uint64_t nx, T* y, uint64
 using namespace spmvk;
 
 extern "C" {
+
+int spmvk_set_hybrid_kernel(const char* name) {
+  return guarded([&] {
+    const std::string v = name ? name : "";
+    HK k;
+    if (v == "auto") k = HK::kAuto;
+    else if (v == "v4") k = HK::kV4;
+    else if (v == "lite") k = HK::kLite;
+    else if (v == "lite8") k = HK::kLite8;
+    else if (v == "lite8_full") k = HK::kLite8Full;
+    else if (v == "litef") k = HK::kLiteF;
+    else if (v == "lite8f") k = HK::kLite8F;
+    else
+      fail(SPMVK_EINVAL, "unknown Hybrid kernel variant '" + v +
+                             "' (auto | v4 | lite | lite8 | lite8_full | litef | lite8f)");
+    hk_slot().store(static_cast<int>(k));
+  });
+}
 
 uint64_t spmvk_hybrid_split_cost(const uint64_t* lens, uint64_t n, uint64_t k) {
   uint64_t overflow = 0;

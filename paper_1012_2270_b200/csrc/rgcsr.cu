@@ -231,7 +231,8 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // All variants give bitwise identical y; they differ in how slots are staged.
 enum class K2 {
   kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
-  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf, kVec2, kVec4
+  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf, kVec2, kVec4,
+  kGrp4, kGrp6, kGrp7, kGrp7Mpf, kGrp8, kGrp8R64, kGrp8Len
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -243,6 +244,17 @@ enum class K2 {
 // config) favour the row-prefetching `pipe` kernel in fp32
 // (profiles/r01_powerlaw.md: 1,070 vs 1,353 us).
 K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
+  // No long rows and <= 10 % padding (stencils, banded): the group-uniform
+  // walk (rgcsr_spmv_grp) -- one batch of slot loads per row, ordered ahead
+  // of the x gathers, next row's group pointers prefetched.  Measured
+  // (profiles/r01_k2_grp.md, back-to-back us): 5-pt 2048^2 fp64 47.2 vs 57.7
+  // (vec2), fp32 35.5 vs 35.7; 7-pt 384^3 fp64 842 vs 934 (lite8), fp32
+  // 607 vs 651 (lite); 27-pt 128^3 fp64 102.6 vs 105.5, fp32 75.5 vs 80.7.
+  if (!h->n_long && h->slots * 10 <= h->nnz * 11) {
+    if (2 * h->slots <= 11 * h->rows) return K2::kGrp6;
+    if (f64) return K2::kGrp8R64;
+    return h->slots <= 12 * h->rows ? K2::kGrp8 : K2::kGrp7Mpf;
+  }
   // <= 5.5 slots per row (5-point class): two / four rows per thread with
   // 128-bit value loads win (5-pt 4096^2: fp64 220 vs 232 us, fp32 152 vs
   // 163 us); from 7 slots on they lose (profiles/r01_k2_sweep3.md)
@@ -265,7 +277,10 @@ bool parse_k2(const std::string& v, K2* out) {
       {"lite", K2::kLite},     {"lite8", K2::kLite8},
       {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full},
       {"lite_mpf", K2::kLiteMpf}, {"lite8_mpf", K2::kLite8Mpf},
-      {"lite8_full_mpf", K2::kLite8FullMpf}, {"vec2", K2::kVec2}, {"vec4", K2::kVec4}};
+      {"lite8_full_mpf", K2::kLite8FullMpf}, {"vec2", K2::kVec2}, {"vec4", K2::kVec4},
+      {"grp4", K2::kGrp4}, {"grp6", K2::kGrp6}, {"grp7", K2::kGrp7},
+      {"grp7_mpf", K2::kGrp7Mpf}, {"grp8", K2::kGrp8}, {"grp8_r64", K2::kGrp8R64},
+      {"grp8_len", K2::kGrp8Len}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -410,7 +425,18 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       SPMVK_LAUNCH("rgcsr_spmv_long");
     }
   };
+  // the group-uniform walk has no long-row split: matrices with long rows
+  // (and, for now, any request on them) take the lite kernel instead
+  if (k >= K2::kGrp4 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
   switch (k) {
+    // group-uniform walk: <T, kScaled, U, MINB, kNoLen, kMpf>
+    case K2::kGrp4: run(rgcsr_spmv_grp<T, kScaled, 4, 8, true, false>); break;
+    case K2::kGrp6: run(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
+    case K2::kGrp7: run(rgcsr_spmv_grp<T, kScaled, 7, 5, true, false>); break;
+    case K2::kGrp7Mpf: run(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true>); break;
+    case K2::kGrp8: run(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
+    case K2::kGrp8R64: run(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
+    case K2::kGrp8Len: run(rgcsr_spmv_grp<T, kScaled, 8, 5, false, false>); break;
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
     case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
     case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;

@@ -214,11 +214,17 @@ __device__ __forceinline__ void lite_tiles_epi(
       }
     }
     if (r >= rows) continue;
-    if (!kMetaPf) len = lens[r];
-    if (len > long_cut) continue;  // handled by rgcsr_spmv_long
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    if (!kMetaPf) {
+      len = ld_stream(lens + r);
+      base = ld_stream(gp + g);
+    }
+    // rows past the cut are rgcsr_spmv_long's: predicated to zero slots rather
+    // than branched around, so the length and group-pointer loads issue
+    // together (a branch on len would let ptxas sink the gp load behind it)
+    const bool mine = len <= long_cut;
+    if (!mine) len = 0;
     const uint32_t s = min(G, rows - g * G);
-    if (!kMetaPf) base = gp[g];
     const uint32_t off = base + (r - g * G);
     const T* __restrict__ vp = values + off;
     const uint32_t* __restrict__ cp = columns + off;
@@ -257,7 +263,7 @@ __device__ __forceinline__ void lite_tiles_epi(
       for (int u = 0; u < U - 1; ++u)
         if (j + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
     }
-    epi(r, acc);
+    if (mine) epi(r, acc);
   }
 }
 
@@ -280,6 +286,118 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
   lite_tiles_epi<T, U, kPrefetchL2, StoreEpi<T, kScaled>, kMetaPf>(
       0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns, x, long_cut,
       StoreEpi<T, kScaled>{y, x_next, scale});
+}
+
+// ---------------------------------------------------------------------------
+// rgcsr_spmv_grp -- group-uniform walk for matrices without long rows.
+//
+// Every row of group g walks the group's full width K_g = (gp[g+1] - gp[g]) / s
+// (uniform across a warp when G is a multiple of 32), so the slot loads
+// depend only on the group pointers -- not on the row length -- and no lane
+// diverges.  A thread's slots past its own length are pads (value 0, column
+// 0): they are loaded (they sit in the same sectors as the neighbours' real
+// slots) but contribute nothing:
+//  * kNoLen = false: gathers and adds predicated on j < len (len loaded in
+//    the same round trip as the group pointers);
+//  * kNoLen = true: row_lengths is not read at all when x[0] is finite.  A
+//    pad adds 0 * x[0] = +-0, and acc + (+-0) == acc bitwise: acc starts at
+//    +0 and a round-to-nearest sum is -0 only for (-0) + (-0), so acc is
+//    never -0.  A non-finite x[0] (0 * inf = NaN) switches the whole launch
+//    (uniform branch) back to length predication.
+// kMpf: the next row's (gp[g], gp[g+1], len) are loaded while this row's
+// slots are in flight, so a row costs two dependent round trips (slots, x)
+// like the ELLPACK kernel.  Per row the adds stay in slot order -> y bitwise
+// spmv_rgcsr's.
+template <class T, int U, bool kNoLen, bool kMpf, class Epi>
+__device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_shift,
+                                              const uint32_t* __restrict__ gp,
+                                              const uint32_t* __restrict__ lens,
+                                              const T* __restrict__ values,
+                                              const uint32_t* __restrict__ columns,
+                                              const T* __restrict__ x, const Epi& epi) {
+  const bool use_len = !kNoLen || !isfinite(__ldg(x));
+  const uint32_t ntiles = (rows + 255) / 256;
+  struct Meta {
+    uint32_t b0, b1, len;
+  };
+  auto load_meta = [&](uint32_t r) {
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    Meta m;
+    m.b0 = ld_stream(gp + g);
+    m.b1 = ld_stream(gp + g + 1);
+    m.len = use_len ? ld_stream(lens + r) : 0u;
+    return m;
+  };
+  Meta nxt{0, 0, 0};
+  if (kMpf) {
+    const uint32_t r0 = blockIdx.x * 256 + threadIdx.x;
+    if (blockIdx.x < ntiles && r0 < rows) nxt = load_meta(r0);
+  }
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r = tile * 256 + threadIdx.x;
+    Meta m;
+    if (kMpf) {
+      m = nxt;
+      const uint32_t rn = r + gridDim.x * 256;
+      if (tile + gridDim.x < ntiles && rn < rows) nxt = load_meta(rn);
+    }
+    if (r >= rows) continue;
+    if (!kMpf) m = load_meta(r);
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t width = m.b1 - m.b0;
+    const uint32_t K = (s == G && g_shift >= 0) ? (width >> g_shift) : width / s;
+    const uint32_t lim = use_len ? m.len : K;
+    const uint32_t off = m.b0 + (r - g * G);
+    const T* __restrict__ vp = values + off;
+    const uint32_t* __restrict__ cp = columns + off;
+    T acc = T(0);
+    uint32_t j = 0;
+    for (; j + U <= K; j += U) {
+      uint32_t c[U];
+      T v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + u * s);
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = ld_stream(cp + u * s);
+      // warp barrier = a ptxas scheduling fence: every slot load (columns AND
+      // values) issues before the first gather waits on a column; without it
+      // ptxas interleaves and the value loads trail by a full DRAM round trip
+      __syncwarp(__activemask());
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j + u < lim ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+      cp += U * s;
+      vp += U * s;
+    }
+    if (j < K) {  // predicated last batch (< U slots)
+      uint32_t c[U - 1];
+      T v[U - 1], xv[U - 1];
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u) v[u] = j + u < K ? ld_stream(vp + u * s) : T(0);
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u) c[u] = j + u < K ? ld_stream(cp + u * s) : 0u;
+      __syncwarp(__activemask());
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u) xv[u] = j + u < lim ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+      for (int u = 0; u < U - 1; ++u)
+        if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    }
+    epi(r, acc);
+  }
+}
+
+template <class T, bool kScaled, int U, int MINB, bool kNoLen, bool kMpf>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t /*long_cut: no long rows on this path*/) {
+  grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>>(
+      rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
 // ---------------------------------------------------------------------------

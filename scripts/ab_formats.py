@@ -22,16 +22,17 @@ def main():
     ap.add_argument("--variants", default="lite8,lite,hybrid")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--group", type=int, default=32)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     L = lib()
     assert L.spmvk_init(0) == 0
     kind, n = (int(v) for v in a.case.split(":"))
-    csr = sk.CsrMatrix.stencil(kind, n)
+    csr = sk.CsrMatrix.stencil(kind, n) if kind else sk.build_csr(gen.powerlaw(n, 7))
     if a.prec == 4:
         csr = sk.build_csr(sk.TripletMatrix(csr.num_rows, csr.num_cols, *csr.to_host()), 4)
     dt = torch.float64 if a.prec == 8 else torch.float32
-    rg = sk.build_rgcsr(csr, 32, a.prec)
+    rg = sk.build_rgcsr(csr, a.group, a.prec)
     hy = sk.build_hybrid(csr, None, a.prec)
     x = torch.from_numpy(gen.random_vector(csr.num_cols, 1)).cuda().to(dt)
     y = torch.empty(csr.num_rows, dtype=dt, device="cuda")
@@ -41,14 +42,25 @@ def main():
     f_hy = L.spmvk_hybrid_spmv_f64 if a.prec == 8 else L.spmvk_hybrid_spmv_f32
 
     def launcher(v):
-        if v == "hybrid":
-            return lambda: f_hy(hy._h, x.data_ptr(), csr.num_cols, y.data_ptr(), csr.num_rows,
-                                s.cuda_stream)
+        if v.startswith("hybrid"):  # hybrid or hybrid:<variant> (spmvk_set_hybrid_kernel)
+            hv = (v.split(":", 1)[1] if ":" in v else "auto").encode()
+            return lambda: (L.spmvk_set_hybrid_kernel(hv),
+                            f_hy(hy._h, x.data_ptr(), csr.num_cols, y.data_ptr(), csr.num_rows,
+                                 s.cuda_stream))
         return lambda: (L.spmvk_set_rgcsr_kernel(v.encode()),
                         f_rg(rg._h, x.data_ptr(), csr.num_cols, y.data_ptr(), csr.num_rows,
                              s.cuda_stream))
 
     res = {v: {"b2b": [], "flushed": []} for v in a.variants.split(",")}
+    y0 = None
+    for v in res:  # every variant's y must be bitwise the first's
+        launcher(v)()
+        torch.cuda.synchronize()
+        if y0 is None:
+            y0 = y.clone()
+        elif not torch.equal(y.view(torch.int64 if a.prec == 8 else torch.int32),
+                             y0.view(torch.int64 if a.prec == 8 else torch.int32)):
+            print(f"{a.case} p{a.prec} {v}: y NOT bitwise equal to {next(iter(res))}", flush=True)
     for _ in range(a.rounds):
         for v in res:
             fn = launcher(v)
@@ -72,8 +84,9 @@ def main():
             torch.cuda.synchronize()
             res[v]["flushed"].append(statistics.median(p.elapsed_time(q) for p, q in per) * 1e3)
     L.spmvk_set_rgcsr_kernel(b"auto")
+    L.spmvk_set_hybrid_kernel(b"auto")
     for v, d in res.items():
-        print(f"{a.case} p{a.prec} {v:12s} b2b us " + " ".join(f"{t:7.2f}" for t in d["b2b"]) +
+        print(f"{a.case} p{a.prec} g{a.group} {v:12s} b2b us " + " ".join(f"{t:7.2f}" for t in d["b2b"]) +
               " | flushed us " + " ".join(f"{t:7.2f}" for t in d["flushed"]), flush=True)
 
 

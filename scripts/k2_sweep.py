@@ -21,8 +21,8 @@ from paper_1012_2270_b200._lib import lib  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--variants", default="auto,lite,lite8,pipe,pipe_hi,tma,wtma,ldg_pf")
-    ap.add_argument("--cases", default="27:128:32,27:128:128,5:1024:32,7:256:32,7:512:32")
+    ap.add_argument("--variants", default="auto,lite,lite8,lite8_mpf,vec2,grp6,grp7_mpf,grp8,grp8_r64")
+    ap.add_argument("--cases", default="27:128:32,27:128:128,5:1024:32,5:2048:32,7:256:32,7:512:32")
     ap.add_argument("--flush", action="store_true",
                     help="read 512 MB before every timed launch (median of per-launch events)")
     ap.add_argument("--precs", default="8,4")

@@ -99,3 +99,15 @@ def test_peak_performance_table():
         assert (p.gflops, p.bytes_per_nnz) == (gf, bpn)
     assert sk.peak_performance(8, False, 282.0).gflops == 2 * sk.peak_performance(8, False, 141.0).gflops
     assert sk.peak_performance(8, True).gflops == 2 * 6545.3 / 12
+
+
+def test_kernel_variant_knobs_validate_names():
+    """The tuning knobs accept their documented names and reject others
+    (EINVAL with the list) -- host-only, no device needed."""
+    L = _lib.lib()
+    for v in (b"auto", b"v4", b"lite", b"lite8", b"lite8_full", b"litef", b"lite8f"):
+        assert L.spmvk_set_hybrid_kernel(v) == 0, v
+    assert L.spmvk_set_hybrid_kernel(b"nope") == _lib.SPMVK_EINVAL
+    assert "lite8_full" in _lib.last_error()
+    assert L.spmvk_set_rgcsr_kernel(b"nope") == _lib.SPMVK_EINVAL
+    assert L.spmvk_set_hybrid_kernel(b"auto") == 0 and L.spmvk_set_rgcsr_kernel(b"auto") == 0

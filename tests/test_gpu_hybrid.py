@@ -15,6 +15,18 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
+HYBRID_VARIANTS = ["auto", "v4", "lite", "lite8", "lite8_full", "litef", "lite8f"]
+
+
+@pytest.fixture(params=HYBRID_VARIANTS)
+def hk(request, cuda):
+    """Runs the test once per Hybrid SpMV kernel variant (all bitwise equal)."""
+    from paper_1012_2270_b200._lib import lib
+    assert lib().spmvk_set_hybrid_kernel(request.param.encode()) == 0
+    yield request.param
+    lib().spmvk_set_hybrid_kernel(b"auto")
+
+
 def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
@@ -40,7 +52,7 @@ def test_example8_golden(cuda, golden):
 
 
 @pytest.mark.parametrize("kind", ["i", "r"])
-def test_small_golden_seeds(cuda, golden, kind):
+def test_small_golden_seeds(cuda, hk, golden, kind):
     g = golden["small"]
     for seed in range(600, 650):
         t = f"s{seed}_{kind}"
@@ -56,7 +68,7 @@ def test_small_golden_seeds(cuda, golden, kind):
         assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), g[f"{t}_hy_y"]), t
 
 
-def test_acceptance_200_seeds(cuda, golden):
+def test_acceptance_200_seeds(cuda, hk, golden):
     g = golden["acceptance"]
     for seed in range(200):
         m = triplets(golden_csr(g, f"a{seed}"))
@@ -77,7 +89,7 @@ def test_device_width_matches_exhaustive_scan(cuda):
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_powerlaw_small_bitwise(cuda, prec):
+def test_powerlaw_small_bitwise(cuda, hk, prec):
     """Config 3's generator at 200k rows: long COO tails through the fused kernel."""
     om = orc.powerlaw(200_000, 7)
     h = sk.build_hybrid(triplets(om), None, prec)
@@ -90,7 +102,7 @@ def test_powerlaw_small_bitwise(cuda, prec):
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_config2_27pt_128_bitwise(cuda, prec):
+def test_config2_27pt_128_bitwise(cuda, hk, prec):
     om = orc.stencil(27, 128)
     h = sk.build_hybrid(sk.CsrMatrix.stencil(27, 128), None, prec)
     want = orc.build_hybrid(om, None, prec)
@@ -180,7 +192,7 @@ def test_ellpack_example_and_shapes(cuda, golden):
         sk.spmv_ellpack(a, np.ones(9))
 
 
-def test_spmv_coo_accumulates(cuda, golden):
+def test_spmv_coo_accumulates(cuda, hk, golden):
     """tests/test_formats.cpp:96-122: the COO part adds into y in array order."""
     single = sk.build_hybrid(sk.canonicalize([(0, 0, 2.0)], 1, 1), 0)  # all entries in COO
     y = np.array([1.0])
@@ -207,7 +219,7 @@ def test_spmv_coo_accumulates(cuda, golden):
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_parts_compose_to_spmv_hybrid(cuda, golden, prec):
+def test_parts_compose_to_spmv_hybrid(cuda, hk, golden, prec):
     """spmv_ellpack(h.ell) then spmv_coo(h.coo) is spmv_hybrid (ellpack.hpp:
     205-210), bitwise, host and device, on the 200 acceptance matrices."""
     g = golden["acceptance"]

@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 VARIANTS = ["auto", "lite", "lite8", "lite8_full", "lite8_l2pf", "lite_l2pf", "vec2", "vec4", "pipe", "pipe_hi", "pipe8",
-            "ldg", "ldg_pf", "tma", "wtma"]
+            "ldg", "ldg_pf", "tma", "wtma", "lite_mpf", "lite8_mpf", "lite8_full_mpf",
+            "grp4", "grp6", "grp7", "grp7_mpf", "grp8", "grp8_r64", "grp8_len"]
 
 
 def dev(x):
@@ -108,6 +109,22 @@ def test_acceptance_200_seeds(cuda, golden, k2):
         assert_rgcsr_equal(a.to_host(), g, f"a{seed}_rg_")
         y = sk.spmv_rgcsr(a, dev(g[f"a{seed}_xi"])).cpu().numpy()
         assert bitwise(y, g[f"a{seed}_rg_yi"]) and bitwise(y, g[f"a{seed}_ref_yi"]), seed
+
+
+@pytest.mark.parametrize("x0", [np.inf, -np.inf, np.nan, -0.0, -2.5])
+def test_padded_walk_exact_for_any_x0(cuda, k2, x0):
+    """The group-uniform kernels load pads (value 0, column 0); with a
+    non-finite x[0] a pad's 0 * x[0] would be NaN, so they must fall back to
+    length predication: y stays bitwise spmv_rgcsr's (rows that never touch
+    column 0 stay finite).  Ragged rows in every group, several G."""
+    om = orc.random_small(4242, allow_zero=True)
+    for G in (3, 4, 32):
+        m = triplets(om)
+        want = orc.build_rgcsr(om, G, 8)
+        x = orc.random_vector(om.cols, 5)
+        x[0] = x0
+        y = sk.spmv_rgcsr(sk.build_rgcsr(m, G), dev(x)).cpu().numpy()
+        assert bitwise(y, orc.spmv_rgcsr(want, x)[0]), (G, x0)
 
 
 def test_padding_monotone_and_single_group_is_ell(cuda):
