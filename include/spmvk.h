@@ -195,14 +195,21 @@ int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx
 int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
                               uint64_t ny, uint64_t* multiply_add_count);
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
-/* Tuning knob (process-wide): which K2 kernel runs — "auto" (default: lite8
- * for fp64, lite — or pipe for irregular matrices — for fp32), "lite" /
- * "lite8" (register-lean thread per row at high occupancy), "lite_l2pf" /
- * "lite8_l2pf" (+ bulk L2 prefetch of the next tile), "pipe" / "pipe_hi" /
- * "pipe8" (row-metadata prefetch, predicated batches), "ldg" / "ldg_pf"
- * (first kernels), "tma" (CTA-wide bulk-async-copy ring), "wtma" (per-warp
- * bulk-async-copy streams).  All give bitwise identical y; the measured
- * comparison is in DESIGN.md §3.  Also read from SPMVK_RGCSR_KERNEL. */
+/* Tuning knob (process-wide): which K2 kernel runs -- "auto" (default: for
+ * matrices without long rows and <= 10 % padding the group-uniform walk,
+ * grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf (fp32);
+ * otherwise lite8 for fp64, lite or pipe for fp32), "grp4" / "grp6" /
+ * "grp7" / "grp7_mpf" / "grp8" / "grp8_r64" / "grp8_len" (group-uniform
+ * walk: U-deep slot batches bound by the group width, scheduling fence
+ * before the x gathers, row_lengths skipped when x[0] is finite; _mpf
+ * prefetches the next row's group pointers; grp8_len predicates on
+ * row_lengths), "lite" / "lite8" / "lite8_full" / "lite*_mpf" (register-lean
+ * thread per row), "vec2" / "vec4" (128-bit loads of 2 / 4 rows),
+ * "lite_l2pf" / "lite8_l2pf" (+ bulk L2 prefetch of the next tile), "pipe" /
+ * "pipe_hi" / "pipe8" (row-metadata prefetch, predicated batches), "ldg" /
+ * "ldg_pf" (first kernels), "tma" (CTA-wide bulk-async-copy ring), "wtma"
+ * (per-warp bulk-async-copy streams).  All give bitwise identical y; the
+ * measured comparison is in DESIGN.md §3.  Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
 /* Tuning knob (process-wide, read at build): rows with more than `cut` slots
  * (default 128) are handled by a warp-per-row kernel instead of one thread
@@ -211,10 +218,11 @@ int spmvk_set_long_row_cut(uint32_t cut);
 
 /* ------------------------------------------------------------------ Hybrid */
 /* Tuning knob (process-wide): Hybrid SpMV kernel variant, "auto" (default:
- * "lite8" for fp64; fp32 "lite8_full" when K1 <= 12, else "lite"), "v4"
- * (first kernel: policy-hinted loads, 4-deep), "lite" / "lite8" /
- * "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at 8 / 5 / 8
- * CTAs per SM).  All give bitwise identical y.  Also read from
+ * "litef"), "v4" (first kernel: policy-hinted loads, 4-deep), "lite" /
+ * "lite8" / "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at
+ * 8 / 5 / 8 CTAs per SM), "litef" / "lite8f" (same, 4-deep at 8 / 8-deep
+ * at 4 CTAs per SM, with a scheduling fence that issues every slot load
+ * before the x gathers).  All give bitwise identical y.  Also read from
  * SPMVK_HYBRID_KERNEL. */
 int spmvk_set_hybrid_kernel(const char* name);
 typedef struct {

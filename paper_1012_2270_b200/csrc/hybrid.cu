@@ -619,10 +619,10 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
   const uint32_t* tp = part != Part::kEll && h->coo ? h->tile_ptr.p : nullptr;
   HK k = static_cast<HK>(hk_slot().load(std::memory_order_relaxed));
   if (k == HK::kAuto) {
-    // measured (scripts/ab_formats.py, profiles/r01_hybrid_variants.md):
-    // fp64 4-deep lite at 8 CTAs / SM (27-pt 104.9 vs v4 105.5 us, power-law
-    // 772 vs 795 us); fp32 v4 (27-pt 77.3 vs 78.0, power-law 689 vs 705 us)
-    k = sizeof(T) == 8 ? HK::kLite : HK::kV4;
+    // measured (scripts/ab_formats.py, profiles/r01_hybrid_variants.md): the
+    // fenced 4-deep lite kernel is best or within 2 % everywhere (7-pt 256^3
+    // fp64 239 vs v4 248 us, fp32 173 vs 180; power-law fp64 748 vs 801)
+    k = HK::kLiteF;
   }
   auto run = [&](auto kern) {
     int per_sm = 0;

@@ -818,8 +818,10 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (auto | lite | lite8 | lite_l2pf | lite8_l2pf | pipe | pipe_hi | "
-                             "pipe8 | ldg | ldg_pf | tma | wtma)");
+                             "' (auto | grp4 | grp6 | grp7 | grp7_mpf | grp8 | grp8_r64 | grp8_len | "
+                             "lite | lite8 | lite8_full | lite_mpf | lite8_mpf | lite8_full_mpf | "
+                             "vec2 | vec4 | lite_l2pf | lite8_l2pf | pipe | pipe_hi | pipe8 | ldg | "
+                             "ldg_pf | tma | wtma)");
     k2_slot().store(static_cast<int>(k));
   });
 }
