@@ -195,6 +195,17 @@ int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx
 int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
                               uint64_t ny, uint64_t* multiply_add_count);
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
+/* L2 persistence window for the gathered vector x (the north star's "x
+ * served ... with L2 persistence windows"): sets the device's persisting-L2
+ * carve-out to min(bytes, cudaDevAttrMaxPersistingL2CacheSize) and the
+ * stream's access-policy window over [x, x + bytes) (hits persisting, misses
+ * streaming; hit_ratio scaled down when x exceeds the carve-out).  Every
+ * kernel later launched on `stream` then keeps x's lines resident while the
+ * matrix streams past.  x == NULL or bytes == 0 resets (no window, carve-out
+ * 0).  `granted` (optional) receives the carve-out in bytes.  Does not change
+ * y.  (No reference counterpart: the CPU reference has no cache control.) */
+int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double hit_ratio,
+                           uint64_t* granted);
 /* Tuning knob (process-wide): which K2 kernel runs -- "auto" (default: for
  * matrices without long rows and <= 10 % padding the group-uniform walk,
  * grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf (fp32);

@@ -77,6 +77,7 @@ SIGNATURES = {
     "spmvk_rgcsr_destroy": (None, [vp]),
     "spmvk_set_rgcsr_kernel": (cint, [C.c_char_p]),
     "spmvk_set_hybrid_kernel": (cint, [C.c_char_p]),
+    "spmvk_stream_persist_x": (cint, [vp, vp, u64, C.c_double, u64p]),
     "spmvk_set_long_row_cut": (cint, [C.c_uint32]),
     "spmvk_csr_choose_ell_width": (cint, [vp, u64p]),
     "spmvk_choose_ell_width": (u64, [vp, u64]),

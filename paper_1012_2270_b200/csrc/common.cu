@@ -1,3 +1,4 @@
+#include <algorithm>
 // Device plumbing shared by all spmvk entry points: last-error slot, device
 // checks, and the uint64 exclusive scan used for group pointers / COO offsets.
 #include "common.cuh"
@@ -162,6 +163,40 @@ int spmvk_init(int device) {
     if (p.major != 10)
       spmvk::fail(SPMVK_ECUDA, std::string("spmvk is built for sm_100a; device ") + p.name +
                                    " is sm_" + std::to_string(p.major * 10 + p.minor));
+  });
+}
+
+int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double hit_ratio,
+                           uint64_t* granted) {
+  return spmvk::guarded([&] {
+    spmvk::require_device();
+    int dev = 0, max_persist = 0, max_window = 0;
+    SPMVK_CUDA(cudaGetDevice(&dev));
+    SPMVK_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    SPMVK_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    cudaStreamAttrValue v{};
+    const auto s = static_cast<cudaStream_t>(stream);
+    uint64_t limit = 0;
+    if (!x || bytes == 0) {  // reset: no window, persisting lines demoted, no carve-out
+      v.accessPolicyWindow.num_bytes = 0;
+      SPMVK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+      SPMVK_CUDA(cudaCtxResetPersistingL2Cache());
+      SPMVK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+    } else {
+      if (!(hit_ratio > 0.0 && hit_ratio <= 1.0))
+        spmvk::fail(SPMVK_EINVAL, "persist_x: hit_ratio must be in (0, 1]");
+      limit = std::min<uint64_t>(bytes, static_cast<uint64_t>(max_persist));
+      SPMVK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
+      const uint64_t win = std::min<uint64_t>(bytes, static_cast<uint64_t>(max_window));
+      v.accessPolicyWindow.base_ptr = const_cast<void*>(x);
+      v.accessPolicyWindow.num_bytes = win;
+      v.accessPolicyWindow.hitRatio =
+          static_cast<float>(hit_ratio * std::min(1.0, static_cast<double>(limit) / win));
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      SPMVK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
+    if (granted) *granted = limit;
   });
 }
 
