@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--group", type=int, default=32)
+    ap.add_argument("--reorder", action="store_true", help="descending row reordering first")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     L = lib()
@@ -32,6 +33,8 @@ def main():
     if a.prec == 4:
         csr = sk.build_csr(sk.TripletMatrix(csr.num_rows, csr.num_cols, *csr.to_host()), 4)
     dt = torch.float64 if a.prec == 8 else torch.float32
+    if a.reorder:
+        csr = sk.apply_descending_permutation(csr)[0]
     rg = sk.build_rgcsr(csr, a.group, a.prec)
     hy = sk.build_hybrid(csr, None, a.prec)
     x = torch.from_numpy(gen.random_vector(csr.num_cols, 1)).cuda().to(dt)
@@ -86,7 +89,7 @@ def main():
     L.spmvk_set_rgcsr_kernel(b"auto")
     L.spmvk_set_hybrid_kernel(b"auto")
     for v, d in res.items():
-        print(f"{a.case} p{a.prec} g{a.group} {v:12s} b2b us " + " ".join(f"{t:7.2f}" for t in d["b2b"]) +
+        print(f"{a.case}{'r' if a.reorder else ''} p{a.prec} g{a.group} {v:12s} b2b us " + " ".join(f"{t:7.2f}" for t in d["b2b"]) +
               " | flushed us " + " ".join(f"{t:7.2f}" for t in d["flushed"]), flush=True)
 
 

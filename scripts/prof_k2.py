@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--variant", default="pipe")
     ap.add_argument("--format", default="rgcsr")
     ap.add_argument("--launches", type=int, default=4)
+    ap.add_argument("--reorder", action="store_true", help="descending row reordering first")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     L = lib()
@@ -29,9 +30,11 @@ def main():
     assert L.spmvk_set_rgcsr_kernel(a.variant.encode()) == 0
     kind, n, G = (int(v) for v in a.case.split(":"))
     if kind == 0:
-        csr = sk.build_csr(gen.powerlaw(n, 7))
+        csr = sk.build_csr(gen.powerlaw(n, 7), a.prec)
     else:
         csr = sk.CsrMatrix.stencil(kind, n)
+    if a.reorder:
+        csr = sk.apply_descending_permutation(csr)[0]
     h = sk.build_rgcsr(csr, G, a.prec) if a.format == "rgcsr" else sk.build_hybrid(csr, None, a.prec)
     del csr
     dt = torch.float64 if a.prec == 8 else torch.float32

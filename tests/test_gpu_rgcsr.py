@@ -168,6 +168,20 @@ def test_edge_shapes(cuda, shape, k2):
         assert bitwise(sk.spmv_rgcsr(a, x), orc.spmv_rgcsr(want, x)[0])
 
 
+@pytest.mark.parametrize("prec", [8, 4])
+def test_powerlaw_long_rows_bitwise(cuda, prec, k2):
+    """Config 3's generator at 200k rows: ~600 rows past the long-row cut (up
+    to 4096 slots) next to short ones -- the long-row paths of every variant."""
+    om = orc.powerlaw(200_000, 7)
+    assert int(om.lens().max()) > 1000
+    for G in (32, 7):
+        want = orc.build_rgcsr(om, G, prec)
+        a = sk.build_rgcsr(triplets(om), G, prec)
+        dt = np.float64 if prec == 8 else np.float32
+        x = orc.random_vector(om.cols, 1).astype(dt)
+        assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), orc.spmv_rgcsr(want, x)[0]), G
+
+
 @pytest.mark.parametrize("G", [32, 64, 128, 256])
 @pytest.mark.parametrize("prec", [8, 4])
 def test_config1_5pt_1024_bitwise(cuda, G, prec, k2):
