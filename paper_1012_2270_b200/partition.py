@@ -435,10 +435,36 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # SPMVK_SHARE_GPU=1: every rank on GPU 0 with gloo plumbing (the fused
+    # exchange's data path is CUDA IPC + the device flag barrier, which works
+    # between processes sharing a GPU) -- exercises the N > 1 bench path on a
+    # one-GPU box; NCCL refuses two ranks on one device
+    share = os.environ.get("SPMVK_SHARE_GPU") == "1"
+    local = 0 if share else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     assert lib().spmvk_init(local) == 0, sk._lib.last_error()
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if share:
+        if getattr(args, "exchange", "fused") != "fused":
+            raise SystemExit("SPMVK_SHARE_GPU=1 supports --exchange fused only")
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cdev = "cpu" if share else "cuda"  # device of the plumbing tensors
+
+    def gather_flat(t):  # all-gather of a small 1-D plumbing tensor, rank order
+        t = t.to(cdev)
+        if share:
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t)
+            return torch.cat(parts)
+        out = torch.empty(world * t.numel(), dtype=t.dtype, device=cdev)
+        dist.all_gather_into_tensor(out, t)
+        return out
+
+    def reduce_scalar(v, op, dtype=torch.float64):
+        t = torch.tensor([v], dtype=dtype, device=cdev)
+        dist.all_reduce(t, op=op)
+        return t
     G = 32
     kind, a_, b_, desc = workloads[args.workload]
     csr = sk.CsrMatrix.stencil(a_, b_) if kind == "stencil" else sk.build_csr(gen.powerlaw(b_, 7))
@@ -453,9 +479,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
         import ctypes as C
         cr = (C.c_uint64 * 2)()
         sk._check(lib().spmvk_csr_column_range(csr._h, me.row_begin, me.row_end, cr))
-        mine = torch.tensor([int(cr[0]), int(cr[1])], dtype=torch.int64, device="cuda")
-        allr = torch.empty(2 * world, dtype=torch.int64, device="cuda")
-        dist.all_gather_into_tensor(allr, mine)
+        allr = gather_flat(torch.tensor([int(cr[0]), int(cr[1])], dtype=torch.int64))
         ranges = [tuple(allr[2 * r: 2 * r + 2].tolist()) for r in range(world)]
     del csr
     L = lib()
@@ -489,8 +513,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             ok, why = 1, ""
         except Exception as e:  # noqa: BLE001 -- reported, then the NCCL path runs
             ok, why = 0, f"rank {rank}: {e}"
-        flag = torch.tensor([ok], device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        flag = reduce_scalar(ok, dist.ReduceOp.MIN, torch.int64)
         if not flag.item():
             reasons = [None] * world
             dist.all_gather_object(reasons, why)
@@ -527,10 +550,16 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     torch.cuda.synchronize()
     if clocks:
         clocks.__exit__(None, None, None)
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    tot_nnz = torch.tensor([nnz_local], device="cuda", dtype=torch.float64)
-    dist.all_reduce(tot_nnz)
+    ms = reduce_scalar(e0.elapsed_time(e1), dist.ReduceOp.MAX)
+    # checksum of this rank's rows of the iterate after warmup + steps
+    # iterations (bitwise across P: the slab arrays are global slices and
+    # every row keeps the reference's order) -- taken before the e2e leg,
+    # which re-uploads each rank's own x slab only
+    xf = it.x[: a.num_cols] if exchange == "allgather" else it.x_current
+    # order-independent bit checksum: wrapping int64 sum of the raw bits
+    part_sum = xf[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
+    sums = gather_flat(part_sum)
+    tot_nnz = reduce_scalar(float(nnz_local), dist.ReduceOp.SUM)
 
     # kernel-only time of this rank's slab SpMV (roofline of the dominant kernel)
     xs = (it.x[: a.num_cols] if exchange == "allgather" else it.x_current).clone()
@@ -543,8 +572,8 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
         slab_spmv(xs, ys[: a.num_rows], xn[: a.num_rows])
         e_.record(stream)
     torch.cuda.synchronize()
-    kern_ms = torch.tensor([sum(s_.elapsed_time(e_) for s_, e_ in kev) / len(kev)], device="cuda")
-    dist.all_reduce(kern_ms, op=dist.ReduceOp.MAX)
+    kern_ms = reduce_scalar(sum(s_.elapsed_time(e_) for s_, e_ in kev) / len(kev),
+                            dist.ReduceOp.MAX)
     slab_bytes = (rg_bytes(a.info, 8) if rg_bytes else 0)
 
     # e2e: every step each rank uploads its x slab from pinned host memory,
@@ -565,15 +594,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             yh[: a.num_rows].copy_(it.y[: a.num_rows], non_blocking=True)
         stream.synchronize()
     torch.cuda.synchronize()
-    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
-    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    # checksum of this rank's rows of the final iterate (bitwise across P: the
-    # slab arrays are global slices and every row keeps the reference's order)
-    xf = it.x[: a.num_cols] if exchange == "allgather" else it.x_current
-    # order-independent bit checksum: wrapping int64 sum of the raw bits
-    part_sum = xf[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
-    sums = torch.empty(world, dtype=torch.int64, device="cuda")
-    dist.all_gather_into_tensor(sums, part_sum)
+    e2e_s = reduce_scalar((time.perf_counter() - t0) / e2e_steps, dist.ReduceOp.MAX)
     dist.barrier()
     if rank == 0:
         step_ms = ms.item() / args.steps
@@ -599,6 +620,9 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
                                 f"slab SpMV (+fused x_next = y/16) + {exchange} exchange"),
                        "halo_entries_rank0": halo,
                        "exchange_fallback": fallback,
+                       "shared_gpu": (f"SPMVK_SHARE_GPU=1: all {world} ranks on GPU 0 (gloo "
+                                      "plumbing; a correctness run, not a scaling number)"
+                                      if share else None),
                        "l2": "per-rank slab streamed from HBM each step (no flush)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved and peak else None,

@@ -194,3 +194,34 @@ def test_two_processes_ipc_barrier(cuda, mode, world, steps):
                 p.kill()
     for p, (out, err) in zip(procs, outs):
         assert p.returncode == 0 and out.strip().endswith("ok"), err[-3000:]
+
+
+def _bench_json(world, workload, steps=6):
+    """bench.py's N > 1 leg under torchrun with every rank on GPU 0
+    (SPMVK_SHARE_GPU=1, gloo plumbing, fused exchange over CUDA IPC)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           "bench.py", "--gpus", str(world), "--workload", workload, "--steps", str(steps),
+           "--warmup", "3", "--distributed"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, SPMVK_SHARE_GPU="1"))
+    assert p.returncode == 0, p.stderr[-3000:]
+    import json
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("workload", ["27pt-128"])
+def test_bench_distributed_shared_gpu_bitwise(cuda, workload):
+    """The driver's scaling run path (bench.py under torchrun, N ranks, fused
+    exchange + flag barrier) on one GPU: after the same number of steps the
+    final iterate's bit checksum is identical at 1, 2 and 3 ranks."""
+    ref = _bench_json(1, workload)
+    assert ref["n_gpus"] == 1 and ref["x_bits_checksum"] != 0
+    for world in (2, 3):
+        d = _bench_json(world, workload)
+        assert d["n_gpus"] == world and d["config"]["exchange_fallback"] is None
+        assert d["config"]["shared_gpu"]
+        assert d["x_bits_checksum"] == ref["x_bits_checksum"], world
+        assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 2 * d["steps"]
