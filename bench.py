@@ -352,7 +352,10 @@ def run_ours(args):
                      "traffic": traffic,
                      # the peak above is a copy (half writes); SpMV traffic is ~98 % reads
                      "read_stream_peak": READ_STREAM_GBS,
-                     "frac_read_stream": achieved / READ_STREAM_GBS},
+                     "frac_read_stream": achieved / READ_STREAM_GBS,
+                     "kernel": "rgcsr_spmv_grp (K2 auto): with x[0] finite it does not read "
+                               "row_lengths (4 B/row of B_fmt), so DRAM traffic (ncu) is "
+                               "~2 % below bytes_per_launch"},
         "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,

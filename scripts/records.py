@@ -57,7 +57,26 @@ def gpu_time_us(fn, stream, flush_buf, fits_l2, steps):
     return statistics.median(per) * 1e3
 
 
+def summary(path):
+    """Markdown table of a records .jsonl (profiles/r01_records.md)."""
+    rs = [json.loads(ln) for ln in open(path) if ln.startswith("{")]
+    print("| matrix | prec | format | G | GPU us | GFLOP/s | B_fmt GB/s (frac of measured peak) "
+          "| B_min GB/s | parity | CPU 1t GF/s | CPU nt GF/s | GPU / CPU-nt |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
+    for r in rs:
+        us = r["median_seconds"] * 1e6
+        bmin = r["B_min"] / r["median_seconds"] / 1e9
+        prec = "f64" if r["precision"] == "double" else "f32"
+        print(f"| {r['matrix_name']} | {prec} | {r['format_name']} | {r['group_size'] or ''} | "
+              f"{us:.1f} | {r['gflops']:.0f} | {r['achieved_GBps']:.0f} "
+              f"({r['roofline_frac_measured']:.3f}) | {bmin:.0f} | {r['parity']} | "
+              f"{r['cpu_gflops_1t']:.2f} | {r['cpu_gflops_nt']:.2f} | "
+              f"{r['gflops'] / r['cpu_gflops_nt']:.0f}x |")
+
+
 def main():
+    if len(sys.argv) == 3 and sys.argv[1] == "--summary":
+        return summary(sys.argv[2])
     ap = argparse.ArgumentParser()
     ap.add_argument("--workloads", default="5pt-1024,27pt-128,powerlaw-8M")
     ap.add_argument("--formats", default="rgcsr32,rgcsr64,rgcsr128,rgcsr256,hybrid")
