@@ -389,6 +389,30 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   // rows longer than h->long_cut go to the warp-per-row kernel (launched second,
   // same stream; the two kernels write disjoint rows of y)
   const uint32_t long_cut = h->n_long ? h->long_cut : 0xffffffffu;
+  // grp kernels: the last argument is the x L2-prefetch length instead of the
+  // long-row cut (they never see long rows).  x is prefetched for short rows
+  // (<= 5.5 slots per row) when it is at most 48 MB: measured with
+  // scripts/cold_spmv.py (flush + SpMV, 3 runs each) 5-pt 2048^2 fp64 49.5-50.5
+  // -> 47.2-47.8 us, fp32 39.1-39.3 -> 38.5-39.0 us, 5-pt 1024^2 neutral; it
+  // costs 4 % on 7-pt 256^3 (x 134 MB: evicted before use) and ~1 % on 27-pt
+  // (profiles/r01_k2_grp.md).  SPMVK_X_PREFETCH=0/1 forces it off/on.
+  static const int xpf_env = [] {
+    const char* e = std::getenv("SPMVK_X_PREFETCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool xpf = xpf_env >= 0 ? xpf_env > 0
+                                : (2 * h->slots <= 11 * h->rows &&
+                                   h->cols * sizeof(T) <= (48ull << 20));
+  auto run_grp = [&](auto kern) {
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
+    kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+                              h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+                              h->columns.p, x, y, x_next, scale,
+                              xpf ? static_cast<uint32_t>(h->cols) : 0u);
+    SPMVK_LAUNCH("rgcsr_spmv_grp");
+  };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -430,13 +454,13 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   if (k >= K2::kGrp4 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
   switch (k) {
     // group-uniform walk: <T, kScaled, U, MINB, kNoLen, kMpf>
-    case K2::kGrp4: run(rgcsr_spmv_grp<T, kScaled, 4, 8, true, false>); break;
-    case K2::kGrp6: run(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
-    case K2::kGrp7: run(rgcsr_spmv_grp<T, kScaled, 7, 5, true, false>); break;
-    case K2::kGrp7Mpf: run(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true>); break;
-    case K2::kGrp8: run(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
-    case K2::kGrp8R64: run(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
-    case K2::kGrp8Len: run(rgcsr_spmv_grp<T, kScaled, 8, 5, false, false>); break;
+    case K2::kGrp4: run_grp(rgcsr_spmv_grp<T, kScaled, 4, 8, true, false>); break;
+    case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
+    case K2::kGrp7: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, false>); break;
+    case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true>); break;
+    case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
+    case K2::kGrp8R64: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
+    case K2::kGrp8Len: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, false, false>); break;
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
     case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
     case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;

@@ -314,7 +314,19 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
                                               const uint32_t* __restrict__ lens,
                                               const T* __restrict__ values,
                                               const uint32_t* __restrict__ columns,
-                                              const T* __restrict__ x, const Epi& epi) {
+                                              const T* __restrict__ x, const Epi& epi,
+                                              uint32_t x_pf_elems = 0) {
+  // x_pf_elems > 0 (matrices that fit in L2): every CTA first bulk-prefetches
+  // its 1/gridDim slice of x[0, x_pf_elems) into L2 (TMA unit, no completion
+  // wait), so a cold launch's x gathers hit L2 instead of paying a second
+  // DRAM round trip behind the slot loads.
+  if (x_pf_elems && threadIdx.x == 0) {
+    const uint64_t bytes = (uint64_t)x_pf_elems * sizeof(T);
+    const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+    const uint64_t b0 = per * blockIdx.x, b1 = min((uint64_t)(bytes & ~15ull), b0 + per);
+    for (uint64_t o = b0; o < b1; o += 65536)
+      bulk_prefetch_l2(reinterpret_cast<const char*>(x) + o, (uint32_t)min((uint64_t)65536, b1 - o));
+  }
   const bool use_len = !kNoLen || !isfinite(__ldg(x));
   const uint32_t ntiles = (rows + 255) / 256;
   struct Meta {
@@ -395,9 +407,10 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t /*long_cut: no long rows on this path*/) {
+    T* __restrict__ x_next, T scale, uint32_t x_pf_elems /* long_cut slot: no long rows here */) {
   grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>>(
-      rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale});
+      rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale},
+      x_pf_elems);
 }
 
 // ---------------------------------------------------------------------------
