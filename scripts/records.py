@@ -43,18 +43,28 @@ def gpu_time_us(fn, stream, flush_buf, fits_l2, steps):
     if not fits_l2:
         total, per = bench.time_launches(fn, stream, steps, 5)
         return per * 1e3
-    per = []
-    for i in range(steps + 3):
-        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # cold launches: K x (read-only L2 flush; SpMV) minus K x flush, each timed
+    # as one event region (per-launch events tick in ~2 us steps)
+    def region(body):
+        for _ in range(3):
+            body()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            body()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / steps
+
+    def flush():
         with torch.cuda.stream(stream):
             flush_buf.sum()
-            a_.record(stream)
-            fn()
-            b_.record(stream)
-        stream.synchronize()
-        if i >= 3:
-            per.append(a_.elapsed_time(b_))
-    return statistics.median(per) * 1e3
+
+    def both():
+        flush()
+        fn()
+    return region(both) - region(flush)
 
 
 def summary(path):
@@ -144,7 +154,7 @@ def main():
                        "roofline_frac_nominal": B / us / 1e3 / NOMINAL_GBS,
                        "roofline_frac_measured": B / us / 1e3 / peak,
                        "convert_ms": conv_ms, "ell_width": k1 if not G else None,
-                       "timing": "L2 flushed per launch" if B < 2 * L2_BYTES else "back-to-back"}
+                       "timing": "L2 flushed per launch (region of K flush+SpMV minus K flushes)" if B < 2 * L2_BYTES else "back-to-back"}
                 del h
                 if R:
                     hs = C.c_void_p()
