@@ -251,6 +251,10 @@ struct spmvk_rgcsr {
   // skip them and a warp-per-row kernel handles them (power-law tails).
   spmvk::DevBuf<uint32_t> long_rows;
   uint64_t n_long = 0;
+  // The same rows split for rgcsr_spmv_long_mixed: quad starts (4 consecutive
+  // long rows of one group, r % 4 == 0, each < kQuadMaxLen slots) and singles.
+  spmvk::DevBuf<uint32_t> long_quads, long_singles;
+  uint64_t n_quads = 0, n_singles = 0;
   uint32_t long_cut = 128;
   // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile.
   mutable std::vector<unsigned> tile_cols;

@@ -132,6 +132,74 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
   }
 }
 
+// Quads for rgcsr_spmv_long_mixed: rows r..r+3 (r % 4 == 0) all long, in one
+// full group of a G % 4 == 0 matrix, each shorter than kQuadMaxLen (the
+// longest rows keep a warp each: a quad walks 64 slots per round, so a
+// 4096-slot row would be its critical path).  SPMVK_LONG_QUADS=0 disables.
+constexpr uint32_t kQuadMaxLen = 1024;
+
+__global__ void gather_u32(uint64_t n, const uint32_t* __restrict__ idx,
+                           const uint32_t* __restrict__ src, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+
+void split_long_rows(spmvk_rgcsr* h, uint32_t G, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("SPMVK_LONG_QUADS");
+    return !e || std::atoi(e) != 0;
+  }();
+  std::vector<uint32_t> lr(h->n_long), len(h->n_long);
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  SPMVK_CUDA(cudaMemcpy(lr.data(), h->long_rows.p, 4 * h->n_long, cudaMemcpyDeviceToHost));
+  {
+    DevBuf<uint32_t> d(h->n_long);
+    gather_u32<<<persistent_grid((h->n_long + 255) / 256, 8), 256, 0, s>>>(
+        h->n_long, h->long_rows.p, h->row_lengths.p, d.p);
+    SPMVK_LAUNCH("gather_u32");
+    SPMVK_CUDA(cudaMemcpyAsync(len.data(), d.p, 4 * h->n_long, cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<uint32_t> quads, singles;
+  for (uint64_t i = 0; i < h->n_long;) {
+    const uint32_t r = lr[i];
+    const uint64_t g = r / G;
+    const bool full = (g + 1) * G <= h->rows;
+    bool quad = on && G % 4 == 0 && r % 4 == 0 && full && i + 3 < h->n_long &&
+                (r + 3) / G == g;
+    for (int k = 0; quad && k < 4; ++k) quad = lr[i + k] == r + k && len[i + k] < kQuadMaxLen;
+    if (quad) {
+      quads.push_back(r);
+      i += 4;
+    } else {
+      singles.push_back(r);
+      ++i;
+    }
+  }
+  // singles longest first: the longest rows bound the phase, start them early
+  std::vector<uint64_t> order(singles.size());
+  for (uint64_t k = 0; k < order.size(); ++k) order[k] = k;
+  std::vector<uint32_t> slen(singles.size());
+  for (uint64_t k = 0, i = 0; k < singles.size(); ++k) {
+    while (lr[i] != singles[k]) ++i;
+    slen[k] = len[i];
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint64_t a, uint64_t b) { return slen[a] > slen[b]; });
+  std::vector<uint32_t> sorted(singles.size());
+  for (uint64_t k = 0; k < order.size(); ++k) sorted[k] = singles[order[k]];
+  h->n_quads = quads.size();
+  h->n_singles = sorted.size();
+  h->long_quads.alloc(h->n_quads);
+  h->long_singles.alloc(h->n_singles);
+  if (h->n_quads)
+    SPMVK_CUDA(cudaMemcpy(h->long_quads.p, quads.data(), 4 * h->n_quads, cudaMemcpyHostToDevice));
+  if (h->n_singles)
+    SPMVK_CUDA(cudaMemcpy(h->long_singles.p, sorted.data(), 4 * h->n_singles,
+                          cudaMemcpyHostToDevice));
+}
+
 spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int prec,
                    cudaStream_t s) {
   if (!a) fail(SPMVK_EINVAL, "null CSR handle");
@@ -191,6 +259,7 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
       long_row_scatter<<<rgrid, 256, 0, s>>>(h->rows, h->long_cut, h->row_lengths.p, pos.p,
                                              h->long_rows.p);
       SPMVK_LAUNCH("long_row_scatter");
+      split_long_rows(h.get(), G, s);
     }
   }
   h->values.alloc(total * static_cast<uint64_t>(prec));
@@ -259,6 +328,10 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
   // 128-bit value loads win (5-pt 4096^2: fp64 220 vs 232 us, fp32 152 vs
   // 163 us); from 7 slots on they lose (profiles/r01_k2_sweep3.md)
   if (!h->n_long && 2 * h->slots <= 11 * h->rows) return K2::kVec2;
+  // long rows: the row-pipelined kernel when the rows are sorted into groups
+  // of similar length (<= 10 % padding, e.g. after descending reordering:
+  // power-law fp64 611 vs 632 us), lite8 for fp64 otherwise (1,425 vs 1,479)
+  if (h->n_long && h->slots * 10 <= h->nnz * 11) return K2::kPipe;
   if (f64) return K2::kLite8;
   if (h->n_long) return K2::kPipe;
   // fp32, short rows (<= ~12 slots): one 8-deep batch per row at full
@@ -366,6 +439,20 @@ void launch_wtma_g(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, c
   else launch_wtma<T, kScaled, 8, NW, NS, CE>(h, x, y, x_next, scale, s);
 }
 
+// The rows past the long-row cut: singles (warp per row, longest first) and
+// quads (four rows per warp) in one launch after the thread-per-row kernel.
+template <class T, bool kScaled>
+void launch_long(const spmvk_rgcsr* h, uint32_t G, int sh, const T* x, T* y, T* x_next, T scale,
+                 cudaStream_t s) {
+  const uint64_t items = h->n_singles + h->n_quads;
+  rgcsr_spmv_long_mixed<T, kScaled><<<persistent_grid((items + 7) / 8, 8), 256, 0, s>>>(
+      static_cast<uint32_t>(h->n_singles), h->long_singles.p, static_cast<uint32_t>(h->n_quads),
+      h->long_quads.p, static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+      h->row_lengths.p, reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, x_next,
+      scale);
+  SPMVK_LAUNCH("rgcsr_spmv_long_mixed");
+}
+
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
@@ -422,13 +509,7 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale, long_cut);
     SPMVK_LAUNCH("rgcsr_spmv (thread per row)");
-    if (h->n_long) {
-      rgcsr_spmv_long<T, kScaled><<<persistent_grid((h->n_long + 7) / 8, 8), 256, 0, s>>>(
-          static_cast<uint32_t>(h->n_long), h->long_rows.p, static_cast<uint32_t>(h->rows), G,
-          sh, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
-          h->columns.p, x, y, x_next, scale);
-      SPMVK_LAUNCH("rgcsr_spmv_long");
-    }
+    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s);
   };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
   auto run_vec = [&](auto kern) {
@@ -441,13 +522,7 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale, long_cut);
     SPMVK_LAUNCH("rgcsr_spmv_vec");
-    if (h->n_long) {
-      rgcsr_spmv_long<T, kScaled><<<persistent_grid((h->n_long + 7) / 8, 8), 256, 0, s>>>(
-          static_cast<uint32_t>(h->n_long), h->long_rows.p, static_cast<uint32_t>(h->rows), G,
-          sh, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
-          h->columns.p, x, y, x_next, scale);
-      SPMVK_LAUNCH("rgcsr_spmv_long");
-    }
+    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s);
   };
   // the group-uniform walk has no long-row split: matrices with long rows
   // (and, for now, any request on them) take the lite kernel instead

@@ -736,6 +736,130 @@ __device__ __forceinline__ void long_rows_epi(
   }
 }
 
+// Four consecutive long rows of one group per warp ("quad": rows r..r+3,
+// r % 4 == 0, G % 4 == 0): lane = 8 q + l works on row q's slots j = l, l+8,
+// ..., so for a fixed j the four rows' slots sit in ONE 32-byte sector (slot j
+// of rows t..t+3 is contiguous) -- a quarter of the uncoalesced sector
+// requests of one row per warp, which is what bounds the long-row phase
+// (l1tex request path, profiles/r01_powerlaw.md).  64 slots per row per
+// round; products staged in shared memory; lane 8 q adds row q's products in
+// slot order, so y stays bitwise.  Singles (the other long rows) take the
+// warp-per-row path above.  One kernel for both lists: item i < n_single is
+// single row single_rows[i], else quad quads[i - n_single].
+template <class T, class Epi>
+__device__ __forceinline__ void long_mixed_epi(
+    uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
+    const uint32_t* __restrict__ quads, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    const Epi& epi) {
+  constexpr int K = 8, W = 32 * K;
+  __shared__ T prod[8][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t items = n_single + n_quad;
+  for (uint32_t i = blockIdx.x * 8 + warp; i < items; i += gridDim.x * 8) {
+    if (i < n_single) {  // one row per warp (as long_rows_epi)
+      const uint32_t r = single_rows[i];
+      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+      const uint32_t t = r - g * G;
+      const uint32_t s = min(G, rows - g * G);
+      const uint32_t len = lens[r];
+      const T* __restrict__ vp = values + gp[g] + t;
+      const uint32_t* __restrict__ cp = columns + gp[g] + t;
+      T acc = T(0);
+      for (uint32_t j0 = 0; j0 < len; j0 += W) {
+        uint32_t c[K];
+        T v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t j = j0 + lane + 32 * k;
+          c[k] = j < len ? ld_stream(cp + (size_t)j * s) : 0u;
+          v[k] = j < len ? ld_stream(vp + (size_t)j * s) : T(0);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const uint32_t j = j0 + lane + 32 * k;
+          if (j < len) prod[warp][lane + 32 * k] = mul_rn(v[k], ld_x(x + c[k]));
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t n = min((uint32_t)W, len - j0);
+          uint32_t q = 0;
+          for (; q + 8 <= n; q += 8) {
+            T p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) p[u] = prod[warp][q + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+          }
+          for (; q < n; ++q) acc = add_rn(acc, prod[warp][q]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) epi(r, acc);
+      continue;
+    }
+    // quad: rows r0..r0+3 of one group
+    const uint32_t r0 = quads[i - n_single];
+    const int q = lane >> 3, l = lane & 7;
+    const uint32_t r = r0 + q;
+    const uint32_t g = g_shift >= 0 ? (r0 >> g_shift) : r0 / G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = lens[r];
+    uint32_t lmax = len;
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    const uint32_t off = gp[g] + (r - g * G);
+    const T* __restrict__ vp = values + off;
+    const uint32_t* __restrict__ cp = columns + off;
+    T* pq = &prod[warp][q * (W / 4)];  // 64 products of row q per round
+    T acc = T(0);
+    for (uint32_t j0 = 0; j0 < lmax; j0 += W / 4) {
+      uint32_t c[K];
+      T v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t j = j0 + l + 8 * k;
+        c[k] = j < len ? ld_stream(cp + (size_t)j * s) : 0u;
+        v[k] = j < len ? ld_stream(vp + (size_t)j * s) : T(0);
+      }
+      __syncwarp();  // scheduling fence: every slot load before the gathers
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t j = j0 + l + 8 * k;
+        if (j < len) pq[l + 8 * k] = mul_rn(v[k], ld_x(x + c[k]));
+      }
+      __syncwarp();
+      if (l == 0 && j0 < len) {
+        const uint32_t n = min((uint32_t)(W / 4), len - j0);
+        uint32_t u0 = 0;
+        for (; u0 + 8 <= n; u0 += 8) {
+          T p[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p[u] = pq[u0 + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+        }
+        for (; u0 < n; ++u0) acc = add_rn(acc, pq[u0]);
+      }
+      __syncwarp();
+    }
+    if (l == 0) epi(r, acc);
+  }
+}
+
+template <class T, bool kScaled>
+__global__ void __launch_bounds__(256) rgcsr_spmv_long_mixed(
+    uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
+    const uint32_t* __restrict__ quads, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  long_mixed_epi<T>(n_single, single_rows, n_quad, quads, rows, G, g_shift, gp, lens, values,
+                    columns, x, StoreEpi<T, kScaled>{y, x_next, scale});
+}
+
 template <class T, bool kScaled>
 __global__ void __launch_bounds__(256) rgcsr_spmv_long(
     uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,

@@ -182,6 +182,25 @@ def test_powerlaw_long_rows_bitwise(cuda, prec, k2):
         assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), orc.spmv_rgcsr(want, x)[0]), G
 
 
+@pytest.mark.parametrize("prec", [8, 4])
+def test_powerlaw_reordered_long_quads_bitwise(cuda, prec, k2):
+    """Descending-reordered power-law rows: the long rows sit together, so most
+    go to the four-rows-per-warp (quad) path of rgcsr_spmv_long_mixed, the
+    longest (>= 1024 slots) stay single.  y bitwise the oracle's on the
+    reordered matrix."""
+    csr = sk.build_csr(triplets(orc.powerlaw(200_000, 7)))  # fp64; fp32 RgCSR casts
+    c2, _ = sk.apply_descending_permutation(csr)
+    rp, col, val = c2.to_host()
+    om = orc.Csr(c2.num_rows, c2.num_cols, rp, col, val)
+    assert int(om.lens()[:8].min()) > 1024 and int((om.lens() > 128).sum()) > 400
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    for G in (32, 64):
+        a = sk.build_rgcsr(c2, G, prec)
+        want = orc.build_rgcsr(om, G, prec)
+        assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(), orc.spmv_rgcsr(want, x)[0]), G
+
+
 @pytest.mark.parametrize("G", [32, 64, 128, 256])
 @pytest.mark.parametrize("prec", [8, 4])
 def test_config1_5pt_1024_bitwise(cuda, G, prec, k2):
