@@ -544,6 +544,22 @@ def spmv_rgcsr(a: RgcsrMatrix, x, y=None, multiply_add_count: bool = False,
     return (y, madds.value) if multiply_add_count else y
 
 
+def persist_x(x, stream: Optional[int] = None, hit_ratio: float = 1.0) -> int:
+    """L2 persistence window over the CUDA tensor ``x`` for kernels launched on
+    ``stream`` (default: torch's current stream) -- spmvk_stream_persist_x.
+    Returns the persisting-L2 carve-out granted in bytes; ``x=None`` resets."""
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    g = C.c_uint64()
+    if x is None:
+        _check(lib().spmvk_stream_persist_x(C.c_void_p(stream), None, 0, 1.0, C.byref(g)))
+    else:
+        _check(lib().spmvk_stream_persist_x(C.c_void_p(stream), C.c_void_p(x.data_ptr()),
+                                            x.numel() * x.element_size(), hit_ratio, C.byref(g)))
+    return g.value
+
+
 # ---------------------------------------------------------------- Hybrid
 def hybrid_split_cost(row_lens, k: int) -> int:
     """hybrid_split_cost (ellpack.hpp:145-150)."""

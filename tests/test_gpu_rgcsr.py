@@ -342,3 +342,38 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=dict(os.environ, PYTHONPATH=root, **env), timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_l2_persistence_window_keeps_results(cuda):
+    """spmvk_stream_persist_x: carve-out + access-policy window over x on a
+    stream; y is unchanged (bitwise) with and after the window, bad ratios are
+    EINVAL, and x == NULL resets."""
+    import ctypes as C
+
+    from paper_1012_2270_b200._lib import SPMVK_EINVAL, lib
+    L = lib()
+    csr = sk.CsrMatrix.stencil(27, 32)
+    a = sk.build_rgcsr(csr, 32)
+    x = dev(orc.random_vector(a.num_cols, 4))
+    want = sk.spmv_rgcsr(a, x).cpu().numpy()
+    s = torch.cuda.Stream()
+    g = C.c_uint64()
+    assert L.spmvk_stream_persist_x(C.c_void_p(s.cuda_stream), C.c_void_p(x.data_ptr()),
+                                    x.numel() * 8, 1.0, C.byref(g)) == 0
+    assert 0 < g.value <= x.numel() * 8
+    y = torch.empty(a.num_rows, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            sk.spmv_rgcsr(a, x, y)
+    s.synchronize()
+    assert bitwise(y.cpu().numpy(), want)
+    assert L.spmvk_stream_persist_x(C.c_void_p(s.cuda_stream), C.c_void_p(x.data_ptr()),
+                                    8, 1.5, None) == SPMVK_EINVAL
+    assert L.spmvk_stream_persist_x(C.c_void_p(s.cuda_stream), None, 0, 1.0, None) == 0
+    with torch.cuda.stream(s):  # the Python wrapper (current stream)
+        assert sk.persist_x(x) > 0
+        sk.spmv_rgcsr(a, x, y)
+        assert sk.persist_x(None) == 0
+        sk.spmv_rgcsr(a, x, y)
+    s.synchronize()
+    assert bitwise(y.cpu().numpy(), want)
