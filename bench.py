@@ -308,7 +308,7 @@ def run_ours(args):
     # ---- variants: fp32 RgCSR, Hybrid fp64/fp32 (same timing method)
     variants = {}
     for label, builder, prec in (("rgcsr_f32_g32", "rg", 4), ("hybrid_f64", "hy", 8),
-                                 ("hybrid_f32", "hy", 4)):
+                                 ("hybrid_f32", "hy", 4), ("csr_f64", "csr", 8)):
         dt = torch.float64 if prec == 8 else torch.float32
         xv = x.to(dt)
         yv = torch.empty(a.num_rows, dtype=dt, device="cuda")
@@ -317,6 +317,10 @@ def run_ours(args):
             h = sk.build_rgcsr(csr, G, prec, stream=sp)
             fn = L.spmvk_rgcsr_spmv_f32
             Bv = rg_bytes(h.info, prec)
+        elif builder == "csr":  # the ingest format's own SpMV (spmv_csr)
+            h = csr
+            fn = L.spmvk_csr_spmv_f64
+            Bv = nnz * 12 + 4 * (a.num_rows + 1) + 8 * (a.num_rows + a.num_cols)
         else:
             h = sk.build_hybrid(csr, None, prec, stream=sp)
             fn = L.spmvk_hybrid_spmv_f64 if prec == 8 else L.spmvk_hybrid_spmv_f32
@@ -333,7 +337,8 @@ def run_ours(args):
         if builder == "hy":
             variants[label]["ell_width"] = h.slots_per_row
             variants[label]["coo_nnz"] = h.coo_nnz()
-        del h
+        if builder != "csr":
+            del h
 
     cpu = cpu_reference(args.workload, args.cpu_reps)
     traffic = committed_traffic(f"{args.workload}/rgcsr_f64_g32")

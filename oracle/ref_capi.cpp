@@ -406,7 +406,8 @@ int ref_run_spmv_bench(const void* h, int fmt, int64_t group, int prec, uint64_t
   });
 }
 
-// Row-slab threaded driver of the UNCHANGED reference spmv_rgcsr / spmv_hybrid:
+// Row-slab threaded driver of the UNCHANGED reference spmv_csr / spmv_rgcsr /
+// spmv_hybrid (fmt 0 / 1 / 2):
 // the matrix is cut into `threads` group-aligned row slabs (each built by the
 // reference's own build_rgcsr / build_hybrid on the slab's entries, columns
 // global) and each std::thread runs the reference kernel on its slab.  y is
@@ -419,6 +420,8 @@ struct RefSlabs {
   std::vector<RgcsrMatrix<float>> rf;
   std::vector<HybridMatrix<double>> hd;
   std::vector<HybridMatrix<float>> hf;
+  std::vector<CsrMatrix<double>> cd;  // fmt 0: the reference's spmv_csr
+  std::vector<CsrMatrix<float>> cf;
   std::size_t cols;
 };
 
@@ -449,7 +452,10 @@ int ref_slabs_build(const void* h, int fmt, uint64_t group, int64_t k1, int prec
         part.push_back(e);
       }
       TripletMatrix tm(r1 - r0, m.num_cols(), std::move(part));
-      if (fmt == 1) {
+      if (fmt == 0) {
+        if (prec == 4) s->cf.push_back(build_csr<float>(tm));
+        else s->cd.push_back(build_csr<double>(tm));
+      } else if (fmt == 1) {
         if (prec == 4) s->rf.push_back(build_rgcsr<float>(tm, group));
         else s->rd.push_back(build_rgcsr<double>(tm, group));
       } else {
@@ -476,11 +482,15 @@ int ref_slabs_spmv(const void* h, const void* x, void* y) {
         if (s->prec == 4) {
           std::span<const float> xs(static_cast<const float*>(x), s->cols);
           std::span<float> ys(static_cast<float*>(y) + r0, r1 - r0);
-          if (s->fmt == 1) spmv_rgcsr(s->rf[t], xs, ys); else spmv_hybrid(s->hf[t], xs, ys);
+          if (s->fmt == 0) spmv_csr(s->cf[t], xs, ys);
+          else if (s->fmt == 1) spmv_rgcsr(s->rf[t], xs, ys);
+          else spmv_hybrid(s->hf[t], xs, ys);
         } else {
           std::span<const double> xs(static_cast<const double*>(x), s->cols);
           std::span<double> ys(static_cast<double*>(y) + r0, r1 - r0);
-          if (s->fmt == 1) spmv_rgcsr(s->rd[t], xs, ys); else spmv_hybrid(s->hd[t], xs, ys);
+          if (s->fmt == 0) spmv_csr(s->cd[t], xs, ys);
+          else if (s->fmt == 1) spmv_rgcsr(s->rd[t], xs, ys);
+          else spmv_hybrid(s->hd[t], xs, ys);
         }
       });
     }
@@ -498,11 +508,15 @@ int ref_slabs_spmv_serial(const void* h, const void* x, void* y) {
       if (s->prec == 4) {
         std::span<const float> xs(static_cast<const float*>(x), s->cols);
         std::span<float> ys(static_cast<float*>(y) + r0, r1 - r0);
-        if (s->fmt == 1) spmv_rgcsr(s->rf[t], xs, ys); else spmv_hybrid(s->hf[t], xs, ys);
+        if (s->fmt == 0) spmv_csr(s->cf[t], xs, ys);
+        else if (s->fmt == 1) spmv_rgcsr(s->rf[t], xs, ys);
+        else spmv_hybrid(s->hf[t], xs, ys);
       } else {
         std::span<const double> xs(static_cast<const double*>(x), s->cols);
         std::span<double> ys(static_cast<double*>(y) + r0, r1 - r0);
-        if (s->fmt == 1) spmv_rgcsr(s->rd[t], xs, ys); else spmv_hybrid(s->hd[t], xs, ys);
+        if (s->fmt == 0) spmv_csr(s->cd[t], xs, ys);
+        else if (s->fmt == 1) spmv_rgcsr(s->rd[t], xs, ys);
+        else spmv_hybrid(s->hd[t], xs, ys);
       }
     }
   });

@@ -7,6 +7,9 @@
 #include <memory>
 #include <string>
 
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -186,6 +189,119 @@ __global__ void __launch_bounds__(256) csr_spmv_kernel(uint64_t rows,
   }
 }
 
+// Tile-staged CSR SpMV (the default): CTA per 256-row tile; the tile's
+// entries [rp[r0], rp[r0+256]) are contiguous, so all 256 threads stream
+// them in coalesced chunks of kCsrChunk entries, each thread forming
+// products val * x[col] for consecutive entries into shared memory; then
+// thread r adds the products of its own row that fall in the chunk, in entry
+// order (acc carried across chunks) -- the reference's rounding sequence, so
+// y stays bitwise, with HBM reads as coalesced as the slot-major formats.
+template <class T, int U, int MINB, uint32_t kCsrChunk>
+__global__ void __launch_bounds__(256, MINB) csr_spmv_staged(uint32_t rows,
+                                                             const uint32_t* __restrict__ rp,
+                                                             const uint32_t* __restrict__ col,
+                                                             const T* __restrict__ val,
+                                                             const T* __restrict__ x,
+                                                             T* __restrict__ y) {
+  __shared__ T prod[kCsrChunk];
+  const uint32_t ntiles = (rows + 255) / 256;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r0 = tile * 256, r = r0 + threadIdx.x;
+    const uint32_t tb = rp[r0], te = rp[min(rows, r0 + 256)];
+    const bool live = r < rows;
+    const uint32_t rb = live ? rp[r] : 0, re = live ? rp[r + 1] : 0;
+    T acc = T(0);
+    for (uint32_t c0 = tb; c0 < te; c0 += kCsrChunk) {
+      const uint32_t n = min(kCsrChunk, te - c0);
+      for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 256 * U) {
+        uint32_t c[U];
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = i0 + u * 256;
+          c[u] = i < n ? ld_stream(col + c0 + i) : 0u;
+          v[u] = i < n ? ld_stream(val + c0 + i) : T(0);
+        }
+        __syncwarp(__activemask());  // scheduling fence: all loads before the gathers
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = i0 + u * 256;
+          if (i < n) prod[i] = mul_rn(v[u], ld_x(x + c[u]));
+        }
+      }
+      __syncthreads();
+      const uint32_t a = max(rb, c0), b = min(re, c0 + n);
+      uint32_t k = a;
+      for (; k + 8 <= b; k += 8) {  // 8 independent LDS in flight, adds in order
+        T p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = prod[k - c0 + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+      }
+      for (; k < b; ++k) acc = add_rn(acc, prod[k - c0]);
+      __syncthreads();
+    }
+    if (live) y[r] = acc;
+  }
+}
+
+// Warp-staged CSR SpMV: as csr_spmv_staged but per WARP (32 rows, whose
+// entries are contiguous too) with a private shared-memory chunk of 32 U
+// products -- no CTA-wide barrier, so warps stay independent and the memory
+// system sees as many requests in flight as the slot-major kernels.
+template <class T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) csr_spmv_warp(uint32_t rows,
+                                                           const uint32_t* __restrict__ rp,
+                                                           const uint32_t* __restrict__ col,
+                                                           const T* __restrict__ val,
+                                                           const T* __restrict__ x,
+                                                           T* __restrict__ y) {
+  constexpr uint32_t CH = 32 * U;
+  __shared__ T prod[8][CH];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* pw = prod[warp];
+  const uint32_t nwt = (rows + 31) / 32;
+  for (uint32_t wt = blockIdx.x * 8 + warp; wt < nwt; wt += gridDim.x * 8) {
+    const uint32_t r = wt * 32 + lane;
+    const bool live = r < rows;
+    const uint32_t rb = live ? rp[r] : 0, re = live ? rp[r + 1] : 0;
+    const uint32_t tb = __shfl_sync(0xffffffffu, rb, 0);
+    const uint32_t te = rp[min(rows, wt * 32 + 32)];
+    T acc = T(0);
+    for (uint32_t c0 = tb; c0 < te; c0 += CH) {
+      const uint32_t n = min(CH, te - c0);
+      uint32_t c[U];
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = lane + 32 * u;
+        c[u] = i < n ? ld_stream(col + c0 + i) : 0u;
+        v[u] = i < n ? ld_stream(val + c0 + i) : T(0);
+      }
+      __syncwarp();  // scheduling fence: every load before the gathers
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = lane + 32 * u;
+        if (i < n) pw[i] = mul_rn(v[u], ld_x(x + c[u]));
+      }
+      __syncwarp();
+      const uint32_t a = max(rb, c0), b = min(re, c0 + n);
+      uint32_t k = a;
+      for (; k + 4 <= b; k += 4) {
+        T p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) p[u] = pw[k - c0 + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = add_rn(acc, p[u]);
+      }
+      for (; k < b; ++k) acc = add_rn(acc, pw[k - c0]);
+      __syncwarp();
+    }
+    if (live) y[r] = acc;
+  }
+}
+
 spmvk_csr* make_csr(uint64_t rows, uint64_t cols, uint64_t nnz, int val_prec) {
   if (val_prec != SPMVK_F32 && val_prec != SPMVK_F64)
     fail(SPMVK_EINVAL, "value precision must be SPMVK_F32 (4) or SPMVK_F64 (8)");
@@ -210,9 +326,29 @@ void csr_spmv(const spmvk_csr* a, const T* x, uint64_t nx, T* y, uint64_t ny, cu
   if (a->val_prec != static_cast<int>(sizeof(T)))
     fail(SPMVK_EINVAL, "spmv_csr: handle precision differs from the entry point");
   if (a->rows == 0) return;
-  csr_spmv_kernel<T><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
-      a->rows, a->row_ptr.p, a->col.p, reinterpret_cast<const T*>(a->val.p), x, y);
-  SPMVK_LAUNCH("csr_spmv_kernel");
+  // SPMVK_CSR_KERNEL: "staged" (default: CTA tile, 1,024-entry chunks, U = 4,
+  // 8 CTAs / SM), "warp" (per-warp chunks), "row" (first kernel, thread per
+  // row).  Measured (scripts/ab_formats.py, profiles/r01_csr.md): staged
+  // 27-pt fp64 163 vs row 413 us, 7-pt 256^3 341 vs 852, power-law 803 vs
+  // 2,090; 5-pt 2048^2 74 vs 74.
+  static const int variant = [] {
+    const char* e = std::getenv("SPMVK_CSR_KERNEL");
+    const std::string v = e ? e : "";
+    return v == "row" ? 1 : v == "warp" ? 2 : 0;
+  }();
+  if (variant == 1) {
+    csr_spmv_kernel<T><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
+        a->rows, a->row_ptr.p, a->col.p, reinterpret_cast<const T*>(a->val.p), x, y);
+    SPMVK_LAUNCH("csr_spmv_kernel");
+    return;
+  }
+  auto kern = variant == 2 ? csr_spmv_warp<T, 8, 5> : csr_spmv_staged<T, 4, 8, 1024>;
+  int per_sm = 0;
+  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  kern<<<persistent_grid((a->rows + 255) / 256, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
+      static_cast<uint32_t>(a->rows), a->row_ptr.p, a->col.p,
+      reinterpret_cast<const T*>(a->val.p), x, y);
+  SPMVK_LAUNCH("csr_spmv_staged");
 }
 
 }  // namespace

@@ -44,7 +44,13 @@ def main():
     f_rg = L.spmvk_rgcsr_spmv_f64 if a.prec == 8 else L.spmvk_rgcsr_spmv_f32
     f_hy = L.spmvk_hybrid_spmv_f64 if a.prec == 8 else L.spmvk_hybrid_spmv_f32
 
+    f_csr = L.spmvk_csr_spmv_f64 if a.prec == 8 else L.spmvk_csr_spmv_f32
+    csr_p = csr  # already in the run's precision
+
     def launcher(v):
+        if v == "csr":  # spmv_csr (SPMVK_CSR_KERNEL=row: the thread-per-row kernel)
+            return lambda: f_csr(csr_p._h, x.data_ptr(), csr.num_cols, y.data_ptr(),
+                                 csr.num_rows, s.cuda_stream)
         if v.startswith("hybrid"):  # hybrid or hybrid:<variant> (spmvk_set_hybrid_kernel)
             hv = (v.split(":", 1)[1] if ":" in v else "auto").encode()
             return lambda: (L.spmvk_set_hybrid_kernel(hv),

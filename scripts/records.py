@@ -89,7 +89,7 @@ def main():
         return summary(sys.argv[2])
     ap = argparse.ArgumentParser()
     ap.add_argument("--workloads", default="5pt-1024,27pt-128,powerlaw-8M")
-    ap.add_argument("--formats", default="rgcsr32,rgcsr64,rgcsr128,rgcsr256,hybrid")
+    ap.add_argument("--formats", default="csr,rgcsr32,rgcsr64,rgcsr128,rgcsr256,hybrid")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--out")
@@ -124,7 +124,13 @@ def main():
                 y = torch.empty(rows, dtype=dt, device="cuda")
                 torch.cuda.synchronize()
                 t = time.perf_counter()
-                if fmt == "hybrid":
+                if fmt == "csr":  # the ingest format itself (spmv_csr, csr.hpp:41-53)
+                    h = c_prec
+                    B = nnz * (prec + 4) + 4 * (rows + 1) + prec * (rows + cols)
+                    fn_c = L.spmvk_csr_spmv_f64 if prec == 8 else L.spmvk_csr_spmv_f32
+                    G, ref_fmt, k1 = None, 0, -1
+                    fr = None
+                elif fmt == "hybrid":
                     h = sk.build_hybrid(c_prec, None, prec, stream=sp)
                     B = bench.hy_bytes(h.info, prec)
                     fn_c = L.spmvk_hybrid_spmv_f64 if prec == 8 else L.spmvk_hybrid_spmv_f32
@@ -142,12 +148,15 @@ def main():
                 fn = lambda: fn_c(h._h, x.data_ptr(), cols, y.data_ptr(), rows, sp)  # noqa: E731
                 us = gpu_time_us(fn, stream, flush_buf, B < 2 * L2_BYTES, args.steps)
                 yg = y.cpu().numpy()
-                rec = {"matrix_name": wl, "format_name": "rgcsr" if G else "hybrid",
+                rec = {"matrix_name": wl, "format_name": fmt if fmt == "csr" else
+                       ("rgcsr" if G else "hybrid"),
                        "group_size": G, "precision": "double" if prec == 8 else "single",
                        "repetitions": args.steps, "nnz": nnz, "median_seconds": us * 1e-6,
-                       "gflops": 2 * nnz / us / 1e3, "fill_percent": fr.fill_percent,
-                       "artificial_zeros": fr.artificial_zeros,
-                       "bytes": fr.bytes_double if prec == 8 else fr.bytes_single,
+                       "gflops": 2 * nnz / us / 1e3,
+                       "fill_percent": fr.fill_percent if fr else 0.0,
+                       "artificial_zeros": fr.artificial_zeros if fr else 0,
+                       "bytes": (fr.bytes_double if prec == 8 else fr.bytes_single) if fr else
+                       B - prec * (rows + cols),
                        "checksum": float(np.sum(yg, dtype=np.float64)),
                        "device": dev_name, "n_gpus": 1, "B_fmt": B, "B_min": B_min,
                        "achieved_GBps": B / us / 1e3,
@@ -155,7 +164,8 @@ def main():
                        "roofline_frac_measured": B / us / 1e3 / peak,
                        "convert_ms": conv_ms, "ell_width": k1 if not G else None,
                        "timing": "L2 flushed per launch (region of K flush+SpMV minus K flushes)" if B < 2 * L2_BYTES else "back-to-back"}
-                del h
+                if fmt != "csr":
+                    del h
                 if R:
                     hs = C.c_void_p()
                     t = time.perf_counter()

@@ -238,3 +238,35 @@ def test_parts_compose_to_spmv_hybrid(cuda, hk, golden, prec):
             yd = sk.spmv_ellpack(h, dev(x))
             sk.spmv_coo(h, dev(x), yd)
             assert bitwise(yd.cpu().numpy(), want), (seed, k1)
+
+
+@pytest.mark.parametrize("kernel", ["staged", "warp", "row"])
+def test_csr_kernels_bitwise_with_long_rows(kernel):
+    """spmv_csr's three kernels (SPMVK_CSR_KERNEL, read once per process, so
+    each runs in a child): stencils, a banded matrix and power-law rows up to
+    ~3,700 entries -- rows that span several staged chunks of 1,024 entries --
+    all bitwise the oracle's spmv_csr, fp64 and fp32."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch
+import oracle as orc
+from helpers import triplets
+from paper_1012_2270_b200 import spmvkit as sk
+mats = [orc.stencil(27, 24), orc.stencil(5, 300), orc.powerlaw(60000, 7),
+        orc.Csr(3, 3, [0, 0, 2, 2], [0, 2], [1.5, -2.0])]
+for prec, dt in ((8, np.float64), (4, np.float32)):
+    for kind, om in enumerate(mats):
+        a = sk.build_csr(triplets(om), prec)
+        x = orc.random_vector(om.cols, 5).astype(dt)
+        y = sk.spmv_csr(a, torch.from_numpy(x).cuda()).cpu().numpy()
+        assert y.tobytes() == orc.spmv_csr(om, x, prec).tobytes(), (prec, kind)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]),
+               SPMVK_CSR_KERNEL=kernel)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
