@@ -152,6 +152,20 @@ def row_lengths(m: TripletMatrix) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- CSR (device)
+def _release(obj, destroy: str):
+    """Frees a handle from __del__; a no-op once interpreter shutdown has torn
+    down this module's globals (the library may already be unloaded)."""
+    h = getattr(obj, "_h", None)
+    lib_mod = _lib
+    if not h or not h.value or lib_mod is None or getattr(lib_mod, "_lib", None) is None:
+        return
+    try:
+        getattr(lib_mod._lib, destroy)(h)
+    except Exception:  # noqa: BLE001 -- never raise from a finalizer
+        pass
+    obj._h = C.c_void_p()
+
+
 class CsrMatrix:
     """Device CSR (build_csr's CsrMatrix, csr.hpp:13-22) owned by a handle."""
 
@@ -184,9 +198,7 @@ class CsrMatrix:
         return int(out[0]), int(out[1])
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
-            _lib._lib.spmvk_csr_destroy(self._h)
-            self._h = C.c_void_p()
+        _release(self, "spmvk_csr_destroy")
 
 
 class MatrixMarketError(RuntimeError):
@@ -493,9 +505,7 @@ class RgcsrMatrix:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
-            _lib._lib.spmvk_rgcsr_destroy(self._h)
-            self._h = C.c_void_p()
+        _release(self, "spmvk_rgcsr_destroy")
 
 
 def build_rgcsr(m, group_size: int, precision=F64, stream: int = 0,
@@ -601,9 +611,7 @@ class HybridMatrix:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value and _lib._lib is not None:
-            _lib._lib.spmvk_hybrid_destroy(self._h)
-            self._h = C.c_void_p()
+        _release(self, "spmvk_hybrid_destroy")
 
 
 def build_hybrid(m, k1: Optional[int] = None, precision=F64, stream: int = 0) -> HybridMatrix:
