@@ -155,15 +155,15 @@ def row_lengths(m: TripletMatrix) -> np.ndarray:
 def _release(obj, destroy: str):
     """Frees a handle from __del__; a no-op once interpreter shutdown has torn
     down this module's globals (the library may already be unloaded)."""
-    h = getattr(obj, "_h", None)
-    lib_mod = _lib
-    if not h or not h.value or lib_mod is None or getattr(lib_mod, "_lib", None) is None:
-        return
     try:
+        h = getattr(obj, "_h", None)
+        lib_mod = _lib
+        if not h or not h.value or lib_mod is None or getattr(lib_mod, "_lib", None) is None:
+            return
         getattr(lib_mod._lib, destroy)(h)
+        obj._h = C.c_void_p()
     except Exception:  # noqa: BLE001 -- never raise from a finalizer
         pass
-    obj._h = C.c_void_p()
 
 
 class CsrMatrix:
@@ -197,7 +197,7 @@ class CsrMatrix:
         _check(lib().spmvk_csr_row_length_range(self._h, out))
         return int(out[0]), int(out[1])
 
-    def __del__(self):
+    def __del__(self, _release=_release):  # bound now: module globals vanish at exit
         _release(self, "spmvk_csr_destroy")
 
 
@@ -504,7 +504,7 @@ class RgcsrMatrix:
                                           _ptr(out["group_pointers"]), _ptr(out["row_lengths"])))
         return out
 
-    def __del__(self):
+    def __del__(self, _release=_release):  # bound now: module globals vanish at exit
         _release(self, "spmvk_rgcsr_destroy")
 
 
@@ -610,7 +610,7 @@ class HybridMatrix:
             "ell_values", "ell_columns", "coo_rows", "coo_columns", "coo_values"))))
         return out
 
-    def __del__(self):
+    def __del__(self, _release=_release):  # bound now: module globals vanish at exit
         _release(self, "spmvk_hybrid_destroy")
 
 

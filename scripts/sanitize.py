@@ -39,5 +39,46 @@ for name, om in mats.items():
     x = orc.random_vector(om.cols, 1)
     want = orc.spmv_rgcsr(orc.build_rgcsr(o2, 32), x)[0]
     assert sk.spmv_rgcsr(a2, torch.from_numpy(x).cuda()).cpu().numpy().tobytes() == want.tobytes()
+# host-span pipeline (pinned x / y, graph-captured chunks), CG, fused dist step
+from paper_1012_2270_b200 import generators as gen  # noqa: E402
+from paper_1012_2270_b200 import partition as pt  # noqa: E402
+csr = sk.CsrMatrix.stencil(7, 48)
+a = sk.build_rgcsr(csr, 32)
+xh = torch.from_numpy(orc.random_vector(a.num_cols, 2)).pin_memory()
+yh = torch.empty(a.num_rows, dtype=torch.float64).pin_memory()
+want = sk.spmv_rgcsr(a, xh.cuda()).cpu().numpy()
+sk.spmv_rgcsr(a, xh.numpy(), yh.numpy())
+assert yh.numpy().tobytes() == want.tobytes()
+b = torch.ones(a.num_rows, dtype=torch.float64, device="cuda")
+xs, it, rel = sk.cg(a, b, tol=1e-8, max_iter=200)
+assert rel < 1e-8, rel
+P, G = 3, 32
+slabs = pt.slab_bounds(csr.num_rows, G, P)
+import ctypes as C  # noqa: E402
+from paper_1012_2270_b200._lib import lib  # noqa: E402
+ranges = []
+for sl in slabs:
+    cr = (C.c_uint64 * 2)()
+    sk._check(lib().spmvk_csr_column_range(csr._h, sl.row_begin, sl.row_end, cr))
+    ranges.append((int(cr[0]), int(cr[1])))
+recv = pt.fused_receive_ranges(slabs, ranges, "halo")
+wins = [pt.ExchangeWindow(csr.num_rows, 8) for _ in slabs]
+x0 = torch.from_numpy(gen.random_vector(csr.num_cols, 1)).cuda()
+its = []
+for sl in slabs:
+    it = pt.FusedIteratedSpmv(sl, recv, sk.build_rgcsr(csr, G, 8, row_range=(sl.row_begin,
+                                                                            sl.row_end)),
+                              wins[sl.rank], P, torch.cuda.current_stream().cuda_stream,
+                              local_windows=wins, barrier=False)
+    it.set_x(x0)
+    its.append(it)
+for _ in range(3):
+    for it in its:
+        it.step()
+torch.cuda.synchronize()
+for it in its:
+    it.close()
+for w in wins:
+    w.close()
 torch.cuda.synchronize()
 print("sanitize pass ok")
