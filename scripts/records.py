@@ -71,15 +71,19 @@ def summary(path):
     """Markdown table of a records .jsonl (profiles/r01_records.md)."""
     rs = [json.loads(ln) for ln in open(path) if ln.startswith("{")]
     print("| matrix | prec | format | G | GPU us | GFLOP/s | B_fmt GB/s (frac of measured peak) "
-          "| B_min GB/s | parity | CPU 1t GF/s | CPU nt GF/s | GPU / CPU-nt |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
+          "| B_min GB/s | ncu DRAM MB / B_fmt MB | ncu L2 hit % | ncu sector eff. % | parity "
+          "| CPU 1t GF/s | CPU nt GF/s | GPU / CPU-nt |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for r in rs:
         us = r["median_seconds"] * 1e6
         bmin = r["B_min"] / r["median_seconds"] / 1e9
         prec = "f64" if r["precision"] == "double" else "f32"
         print(f"| {r['matrix_name']} | {prec} | {r['format_name']} | {r['group_size'] or ''} | "
               f"{us:.1f} | {r['gflops']:.0f} | {r['achieved_GBps']:.0f} "
-              f"({r['roofline_frac_measured']:.3f}) | {bmin:.0f} | {r['parity']} | "
+              f"({r['roofline_frac_measured']:.3f}) | {bmin:.0f} | "
+              f"{r.get('ncu_dram_bytes', 0) / 1e6:.0f} / {r['B_fmt'] / 1e6:.0f} | "
+              f"{r.get('ncu_l2_hit_pct', 0):.1f} | {r.get('ncu_sector_efficiency_pct', 0):.1f} | "
+              f"{r['parity']} | "
               f"{r['cpu_gflops_1t']:.2f} | {r['cpu_gflops_nt']:.2f} | "
               f"{r['gflops'] / r['cpu_gflops_nt']:.0f}x |")
 
