@@ -29,11 +29,13 @@ for n in (128, 256, 384):
         torch.cuda.synchronize()
         return time.perf_counter() - t, it
     run(100)  # warm-up
-    t1, _ = run(100)
-    t2, it = run(300)
-    dt = (t2 - t1) * it / 200  # per-iteration cost x iterations, capture/setup cancelled
+    # per-iteration cost from the difference of two lengths (allocation,
+    # capture and setup cancel), best of three pairs
+    per = min((run(1000)[0] - run(200)[0]) / 800 for _ in range(3))
+    it = 800
+    dt = per * it
     B = bench.rg_bytes(a.info, 8) + 11 * 8 * N
-    print(json.dumps({"case": f"7pt-{n}", "rows": N, "iterations": it, "ms_per_iter": dt / it * 1e3,
+    print(json.dumps({"case": f"7pt-{n}", "rows": N, "ms_per_iter": dt / it * 1e3,
                       "bytes_per_iter": B, "GBs": B / (dt / it) / 1e9,
                       "frac_of_copy_peak": B / (dt / it) / 1e9 / peak}),
           flush=True)
