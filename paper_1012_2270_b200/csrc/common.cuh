@@ -256,8 +256,10 @@ struct spmvk_rgcsr {
   spmvk::DevBuf<uint32_t> long_quads, long_singles;
   uint64_t n_quads = 0, n_singles = 0;
   uint32_t long_cut = 128;
-  // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile.
+  // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile
+  // (host copy), and the same on the device for rgcsr_spmv_grpx.
   mutable std::vector<unsigned> tile_cols;
+  mutable spmvk::DevBuf<unsigned> tile_cols_dev;
   // Process-unique id: keys the host-span pipeline's captured CUDA graph
   // (a recycled handle address must not replay a graph of freed arrays).
   const uint64_t serial = next_serial();

@@ -301,7 +301,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 enum class K2 {
   kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
   kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf, kVec2, kVec4,
-  kGrp4, kGrp6, kGrp7, kGrp7Mpf, kGrp8, kGrp8R64, kGrp8Len
+  kGrp4, kGrp6, kGrp7, kGrp7Mpf, kGrp8, kGrp8R64, kGrp8Len, kGrpX, kGrpX8
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -353,7 +353,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"lite8_full_mpf", K2::kLite8FullMpf}, {"vec2", K2::kVec2}, {"vec4", K2::kVec4},
       {"grp4", K2::kGrp4}, {"grp6", K2::kGrp6}, {"grp7", K2::kGrp7},
       {"grp7_mpf", K2::kGrp7Mpf}, {"grp8", K2::kGrp8}, {"grp8_r64", K2::kGrp8R64},
-      {"grp8_len", K2::kGrp8Len}};
+      {"grp8_len", K2::kGrp8Len}, {"grpx", K2::kGrpX}, {"grpx8", K2::kGrpX8}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -500,6 +500,31 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               xpf ? static_cast<uint32_t>(h->cols) : 0u);
     SPMVK_LAUNCH("rgcsr_spmv_grp");
   };
+  // x staged in shared memory per tile (narrow-band matrices)
+  auto run_grpx = [&](auto kern) {
+    {
+      std::lock_guard<std::mutex> lk(h->part_mu);
+      if (!h->tile_cols_dev.p) {
+        const uint32_t tiles = static_cast<uint32_t>((h->rows + 255) / 256);
+        h->tile_cols_dev.alloc(2 * uint64_t(tiles));
+        std::vector<unsigned> init(2 * uint64_t(tiles));
+        for (uint32_t k = 0; k < tiles; ++k) init[2 * k] = 0xffffffffu, init[2 * k + 1] = 0;
+        SPMVK_CUDA(cudaMemcpy(h->tile_cols_dev.p, init.data(), 8ull * tiles,
+                              cudaMemcpyHostToDevice));
+        chunk_column_ranges<<<persistent_grid(tiles, 8), 256>>>(
+            static_cast<uint32_t>(h->rows), G, 256, h->group_pointers.p, h->row_lengths.p,
+            h->columns.p, h->tile_cols_dev.p);
+        SPMVK_LAUNCH("chunk_column_ranges");
+        SPMVK_CUDA(cudaDeviceSynchronize());
+      }
+    }
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    kern<<<persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
+        static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p, h->row_lengths.p,
+        reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, h->tile_cols_dev.p);
+    SPMVK_LAUNCH("rgcsr_spmv_grpx");
+  };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -536,6 +561,14 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
     case K2::kGrp8R64: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
     case K2::kGrp8Len: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, false, false>); break;
+    case K2::kGrpX:  // plain y only (the scaled / iterated form falls back)
+      if constexpr (!kScaled) run_grpx(rgcsr_spmv_grpx<T, 6, 5, 4096>);
+      else run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>);
+      break;
+    case K2::kGrpX8:
+      if constexpr (!kScaled) run_grpx(rgcsr_spmv_grpx<T, 8, 4, 4096>);
+      else run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>);
+      break;
     case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
     case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
     case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;

@@ -413,6 +413,60 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
       x_pf_elems);
 }
 
+// x staged in shared memory (the north star's "x is staged in shared memory
+// when the matrix is banded"): per 256-row tile the CTA copies x[lo..hi] --
+// the tile's column range, tile_cols[2t..2t+1] -- into shared memory with
+// coalesced loads, then the group-uniform walk gathers from there.  Tiles
+// whose range exceeds XCAP elements gather from global memory as usual
+// (uniform per CTA).  Same per-row order -> y bitwise.
+template <class T, int U, int MINB, int XCAP>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grpx(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    const uint32_t* __restrict__ tile_cols) {
+  __shared__ T xs[XCAP];
+  const bool use_len = !isfinite(__ldg(x));
+  const uint32_t ntiles = (rows + 255) / 256;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t lo = tile_cols[2 * tile], hi = tile_cols[2 * tile + 1];
+    const bool staged = lo <= hi && hi - lo < (uint32_t)XCAP;
+    if (staged)
+      for (uint32_t i = threadIdx.x; i <= hi - lo; i += 256) xs[i] = __ldg(x + lo + i);
+    __syncthreads();
+    const uint32_t r = tile * 256 + threadIdx.x;
+    if (r < rows) {
+      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+      const uint32_t b0 = ld_stream(gp + g), b1 = ld_stream(gp + g + 1);
+      const uint32_t len = use_len ? ld_stream(lens + r) : 0u;
+      const uint32_t s = min(G, rows - g * G);
+      const uint32_t K = (s == G && g_shift >= 0) ? ((b1 - b0) >> g_shift) : (b1 - b0) / s;
+      const uint32_t lim = use_len ? len : K;
+      const uint32_t off = b0 + (r - g * G);
+      T acc = T(0);
+      for (uint32_t j = 0; j < K; j += U) {
+        uint32_t c[U];
+        T v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool in = j + u < K;
+          v[u] = in ? ld_stream(values + off + (j + u) * s) : T(0);
+          c[u] = in ? ld_stream(columns + off + (j + u) * s) : 0u;
+        }
+        __syncwarp(__activemask());  // scheduling fence (see grp_tiles_epi)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          xv[u] = j + u < lim ? (staged ? xs[c[u] - lo] : ld_x(x + c[u])) : T(0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+      }
+      y[r] = acc;
+    }
+    __syncthreads();  // xs is rewritten for the next tile
+  }
+}
+
 // ---------------------------------------------------------------------------
 // rgcsr_spmv_vec -- 128-bit vectorised slot loads (north_star subsystem 2).
 //

@@ -28,8 +28,12 @@ def main():
     torch.cuda.set_device(0)
     L = lib()
     assert L.spmvk_init(0) == 0
-    kind, n = (int(v) for v in a.case.split(":"))
-    csr = sk.CsrMatrix.stencil(kind, n) if kind else sk.build_csr(gen.powerlaw(n, 7))
+    if a.case.startswith("b:"):  # b:<rows>:<half bandwidth> -- banded_matrix (synthetic.cpp)
+        _, n, hbw = a.case.split(":")
+        csr = sk.build_csr(gen.banded(int(n), int(hbw), 3))
+    else:
+        kind, n = (int(v) for v in a.case.split(":"))
+        csr = sk.CsrMatrix.stencil(kind, n) if kind else sk.build_csr(gen.powerlaw(n, 7))
     if a.prec == 4:
         csr = sk.build_csr(sk.TripletMatrix(csr.num_rows, csr.num_cols, *csr.to_host()), 4)
     dt = torch.float64 if a.prec == 8 else torch.float32

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 VARIANTS = ["auto", "lite", "lite8", "lite8_full", "lite8_l2pf", "lite_l2pf", "vec2", "vec4", "pipe", "pipe_hi", "pipe8",
             "ldg", "ldg_pf", "tma", "wtma", "lite_mpf", "lite8_mpf", "lite8_full_mpf",
-            "grp4", "grp6", "grp7", "grp7_mpf", "grp8", "grp8_r64", "grp8_len"]
+            "grp4", "grp6", "grp7", "grp7_mpf", "grp8", "grp8_r64", "grp8_len", "grpx", "grpx8"]
 
 
 def dev(x):
