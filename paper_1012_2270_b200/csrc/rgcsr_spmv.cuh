@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grpx(
         __syncwarp(__activemask());  // scheduling fence (see grp_tiles_epi)
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          xv[u] = j + u < lim ? (staged ? xs[c[u] - lo] : ld_x(x + c[u])) : T(0);
+          // pads (column 0) and any column outside the staged range read global x
+          xv[u] = j + u < lim ? (staged && c[u] - lo <= hi - lo ? xs[c[u] - lo] : ld_x(x + c[u]))
+                              : T(0);
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
