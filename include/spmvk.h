@@ -214,7 +214,9 @@ int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double h
  * walk: U-deep slot batches bound by the group width, scheduling fence
  * before the x gathers, row_lengths skipped when x[0] is finite; _mpf
  * prefetches the next row's group pointers; grp8_len predicates on
- * row_lengths), "lite" / "lite8" / "lite8_full" / "lite*_mpf" (register-lean
+ * row_lengths), "grpx" / "grpx8" (same walk with x staged in shared memory
+ * per 256-row tile, for banded matrices; measured slower), "lite" / "lite8" /
+ * "lite8_full" / "lite*_mpf" (register-lean
  * thread per row), "vec2" / "vec4" (128-bit loads of 2 / 4 rows),
  * "lite_l2pf" / "lite8_l2pf" (+ bulk L2 prefetch of the next tile), "pipe" /
  * "pipe_hi" / "pipe8" (row-metadata prefetch, predicated batches), "ldg" /

@@ -951,6 +951,7 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
                              "' (auto | grp4 | grp6 | grp7 | grp7_mpf | grp8 | grp8_r64 | grp8_len | "
+                             "grpx | grpx8 | "
                              "lite | lite8 | lite8_full | lite_mpf | lite8_mpf | lite8_full_mpf | "
                              "vec2 | vec4 | lite_l2pf | lite8_l2pf | pipe | pipe_hi | pipe8 | ldg | "
                              "ldg_pf | tma | wtma)");
