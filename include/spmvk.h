@@ -323,6 +323,14 @@ void spmvk_hybrid_destroy(spmvk_hybrid* h);
 int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_t n, double tol,
                        uint64_t max_iter, uint64_t check_every, uint64_t* iters,
                        double* rel_residual, void* stream);
+/* y = A x and dot_out (device scalar) = sum_r x[x_offset + r] * y[r] -- CG's
+ * p.q fused into the SpMV's row epilogue (rows of a square matrix or of a row
+ * slab whose rows start at global row x_offset).  Deterministic (fixed
+ * per-CTA partials, fixed reduction order); falls back to the SpMV followed
+ * by spmvk_dot_f64 for matrices with long rows or > 10 % padding.  No
+ * reference counterpart (CG is not in the reference). */
+int spmvk_rgcsr_spmv_dot_f64(const spmvk_rgcsr* a, const double* x, uint64_t nx, double* y,
+                             uint64_t ny, uint64_t x_offset, double* dot_out, void* stream);
 /* out_dev[0] = a . b (deterministic), device pointers. */
 int spmvk_dot_f64(const double* a, const double* b, uint64_t n, double* out_dev, void* stream);
 /* CG building blocks for the row-slab distributed solver (device pointers,

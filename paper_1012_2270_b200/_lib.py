@@ -93,6 +93,7 @@ SIGNATURES = {
     "spmvk_cg_solve_f64": (cint, [vp, vp, vp, u64, C.c_double, u64, u64, u64p,
                                   C.POINTER(C.c_double), vp]),
     "spmvk_dot_f64": (cint, [vp, vp, u64, vp, vp]),
+    "spmvk_rgcsr_spmv_dot_f64": (cint, [vp, vp, u64, vp, u64, u64, vp, vp]),
     "spmvk_cg_update_f64": (cint, [u64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvk_cg_direction_f64": (cint, [u64, vp, vp, vp, vp, vp]),
     "spmvk_ellpack_build": (cint, [vp, u64, cint, vp, C.POINTER(vp)]),

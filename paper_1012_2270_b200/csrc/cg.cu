@@ -3,11 +3,12 @@
 //
 // Device-resident, host-sync-free iteration: every scalar (rr, pAp, alpha,
 // beta) lives in device memory and the kernels read it there, so one CG
-// iteration is 3 launches (SpMV+dot, update+dot, direction) that can be
+// iteration is a few launches (SpMV with the p.q dot fused into its
+// epilogue, update+dot, direction) that can be
 // captured in a CUDA graph.  Dot products are deterministic: per-CTA partials
 // of a fixed grid reduced in a fixed order by one CTA.
-//   1. q = A p                         (K2, y = A x with the default variant)
-//      pAp = p . q                     (dot_partials + dot_finish)
+//   1. q = A p, pAp = p . q            (spmvk_rgcsr_spmv_dot_f64: grp walk +
+//                                       DotEpi, per-CTA partials + finish)
 //   2. alpha = rr / pAp;  x += alpha p;  r -= alpha q;  rr' = r . r   (fused)
 //   3. beta = rr' / rr;   p = r + beta p;  rr = rr'
 #include <cmath>
@@ -190,10 +191,9 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
     uint64_t k = 0;
     if (check_every == 0) check_every = 10;
     auto iteration = [&](cudaStream_t st) {
-      if (spmvk_rgcsr_spmv_f64(a, p.p, n, q.p, n, st) != SPMVK_OK)
+      // q = A p with pAp = p.q fused into the SpMV epilogue
+      if (spmvk_rgcsr_spmv_dot_f64(a, p.p, n, q.p, n, 0, pap, st) != SPMVK_OK)
         fail(SPMVK_ECUDA, std::string("cg spmv: ") + spmvk_last_error());
-      dot_partials<<<grid, kDotThreads, 0, st>>>(n, p.p, q.p, part.p);
-      dot_finish<<<1, kDotThreads, 0, st>>>(part.p, kDotBlocks, pap);
       cg_update<<<grid, kDotThreads, 0, st>>>(n, rr, pap, p.p, q.p, x, r.p, part.p);
       dot_finish<<<1, kDotThreads, 0, st>>>(part.p, kDotBlocks, rrn);
       cg_direction<<<grid, kDotThreads, 0, st>>>(n, r.p, p.p, rr, rrn);
@@ -218,6 +218,11 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
     SPMVK_CUDA(cudaStreamWaitEvent(cs, ev, 0));
     try {
       if (check_every >= 2 && max_iter >= check_every && res > tol) {
+        // one eager fused SpMV+dot first: its per-thread partials buffer is
+        // allocated on first use, which must not happen during the capture
+        // (q and pAp are recomputed by the first captured iteration)
+        if (spmvk_rgcsr_spmv_dot_f64(a, p.p, n, q.p, n, 0, pap, cs) != SPMVK_OK)
+          fail(SPMVK_ECUDA, std::string("cg spmv: ") + spmvk_last_error());
         SPMVK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         for (uint64_t i = 0; i < check_every; ++i) iteration(cs);
         SPMVK_CUDA(cudaStreamEndCapture(cs, &graph));

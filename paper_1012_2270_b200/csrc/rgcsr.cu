@@ -587,6 +587,48 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   }
 }
 
+// y = A x plus dot_out = sum_r x[x_offset + r] * y[r] (CG's p.q), fused into
+// the grp walk's epilogue when the matrix takes that kernel (no long rows,
+// <= 10 % padding); otherwise the plain SpMV then a separate dot.
+void spmv_dot_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y, uint64_t ny,
+                  uint64_t x_offset, double* dot_out, cudaStream_t s) {
+  check_spmv_args<double>(h, nx, ny);
+  if (!dot_out) fail(SPMVK_EINVAL, "spmv_dot: null dot output");
+  if (x_offset + h->rows > nx) fail(SPMVK_EINVAL, "spmv_dot: x_offset + rows exceeds x");
+  if (h->rows == 0) {
+    SPMVK_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), s));
+    return;
+  }
+  if (h->n_long || h->slots * 10 > h->nnz * 11) {
+    launch_spmv<double, false>(h, x, y, nullptr, 0.0, s);
+    if (spmvk_dot_f64(x + x_offset, y, h->rows, dot_out, s) != SPMVK_OK)
+      fail(SPMVK_ECUDA, std::string("spmv_dot: ") + spmvk_last_error());
+    return;
+  }
+  const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
+  const int sh = pow2_shift(h->group_size);
+  auto kern = 2 * h->slots <= 11 * h->rows ? rgcsr_spmv_dot_grp<double, 6, 5>
+                                           : rgcsr_spmv_dot_grp<double, 8, 4>;
+  int per_sm = 0;
+  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
+  static thread_local DevBuf<double> part;  // per host thread: stream-ordered reuse
+  if (part.n < grid) {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    SPMVK_CUDA(cudaStreamIsCapturing(s, &cst));
+    if (cst != cudaStreamCaptureStatusNone)
+      fail(SPMVK_EINVAL, "spmv_dot: first call on this thread is inside a stream capture; "
+                         "call it once eagerly first");
+    part.alloc(static_cast<uint64_t>(sm_count()) * 8 > grid ? sm_count() * 8ull : grid);
+  }
+  kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+                            h->row_lengths.p, reinterpret_cast<const double*>(h->values.p),
+                            h->columns.p, x, y, x + x_offset, part.p);
+  SPMVK_LAUNCH("rgcsr_spmv_dot_grp");
+  rgcsr_dot_finish<<<1, 256, 0, s>>>(part.p, static_cast<int>(grid), dot_out);
+  SPMVK_LAUNCH("rgcsr_dot_finish");
+}
+
 bool pinned(const void* p, void** mapped = nullptr) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -942,6 +984,14 @@ int spmvk_set_long_row_cut(uint32_t cut) {
   return guarded([&] {
     if (cut == 0) fail(SPMVK_EINVAL, "long-row cut must be positive");
     long_cut_slot().store(cut);
+  });
+}
+
+int spmvk_rgcsr_spmv_dot_f64(const spmvk_rgcsr* a, const double* x, uint64_t nx, double* y,
+                             uint64_t ny, uint64_t x_offset, double* dot_out, void* stream) {
+  return guarded([&] {
+    require_device();
+    spmv_dot_f64(a, x, nx, y, ny, x_offset, dot_out, as_stream(stream));
   });
 }
 

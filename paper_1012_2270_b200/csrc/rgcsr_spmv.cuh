@@ -413,6 +413,56 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
       x_pf_elems);
 }
 
+// SpMV with the CG dot fused into the row epilogue: y = A x and, per CTA, the
+// partial sum of xself[r] * y[r] over the rows it produced (xself = the
+// slab's own rows of x), for p.q in conjugate gradients -- saves the dot
+// kernel's second pass over p and q.  Deterministic: each thread adds its
+// rows in tile order, then a fixed block reduction; the per-CTA partials are
+// summed in CTA order by rgcsr_dot_finish.
+template <class T>
+struct DotEpi {
+  T* __restrict__ y;
+  const T* __restrict__ xself;
+  double* acc;
+  __device__ __forceinline__ void operator()(uint32_t r, T v) const {
+    y[r] = v;
+    *acc += static_cast<double>(xself[r]) * static_cast<double>(v);
+  }
+};
+
+__device__ __forceinline__ double block_sum_256(double v) {
+  __shared__ double sh[8];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = threadIdx.x < 8 ? sh[threadIdx.x] : 0.0;
+  if (threadIdx.x < 32)
+    for (int o = 4; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+template <class T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_dot_grp(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    const T* __restrict__ xself, double* __restrict__ part) {
+  double acc = 0.0;
+  grp_tiles_epi<T, U, true, true, DotEpi<T>>(rows, G, g_shift, gp, lens, values, columns, x,
+                                             DotEpi<T>{y, xself, &acc});
+  acc = block_sum_256(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+static __global__ void __launch_bounds__(256) rgcsr_dot_finish(const double* __restrict__ part, int np,
+                                                        double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += 256) s += part[i];
+  s = block_sum_256(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
 // x staged in shared memory (the north star's "x is staged in shared memory
 // when the matrix is banded"): per 256-row tile the CTA copies x[lo..hi] --
 // the tile's column range, tile_cols[2t..2t+1] -- into shared memory with

@@ -213,8 +213,11 @@ def distributed_cg(slab: Slab, world: int, num_cols: int, b, ops, all_gather, al
     k = 0
     while k < max_iter and res > tol:
         all_gather(p_full, p_local)
-        ops.spmv(p_full[:num_cols], q[:n])
-        ops.dot(p_local[:n], q[:n], pap)
+        if hasattr(ops, "spmv_dot"):  # q = A p with p.q fused into the SpMV epilogue
+            ops.spmv_dot(p_full[:num_cols], q[:n], pap, slab.row_begin)
+        else:
+            ops.spmv(p_full[:num_cols], q[:n])
+            ops.dot(p_local[:n], q[:n], pap)
         all_reduce(pap)
         ops.update(rr, pap, p_local[:n], q[:n], x[:n], r[:n], rrn)
         all_reduce(rrn)
@@ -240,6 +243,11 @@ class GpuCgOps:
     def spmv(self, p_full, q):
         self._ok(self.L.spmvk_rgcsr_spmv_f64(self.a._h, p_full.data_ptr(), p_full.numel(),
                                              q.data_ptr(), q.numel(), self.s))
+
+    def spmv_dot(self, p_full, q, out, x_offset):
+        self._ok(self.L.spmvk_rgcsr_spmv_dot_f64(self.a._h, p_full.data_ptr(), p_full.numel(),
+                                                 q.data_ptr(), q.numel(), x_offset,
+                                                 out.data_ptr(), self.s))
 
     def dot(self, a, b, out):
         self._ok(self.L.spmvk_dot_f64(a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),

@@ -1,8 +1,9 @@
 """CG iteration throughput (spmvk_cg_solve_f64, graph-replayed iterations) on
 the 7-point stencils: time for a fixed iteration count (tol = 0), bytes per
-iteration = the SpMV's B_fmt + the vector traffic of the other kernels
-(p.q: 2N reads; update: x, p, r, q read, x, r written; direction: r, p read,
-p written -> 11 N doubles), achieved GB/s vs the measured copy peak."""
+iteration = the SpMV's B_fmt (p.q is fused into its epilogue) + the vector
+traffic of the other kernels (update: x, p, r, q read, x, r written;
+direction: r, p read, p written -> 9 N doubles), achieved GB/s vs the
+measured copy peak."""
 import json
 import os
 import sys
@@ -31,10 +32,11 @@ for n in (128, 256, 384):
     run(100)  # warm-up
     # per-iteration cost from the difference of two lengths (allocation,
     # capture and setup cancel), best of three pairs
-    per = min((run(1000)[0] - run(200)[0]) / 800 for _ in range(3))
-    it = 800
+    import statistics
+    per = statistics.median((run(2000)[0] - run(400)[0]) / 1600 for _ in range(5))
+    it = 1600
     dt = per * it
-    B = bench.rg_bytes(a.info, 8) + 11 * 8 * N
+    B = bench.rg_bytes(a.info, 8) + 9 * 8 * N
     print(json.dumps({"case": f"7pt-{n}", "rows": N, "ms_per_iter": dt / it * 1e3,
                       "bytes_per_iter": B, "GBs": B / (dt / it) / 1e9,
                       "frac_of_copy_peak": B / (dt / it) / 1e9 / peak}),

@@ -68,3 +68,41 @@ def test_distributed_cg_world1_nccl_matches_single_gpu_solver(cuda, tmp_path):
         dist.destroy_process_group()
     assert it1 == it2 == 25
     assert torch.equal(x1.view(torch.int64), x2.view(torch.int64))
+
+
+def test_spmv_dot_fused(cuda):
+    """spmvk_rgcsr_spmv_dot_f64: y bitwise the plain SpMV's, dot = x[off:].y to
+    1e-12 (relative), bitwise repeatable; row slabs use x_offset; matrices with
+    long rows take the unfused fallback."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_1012_2270_b200 import generators as gen
+    from paper_1012_2270_b200 import spmvkit as sk
+    from paper_1012_2270_b200._lib import lib
+    L = lib()
+    cases = [(sk.CsrMatrix.stencil(7, 40), None), (sk.CsrMatrix.stencil(5, 300), None),
+             (sk.CsrMatrix.stencil(7, 40), (32 * 700, 32 * 1400)),
+             (sk.build_csr(gen.powerlaw(30000, 7)), None)]
+    for csr, rr in cases:
+        a = sk.build_rgcsr(csr, 32, row_range=rr)
+        x = torch.from_numpy(gen.random_vector(csr.num_cols, 3)).cuda()
+        off = rr[0] if rr else 0
+        want = sk.spmv_rgcsr(a, x).cpu().numpy()
+        outs = []
+        for _ in range(2):
+            y = torch.empty(a.num_rows, dtype=torch.float64, device="cuda")
+            d = torch.zeros(1, dtype=torch.float64, device="cuda")
+            assert L.spmvk_rgcsr_spmv_dot_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(),
+                                              y.numel(), off, d.data_ptr(), None) == 0
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == want.tobytes()
+            outs.append(d.item())
+        ref = float(np.dot(x.cpu().numpy()[off:off + a.num_rows], want))
+        assert outs[0] == outs[1]  # deterministic
+        assert abs(outs[0] - ref) <= 1e-12 * max(1.0, abs(ref)), (outs[0], ref)
+    bad = torch.zeros(1, dtype=torch.float64, device="cuda")
+    assert L.spmvk_rgcsr_spmv_dot_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(), y.numel(),
+                                      x.numel(), bad.data_ptr(), None) != 0  # offset too large
