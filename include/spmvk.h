@@ -376,6 +376,15 @@ int spmvk_dist_open_local(const spmvk_window* const* windows, int rank, int worl
  * not consulted). */
 int spmvk_dist_set_rows(spmvk_dist* d, uint64_t row_begin, uint64_t row_end,
                         const uint64_t* receive_ranges);
+/* Distributed CG direction step with the p exchange fused in: for this
+ * rank's rows p_new = r_local + (rr_new / rr) p_old (p_old = the window's
+ * current buffer), stored into the next buffer of the own window and of every
+ * peer window whose receive range covers the row (NVLink stores -- no
+ * all-gather); then rr = rr_new, the buffer flip and (barrier != 0) the flag
+ * barrier.  The slab SpMV of the next iteration reads p from the window
+ * (spmvk_window_x(window, current)).  fp64 only. */
+int spmvk_dist_cg_direction_f64(spmvk_dist* d, const double* r_local, double* rr,
+                                const double* rr_new, int barrier, void* stream);
 /* One step: y = A_slab x[cur] (slab-local y, device), x_next = y * scale
  * stored into x[1-cur] of every window whose receive range covers the row,
  * then (barrier != 0) the device barrier; cur flips.  barrier = 0 is for

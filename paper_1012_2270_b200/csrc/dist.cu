@@ -142,21 +142,18 @@ spmvk_dist* new_dist(const spmvk_window* own, int rank, int world) {
   return d;
 }
 
-template <class T>
-void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, cudaStream_t s) {
-  if (!d || !a) fail(SPMVK_EINVAL, "dist_step: null handle");
-  if (d->prec != static_cast<int>(sizeof(T)) || a->prec != d->prec)
-    fail(SPMVK_EINVAL, "dist_step: precision differs from the window / entry point");
-  if (d->row_end < d->row_begin || a->rows != d->row_end - d->row_begin)
-    fail(SPMVK_EINVAL, "dist_step: slab rows differ from the rows set with spmvk_dist_set_rows");
-  if (a->cols > d->n || d->row_end > d->n)
-    fail(SPMVK_EINVAL, "dist_step: slab reaches past the window length");
+void check_open(const spmvk_dist* d, const char* who) {
   for (int q = 0; q < d->world; ++q)
-    if (!d->base[q]) fail(SPMVK_EINVAL, "dist_step: window of rank " + std::to_string(q) +
-                                            " not opened");
+    if (!d->base[q]) fail(SPMVK_EINVAL, std::string(who) + ": window of rank " +
+                                            std::to_string(q) + " not opened");
+}
+
+// Routing of this rank's next-buffer stores: own rows to x[1-cur] of the own
+// window, and every row a peer receives to that peer's x[1-cur].
+template <class T>
+PeerEpi<T> peer_routing(const spmvk_dist* d, T* y, T scale) {
   const uint64_t xb = d->own->x_bytes();
   const int cur = d->own->cur;
-  const T* x = reinterpret_cast<const T*>(d->base[d->rank] + cur * xb);
   PeerEpi<T> epi{};
   epi.y = y;
   epi.scale = scale;
@@ -181,6 +178,37 @@ void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, 
   epi.ps.n = n;
   epi.int_lo = static_cast<uint32_t>(ilo);
   epi.int_hi = static_cast<uint32_t>(std::max(ilo, ihi));
+  return epi;
+}
+
+// End of a step: flip the window's current buffer and (optionally) run the
+// flag barrier that orders this step's remote stores before the next step.
+void finish_step(spmvk_dist* d, int barrier, cudaStream_t s) {
+  const uint64_t xb = d->own->x_bytes();
+  d->own->cur = 1 - d->own->cur;
+  if (barrier) {
+    const unsigned long long epoch = ++d->own->epoch;
+    FlagSet fs{};
+    for (int q = 0; q < d->world; ++q)
+      fs.remote[q] = reinterpret_cast<unsigned long long*>(d->base[q] + 2 * xb) + d->rank;
+    dist_barrier<<<1, 32, 0, s>>>(fs, d->own->flags(), d->world, epoch);
+    SPMVK_LAUNCH("dist_barrier");
+  }
+}
+
+template <class T>
+void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, cudaStream_t s) {
+  if (!d || !a) fail(SPMVK_EINVAL, "dist_step: null handle");
+  if (d->prec != static_cast<int>(sizeof(T)) || a->prec != d->prec)
+    fail(SPMVK_EINVAL, "dist_step: precision differs from the window / entry point");
+  if (d->row_end < d->row_begin || a->rows != d->row_end - d->row_begin)
+    fail(SPMVK_EINVAL, "dist_step: slab rows differ from the rows set with spmvk_dist_set_rows");
+  if (a->cols > d->n || d->row_end > d->n)
+    fail(SPMVK_EINVAL, "dist_step: slab reaches past the window length");
+  check_open(d, "dist_step");
+  const uint64_t xb = d->own->x_bytes();
+  const T* x = reinterpret_cast<const T*>(d->base[d->rank] + d->own->cur * xb);
+  const PeerEpi<T> epi = peer_routing<T>(d, y, scale);
   if (a->rows) {
     const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(a->group_size, 0xffffffffull));
     const int sh = pow2_shift(a->group_size);
@@ -208,15 +236,60 @@ void dist_step(spmvk_dist* d, const spmvk_rgcsr* a, T scale, T* y, int barrier, 
       SPMVK_LAUNCH("rgcsr_spmv_long_dist");
     }
   }
-  d->own->cur = 1 - cur;
-  if (barrier) {
-    const unsigned long long epoch = ++d->own->epoch;
-    FlagSet fs{};
-    for (int q = 0; q < d->world; ++q)
-      fs.remote[q] = reinterpret_cast<unsigned long long*>(d->base[q] + 2 * xb) + d->rank;
-    dist_barrier<<<1, 32, 0, s>>>(fs, d->own->flags(), d->world, epoch);
-    SPMVK_LAUNCH("dist_barrier");
+  finish_step(d, barrier, s);
+}
+
+// Distributed CG's direction update with the p exchange fused in (the
+// compute step followed by a collective, as one kernel): p_new = r + beta
+// p_old for this rank's rows (beta = rr_new / rr from device memory; p_old
+// read from x[cur] of the own window), stored into x[1-cur] of the own window
+// and of every peer whose receive range covers the row -- the halo of p
+// travels as NVLink stores, no all-gather.  Then rr = rr_new, the flip and
+// the flag barrier.  The arithmetic is cg_direction's (cg.cu), so at world
+// size 1 the iterate is bitwise the single-GPU solver's.
+__global__ void __launch_bounds__(256) dist_cg_direction(uint32_t n,
+                                                         const double* __restrict__ r,
+                                                         const double* __restrict__ p_old,
+                                                         const double* __restrict__ rr,
+                                                         const double* __restrict__ rr_new,
+                                                         PeerEpi<double> route) {
+  const double beta = *rr_new / *rr;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+    const double v = r[i] + beta * p_old[i];
+    const uint32_t gr = route.row0 + i;
+    route.self[gr] = v;
+    if (gr >= route.int_lo && gr < route.int_hi) continue;
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q < route.ps.n && gr >= route.ps.lo[q] && gr < route.ps.hi[q]) route.ps.dst[q][gr] = v;
   }
+}
+
+__global__ void dist_copy_scalar(const double* __restrict__ src, double* __restrict__ dst) {
+  *dst = *src;
+}
+
+void dist_cg_direction_f64(spmvk_dist* d, const double* r, double* rr, const double* rr_new,
+                           int barrier, cudaStream_t s) {
+  if (!d || !r || !rr || !rr_new) fail(SPMVK_EINVAL, "dist_cg_direction: null argument");
+  if (d->prec != SPMVK_F64) fail(SPMVK_EINVAL, "dist_cg_direction: fp64 window required");
+  if (d->row_end < d->row_begin || d->row_end > d->n)
+    fail(SPMVK_EINVAL, "dist_cg_direction: rows not set (spmvk_dist_set_rows)");
+  check_open(d, "dist_cg_direction");
+  const uint64_t rows = d->row_end - d->row_begin;
+  const uint64_t xb = d->own->x_bytes();
+  const double* p_old =
+      reinterpret_cast<const double*>(d->base[d->rank] + d->own->cur * xb) + d->row_begin;
+  const PeerEpi<double> route = peer_routing<double>(d, nullptr, 1.0);
+  if (rows) {
+    // grid of cg.cu's kDotBlocks (592) CTAs: same index mapping per thread
+    dist_cg_direction<<<592, 256, 0, s>>>(static_cast<uint32_t>(rows), r, p_old, rr, rr_new,
+                                          route);
+    SPMVK_LAUNCH("dist_cg_direction");
+  }
+  dist_copy_scalar<<<1, 1, 0, s>>>(rr_new, rr);
+  SPMVK_LAUNCH("dist_copy_scalar");
+  finish_step(d, barrier, s);
 }
 
 }  // namespace
@@ -328,6 +401,11 @@ int spmvk_dist_step_f64(spmvk_dist* d, const spmvk_rgcsr* slab, double scale, do
 int spmvk_dist_step_f32(spmvk_dist* d, const spmvk_rgcsr* slab, float scale, float* y,
                         int barrier, void* stream) {
   return guarded([&] { dist_step<float>(d, slab, scale, y, barrier, as_stream(stream)); });
+}
+
+int spmvk_dist_cg_direction_f64(spmvk_dist* d, const double* r_local, double* rr,
+                                const double* rr_new, int barrier, void* stream) {
+  return guarded([&] { dist_cg_direction_f64(d, r_local, rr, rr_new, barrier, as_stream(stream)); });
 }
 
 int spmvk_dist_current(const spmvk_dist* d, int* buffer) {

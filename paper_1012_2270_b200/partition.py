@@ -228,6 +228,99 @@ def distributed_cg(slab: Slab, world: int, num_cols: int, b, ops, all_gather, al
     return x[:n], k, res
 
 
+class FusedCgRank:
+    """One rank of the distributed CG whose p exchange is fused into the
+    direction step (spmvk_dist_cg_direction_f64): p lives in the rank's
+    exchange window, the direction kernel stores p_new into the next buffer
+    of its own window and of every peer that reads the row (NVLink stores),
+    then the flag barrier -- no all-gather.  The dots stay scalar all-reduces.
+    ``a`` is the rank's slab RgCSR (columns global), ``fused`` its
+    FusedIteratedSpmv-style dist handle (window + routing, set up by the
+    caller), ``b`` its rows of the right-hand side."""
+
+    def __init__(self, slab: Slab, a, fused, b, stream: int):
+        import torch
+        from ._lib import lib
+        self.slab, self.a, self.f, self.s, self.L = slab, a, fused, stream or None, lib()
+        n = slab.rows
+        dev = b.device
+        self.x = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self.r = b.clone() if n else torch.zeros(1, dtype=torch.float64, device=dev)
+        self.q = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self.sc = torch.zeros(6, dtype=torch.float64, device=dev)  # rr pap rrn bb one zero
+        self.sc[4] = 1.0
+        self.rr, self.pap, self.rrn, self.bb = (self.sc[i:i + 1] for i in range(4))
+
+    def _ok(self, rc):
+        if rc:
+            from . import spmvkit as sk
+            sk._check(rc)
+
+    def p_current(self):
+        return self.f.window.x[self.f.cur]
+
+    def start(self, barrier: bool):
+        """p = r in every window that reads it (a direction step with beta = 0
+        over a zeroed p_old), local dots r.r and b.b into rr / bb."""
+        sl = self.slab
+        self.p_current()[sl.row_begin:sl.row_end].zero_()
+        self._ok(self.L.spmvk_dist_cg_direction_f64(
+            self.f._d, self.r.data_ptr(), self.sc[4:5].data_ptr(), self.sc[5:6].data_ptr(),
+            1 if barrier else 0, self.s))
+        n = sl.rows
+        self._ok(self.L.spmvk_dot_f64(self.r.data_ptr(), self.r.data_ptr(), n, self.rr.data_ptr(),
+                                      self.s))
+
+    def spmv_dot(self):
+        sl = self.slab
+        p = self.p_current()
+        self._ok(self.L.spmvk_rgcsr_spmv_dot_f64(self.a._h, p.data_ptr(), self.a.num_cols,
+                                                 self.q.data_ptr(), sl.rows, sl.row_begin,
+                                                 self.pap.data_ptr(), self.s))
+
+    def update(self):
+        sl = self.slab
+        p_local = self.p_current()[sl.row_begin:sl.row_end]
+        self._ok(self.L.spmvk_cg_update_f64(sl.rows, self.rr.data_ptr(), self.pap.data_ptr(),
+                                            p_local.data_ptr(), self.q.data_ptr(),
+                                            self.x.data_ptr(), self.r.data_ptr(),
+                                            self.rrn.data_ptr(), self.s))
+
+    def direction(self, barrier: bool):
+        self._ok(self.L.spmvk_dist_cg_direction_f64(self.f._d, self.r.data_ptr(),
+                                                    self.rr.data_ptr(), self.rrn.data_ptr(),
+                                                    1 if barrier else 0, self.s))
+
+
+def fused_cg(ranks, all_reduce, b_dot, tol: float = 1e-10, max_iter: int = 1000,
+             check_every: int = 10, barrier: bool = True):
+    """Drives FusedCgRank objects through CG.  ``ranks`` are the ranks this
+    process steps (one per process on a node; all of them, stepped in turn
+    with barrier=False, when a test runs every rank on one GPU);
+    ``all_reduce(tensors)`` sums the given per-rank 1-element tensors in rank
+    order and writes the sum back into each; ``b_dot`` = global b.b.
+    Returns (iterations, relative residual)."""
+    bnorm = float(b_dot) ** 0.5 or 1.0
+    for rk in ranks:
+        rk.start(barrier)
+    all_reduce([rk.rr for rk in ranks])
+    res = float(ranks[0].rr.item()) ** 0.5 / bnorm
+    k = 0
+    while k < max_iter and res > tol:
+        for rk in ranks:
+            rk.spmv_dot()
+        all_reduce([rk.pap for rk in ranks])
+        for rk in ranks:
+            rk.update()
+        all_reduce([rk.rrn for rk in ranks])
+        for rk in ranks:
+            rk.direction(barrier)
+        k += 1
+        if k % check_every == 0 or k == max_iter:
+            res = float(ranks[0].rr.item()) ** 0.5 / bnorm
+    return k, res
+
+
 class GpuCgOps:
     """distributed_cg's slab kernels through the C-ABI (fp64, one stream)."""
 

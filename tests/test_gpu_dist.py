@@ -225,3 +225,49 @@ def test_bench_distributed_shared_gpu_bitwise(cuda, workload):
         assert d["config"]["shared_gpu"]
         assert d["x_bits_checksum"] == ref["x_bits_checksum"], world
         assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 2 * d["steps"]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_fused_cg_local_ranks(cuda, P):
+    """Distributed CG with the p exchange fused into the direction step
+    (spmvk_dist_cg_direction_f64: p_new stored into the peers' windows, no
+    all-gather), P ranks on one GPU stepped in turn.  P = 1 is bitwise the
+    single-GPU solver (same kernels, same dots); P > 1 differs only in the
+    dots' summation order."""
+    csr = sk.CsrMatrix.stencil(7, 24)
+    N, G, iters = csr.num_rows, 32, 40
+    b = torch.from_numpy(gen.random_vector(N, 9)).cuda()
+    a_full = sk.build_rgcsr(csr, G)
+    x1, it1, _ = sk.cg(a_full, b, tol=0.0, max_iter=iters, check_every=10)
+    assert it1 == iters
+    slabs = pt.slab_bounds(N, G, P)
+    recv = pt.fused_receive_ranges(slabs, column_ranges(csr, slabs), "halo")
+    wins = [pt.ExchangeWindow(N, 8) for _ in slabs]
+    s = torch.cuda.current_stream().cuda_stream
+    ranks = []
+    for sl in slabs:
+        a = sk.build_rgcsr(csr, G, row_range=(sl.row_begin, sl.row_end))
+        f = pt.FusedIteratedSpmv(sl, recv, a, wins[sl.rank], P, s, local_windows=wins,
+                                 barrier=False)
+        ranks.append(pt.FusedCgRank(sl, a, f, b[sl.row_begin:sl.row_end], s))
+
+    def all_reduce(ts):
+        total = ts[0].clone()
+        for t in ts[1:]:
+            total += t
+        for t in ts:
+            t.copy_(total)
+
+    k, res = pt.fused_cg(ranks, all_reduce, float(torch.dot(b, b)), tol=0.0, max_iter=iters,
+                         check_every=10, barrier=False)
+    assert k == iters
+    x = torch.cat([rk.x[: rk.slab.rows] for rk in ranks]).cpu().numpy()
+    want = x1.cpu().numpy()
+    if P == 1:
+        assert bitwise(x, want)
+    else:
+        assert np.abs(x - want).max() <= 1e-10 * np.abs(want).max()
+    for rk in ranks:
+        rk.f.close()
+    for w in wins:
+        w.close()
