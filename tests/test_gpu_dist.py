@@ -271,3 +271,76 @@ def test_fused_cg_local_ranks(cuda, P):
         rk.f.close()
     for w in wins:
         w.close()
+
+
+CG_CHILD = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+from paper_1012_2270_b200 import generators as gen, partition as pt, spmvkit as sk
+from paper_1012_2270_b200._lib import lib
+from test_gpu_dist import column_ranges
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + os.environ["PORT"],
+                        rank=rank, world_size=world)
+torch.cuda.set_device(0)
+assert lib().spmvk_init(0) == 0
+G, iters = 32, 30
+csr = sk.CsrMatrix.stencil(7, 24)
+N = csr.num_rows
+b = torch.from_numpy(gen.random_vector(N, 9)).cuda()
+x1, _, _ = sk.cg(sk.build_rgcsr(csr, G), b, tol=0.0, max_iter=iters, check_every=10)
+slabs = pt.slab_bounds(N, G, world)
+me = slabs[rank]
+recv = pt.fused_receive_ranges(slabs, column_ranges(csr, slabs), "halo")
+a = sk.build_rgcsr(csr, G, 8, row_range=(me.row_begin, me.row_end))
+win = pt.ExchangeWindow(N, 8)
+hs = [None] * world
+dist.all_gather_object(hs, win.ipc_handle())
+s = torch.cuda.Stream()
+f = pt.FusedIteratedSpmv(me, recv, a, win, world, s.cuda_stream, handles=hs)
+with torch.cuda.stream(s):
+    rk = pt.FusedCgRank(me, a, f, b[me.row_begin:me.row_end], s.cuda_stream)
+s.synchronize()
+dist.barrier()
+
+def all_reduce(ts):  # scalars through the host (gloo): rank-order sum
+    s.synchronize()
+    v = ts[0].cpu()
+    dist.all_reduce(v)
+    ts[0].copy_(v.cuda())
+
+k, res = pt.fused_cg([rk], all_reduce, float(torch.dot(b, b)), tol=0.0, max_iter=iters,
+                     check_every=10, barrier=True)
+s.synchronize()
+x = rk.x[: me.rows]
+want = x1[me.row_begin:me.row_end]
+ok = k == iters and float((x - want).abs().max()) <= 1e-10 * float(x1.abs().max())
+f.close()
+dist.barrier()
+win.close()
+print("ok" if ok else "MISMATCH", flush=True)
+'''
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_cg_ipc_processes(cuda, world):
+    """The fused-exchange CG across real processes: CUDA IPC peer windows,
+    p_new stored by the direction kernel into the peers' windows, the flag
+    barrier every iteration, dots all-reduced over gloo; x matches the
+    single-GPU solver to 1e-10."""
+    port = free_port()
+    procs = [subprocess.Popen([sys.executable, "-c", CG_CHILD], cwd=ROOT, stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True,
+                              env=dict(os.environ, ROOT=ROOT, RANK=str(r), WORLD_SIZE=str(world),
+                                       PORT=port))
+             for r in range(world)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=300))
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, (out, err) in zip(procs, outs):
+        assert p.returncode == 0 and out.strip().endswith("ok"), err[-3000:]
