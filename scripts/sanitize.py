@@ -80,5 +80,31 @@ for it in its:
     it.close()
 for w in wins:
     w.close()
+# fused-exchange distributed CG on local windows (direction kernel -> peer stores)
+wins = [pt.ExchangeWindow(csr.num_rows, 8) for _ in slabs]
+s0 = torch.cuda.current_stream().cuda_stream
+ranks = []
+for sl in slabs:
+    a_s = sk.build_rgcsr(csr, G, 8, row_range=(sl.row_begin, sl.row_end))
+    f = pt.FusedIteratedSpmv(sl, recv, a_s, wins[sl.rank], P, s0, local_windows=wins,
+                             barrier=False)
+    ranks.append(pt.FusedCgRank(sl, a_s, f, b[sl.row_begin:sl.row_end], s0))
+
+
+def all_reduce(ts):
+    total = ts[0].clone()
+    for t in ts[1:]:
+        total += t
+    for t in ts:
+        t.copy_(total)
+
+
+pt.fused_cg(ranks, all_reduce, float(torch.dot(b, b)), tol=0.0, max_iter=5, check_every=5,
+            barrier=False)
+torch.cuda.synchronize()
+for rk in ranks:
+    rk.f.close()
+for w in wins:
+    w.close()
 torch.cuda.synchronize()
 print("sanitize pass ok")
