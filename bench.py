@@ -327,13 +327,16 @@ def run_ours(args):
             Bv = hy_bytes(h.info, prec)
         torch.cuda.synchronize()
         tconv = time.perf_counter() - tt
-        _, pv = time_launches(lambda: fn(h._h, xv.data_ptr(), h.num_cols, yv.data_ptr(),
-                                         h.num_rows, sp), stream, args.steps, args.warmup)
+        vclk = ClockSampler(0)
+        with vclk:
+            _, pv = time_launches(lambda: fn(h._h, xv.data_ptr(), h.num_cols, yv.data_ptr(),
+                                             h.num_rows, sp), stream, args.steps, args.warmup)
         km = pv
         variants[label] = {"gflops": 2.0 * nnz / (km * 1e-3) / 1e9, "kernel_us": km * 1e3,
                            "bytes": Bv, "achieved_gbs": Bv / (km * 1e-3) / 1e9,
                            "frac_of_peak": Bv / (km * 1e-3) / 1e9 / peak,
-                           "convert_ms": tconv * 1e3}
+                           "convert_ms": tconv * 1e3,
+                           "sm_mhz": vclk.summary().get("sm_mhz")}
         if builder == "hy":
             variants[label]["ell_width"] = h.slots_per_row
             variants[label]["coo_nnz"] = h.coo_nnz()
