@@ -284,4 +284,8 @@ struct spmvk_hybrid {
   // tile_ptr[t]: first COO entry of row tile t (256 rows); kernel metadata,
   // (N/256 + 1) words, not part of the reference's arrays.
   spmvk::DevBuf<uint32_t> tile_ptr;
+  // coo_row_ptr[r]: first COO entry of row r (rows + 1 words, kernel
+  // metadata): tiles whose COO range is huge (rows with long COO tails sorted
+  // together) walk each row's run in its own thread instead of staging.
+  spmvk::DevBuf<uint32_t> coo_row_ptr;
 };

@@ -143,6 +143,14 @@ __global__ void hybrid_coo_fill(uint64_t rows, uint32_t k1, const uint32_t* __re
   }
 }
 
+// coo_row_ptr[r] = off[r] (exclusive scan of the rows' COO counts), [rows] = total.
+__global__ void narrow_offsets(uint64_t rows, const uint64_t* __restrict__ off, uint64_t total,
+                               uint32_t* __restrict__ out) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r <= rows;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    out[r] = static_cast<uint32_t>(r < rows ? off[r] : total);
+}
+
 // tile_ptr[t] = first COO entry whose row >= t * kRowsPerTile (lower bound).
 __global__ void coo_tile_bounds(uint64_t ntiles, uint64_t rows, uint64_t n,
                                 const uint32_t* __restrict__ cr, uint32_t* __restrict__ tp) {
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
     const uint32_t* __restrict__ cc, const T* __restrict__ cv, const T* __restrict__ x,
-    T* __restrict__ y) {
+    T* __restrict__ y, const uint32_t* __restrict__ /*crp: staged only*/) {
   __shared__ T prod[kCooTile];
   __shared__ uint32_t prow[kCooTile];
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
@@ -388,6 +396,39 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
 // The tile's COO range [tile_ptr[tile], tile_ptr[tile+1]) staged through
 // shared memory (same scheme as hybrid_spmv_kernel): products in parallel,
 // then each live row adds its own products in array order.
+// Tiles with more than kWalkCoo COO entries: each thread adds its own row's
+// run [crp[r], crp[r+1]) in array order (4 loads in flight, then gathers),
+// so the tile's heavy rows progress in parallel instead of one staged chunk
+// at a time (a reordered power-law matrix puts ~500k COO entries of its 256
+// longest rows in one tile).  Same rounding sequence -> y bitwise.
+constexpr uint32_t kWalkCoo = 16 * kCooTile;
+
+template <class T>
+__device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
+                                          const uint32_t* __restrict__ crp,
+                                          const uint32_t* __restrict__ cc,
+                                          const T* __restrict__ cv, const T* __restrict__ x) {
+  if (!live) return acc;
+  const uint32_t cb = crp[r], ce = crp[r + 1];
+  constexpr int U = 4;  // fits the 32-register budget of the 8-CTA/SM kernels
+  for (uint32_t k = cb; k < ce; k += U) {
+    uint32_t c[U];
+    T v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = k + u < ce ? ld_stream(cc + k + u) : 0u;
+      v[u] = k + u < ce ? ld_stream(cv + k + u) : T(0);
+    }
+    __syncwarp(__activemask());  // scheduling fence: loads before gathers
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = k + u < ce ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + u < ce) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+  }
+  return acc;
+}
+
 template <class T>
 __device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool live, T acc,
                                                  const uint32_t* __restrict__ tile_ptr,
@@ -441,7 +482,7 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
     const uint32_t* __restrict__ cc, const T* __restrict__ cv, const T* __restrict__ x,
-    T* __restrict__ y) {
+    T* __restrict__ y, const uint32_t* __restrict__ crp) {
   const uint32_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   const size_t step = (size_t)U * rows;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -489,7 +530,12 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
           if (j + u < k1) acc = add_rn(acc, mul_rn(v[u], xv[u]));
       }
     }
-    if constexpr (kCoo) acc = coo_tile_accumulate<T>(tile, r, live, acc, tile_ptr, cr, cc, cv, x);
+    if constexpr (kCoo) {
+      if (crp && tile_ptr[tile + 1] - tile_ptr[tile] > kWalkCoo)  // CTA-uniform
+        acc = coo_row_walk<T>(r, live, acc, crp, cc, cv, x);
+      else
+        acc = coo_tile_accumulate<T>(tile, r, live, acc, tile_ptr, cr, cc, cv, x);
+    }
     if (live) y[r] = acc;
   }
 }
@@ -534,6 +580,10 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
         reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
         reinterpret_cast<T*>(h->coo_values.p));
     SPMVK_LAUNCH("hybrid_coo_fill");
+    h->coo_row_ptr.alloc(a->rows + 1);
+    narrow_offsets<<<persistent_grid((a->rows + 256) / 256, 8), 256, 0, s>>>(
+        a->rows, off.p, coo, h->coo_row_ptr.p);
+    SPMVK_LAUNCH("narrow_offsets");
     const uint64_t ntiles = (a->rows + kRowsPerTile - 1) / kRowsPerTile;
     h->tile_ptr.alloc(ntiles + 1);
     coo_tile_bounds<<<persistent_grid((ntiles + 256) / 256, 4), 256, 0, s>>>(
@@ -630,7 +680,7 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), kRowsPerTile, 0, s>>>(
         static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
         h->ell_columns.p, tp, h->coo_rows.p, h->coo_columns.p,
-        reinterpret_cast<const T*>(h->coo_values.p), x, y);
+        reinterpret_cast<const T*>(h->coo_values.p), x, y, h->coo_row_ptr.p);
     SPMVK_LAUNCH("hybrid_spmv");
   };
   const bool acc = part == Part::kCoo, coo = tp != nullptr;

@@ -270,3 +270,21 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_hybrid_reordered_powerlaw_walks_heavy_tiles(cuda, hk, prec):
+    """Descending-reordered power-law rows put the long COO tails together: the
+    first tiles hold > 16k COO entries and switch from chunk staging to one
+    thread per row walking its own COO run.  y bitwise the oracle's; the
+    spmv_coo-only part too."""
+    csr = sk.build_csr(triplets(orc.powerlaw(200_000, 7)))
+    c2, _ = sk.apply_descending_permutation(csr)
+    rp, col, val = c2.to_host()
+    om = orc.Csr(c2.num_rows, c2.num_cols, rp, col, val)
+    h = sk.build_hybrid(c2, None, prec)
+    want = orc.build_hybrid(om, None, prec)
+    assert h.coo_nnz() > 16 * 1024 * 2
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), orc.spmv_hybrid(want, x))
