@@ -288,4 +288,9 @@ struct spmvk_hybrid {
   // metadata): tiles whose COO range is huge (rows with long COO tails sorted
   // together) walk each row's run in its own thread instead of staging.
   spmvk::DevBuf<uint32_t> coo_row_ptr;
+  // Rows of walked tiles whose COO run exceeds kHeavyRun: their COO tail is
+  // added after the main kernel by a warp per row (hybrid_heavy_rows).
+  spmvk::DevBuf<uint32_t> heavy_rows;
+  std::vector<uint32_t> heavy_rows_host;  // the same list, to clip it to a row limit
+  uint64_t n_heavy = 0;
 };

@@ -402,6 +402,9 @@ __global__ void __launch_bounds__(kRowsPerTile) hybrid_spmv_kernel(
 // at a time (a reordered power-law matrix puts ~500k COO entries of its 256
 // longest rows in one tile).  Same rounding sequence -> y bitwise.
 constexpr uint32_t kWalkCoo = 16 * kCooTile;
+// Runs longer than this in walked tiles go to hybrid_heavy_rows (the walk
+// skips them): one thread would need run/4 dependent round trips.
+constexpr uint32_t kHeavyRun = 256;
 
 template <class T>
 __device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
@@ -410,6 +413,7 @@ __device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
                                           const T* __restrict__ cv, const T* __restrict__ x) {
   if (!live) return acc;
   const uint32_t cb = crp[r], ce = crp[r + 1];
+  if (ce - cb > kHeavyRun) return acc;  // added later by hybrid_heavy_rows
   constexpr int U = 4;  // fits the 32-register budget of the 8-CTA/SM kernels
   for (uint32_t k = cb; k < ce; k += U) {
     uint32_t c[U];
@@ -470,6 +474,59 @@ __device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool
     __syncthreads();
   }
   return acc;
+}
+
+// The COO tails of the heavy rows (see kHeavyRun), after the main kernel has
+// stored each row's ELL part (or, for spmv_coo, left y untouched): a warp per
+// row loads 256 consecutive COO entries per round (8 per lane, coalesced),
+// forms the products in parallel, stages them in shared memory, and lane 0
+// adds them in array order onto y[r] -- the reference's rounding sequence.
+template <class T>
+__global__ void __launch_bounds__(256) hybrid_heavy_rows(uint32_t n, const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ crp,
+                                                         const uint32_t* __restrict__ cc,
+                                                         const T* __restrict__ cv,
+                                                         const T* __restrict__ x,
+                                                         T* __restrict__ y) {
+  constexpr int K = 8, W = 32 * K;
+  __shared__ T prod[8][W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    const uint32_t r = rows[i];
+    const uint32_t cb = crp[r], ce = crp[r + 1];
+    T acc = y[r];
+    for (uint32_t k0 = cb; k0 < ce; k0 += W) {
+      uint32_t c[K];
+      T v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t e = k0 + lane + 32 * k;
+        c[k] = e < ce ? ld_stream(cc + e) : 0u;
+        v[k] = e < ce ? ld_stream(cv + e) : T(0);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t e = k0 + lane + 32 * k;
+        if (e < ce) prod[warp][lane + 32 * k] = mul_rn(v[k], ld_x(x + c[k]));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t m = min((uint32_t)W, ce - k0);
+        uint32_t q = 0;
+        for (; q + 8 <= m; q += 8) {
+          T p[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p[u] = prod[warp][q + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
+        }
+        for (; q < m; ++q) acc = add_rn(acc, prod[warp][q]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) y[r] = acc;
+  }
 }
 
 // Register-lean form of hybrid_spmv_kernel (the RgCSR `lite` recipe applied
@@ -589,6 +646,26 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
     coo_tile_bounds<<<persistent_grid((ntiles + 256) / 256, 4), 256, 0, s>>>(
         ntiles, a->rows, coo, h->coo_rows.p, h->tile_ptr.p);
     SPMVK_LAUNCH("coo_tile_bounds");
+    // heavy rows: runs > kHeavyRun inside tiles that walk (> kWalkCoo entries)
+    std::vector<uint32_t> tp(ntiles + 1);
+    SPMVK_CUDA(cudaMemcpyAsync(tp.data(), h->tile_ptr.p, 4 * (ntiles + 1),
+                               cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> heavy;
+    for (uint64_t t = 0; t < ntiles; ++t) {
+      if (tp[t + 1] - tp[t] <= kWalkCoo) continue;
+      const uint64_t r0 = t * kRowsPerTile, r1 = std::min<uint64_t>(a->rows, r0 + kRowsPerTile);
+      std::vector<uint32_t> crp(r1 - r0 + 1);
+      SPMVK_CUDA(cudaMemcpy(crp.data(), h->coo_row_ptr.p + r0, 4 * (r1 - r0 + 1),
+                            cudaMemcpyDeviceToHost));
+      for (uint64_t r = r0; r < r1; ++r)
+        if (crp[r - r0 + 1] - crp[r - r0] > kHeavyRun) heavy.push_back(static_cast<uint32_t>(r));
+    }
+    h->n_heavy = heavy.size();
+    h->heavy_rows_host = heavy;
+    h->heavy_rows.alloc(h->n_heavy);
+    if (h->n_heavy)
+      SPMVK_CUDA(cudaMemcpy(h->heavy_rows.p, heavy.data(), 4 * h->n_heavy, cudaMemcpyHostToDevice));
   }
   DevBuf<unsigned long long> cnt(1);
   SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
@@ -684,6 +761,18 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     SPMVK_LAUNCH("hybrid_spmv");
   };
   const bool acc = part == Part::kCoo, coo = tp != nullptr;
+  // after the main kernel (any variant but v4, which stages every tile): the
+  // heavy rows' COO tails, warp per row, onto the y the main kernel stored
+  auto heavy = [&]() {
+    if (k == HK::kV4 || !coo || !h->n_heavy) return;
+    const auto& hr = h->heavy_rows_host;
+    const uint64_t n = std::lower_bound(hr.begin(), hr.end(), rows) - hr.begin();
+    if (!n) return;
+    hybrid_heavy_rows<T><<<persistent_grid((n + 7) / 8, 8), 256, 0, s>>>(
+        static_cast<uint32_t>(n), h->heavy_rows.p, h->coo_row_ptr.p, h->coo_columns.p,
+        reinterpret_cast<const T*>(h->coo_values.p), x, y);
+    SPMVK_LAUNCH("hybrid_heavy_rows");
+  };
   switch (k) {
     case HK::kV4:
       if (acc) run(hybrid_spmv_kernel<T, 4, true>); else run(hybrid_spmv_kernel<T, 4>);
@@ -714,6 +803,7 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
       else run(hybrid_spmv_lite<T, 8, 5, false, false>);
       break;
   }
+  heavy();
 }
 
 template <class T>
