@@ -39,6 +39,9 @@ for name, om in mats.items():
     x = orc.random_vector(om.cols, 1)
     want = orc.spmv_rgcsr(orc.build_rgcsr(o2, 32), x)[0]
     assert sk.spmv_rgcsr(a2, torch.from_numpy(x).cuda()).cpu().numpy().tobytes() == want.tobytes()
+    h2 = sk.build_hybrid(c2)  # reordered: walked tiles + heavy COO rows
+    want = orc.spmv_hybrid(orc.build_hybrid(o2, None, 8), x)
+    assert sk.spmv_hybrid(h2, torch.from_numpy(x).cuda()).cpu().numpy().tobytes() == want.tobytes()
 # host-span pipeline (pinned x / y, graph-captured chunks), CG, fused dist step
 from paper_1012_2270_b200 import generators as gen  # noqa: E402
 from paper_1012_2270_b200 import partition as pt  # noqa: E402
