@@ -1,6 +1,7 @@
 """e2e host-span SpMV (bench.py's e2e leg) per workload: pinned host x/y
-through spmvk_rgcsr_spmv_host_*, median of 30 calls.  Run once per
-SPMVK_PIPE_MODE (unset = streamed, graph = chunked graph pipeline)."""
+through spmvk_rgcsr_spmv_host_* (the chunked, graph-captured pipeline),
+median of 30 calls; SPMVK_PIPE_CHUNKS / SPMVK_PIPE_MAPPED_Y select its
+shapes."""
 import json
 import os
 import statistics
@@ -34,7 +35,7 @@ for kind, n in ((27, 128), (7, 256), (5, 2048)):
         ok = torch.equal(yh.view(torch.int64 if prec == 8 else torch.int32),
                          want.view(torch.int64 if prec == 8 else torch.int32))
         med = statistics.median(ts[5:])
-        print(json.dumps({"mode": os.environ.get("SPMVK_PIPE_MODE", "stream"),
+        print(json.dumps({"chunks": os.environ.get("SPMVK_PIPE_CHUNKS", "ramp"),
                           "case": f"{kind}pt-{n}", "prec": prec, "ms": round(med * 1e3, 3),
                           "GBs_pcie": round((a.num_cols + a.num_rows) * prec / med / 1e9, 1),
                           "gflops": round(2 * a.nnz() / med / 1e9, 1), "bitwise": ok}), flush=True)
