@@ -288,3 +288,27 @@ def test_hybrid_reordered_powerlaw_walks_heavy_tiles(cuda, hk, prec):
     dt = np.float64 if prec == 8 else np.float32
     x = orc.random_vector(om.cols, 1).astype(dt)
     assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), orc.spmv_hybrid(want, x))
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("x0", [np.inf, np.nan, -0.0])
+def test_nonfinite_x_matches_reference(cuda, hk, prec, x0):
+    """Non-finite x[0]: the reference's spmv_ellpack adds every pad's 0 * x[0]
+    (NaN for an infinite x[0]) -- the device Hybrid must do the same, and
+    spmv_csr must not.  NaN positions must match (fp32 NaN payloads are the
+    GPU's canonical NaN); everything else bitwise."""
+    om = orc.powerlaw(3000, 7)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 4).astype(dt)
+    x[0] = x0
+    m = triplets(om)
+    h = sk.build_hybrid(m, None, prec)
+    c = sk.build_csr(m, prec)
+    for got, ref in ((sk.spmv_hybrid(h, dev(x)).cpu().numpy(),
+                      orc.spmv_hybrid(orc.build_hybrid(om, None, prec), x)),
+                     (sk.spmv_csr(c, dev(x)).cpu().numpy(), orc.spmv_csr(om, x, prec))):
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(got), nan)
+        assert bitwise(got[~nan], ref[~nan])
+        if prec == 8:
+            assert bitwise(got, ref)
