@@ -312,3 +312,19 @@ def test_nonfinite_x_matches_reference(cuda, hk, prec, x0):
         assert bitwise(got[~nan], ref[~nan])
         if prec == 8:
             assert bitwise(got, ref)
+
+
+def test_hybrid_all_coo_walk_and_heavy(cuda, hk):
+    """K1 = 0 (everything in COO) on the reordered power-law matrix: most tiles
+    exceed the walk threshold and many rows are heavy -- the COO-only kernel,
+    the per-row walk and the heavy-row kernel carry the whole product, and
+    spmv_coo's accumulate form composes with them."""
+    csr = sk.build_csr(triplets(orc.powerlaw(100_000, 7)))
+    c2, _ = sk.apply_descending_permutation(csr)
+    rp, col, val = c2.to_host()
+    om = orc.Csr(c2.num_rows, c2.num_cols, rp, col, val)
+    h = sk.build_hybrid(c2, 0)
+    want = orc.build_hybrid(om, 0, 8)
+    x = orc.random_vector(om.cols, 2)
+    assert h.coo_nnz() == om.nnz
+    assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), orc.spmv_hybrid(want, x))
