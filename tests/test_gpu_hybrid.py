@@ -328,3 +328,16 @@ def test_hybrid_all_coo_walk_and_heavy(cuda, hk):
     x = orc.random_vector(om.cols, 2)
     assert h.coo_nnz() == om.nnz
     assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), orc.spmv_hybrid(want, x))
+
+
+def test_parts_compose_on_heavy_tiles(cuda, hk):
+    """spmv_ellpack then spmv_coo (accumulating in place) equals spmv_hybrid
+    bitwise on the reordered power-law matrix, whose COO part goes through the
+    per-row walk and the heavy-row kernel -- the accumulate form of both."""
+    csr = sk.build_csr(triplets(orc.powerlaw(100_000, 7)))
+    c2, _ = sk.apply_descending_permutation(csr)
+    h = sk.build_hybrid(c2)
+    x = dev(orc.random_vector(c2.num_cols, 6))
+    y = sk.spmv_ellpack(h, x)
+    sk.spmv_coo(h, x, y)
+    assert bitwise(y.cpu().numpy(), sk.spmv_hybrid(h, x).cpu().numpy())
