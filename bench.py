@@ -132,11 +132,55 @@ def make_csr(workload):
 
 
 def host_csr(workload):
-    """Host CSR of the same workload (for the CPU reference)."""
-    from paper_1012_2270_b200 import generators as gen
+    """Host CSR of the same workload for the CPU reference, made by the ORACLE's
+    generators (oracle/oracle.c, test infrastructure), so the reference arm
+    never loads the product library."""
+    import oracle as orc
     kind, a, b, _ = WORKLOADS[workload]
-    m = gen.stencil(a, b) if kind == "stencil" else gen.powerlaw(b, 7)
-    return m.num_rows, m.num_cols, m.row_ptr, m.col, m.val
+    return orc.stencil(a, b) if kind == "stencil" else orc.powerlaw(b, 7)
+
+
+GOLDEN_KEY = {"27pt-128": "27pt_128", "5pt-1024": "5pt_1024", "powerlaw-8M": "powerlaw_8M"}
+
+
+def golden_checksum(workload):
+    """Sequential sum of the reference's fp64 y (tests/golden/shapes.json,
+    generated from the unmodified reference by oracle/make_golden.py), or None."""
+    key = GOLDEN_KEY.get(workload)
+    if key is None:
+        return None
+    with open(os.path.join(ROOT, "tests", "golden", "shapes.json")) as f:
+        return json.load(f)[key]["checksum_reference"]
+
+
+L2_NOTE = {
+    "27pt-128": "inputs larger than L2: 681 MB matrix vs 126 MB L2 (no flush); x stays L2-resident",
+    "5pt-1024": "matrix (84 MB) fits in the 126 MB L2: back-to-back launches re-read it from L2",
+    "7pt-512": "inputs larger than L2: 13.4 GB matrix (no flush)",
+    "powerlaw-8M": "inputs larger than L2: 6.9 GB matrix (no flush)",
+}
+
+
+def bench_config(workload, n_gpus, exchange="fused"):
+    """The `config` dict both arms print (identical for the same workload / N)."""
+    cfg = {"workload": workload, "description": WORKLOADS[workload][3], "format": "rgcsr",
+           "group_size": 32, "precision": "fp64", "l2": L2_NOTE[workload]}
+    if n_gpus == 1:
+        cfg["parallelism"] = "single GPU"
+    else:
+        cfg["parallelism"] = f"row-slab x{n_gpus}, iterated x <- (A x) * 2^-4, {exchange} x exchange"
+    return cfg
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------- timing helpers
@@ -178,47 +222,137 @@ def hy_bytes(info, sv):
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference(workload, sample_reps, threads=None, fmt="rgcsr", G=32, prec=8):
-    """Times the reference CPU SpMV on the host cores.  kind 'reference' = the
-    unmodified reference (oracle/_ref), else the plain-C port (oracle)."""
+def cpu_reference(workload, sample_reps, threads=None, G=32, prec=8, budget_s=12.0):
+    """Times the reference CPU spmv_rgcsr on the host cores, twice: on all
+    host threads (group-aligned row slabs, one std::thread each, running the
+    unchanged reference template; bitwise equal to one thread) and on ONE core
+    (the same slabs in sequence: the reference's own single-threaded SpMV).
+    kind 'reference' = the unmodified reference compiled in place
+    (oracle/_ref), else the plain-C port (oracle/oracle.c, one core).  Each
+    leg is a bounded sample of about `budget_s` seconds."""
     import ctypes as C
     import oracle as orc
-    rows, cols, rp, col, val = host_csr(workload)
-    threads = threads or os.cpu_count() or 1
+    m = host_csr(workload)
+    rows, cols, nnz = m.rows, m.cols, m.nnz
+    threads = threads or len(os.sched_getaffinity(0)) or 1
     dt = np.float64 if prec == 8 else np.float32
     x = orc.random_vector(cols, 1).astype(dt)
     y = np.empty(rows, dt)
-    m = orc.Csr(rows, cols, rp, col, val)
-    nnz = m.nnz
-    if orc.ref_available():
-        r = orc.RefMatrix.from_csr(m)
-        h = C.c_void_p()
-        orc._rcheck(orc.R().ref_slabs_build(r.h, 1 if fmt == "rgcsr" else 2, G, -1, prec,
-                                            threads, C.byref(h)))
-        run = lambda: orc._rcheck(orc.R().ref_slabs_spmv(h, x.ctypes.data, y.ctypes.data))  # noqa: E731
-        kind = "reference"
-        cleanup = lambda: orc.R().ref_slabs_free(h)  # noqa: E731
-        used = threads
-    else:
-        a = orc.build_rgcsr(m, G, prec)
-        run = lambda: orc.spmv_rgcsr(a, x)  # noqa: E731
-        kind, used, cleanup = "port", 1, (lambda: None)
-    t = time.perf_counter()
-    run()
-    # bounded sample: at most ~20 s of CPU SpMVs (config 5 is ~0.3 s per SpMV)
-    sample_reps = max(3, min(sample_reps, int(20.0 / max(time.perf_counter() - t, 1e-6))))
-    times = []
-    for _ in range(sample_reps):
+
+    def timed(run):
         t = time.perf_counter()
         run()
-        times.append(time.perf_counter() - t)
-    cleanup()
-    med = statistics.median(times)
-    return {"value": 2.0 * nnz / med / 1e9, "unit": "GFLOP/s", "cores": used, "kind": kind,
-            "sample": f"{sample_reps} full {fmt} SpMVs of {workload} ({WORKLOADS[workload][3]}), "
-                      f"{'fp64' if prec == 8 else 'fp32'}, median; {used} row-slab threads of the "
-                      f"{'unmodified reference spmv_rgcsr' if kind == 'reference' else 'C port'}",
-            "seconds_per_spmv": med}
+        first = time.perf_counter() - t
+        reps = max(3, min(sample_reps, int(budget_s / max(first, 1e-6))))
+        times = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t)
+        return statistics.median(times), reps
+
+    if orc.ref_available():
+        r = orc.RefMatrix.from_csr(m)
+        del m
+        h = C.c_void_p()
+        orc._rcheck(orc.R().ref_slabs_build(r.h, 1, G, -1, prec, threads, C.byref(h)))
+        del r
+        med_nt, reps_nt = timed(lambda: orc._rcheck(
+            orc.R().ref_slabs_spmv(h, x.ctypes.data, y.ctypes.data)))
+        med_1t, reps_1t = timed(lambda: orc._rcheck(
+            orc.R().ref_slabs_spmv_serial(h, x.ctypes.data, y.ctypes.data)))
+        orc.R().ref_slabs_free(h)
+        kind, used = "reference", threads
+    else:
+        a = orc.build_rgcsr(m, G, prec)
+        del m
+
+        def run():
+            y[:] = orc.spmv_rgcsr(a, x)[0]
+        med_1t, reps_1t = timed(run)
+        med_nt, reps_nt, kind, used = med_1t, reps_1t, "port", 1
+    gf = lambda t: 2.0 * nnz / t / 1e9  # noqa: E731
+    what = "unmodified reference spmv_rgcsr" if kind == "reference" else "plain-C port"
+    return {"value": gf(med_nt), "unit": "GFLOP/s", "cores": used, "kind": kind,
+            "sample": (f"median of {reps_nt} full SpMVs of {workload} "
+                       f"({WORKLOADS[workload][3]}), RgCSR G={G}, "
+                       f"{'fp64' if prec == 8 else 'fp32'}, {used} row-slab threads of the {what}; "
+                       f"1-core leg: median of {reps_1t}"),
+            "value_1core": gf(med_1t), "seconds_per_spmv": med_nt,
+            "seconds_per_spmv_1core": med_1t, "cpu_model": cpu_model(),
+            "host_threads": os.cpu_count(), "checksum": float(np.cumsum(y.astype(np.float64))[-1])}
+
+
+def cpu_baseline_block(c):
+    return {k: c[k] for k in ("value", "unit", "cores", "kind", "sample", "value_1core",
+                              "cpu_model", "host_threads")}
+
+
+# ---------------------------------------------------------------- scaling anchor
+def scale_anchor(args, peak):
+    """BASELINE configs[4] at N = 1: 7-point 512^3 fp64 (938 M nnz, 13.4 GB of
+    RgCSR), the matrix the N > 1 scaling runs shard.  One step is the
+    iterated product's x <- (A x) * 2^-4 (the scaled K2 epilogue), 100 steps
+    as the config names, timed like the headline; the iterate's bit checksum
+    is compared with the device CSR kernel's iterate (an independent kernel;
+    the reference comparison of this iterate is tests/test_gpu_config5.py)."""
+    import torch
+    from paper_1012_2270_b200 import generators as gen
+    from paper_1012_2270_b200 import spmvkit as sk
+    from paper_1012_2270_b200._lib import lib
+    L = lib()
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    t = time.perf_counter()
+    csr = sk.CsrMatrix.stencil(7, 512, stream=sp)
+    a = sk.build_rgcsr(csr, 32, 8, stream=sp)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t
+    n = a.num_rows
+    x0 = torch.from_numpy(gen.random_vector(n, 1)).cuda()
+    xs = [x0.clone(), torch.empty_like(x0)]
+    y = torch.empty_like(x0)
+    cur = [0]
+
+    def step():
+        xa, xb = xs[cur[0]], xs[1 - cur[0]]
+        L.spmvk_rgcsr_spmv_scaled_f64(a._h, xa.data_ptr(), n, y.data_ptr(), n, xb.data_ptr(),
+                                      0.0625, sp)
+        cur[0] = 1 - cur[0]
+    iters = 100
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    xs[0].copy_(x0)
+    cur[0] = 0
+    clk = ClockSampler(0)
+    with clk:
+        total, per = time_launches(step, stream, iters, 0)
+    bits = int(xs[cur[0]].view(torch.int64).sum().item())
+    # the same 100 iterations through the device CSR kernel (spmv_csr) + scale
+    xc = x0.clone()
+    yc = torch.empty_like(x0)
+    for _ in range(iters):
+        sk._check(L.spmvk_csr_spmv_f64(csr._h, xc.data_ptr(), n, yc.data_ptr(), n, sp))
+        with torch.cuda.stream(stream):
+            torch.mul(yc, 0.0625, out=xc)
+    torch.cuda.synchronize()
+    bits_csr = int(xc.view(torch.int64).sum().item())
+    B = rg_bytes(a.info, 8)
+    nnz = a.nnz()
+    out = {"workload": "7pt-512", "description": WORKLOADS["7pt-512"][3], "n_gpus": 1,
+           "iterations": iters, "ms_per_step": per,
+           "gflops": 2.0 * nnz / (per * 1e-3) / 1e9,
+           "roofline": {"achieved": B / (per * 1e-3) / 1e9, "peak": peak,
+                        "frac": B / (per * 1e-3) / 1e9 / peak, "bytes_per_launch": B},
+           "build_s": t_build, "x_bits_checksum": bits,
+           "parity": "bitwise == device spmv_csr iterate" if bits == bits_csr else "MISMATCH",
+           "sm_mhz": clk.summary().get("sm_mhz")}
+    del a, csr, xs, y, xc, yc
+    torch.cuda.empty_cache()
+    if bits != bits_csr:
+        raise SystemExit("parity gate failed: 7pt-512 iterate differs from the CSR kernel's")
+    return out
 
 
 # ---------------------------------------------------------------- arms
@@ -227,17 +361,20 @@ def run_reference_arm(args):
     if rank != 0:
         return
     steps = args.steps
+    n = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     base = cpu_reference(args.workload, max(steps, 1))
-    line = {"metric": METRIC, "value": base["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
+    golden = golden_checksum(args.workload)
+    if golden is not None and base["checksum"] != golden:
+        raise SystemExit(f"reference checksum {base['checksum']!r} != golden {golden!r}")
+    line = {"metric": METRIC, "value": base["value"], "unit": "GFLOP/s", "n_gpus": n,
             "steps": steps, "warmup": args.warmup,
             "ms_per_step": base["seconds_per_spmv"] * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "format": "rgcsr", "group_size": 32,
-                       "description": WORKLOADS[args.workload][3]},
-            "impl": "reference", "cpu_baseline": {k: base[k] for k in
-                                                  ("value", "unit", "cores", "kind", "sample")},
+            "config": bench_config(args.workload, n, args.exchange),
+            "impl": "reference", "cpu_baseline": cpu_baseline_block(base),
             "e2e": {"value": base["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "checksum": base["checksum"]}
     print(json.dumps(line), flush=True)
 
 
@@ -249,7 +386,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.distributed:
         from paper_1012_2270_b200 import partition
-        return partition.bench_distributed(args, METRIC, WORKLOADS, ClockSampler, peaks(), rg_bytes)
+        return partition.bench_distributed(
+            args, METRIC, WORKLOADS, ClockSampler, peaks(), rg_bytes,
+            config_fn=lambda n, ex: bench_config(args.workload, n, ex),
+            cpu_fn=lambda: cpu_baseline_block(cpu_reference(args.workload, args.cpu_reps)),
+            traffic=committed_traffic(f"{args.workload}/rgcsr_f64_g32"))
 
     torch.cuda.set_device(0)
     assert lib().spmvk_init(0) == 0, sk._lib.last_error()
@@ -285,8 +426,12 @@ def run_ours(args):
     achieved = B / (kern_ms * 1e-3) / 1e9
     value = 2.0 * nnz / (ms * 1e-3) / 1e9
 
-    # parity gate on the measured output (checksum vs the committed golden)
+    # parity gate on the measured output: the sequential sum of y must equal
+    # the unmodified reference's (tests/golden/shapes.json) bit for bit
     ysum = float(np.cumsum(y.cpu().numpy())[-1])
+    golden = golden_checksum(args.workload)
+    if golden is not None and ysum != golden:
+        raise SystemExit(f"parity gate failed: GPU checksum {ysum!r} != reference {golden!r}")
 
     # ---- e2e: reference-facing C-ABI span overload with pinned HOST buffers
     xpin = torch.from_numpy(xh).pin_memory()
@@ -343,17 +488,18 @@ def run_ours(args):
         if builder != "csr":
             del h
 
+    anchor = scale_anchor(args, peak) if args.workload != "7pt-512" else None
     cpu = cpu_reference(args.workload, args.cpu_reps)
+    if cpu["checksum"] != ysum:
+        raise SystemExit(f"parity gate failed: GPU checksum {ysum!r} != CPU reference "
+                         f"{cpu['checksum']!r}")
     traffic = committed_traffic(f"{args.workload}/rgcsr_f64_g32")
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "description": WORKLOADS[args.workload][3],
-                   "format": "rgcsr", "group_size": G, "nnz": nnz, "rows": a.num_rows,
-                   "slots": a.slot_count(), "parallelism": "single GPU",
-                   "l2": "inputs larger than L2: matrix %.0f MB vs 126 MB L2; x stays L2-resident"
-                         % (B / 1e6)},
+        "config": bench_config(args.workload, 1, args.exchange),
+        "shape": {"nnz": nnz, "rows": a.num_rows, "slots": a.slot_count()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "bytes_per_launch": B, "kernel_us": kern_ms * 1e3,
@@ -364,7 +510,7 @@ def run_ours(args):
                      "kernel": "rgcsr_spmv_grp (K2 auto): with x[0] finite it does not read "
                                "row_lengths (4 B/row of B_fmt), so DRAM traffic (ncu) is "
                                "~2 % below bytes_per_launch"},
-        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": cpu_baseline_block(cpu),
         "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,
                 "ms_per_step": e2e_s * 1e3,
@@ -372,8 +518,11 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
         "checksum": ysum,
+        "parity": ("checksum == the unmodified reference's (CPU run above and the golden)"
+                   if golden is not None else "checksum == the CPU reference run above"),
         "convert_ms": {"csr_ingest": t_csr * 1e3, "rgcsr_g32_f64": t_conv * 1e3},
         "variants": variants,
+        "scale_anchor": anchor,
     }
     print(json.dumps(line), flush=True)
 

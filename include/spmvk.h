@@ -394,6 +394,13 @@ int spmvk_dist_step_f64(spmvk_dist* d, const spmvk_rgcsr* slab, double scale, do
 int spmvk_dist_step_f32(spmvk_dist* d, const spmvk_rgcsr* slab, float scale, float* y,
                         int barrier, void* stream);
 int spmvk_dist_current(const spmvk_dist* d, int* buffer);
+/* Bound on one barrier's wait for a peer (default 30 s).  A barrier that
+ * times out records the peer in the window's status word and returns; every
+ * later barrier of the window then returns at once (no hang). */
+int spmvk_dist_set_timeout_ms(spmvk_dist* d, uint64_t ms);
+/* Synchronises `stream` and returns SPMVK_ENCCL (message names the missing
+ * rank) if a barrier of this rank's window timed out, else SPMVK_OK. */
+int spmvk_dist_status(const spmvk_dist* d, void* stream);
 void spmvk_dist_destroy(spmvk_dist* d);
 
 /* ------------------------------------------------------------------ host generators

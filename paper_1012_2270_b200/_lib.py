@@ -116,6 +116,8 @@ SIGNATURES = {
     "spmvk_dist_step_f32": (cint, [vp, vp, C.c_float, vp, cint, vp]),
     "spmvk_dist_cg_direction_f64": (cint, [vp, vp, vp, vp, C.c_int, vp]),
     "spmvk_dist_current": (cint, [vp, C.POINTER(cint)]),
+    "spmvk_dist_set_timeout_ms": (cint, [vp, u64]),
+    "spmvk_dist_status": (cint, [vp, vp]),
     "spmvk_dist_destroy": (None, [vp]),
     "spmvk_gen_random_vector": (None, [u64, u64, vp]),
     "spmvk_gen_stencil": (u64, [cint, u64, vp, vp, vp]),

@@ -112,13 +112,6 @@ __global__ void __launch_bounds__(kDotThreads) cg_init(uint64_t n, const double*
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// Per-thread partials buffer of the fixed-grid dots (stream-ordered reuse:
-// calls issued from one host thread must share one stream).
-DevBuf<double>& dot_scratch() {
-  static thread_local DevBuf<double> part;
-  if (part.n < (uint64_t)kDotBlocks) part.alloc(kDotBlocks);
-  return part;
-}
 
 }  // namespace
 }  // namespace spmvk
@@ -130,10 +123,10 @@ extern "C" {
 int spmvk_dot_f64(const double* a, const double* b, uint64_t n, double* out_dev, void* stream) {
   return guarded([&] {
     cudaStream_t s = as_stream(stream);
-    DevBuf<double>& part = dot_scratch();
-    dot_partials<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, part.p);
+    double* part = stream_scratch(s, kDotBlocks);
+    dot_partials<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, part);
     SPMVK_LAUNCH("dot_partials");
-    dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, out_dev);
+    dot_finish<<<1, kDotThreads, 0, s>>>(part, kDotBlocks, out_dev);
     SPMVK_LAUNCH("dot_finish");
   });
 }
@@ -142,10 +135,10 @@ int spmvk_cg_update_f64(uint64_t n, const double* rr, const double* pap, const d
                         const double* q, double* x, double* r, double* rr_new, void* stream) {
   return guarded([&] {
     cudaStream_t s = as_stream(stream);
-    DevBuf<double>& part = dot_scratch();
-    cg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, rr, pap, p, q, x, r, part.p);
+    double* part = stream_scratch(s, kDotBlocks);
+    cg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, rr, pap, p, q, x, r, part);
     SPMVK_LAUNCH("cg_update");
-    dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, rr_new);
+    dot_finish<<<1, kDotThreads, 0, s>>>(part, kDotBlocks, rr_new);
     SPMVK_LAUNCH("dot_finish");
   });
 }
@@ -169,19 +162,20 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
     if (a->rows != n || a->cols != n) fail(SPMVK_EINVAL, "cg: matrix must be square n x n");
     if (a->prec != SPMVK_F64) fail(SPMVK_EINVAL, "cg: fp64 RgCSR required");
     cudaStream_t s = as_stream(stream);
-    DevBuf<double> r(n), p(n), q(n), part(kDotBlocks), sc(4);  // sc: rr, pAp, rr_new, bb
+    DevBuf<double> r(n), p(n), q(n), partb(kDotBlocks), sc(4);  // sc: rr, pAp, rr_new, bb
+    double* part = partb.p;
     double* rr = sc.p;
     double* pap = sc.p + 1;
     double* rrn = sc.p + 2;
     double* bb = sc.p + 3;
     const unsigned grid = kDotBlocks;
     // bb = b.b ; q = A x ; r = b - q ; p = r ; rr = r.r
-    dot_partials<<<grid, kDotThreads, 0, s>>>(n, b, b, part.p);
-    dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, bb);
+    dot_partials<<<grid, kDotThreads, 0, s>>>(n, b, b, part);
+    dot_finish<<<1, kDotThreads, 0, s>>>(part, kDotBlocks, bb);
     if (spmvk_rgcsr_spmv_f64(a, x, n, q.p, n, s) != SPMVK_OK)
       fail(SPMVK_ECUDA, std::string("cg spmv: ") + spmvk_last_error());
-    cg_init<<<grid, kDotThreads, 0, s>>>(n, b, q.p, r.p, p.p, part.p);
-    dot_finish<<<1, kDotThreads, 0, s>>>(part.p, kDotBlocks, rr);
+    cg_init<<<grid, kDotThreads, 0, s>>>(n, b, q.p, r.p, p.p, part);
+    dot_finish<<<1, kDotThreads, 0, s>>>(part, kDotBlocks, rr);
     SPMVK_LAUNCH("cg_init");
     double h[4];
     SPMVK_CUDA(cudaMemcpyAsync(h, sc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -194,8 +188,8 @@ int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_
       // q = A p with pAp = p.q fused into the SpMV epilogue
       if (spmvk_rgcsr_spmv_dot_f64(a, p.p, n, q.p, n, 0, pap, st) != SPMVK_OK)
         fail(SPMVK_ECUDA, std::string("cg spmv: ") + spmvk_last_error());
-      cg_update<<<grid, kDotThreads, 0, st>>>(n, rr, pap, p.p, q.p, x, r.p, part.p);
-      dot_finish<<<1, kDotThreads, 0, st>>>(part.p, kDotBlocks, rrn);
+      cg_update<<<grid, kDotThreads, 0, st>>>(n, rr, pap, p.p, q.p, x, r.p, part);
+      dot_finish<<<1, kDotThreads, 0, st>>>(part, kDotBlocks, rrn);
       cg_direction<<<grid, kDotThreads, 0, st>>>(n, r.p, p.p, rr, rrn);
       copy_scalar<<<1, 1, 0, st>>>(rrn, rr);
       SPMVK_LAUNCH("cg iteration");

@@ -3,6 +3,8 @@
 // checks, and the uint64 exclusive scan used for group pointers / COO offsets.
 #include "common.cuh"
 
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,6 +42,28 @@ void require_device() {
 HostStage& host_stage() {
   static thread_local HostStage st;
   return st;
+}
+
+// Scratch keyed by (device, stream): work on one stream is ordered, so calls
+// from any host thread on the same stream may share it, and two streams
+// never do (a per-host-thread buffer raced when one thread drove several
+// streams).  Grows only outside stream capture.
+double* stream_scratch(cudaStream_t s, uint64_t n) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, DevBuf<double>> bufs;
+  int dev = 0;
+  SPMVK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  DevBuf<double>& b = bufs[{dev, s}];
+  if (b.n < n) {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    SPMVK_CUDA(cudaStreamIsCapturing(s, &cst));
+    if (cst != cudaStreamCaptureStatusNone)
+      fail(SPMVK_EINVAL, "first reduction on this stream is inside a stream capture; "
+                         "call it once eagerly first");
+    b.alloc(n);
+  }
+  return b.p;
 }
 
 // ---------------------------------------------------------------- scan

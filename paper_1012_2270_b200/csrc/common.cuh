@@ -184,6 +184,12 @@ __device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
   return v;
 }
 
+// 1D bulk prefetch of [src, src + bytes) into L2 through the TMA unit (no
+// completion tracking); src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Separately rounded multiply and add: the reference's `acc += v * x[c]`
 // compiled without FMA contraction (core/CMakeLists.txt has no -march).
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -226,6 +232,8 @@ struct HostStage {
   }
 };
 HostStage& host_stage();
+// Device scratch of >= n doubles private to (current device, stream s).
+double* stream_scratch(cudaStream_t s, uint64_t n);
 
 }  // namespace spmvk
 
@@ -242,11 +250,8 @@ struct spmvk_rgcsr {
   int prec = SPMVK_F64;
   spmvk::DevBuf<unsigned char> values;  // slots * prec bytes
   spmvk::DevBuf<uint32_t> columns, group_pointers, row_lengths;
-  // K2 launch metadata (not part of the reference arrays): the slot-balanced
-  // wave split of rgcsr_spmv_wtma for the grid it was computed for.
+  // Guards the lazily computed launch metadata below (tile_cols).
   mutable std::mutex part_mu;
-  mutable spmvk::DevBuf<uint32_t> part;
-  mutable uint32_t part_W = 0;
   // Rows longer than long_cut (ascending ids): K2's thread-per-row kernels
   // skip them and a warp-per-row kernel handles them (power-law tails).
   spmvk::DevBuf<uint32_t> long_rows;
@@ -256,10 +261,8 @@ struct spmvk_rgcsr {
   spmvk::DevBuf<uint32_t> long_quads, long_singles;
   uint64_t n_quads = 0, n_singles = 0;
   uint32_t long_cut = 128;
-  // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile
-  // (host copy), and the same on the device for rgcsr_spmv_grpx.
+  // Pipelined host-span SpMV: x column range [min, max] of each 256-row tile.
   mutable std::vector<unsigned> tile_cols;
-  mutable spmvk::DevBuf<unsigned> tile_cols_dev;
   // Process-unique id: keys the host-span pipeline's captured CUDA graph
   // (a recycled handle address must not replay a graph of freed arrays).
   const uint64_t serial = next_serial();

@@ -53,6 +53,7 @@ struct spmvk_dist {
   bool ipc[spmvk::kMaxPeers] = {};             // opened with cudaIpcOpenMemHandle
   uint64_t row_begin = 0, row_end = 0;
   uint64_t lo[spmvk::kMaxPeers] = {}, hi[spmvk::kMaxPeers] = {};  // rows each rank receives
+  uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;  // barrier wait bound (set_timeout_ms)
   ~spmvk_dist() {
     for (int q = 0; q < world; ++q)
       if (ipc[q] && base[q]) cudaIpcCloseMemHandle(base[q]);
@@ -63,6 +64,15 @@ namespace spmvk {
 namespace {
 
 constexpr uint64_t kFlagBytes = 64 * sizeof(unsigned long long);
+// Flag word kFlagStatus of a window: 0, or 1 + the rank a barrier of this
+// window's owner gave up waiting for (spmvk_dist_status reads it).
+constexpr int kFlagStatus = 63;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -82,13 +92,25 @@ struct FlagSet {
 // stream (the SpMV, including its remote stores) completed before this one
 // started; the system-scope fence + release make those stores visible to the
 // peer before it sees the flag.
-__global__ void dist_barrier(FlagSet fs, const unsigned long long* mine, int world,
-                             unsigned long long epoch) {
+// The wait is bounded: after timeout_ns without the peer's flag the barrier
+// records 1 + q in the window's status word and returns, and every later
+// barrier of this window returns at once -- a dead peer turns into an error
+// (spmvk_dist_status -> SPMVK_ENCCL), not a hung GPU.
+__global__ void dist_barrier(FlagSet fs, unsigned long long* mine, int world,
+                             unsigned long long epoch, uint64_t timeout_ns) {
   const int q = threadIdx.x;
   if (q < world) {
     __threadfence_system();
     st_release_sys(fs.remote[q], epoch);
-    while (ld_acquire_sys(mine + q) < epoch) __nanosleep(64);
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(mine + q) < epoch) {
+      if (*(volatile unsigned long long*)(mine + kFlagStatus)) break;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicCAS(mine + kFlagStatus, 0ull, (unsigned long long)(q + 1));
+        break;
+      }
+      __nanosleep(256);
+    }
   }
   __syncthreads();
 }
@@ -99,7 +121,7 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_dist(
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, uint32_t long_cut,
     PeerEpi<T> epi) {
-  lite_tiles_epi<T, U, false>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns,
+  lite_tiles_epi<T, U>(0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns,
                               x, long_cut, epi);
 }
 
@@ -191,7 +213,7 @@ void finish_step(spmvk_dist* d, int barrier, cudaStream_t s) {
     FlagSet fs{};
     for (int q = 0; q < d->world; ++q)
       fs.remote[q] = reinterpret_cast<unsigned long long*>(d->base[q] + 2 * xb) + d->rank;
-    dist_barrier<<<1, 32, 0, s>>>(fs, d->own->flags(), d->world, epoch);
+    dist_barrier<<<1, 32, 0, s>>>(fs, d->own->flags(), d->world, epoch, d->timeout_ns);
     SPMVK_LAUNCH("dist_barrier");
   }
 }
@@ -368,6 +390,12 @@ int spmvk_dist_open_local(const spmvk_window* const* windows, int rank, int worl
       cudaPointerAttributes at{};
       SPMVK_CUDA(cudaPointerGetAttributes(&at, windows[q]->mem.p));
       if (at.device != dev) {  // a window on another GPU of this process: map it
+        int can = 0;
+        SPMVK_CUDA(cudaDeviceCanAccessPeer(&can, dev, at.device));
+        if (!can)
+          fail(SPMVK_ENCCL, "dist_open_local: GPU " + std::to_string(dev) +
+                                " cannot access GPU " + std::to_string(at.device) +
+                                " peer-to-peer (use the NCCL exchange)");
         const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
         if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
         else SPMVK_CUDA(e);
@@ -406,6 +434,29 @@ int spmvk_dist_step_f32(spmvk_dist* d, const spmvk_rgcsr* slab, float scale, flo
 int spmvk_dist_cg_direction_f64(spmvk_dist* d, const double* r_local, double* rr,
                                 const double* rr_new, int barrier, void* stream) {
   return guarded([&] { dist_cg_direction_f64(d, r_local, rr, rr_new, barrier, as_stream(stream)); });
+}
+
+int spmvk_dist_set_timeout_ms(spmvk_dist* d, uint64_t ms) {
+  return guarded([&] {
+    if (!d) fail(SPMVK_EINVAL, "dist_set_timeout_ms: null handle");
+    if (ms == 0) fail(SPMVK_EINVAL, "dist_set_timeout_ms: timeout must be positive");
+    d->timeout_ns = ms * 1000ull * 1000ull;
+  });
+}
+
+int spmvk_dist_status(const spmvk_dist* d, void* stream) {
+  return guarded([&] {
+    if (!d) fail(SPMVK_EINVAL, "dist_status: null handle");
+    unsigned long long v = 0;
+    cudaStream_t s = as_stream(stream);
+    SPMVK_CUDA(cudaMemcpyAsync(&v, d->own->flags() + kFlagStatus, sizeof(v),
+                               cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    if (v)
+      fail(SPMVK_ENCCL, "dist barrier of rank " + std::to_string(d->rank) +
+                            " timed out waiting for rank " + std::to_string(v - 1) +
+                            " (peer dead or not stepping)");
+  });
 }
 
 int spmvk_dist_current(const spmvk_dist* d, int* buffer) {

@@ -298,11 +298,10 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 
 // K2 variant selection: spmvk_set_rgcsr_kernel() or SPMVK_RGCSR_KERNEL.
 // All variants give bitwise identical y; they differ in how slots are staged.
-enum class K2 {
-  kAuto, kWtma, kPipe, kPipeHi, kPipe8, kTma, kLdg, kLdgPf, kLite, kLite8, kLite8Pf, kLitePf,
-  kLite8Full, kLiteMpf, kLite8Mpf, kLite8FullMpf, kVec2, kVec4,
-  kGrp4, kGrp6, kGrp7, kGrp7Mpf, kGrp8, kGrp8R64, kGrp8Len, kGrpX, kGrpX8
-};
+// Round 2 pruned the variants that never won a measured case (TMA rings,
+// L2 bulk prefetch, x staged in shared memory, policy-hinted ldg, deeper
+// pipes; numbers in profiles/r02_k2_pruned.md).
+enum class K2 { kAuto, kPipe, kLite, kLite8, kLite8Full, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
 // stencil shapes (profiles/r01_k2_sweep.md): the register-lean tile kernel —
@@ -343,17 +342,10 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
 
 bool parse_k2(const std::string& v, K2* out) {
   static const std::pair<const char*, K2> names[] = {
-      {"auto", K2::kAuto},   {"wtma", K2::kWtma},
-      {"pipe", K2::kPipe},      {"pipe_hi", K2::kPipeHi},
-      {"pipe8", K2::kPipe8},
-      {"tma", K2::kTma},     {"ldg", K2::kLdg},        {"ldg_pf", K2::kLdgPf},
-      {"lite", K2::kLite},     {"lite8", K2::kLite8},
-      {"lite8_l2pf", K2::kLite8Pf}, {"lite_l2pf", K2::kLitePf}, {"lite8_full", K2::kLite8Full},
-      {"lite_mpf", K2::kLiteMpf}, {"lite8_mpf", K2::kLite8Mpf},
-      {"lite8_full_mpf", K2::kLite8FullMpf}, {"vec2", K2::kVec2}, {"vec4", K2::kVec4},
-      {"grp4", K2::kGrp4}, {"grp6", K2::kGrp6}, {"grp7", K2::kGrp7},
-      {"grp7_mpf", K2::kGrp7Mpf}, {"grp8", K2::kGrp8}, {"grp8_r64", K2::kGrp8R64},
-      {"grp8_len", K2::kGrp8Len}, {"grpx", K2::kGrpX}, {"grpx8", K2::kGrpX8}};
+      {"auto", K2::kAuto},         {"pipe", K2::kPipe},         {"lite", K2::kLite},
+      {"lite8", K2::kLite8},       {"lite8_full", K2::kLite8Full}, {"vec2", K2::kVec2},
+      {"grp6", K2::kGrp6},         {"grp7_mpf", K2::kGrp7Mpf},  {"grp8", K2::kGrp8},
+      {"grp8_r64", K2::kGrp8R64}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -374,71 +366,6 @@ std::atomic<int>& k2_slot() {
 
 K2 k2_choice() { return static_cast<K2>(k2_slot().load(std::memory_order_relaxed)); }
 
-template <class T, bool kScaled, int NW, int NS, int CE>
-void launch_tma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
-  constexpr size_t smem = tma_smem_bytes<T, NS, CE>();
-  auto kern = rgcsr_spmv_tma<T, kScaled, NW, NS, CE>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  const uint32_t G = static_cast<uint32_t>(h->group_size);
-  const uint32_t gpt = (NW * 32) / G;
-  const uint32_t ntiles = static_cast<uint32_t>((h->groups + gpt - 1) / gpt);
-  int per_sm = 0;
-  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, smem));
-  kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), (NW + 1) * 32, smem, s>>>(
-      static_cast<uint32_t>(h->rows), G, pow2_shift(G), static_cast<uint32_t>(h->groups), gpt,
-      ntiles, h->group_pointers.p, h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
-      h->columns.p, x, y, x_next, scale);
-  SPMVK_LAUNCH("rgcsr_spmv_tma");
-}
-
-// Per-warp bulk-copy streams (rgcsr_spmv_wtma), one CTA per SM: 8 warps x a
-// 4-stage ring of 512 (fp64) / 3 x 1024 (fp32) elements, ~192 KB of shared
-// memory per SM in flight; x gathers in batches of 8.
-template <class T, bool kScaled, int R, int NW, int NS, int CE>
-void launch_wtma(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
-  constexpr size_t smem = wtma_smem_bytes<T, NS, CE, NW>();
-  auto kern = rgcsr_spmv_wtma<T, kScaled, R, NS, CE, NW, 8>;
-  static std::once_flag once;  // per instantiation
-  std::call_once(once, [&] {
-    SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  });
-  const uint32_t G = static_cast<uint32_t>(h->group_size);
-  const uint32_t gpw = G >= 32 ? 1 : 32 / G;
-  const uint32_t nwaves = static_cast<uint32_t>((h->groups + gpw - 1) / gpw);
-  const unsigned grid = static_cast<unsigned>(sm_count());
-  const uint32_t W = grid * NW;
-  {
-    std::lock_guard<std::mutex> lk(h->part_mu);
-    if (h->part_W != W) {
-      h->part.alloc(W + 1);
-      wave_partition<<<(W + 256) / 256, 256, 0, s>>>(W, nwaves, gpw,
-                                                     static_cast<uint32_t>(h->groups),
-                                                     h->group_pointers.p, h->part.p);
-      SPMVK_LAUNCH("wave_partition");
-      h->part_W = W;
-    }
-  }
-  kern<<<grid, NW * 32, smem, s>>>(static_cast<uint32_t>(h->rows), G,
-                                   static_cast<uint32_t>(h->groups), gpw, nwaves, h->part.p,
-                                   h->group_pointers.p, h->row_lengths.p,
-                                   reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y,
-                                   x_next, scale);
-  SPMVK_LAUNCH("rgcsr_spmv_wtma");
-}
-
-template <class T, bool kScaled, int NW, int NS, int CE>
-void launch_wtma_g(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
-  const uint64_t G = h->group_size;
-  if (G <= 32) launch_wtma<T, kScaled, 1, NW, NS, CE>(h, x, y, x_next, scale, s);
-  else if (G <= 64) launch_wtma<T, kScaled, 2, NW, NS, CE>(h, x, y, x_next, scale, s);
-  else if (G <= 128) launch_wtma<T, kScaled, 4, NW, NS, CE>(h, x, y, x_next, scale, s);
-  else launch_wtma<T, kScaled, 8, NW, NS, CE>(h, x, y, x_next, scale, s);
-}
-
 // The rows past the long-row cut: singles (warp per row, longest first) and
 // quads (four rows per warp) in one launch after the thread-per-row kernel.
 template <class T, bool kScaled>
@@ -453,23 +380,30 @@ void launch_long(const spmvk_rgcsr* h, uint32_t G, int sh, const T* x, T* y, T* 
   SPMVK_LAUNCH("rgcsr_spmv_long_mixed");
 }
 
+// A matrix without stored slots (nnz = 0, e.g. cols = 0): every row sums
+// nothing, so y = +0 (the reference's acc start) -- without touching x, which
+// may be a zero-length (null) array.
+template <class T, bool kScaled>
+__global__ void spmv_empty(uint64_t rows, T* __restrict__ y, T* __restrict__ x_next, T scale) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    y[r] = T(0);
+    if (kScaled) x_next[r] = mul_rn(T(0), scale);
+  }
+}
+
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
+  if (h->slots == 0) {
+    spmv_empty<T, kScaled><<<persistent_grid((h->rows + 255) / 256, 8), 256, 0, s>>>(
+        h->rows, y, x_next, scale);
+    SPMVK_LAUNCH("spmv_empty");
+    return;
+  }
   constexpr bool f64 = sizeof(T) == 8;
   K2 k = k2_choice();
   if (k == K2::kAuto) k = auto_k2(h, f64);
-  if (k == K2::kWtma && h->group_size <= 256) {
-    launch_wtma_g<T, kScaled, 8, f64 ? 4 : 3, f64 ? 512 : 1024>(h, x, y, x_next, scale, s);
-    return;
-  }
-  if (k == K2::kTma && h->group_size <= 256) {
-    if constexpr (sizeof(T) == 8)
-      launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
-    else
-      launch_tma<T, kScaled, 8, 4, 2048>(h, x, y, x_next, scale, s);
-    return;
-  }
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
   constexpr int U = sizeof(T) == 8 ? 4 : 8;
@@ -487,9 +421,12 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     const char* e = std::getenv("SPMVK_X_PREFETCH");
     return e ? std::atoi(e) : -1;
   }();
-  const bool xpf = xpf_env >= 0 ? xpf_env > 0
-                                : (2 * h->slots <= 11 * h->rows &&
-                                   h->cols * sizeof(T) <= (48ull << 20));
+  // cp.async.bulk.prefetch needs a 16-byte aligned start: an offset view of
+  // x (only 4- or 8-byte aligned) is gathered without the prefetch
+  const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const bool xpf = x_aligned && (xpf_env >= 0 ? xpf_env > 0
+                                              : (2 * h->slots <= 11 * h->rows &&
+                                                 h->cols * sizeof(T) <= (48ull << 20)));
   auto run_grp = [&](auto kern) {
     int per_sm = 0;
     SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
@@ -499,31 +436,6 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               h->columns.p, x, y, x_next, scale,
                               xpf ? static_cast<uint32_t>(h->cols) : 0u);
     SPMVK_LAUNCH("rgcsr_spmv_grp");
-  };
-  // x staged in shared memory per tile (narrow-band matrices)
-  auto run_grpx = [&](auto kern) {
-    {
-      std::lock_guard<std::mutex> lk(h->part_mu);
-      if (!h->tile_cols_dev.p) {
-        const uint32_t tiles = static_cast<uint32_t>((h->rows + 255) / 256);
-        h->tile_cols_dev.alloc(2 * uint64_t(tiles));
-        std::vector<unsigned> init(2 * uint64_t(tiles));
-        for (uint32_t k = 0; k < tiles; ++k) init[2 * k] = 0xffffffffu, init[2 * k + 1] = 0;
-        SPMVK_CUDA(cudaMemcpy(h->tile_cols_dev.p, init.data(), 8ull * tiles,
-                              cudaMemcpyHostToDevice));
-        chunk_column_ranges<<<persistent_grid(tiles, 8), 256>>>(
-            static_cast<uint32_t>(h->rows), G, 256, h->group_pointers.p, h->row_lengths.p,
-            h->columns.p, h->tile_cols_dev.p);
-        SPMVK_LAUNCH("chunk_column_ranges");
-        SPMVK_CUDA(cudaDeviceSynchronize());
-      }
-    }
-    int per_sm = 0;
-    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
-    kern<<<persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
-        static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p, h->row_lengths.p,
-        reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, h->tile_cols_dev.p);
-    SPMVK_LAUNCH("rgcsr_spmv_grpx");
   };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
@@ -551,38 +463,17 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   };
   // the group-uniform walk has no long-row split: matrices with long rows
   // (and, for now, any request on them) take the lite kernel instead
-  if (k >= K2::kGrp4 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
+  if (k >= K2::kGrp6 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
   switch (k) {
     // group-uniform walk: <T, kScaled, U, MINB, kNoLen, kMpf>
-    case K2::kGrp4: run_grp(rgcsr_spmv_grp<T, kScaled, 4, 8, true, false>); break;
     case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
-    case K2::kGrp7: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, false>); break;
     case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true>); break;
     case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
     case K2::kGrp8R64: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
-    case K2::kGrp8Len: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, false, false>); break;
-    case K2::kGrpX:  // plain y only (the scaled / iterated form falls back)
-      if constexpr (!kScaled) run_grpx(rgcsr_spmv_grpx<T, 6, 5, 4096>);
-      else run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>);
-      break;
-    case K2::kGrpX8:
-      if constexpr (!kScaled) run_grpx(rgcsr_spmv_grpx<T, 8, 4, 4096>);
-      else run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>);
-      break;
-    case K2::kPipeHi: run(rgcsr_spmv_pipe<T, kScaled, U, 5>); break;
-    case K2::kPipe8: run(rgcsr_spmv_pipe<T, kScaled, 8, 3>); break;
-    case K2::kLdgPf: run(rgcsr_spmv_ldg<T, kScaled, U, true>); break;
-    case K2::kLdg: run(rgcsr_spmv_ldg<T, kScaled, U, false>); break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
-    case K2::kLiteMpf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, false, true>); break;
-    case K2::kLite8Mpf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, false, true>); break;
-    case K2::kLite8FullMpf: run(rgcsr_spmv_lite<T, kScaled, 8, 8, false, true>); break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
-    case K2::kVec4: run_vec(rgcsr_spmv_vec<T, kScaled, 4, 4>); break;
-    case K2::kLite8Pf: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
-    case K2::kLitePf: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
   }
 }
@@ -599,7 +490,7 @@ void spmv_dot_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
     SPMVK_CUDA(cudaMemsetAsync(dot_out, 0, sizeof(double), s));
     return;
   }
-  if (h->n_long || h->slots * 10 > h->nnz * 11) {
+  if (h->n_long || h->slots == 0 || h->slots * 10 > h->nnz * 11) {
     launch_spmv<double, false>(h, x, y, nullptr, 0.0, s);
     if (spmvk_dot_f64(x + x_offset, y, h->rows, dot_out, s) != SPMVK_OK)
       fail(SPMVK_ECUDA, std::string("spmv_dot: ") + spmvk_last_error());
@@ -612,20 +503,12 @@ void spmv_dot_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
   int per_sm = 0;
   SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
   const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
-  static thread_local DevBuf<double> part;  // per host thread: stream-ordered reuse
-  if (part.n < grid) {
-    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
-    SPMVK_CUDA(cudaStreamIsCapturing(s, &cst));
-    if (cst != cudaStreamCaptureStatusNone)
-      fail(SPMVK_EINVAL, "spmv_dot: first call on this thread is inside a stream capture; "
-                         "call it once eagerly first");
-    part.alloc(static_cast<uint64_t>(sm_count()) * 8 > grid ? sm_count() * 8ull : grid);
-  }
+  double* part = stream_scratch(s, std::max<uint64_t>(grid, sm_count() * 8ull));
   kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
                             h->row_lengths.p, reinterpret_cast<const double*>(h->values.p),
-                            h->columns.p, x, y, x + x_offset, part.p);
+                            h->columns.p, x, y, x + x_offset, part);
   SPMVK_LAUNCH("rgcsr_spmv_dot_grp");
-  rgcsr_dot_finish<<<1, 256, 0, s>>>(part.p, static_cast<int>(grid), dot_out);
+  rgcsr_dot_finish<<<1, 256, 0, s>>>(part, static_cast<int>(grid), dot_out);
   SPMVK_LAUNCH("rgcsr_dot_finish");
 }
 
@@ -1000,11 +883,8 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     K2 k;
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
-                             "' (auto | grp4 | grp6 | grp7 | grp7_mpf | grp8 | grp8_r64 | grp8_len | "
-                             "grpx | grpx8 | "
-                             "lite | lite8 | lite8_full | lite_mpf | lite8_mpf | lite8_full_mpf | "
-                             "vec2 | vec4 | lite_l2pf | lite8_l2pf | pipe | pipe_hi | pipe8 | ldg | "
-                             "ldg_pf | tma | wtma)");
+                             "' (auto | grp6 | grp7_mpf | grp8 | grp8_r64 | lite | lite8 | "
+                             "lite8_full | vec2 | pipe)");
     k2_slot().store(static_cast<int>(k));
   });
 }

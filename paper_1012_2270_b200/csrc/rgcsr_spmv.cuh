@@ -4,24 +4,19 @@
 // (rgcsr.hpp:87-93): acc = ((0 + v0*x0) + v1*x1) + ..., product and sum
 // rounded separately, so y is bitwise spmv_rgcsr's y.  They differ only in
 // how the group-interleaved slots reach the SMs (measured comparison in
-// DESIGN.md §3 and profiles/r01_k2_sweep*.md):
+// DESIGN.md §3 and profiles/r01_k2_sweep*.md; the variants that never won a
+// case -- per-warp / per-CTA TMA bulk-copy rings, L2 bulk prefetch of tiles,
+// x staged in shared memory, the policy-hinted ldg kernels -- were removed in
+// round 2 and their numbers kept in profiles/r02_k2_pruned.md):
 //
-//  * rgcsr_spmv_lite — the default: register-lean thread per row at high
-//    occupancy (below); rgcsr_spmv_long takes the rows past the long-row cut.
+//  * rgcsr_spmv_grp  — group-uniform walk (default without long rows).
+//  * rgcsr_spmv_lite — register-lean thread per row at high occupancy.
+//  * rgcsr_spmv_vec  — 128-bit vector slot loads, R rows per thread.
 //  * rgcsr_spmv_pipe — row- and batch-pipelined thread per row.
-//  * rgcsr_spmv_ldg  — thread per row, slots streamed straight from HBM with
-//    L1-no-allocate / L2-evict-first loads, U-deep batches; with kPrefetch the
-//    next batch's loads are issued before the current batch's x gathers.
-//  * rgcsr_spmv_tma  — persistent CTAs with one producer warp that streams the
-//    CTA's contiguous slab range [gp[g0], gp[g1]) through an NS-stage shared
-//    memory ring with 1D bulk async copies (cp.async.bulk -> UBLKCP,
-//    mbarrier complete_tx), and NW consumer warps, thread per row, reading
-//    their slots from shared memory (stride s, conflict-free) and gathering x
-//    through the read-only path.  Memory-level parallelism then no longer
-//    depends on the consumers' dependent add chains.
+//  * rgcsr_spmv_long_mixed — the rows past the long-row cut (warp per row,
+//    or four rows per warp).
 #pragma once
 #include "common.cuh"
-#include "tma.cuh"
 
 namespace spmvk {
 
@@ -107,29 +102,6 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
   }
 }
 
-// Bulk L2 prefetch (cp.async.bulk.prefetch -> the TMA unit) of the contiguous
-// slot range of 256-row tile `tile`: its groups' slabs [gp[g0], gp[g1]).
-// Used by the lite*_l2pf variants (measured slower; kept for the record).
-template <class T>
-__device__ __forceinline__ void prefetch_tile(uint32_t tile, uint32_t rows, uint32_t G,
-                                              uint32_t groups, const uint32_t* __restrict__ gp,
-                                              const T* __restrict__ values,
-                                              const uint32_t* __restrict__ columns) {
-  const uint32_t r0 = tile * 256;
-  if (r0 >= rows) return;
-  const uint32_t g0 = r0 / G, g1 = min(groups, (min(rows, r0 + 256) + G - 1) / G);
-  const uint64_t s0 = gp[g0], s1 = gp[g1];
-  if (s1 <= s0) return;
-  const uint64_t vb = (s0 * sizeof(T)) & ~15ull, ve = (s1 * sizeof(T) + 15) & ~15ull;
-  const uint64_t cb = (s0 * 4) & ~15ull, ce = (s1 * 4 + 15) & ~15ull;
-  const char* vbase = reinterpret_cast<const char*>(values);
-  const char* cbase = reinterpret_cast<const char*>(columns);
-  for (uint64_t o = vb; o < ve; o += 65536)
-    bulk_prefetch_l2(vbase + o, (uint32_t)min((uint64_t)65536, ve - o));
-  for (uint64_t o = cb; o < ce; o += 65536)
-    bulk_prefetch_l2(cbase + o, (uint32_t)min((uint64_t)65536, ce - o));
-}
-
 // Lean thread-per-row kernel built for occupancy (the default K2): a CTA
 // handles 256-row tiles (CTA-stride), each thread walks its row in U-deep
 // batches with 32-bit strided pointers (no prefetch buffers, no cache-policy
@@ -180,45 +152,18 @@ struct PeerEpi {
   }
 };
 
-template <class T, int U, bool kPrefetchL2, class Epi, bool kMetaPf = false>
+template <class T, int U, class Epi>
 __device__ __forceinline__ void lite_tiles_epi(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
     uint32_t long_cut, const Epi& epi) {
-  if (kPrefetchL2 && threadIdx.x == 0) {
-    const uint32_t groups = (rows + G - 1) / G;
-    if (tile_begin + blockIdx.x < tile_end)
-      prefetch_tile<T>(tile_begin + blockIdx.x, rows, G, groups, gp, values, columns);
-  }
-  uint32_t len_n = 0, base_n = 0;
-  if (kMetaPf) {
-    const uint32_t r0 = (tile_begin + blockIdx.x) * 256 + threadIdx.x;
-    if (tile_begin + blockIdx.x < tile_end && r0 < rows) {
-      len_n = lens[r0];
-      base_n = gp[g_shift >= 0 ? (r0 >> g_shift) : r0 / G];
-    }
-  }
   for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
-    if (kPrefetchL2 && threadIdx.x == 0 && tile + gridDim.x < tile_end)
-      prefetch_tile<T>(tile + gridDim.x, rows, G, (rows + G - 1) / G, gp, values, columns);
     const uint32_t r = tile * 256 + threadIdx.x;
-    uint32_t len, base;
-    if (kMetaPf) {
-      len = len_n;
-      base = base_n;
-      const uint32_t rn = r + gridDim.x * 256;
-      if (tile + gridDim.x < tile_end && rn < rows) {
-        len_n = lens[rn];
-        base_n = gp[g_shift >= 0 ? (rn >> g_shift) : rn / G];
-      }
-    }
     if (r >= rows) continue;
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-    if (!kMetaPf) {
-      len = ld_stream(lens + r);
-      base = ld_stream(gp + g);
-    }
+    uint32_t len = ld_stream(lens + r);
+    const uint32_t base = ld_stream(gp + g);
     // rows past the cut are rgcsr_spmv_long's: predicated to zero slots rather
     // than branched around, so the length and group-pointer loads issue
     // together (a branch on len would let ptxas sink the gp load behind it)
@@ -267,23 +212,23 @@ __device__ __forceinline__ void lite_tiles_epi(
   }
 }
 
-template <class T, bool kScaled, int U, bool kPrefetchL2 = false>
+template <class T, bool kScaled, int U>
 __device__ __forceinline__ void lite_tiles(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
     T* __restrict__ y, T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles_epi<T, U, kPrefetchL2>(tile_begin, tile_end, rows, G, g_shift, gp, lens, values,
+  lite_tiles_epi<T, U>(tile_begin, tile_end, rows, G, g_shift, gp, lens, values,
                                     columns, x, long_cut, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
-template <class T, bool kScaled, int U, int MINB, bool kPrefetchL2 = false, bool kMetaPf = false>
+template <class T, bool kScaled, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles_epi<T, U, kPrefetchL2, StoreEpi<T, kScaled>, kMetaPf>(
+  lite_tiles_epi<T, U, StoreEpi<T, kScaled>>(
       0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns, x, long_cut,
       StoreEpi<T, kScaled>{y, x_next, scale});
 }
@@ -461,62 +406,6 @@ static __global__ void __launch_bounds__(256) rgcsr_dot_finish(const double* __r
   for (int i = threadIdx.x; i < np; i += 256) s += part[i];
   s = block_sum_256(s);
   if (threadIdx.x == 0) *out = s;
-}
-
-// x staged in shared memory (the north star's "x is staged in shared memory
-// when the matrix is banded"): per 256-row tile the CTA copies x[lo..hi] --
-// the tile's column range, tile_cols[2t..2t+1] -- into shared memory with
-// coalesced loads, then the group-uniform walk gathers from there.  Tiles
-// whose range exceeds XCAP elements gather from global memory as usual
-// (uniform per CTA).  Same per-row order -> y bitwise.
-template <class T, int U, int MINB, int XCAP>
-__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grpx(
-    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
-    const uint32_t* __restrict__ lens, const T* __restrict__ values,
-    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    const uint32_t* __restrict__ tile_cols) {
-  __shared__ T xs[XCAP];
-  const bool use_len = !isfinite(__ldg(x));
-  const uint32_t ntiles = (rows + 255) / 256;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t lo = tile_cols[2 * tile], hi = tile_cols[2 * tile + 1];
-    const bool staged = lo <= hi && hi - lo < (uint32_t)XCAP;
-    if (staged)
-      for (uint32_t i = threadIdx.x; i <= hi - lo; i += 256) xs[i] = __ldg(x + lo + i);
-    __syncthreads();
-    const uint32_t r = tile * 256 + threadIdx.x;
-    if (r < rows) {
-      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-      const uint32_t b0 = ld_stream(gp + g), b1 = ld_stream(gp + g + 1);
-      const uint32_t len = use_len ? ld_stream(lens + r) : 0u;
-      const uint32_t s = min(G, rows - g * G);
-      const uint32_t K = (s == G && g_shift >= 0) ? ((b1 - b0) >> g_shift) : (b1 - b0) / s;
-      const uint32_t lim = use_len ? len : K;
-      const uint32_t off = b0 + (r - g * G);
-      T acc = T(0);
-      for (uint32_t j = 0; j < K; j += U) {
-        uint32_t c[U];
-        T v[U], xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool in = j + u < K;
-          v[u] = in ? ld_stream(values + off + (j + u) * s) : T(0);
-          c[u] = in ? ld_stream(columns + off + (j + u) * s) : 0u;
-        }
-        __syncwarp(__activemask());  // scheduling fence (see grp_tiles_epi)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          // pads (column 0) and any column outside the staged range read global x
-          xv[u] = j + u < lim ? (staged && c[u] - lo <= hi - lo ? xs[c[u] - lo] : ld_x(x + c[u]))
-                              : T(0);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
-      }
-      y[r] = acc;
-    }
-    __syncthreads();  // xs is rewritten for the next tile
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -712,73 +601,6 @@ static __global__ void chunk_column_ranges(uint32_t rows, uint32_t G, uint32_t c
   }
 }
 
-template <class T, bool kScaled, int U, bool kPrefetch, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_ldg(
-    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
-    const uint32_t* __restrict__ lens, const T* __restrict__ values,
-    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-    const uint32_t t = r - g * G;
-    const uint32_t s = min(G, rows - g * G);
-    const uint32_t len = lens[r];
-    if (len > long_cut) continue;  // handled by rgcsr_spmv_long
-    const T* __restrict__ vp = values + gp[g] + t;
-    const uint32_t* __restrict__ cp = columns + gp[g] + t;
-    T acc = T(0);
-    const uint32_t full = len / U * U;
-    uint32_t cA[U];
-    T vA[U];
-    if (kPrefetch && full) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        cA[u] = ld_stream(cp + (size_t)u * s, pf);
-        vA[u] = ld_stream(vp + (size_t)u * s, pf);
-      }
-    }
-    uint32_t j = 0;
-    for (; j < full; j += U) {
-      if (!kPrefetch) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cA[u] = ld_stream(cp + (size_t)(j + u) * s, pf);
-          vA[u] = ld_stream(vp + (size_t)(j + u) * s, pf);
-        }
-      }
-      uint32_t cB[U];
-      T vB[U];
-      const bool more = kPrefetch && j + U < full;
-      if (more) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cB[u] = ld_stream(cp + (size_t)(j + U + u) * s, pf);
-          vB[u] = ld_stream(vp + (size_t)(j + U + u) * s, pf);
-        }
-      }
-      T xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cA[u], pl);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(vA[u], xv[u]));
-      if (more) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cA[u] = cB[u];
-          vA[u] = vB[u];
-        }
-      }
-    }
-    for (; j < len; ++j) {
-      const uint32_t c = ld_stream(cp + (size_t)j * s, pf);
-      acc = add_rn(acc, mul_rn(ld_stream(vp + (size_t)j * s, pf), ld_x(x + c, pl)));
-    }
-    y[r] = acc;
-    if (kScaled) x_next[r] = mul_rn(acc, scale);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // rgcsr_spmv_long — the rows longer than kLongRow (power-law tails), one warp
 // per row.  A thread-per-row kernel would serialise a 4096-slot row in one
@@ -964,330 +786,6 @@ __global__ void __launch_bounds__(256) rgcsr_spmv_long_mixed(
     T* __restrict__ y, T* __restrict__ x_next, T scale) {
   long_mixed_epi<T>(n_single, single_rows, n_quad, quads, rows, G, g_shift, gp, lens, values,
                     columns, x, StoreEpi<T, kScaled>{y, x_next, scale});
-}
-
-template <class T, bool kScaled>
-__global__ void __launch_bounds__(256) rgcsr_spmv_long(
-    uint32_t nlong, const uint32_t* __restrict__ long_rows, uint32_t rows, uint32_t G,
-    int g_shift, const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
-    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
-    T* __restrict__ y, T* __restrict__ x_next, T scale) {
-  long_rows_epi<T>(nlong, long_rows, rows, G, g_shift, gp, lens, values, columns, x,
-                   StoreEpi<T, kScaled>{y, x_next, scale});
-}
-
-// ---------------------------------------------------------------------------
-// rgcsr_spmv_wtma — per-warp bulk-copy streams (experimental variant).
-//
-// Every warp owns a contiguous range of "waves" (a wave is the rows one warp
-// covers at once: one group when G >= 32, lane l then holding rows
-// t = l + 32 i, i < R; floor(32/G) groups when G < 32), balanced across warps
-// by slot count with a binary search over the group pointers.  Because the
-// groups of a range are contiguous in memory, the warp's slots form ONE
-// contiguous element range [gp[first], gp[last]); lane 0 streams it through a
-// private NS-stage shared-memory ring of CE-element chunks with 1D bulk async
-// copies (cp.async.bulk -> UBLKCP, mbarrier complete_tx), refilling a stage
-// as soon as the warp has consumed it.  No CTA-wide barrier exists: each warp
-// is its own producer/consumer, so bytes in flight (NS * CE * (S + 4) per
-// warp) no longer depend on registers, row length or the add chains.  Lanes
-// read their slots from shared memory at stride s (conflict-free), gather x
-// through the read-only path in batches, and add in slot order (bitwise the
-// reference).  The next wave's row lengths / group pointers are prefetched.
-template <class T, int NS, int CE, int NW>
-constexpr size_t wtma_smem_bytes() {
-  return (size_t)NW * NS * CE * (sizeof(T) + sizeof(uint32_t)) + (size_t)NW * NS * 8;
-}
-
-// part[i] = first wave of warp i (part[W] = nwaves): slot-balanced split, the
-// smallest wave whose first slot is >= total * i / W.  Computed once per
-// (handle, grid) and cached.
-static __global__ void wave_partition(uint32_t W, uint32_t nwaves, uint32_t gpw, uint32_t groups,
-                               const uint32_t* __restrict__ gp, uint32_t* __restrict__ part) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > W) return;
-  const uint64_t total = gp[groups];
-  if (i == 0 || i == W || total == 0) {
-    part[i] = (i == 0) ? 0 : nwaves;
-    return;
-  }
-  const uint64_t slot = total * i / W;
-  uint32_t lo = 0, hi = nwaves;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (gp[min((uint64_t)mid * gpw, (uint64_t)groups)] < slot) lo = mid + 1; else hi = mid;
-  }
-  part[i] = lo;
-}
-
-template <class T, bool kScaled, int R, int NS, int CE, int NW, int U>
-__global__ void __launch_bounds__(NW * 32, 1) rgcsr_spmv_wtma(
-    uint32_t rows, uint32_t G, uint32_t groups, uint32_t gpw, uint32_t nwaves,
-    const uint32_t* __restrict__ part,
-    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
-    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
-    T* __restrict__ y, T* __restrict__ x_next, T scale) {
-  static_assert(CE % 4 == 0, "chunks must keep 16-byte alignment");
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* vbuf = reinterpret_cast<T*>(smem) + (size_t)warp * NS * CE;
-  uint32_t* cbuf = reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(smem) + (size_t)NW * NS * CE) +
-                   (size_t)warp * NS * CE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint32_t*>(
-                       reinterpret_cast<T*>(smem) + (size_t)NW * NS * CE) + (size_t)NW * NS * CE) +
-                   warp * NS;
-  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-
-  // ---- this warp's wave range (slot-balanced, precomputed by wave_partition)
-  const uint32_t wg = blockIdx.x * NW + warp;
-  auto wave_start = [&](uint32_t w) -> uint64_t {
-    return gp[min((uint64_t)w * gpw, (uint64_t)groups)];
-  };
-  const uint32_t w0 = part[wg], w1 = part[wg + 1];
-  if (w0 >= w1) return;
-
-  const uint64_t s0 = wave_start(w0) & ~3ull;
-  const uint64_t s1 = (wave_start(w1) + 3) & ~3ull;
-  const uint32_t nchunks = (uint32_t)((s1 - s0 + CE - 1) / CE);
-
-  if (lane == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  auto issue = [&](uint32_t k) {
-    const uint32_t stage = k % NS;
-    const uint64_t c = s0 + (uint64_t)k * CE;
-    const uint32_t n = (uint32_t)min((uint64_t)CE, s1 - c);
-    mbar_arrive_expect_tx(&full[stage], n * (uint32_t)(sizeof(T) + sizeof(uint32_t)));
-    bulk_g2s(vbuf + stage * CE, values + c, n * (uint32_t)sizeof(T), &full[stage], pf);
-    bulk_g2s(cbuf + stage * CE, columns + c, n * 4u, &full[stage], pf);
-  };
-  if (lane == 0)
-    for (uint32_t k = 0; k < nchunks && k < (uint32_t)NS; ++k) issue(k);
-
-  // ---- per-lane row state of the current wave
-  const uint32_t wave_rows = G >= 32 ? G : gpw * G;
-  uint32_t row[R], rem[R], s[R];
-  uint64_t off[R];
-  T acc[R];
-  uint32_t nlen[R], nbase[R];  // prefetched metadata of the next wave
-  uint64_t nend = 0, wave_end = 0;
-  auto row_of = [&](uint32_t w, int i) -> uint32_t {
-    const uint32_t lr = lane + 32u * i;
-    return lr < wave_rows ? w * wave_rows + lr : 0xffffffffu;
-  };
-  auto group_of = [&](uint32_t r) -> uint32_t { return r / G; };
-  auto fetch_meta = [&](uint32_t w) {
-    nend = w < w1 ? wave_start(w + 1) : 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint32_t r = row_of(w, i);
-      nlen[i] = 0;
-      nbase[i] = 0;
-      if (w < w1 && r < rows) {
-        nlen[i] = lens[r];
-        nbase[i] = gp[group_of(r)];
-      }
-    }
-  };
-  uint32_t w = w0;
-  auto start_wave = [&]() {
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      row[i] = row_of(w, i);
-      const bool live = row[i] < rows;
-      const uint32_t g = live ? group_of(row[i]) : 0;
-      s[i] = live ? min(G, rows - g * G) : 1;
-      rem[i] = nlen[i];
-      off[i] = (uint64_t)nbase[i] + (live ? row[i] - g * G : 0);
-      acc[i] = T(0);
-    }
-    wave_end = nend;
-    fetch_meta(w + 1);
-  };
-  auto finish_wave = [&]() {
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (row[i] < rows) {
-        y[row[i]] = acc[i];
-        if (kScaled) x_next[row[i]] = mul_rn(acc[i], scale);
-      }
-    ++w;
-  };
-  fetch_meta(w0);
-  start_wave();
-
-  for (uint32_t k = 0; k < nchunks; ++k) {
-    const uint32_t stage = k % NS;
-    mbar_wait(&full[stage], (k / NS) & 1);
-    const uint64_t cbeg = s0 + (uint64_t)k * CE, cend = min(cbeg + CE, s1);
-    const T* vb = vbuf + stage * CE;
-    const uint32_t* cb = cbuf + stage * CE;
-    for (;;) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        uint32_t nb = 0;
-        if (rem[i] && off[i] < cend)  // off >= cbeg, so the distance fits 32 bits
-          nb = min(rem[i], ((uint32_t)(cend - off[i]) + s[i] - 1) / s[i]);
-        uint32_t idx = (uint32_t)(off[i] - cbeg);
-        const uint32_t si = s[i];
-        uint32_t q = 0;
-        for (; q + U <= nb; q += U) {
-          uint32_t cc[U];
-          T vv[U], xv[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            cc[u] = cb[idx + u * si];
-            vv[u] = vb[idx + u * si];
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cc[u], pl);
-#pragma unroll
-          for (int u = 0; u < U; ++u) acc[i] = add_rn(acc[i], mul_rn(vv[u], xv[u]));
-          idx += U * si;
-        }
-        if (q < nb) {  // tail: gather all remaining x first, then add in order
-          uint32_t cc[U];
-          T vv[U], xv[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool ok = q + u < nb;
-            cc[u] = ok ? cb[idx + u * si] : 0;
-            vv[u] = ok ? vb[idx + u * si] : T(0);
-            xv[u] = ok ? ld_x(x + cc[u], pl) : T(0);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (q + u < nb) acc[i] = add_rn(acc[i], mul_rn(vv[u], xv[u]));
-        }
-        rem[i] -= nb;
-        off[i] += (uint64_t)nb * si;
-      }
-      if (w >= w1 || wave_end > cend) break;
-      finish_wave();  // every slot of this wave lies in chunks <= k
-      if (w >= w1) break;
-      start_wave();
-    }
-    __syncwarp();
-    if (lane == 0 && k + NS < nchunks) {
-      // consumed stage -> async-proxy overwrite: order the generic reads first
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + NS);
-    }
-  }
-  while (w < w1) {  // waves whose slots all precede the last chunk end (or are empty)
-    finish_wave();
-    if (w < w1) start_wave();
-  }
-}
-
-// Shared-memory footprint of rgcsr_spmv_tma<T, NW, NS, CE>.
-template <class T, int NS, int CE>
-constexpr size_t tma_smem_bytes() {
-  return (size_t)NS * CE * (sizeof(T) + sizeof(uint32_t)) + 2 * NS * sizeof(uint64_t);
-}
-
-template <class T, bool kScaled, int NW, int NS, int CE>
-__global__ void __launch_bounds__((NW + 1) * 32) rgcsr_spmv_tma(
-    uint32_t rows, uint32_t G, int g_shift, uint32_t groups, uint32_t gpt, uint32_t ntiles,
-    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
-    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
-    T* __restrict__ y, T* __restrict__ x_next, T scale) {
-  static_assert(CE % 4 == 0, "chunks must keep 16-byte alignment");
-  extern __shared__ __align__(128) unsigned char smem[];
-  T* vbuf = reinterpret_cast<T*>(smem);
-  uint32_t* cbuf = reinterpret_cast<uint32_t*>(vbuf + NS * CE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + NS * CE);
-  uint64_t* empty = full + NS;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == NW) {  // ---------------- producer: one elected lane
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
-      for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t g0 = tile * gpt, g1 = min(g0 + gpt, groups);
-        const uint64_t s0 = gp[g0] & ~3ull, s1 = ((uint64_t)gp[g1] + 3) & ~3ull;
-        for (uint64_t c = s0; c < s1; c += CE, ++it) {
-          const uint32_t stage = it % NS, ph = (it / NS) & 1;
-          mbar_wait(&empty[stage], ph ^ 1);
-          const uint32_t n = (uint32_t)min((uint64_t)CE, s1 - c);
-          mbar_arrive_expect_tx(&full[stage], n * (uint32_t)(sizeof(T) + sizeof(uint32_t)));
-          bulk_g2s(vbuf + stage * CE, values + c, n * (uint32_t)sizeof(T), &full[stage], pol);
-          bulk_g2s(cbuf + stage * CE, columns + c, n * 4u, &full[stage], pol);
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers: thread per row of the tile
-  const uint64_t pl = policy_evict_last();
-  constexpr int U = sizeof(T) == 8 ? 4 : 8;
-  uint32_t it = 0;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t g0 = tile * gpt, g1 = min(g0 + gpt, groups);
-    const uint64_t s0 = gp[g0] & ~3ull, s1 = ((uint64_t)gp[g1] + 3) & ~3ull;
-    const uint32_t r = g0 * G + warp * 32 + lane;
-    const bool live = r < min(g1 * G, rows);
-    uint32_t len = 0, s = 1;
-    uint64_t off = 0;
-    if (live) {
-      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-      const uint32_t t = r - g * G;
-      s = min(G, rows - g * G);
-      len = lens[r];
-      off = (uint64_t)gp[g] + t;
-    }
-    uint32_t j = 0;
-    T acc = T(0);
-    for (uint64_t c = s0; c < s1; c += CE, ++it) {
-      const uint32_t stage = it % NS, ph = (it / NS) & 1;
-      mbar_wait(&full[stage], ph);
-      const uint64_t cend = min(c + CE, s1);
-      uint32_t nb = 0;
-      if (j < len && off < cend) nb = min(len - j, (uint32_t)((cend - off + s - 1) / s));
-      const T* vb = vbuf + stage * CE;
-      const uint32_t* cb = cbuf + stage * CE;
-      uint32_t i = (uint32_t)(off - c);
-      uint32_t k = 0;
-      for (; k + U <= nb; k += U) {
-        uint32_t cc[U];
-        T vv[U], xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cc[u] = cb[i + u * s];
-          vv[u] = vb[i + u * s];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + cc[u], pl);
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(vv[u], xv[u]));
-        i += U * s;
-      }
-      for (; k < nb; ++k) {
-        acc = add_rn(acc, mul_rn(vb[i], ld_x(x + cb[i], pl)));
-        i += s;
-      }
-      j += nb;
-      off += (uint64_t)nb * s;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-    }
-    if (live) {
-      y[r] = acc;
-      if (kScaled) x_next[r] = mul_rn(acc, scale);
-    }
-  }
 }
 
 }  // namespace spmvk

@@ -243,13 +243,25 @@ class FusedCgRank:
         from ._lib import lib
         self.slab, self.a, self.f, self.s, self.L = slab, a, fused, stream or None, lib()
         n = slab.rows
-        dev = b.device
-        self.x = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self.r = b.clone() if n else torch.zeros(1, dtype=torch.float64, device=dev)
-        self.q = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
-        self.sc = torch.zeros(6, dtype=torch.float64, device=dev)  # rr pap rrn bb one zero
-        self.sc[4] = 1.0
+        dev = self.dev = b.device
+        # the setup runs on the stream the C calls use (ordered before them)
+        with self._on_stream():
+            self.x = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+            self.r = b.clone() if n else torch.zeros(1, dtype=torch.float64, device=dev)
+            self.q = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+            # rr pap rrn bb | 1.0 0.0: the start step's beta = 0 / 1 (it copies
+            # sc[5] into sc[4], so start() re-seeds both every time)
+            self.sc = torch.zeros(6, dtype=torch.float64, device=dev)
         self.rr, self.pap, self.rrn, self.bb = (self.sc[i:i + 1] for i in range(4))
+
+    def _on_stream(self):
+        import contextlib
+        import torch
+        if not self.s:
+            return contextlib.nullcontext()
+        ext = torch.cuda.ExternalStream(self.s, device=self.dev)
+        ext.wait_stream(torch.cuda.current_stream(self.dev))  # inputs made on torch's stream
+        return torch.cuda.stream(ext)
 
     def _ok(self, rc):
         if rc:
@@ -263,7 +275,10 @@ class FusedCgRank:
         """p = r in every window that reads it (a direction step with beta = 0
         over a zeroed p_old), local dots r.r and b.b into rr / bb."""
         sl = self.slab
-        self.p_current()[sl.row_begin:sl.row_end].zero_()
+        with self._on_stream():
+            self.p_current()[sl.row_begin:sl.row_end].zero_()
+            self.sc[4].fill_(1.0)
+            self.sc[5].fill_(0.0)
         self._ok(self.L.spmvk_dist_cg_direction_f64(
             self.f._d, self.r.data_ptr(), self.sc[4:5].data_ptr(), self.sc[5:6].data_ptr(),
             1 if barrier else 0, self.s))
@@ -523,10 +538,13 @@ class FusedIteratedSpmv:
 
 # ---------------------------------------------------------------- bench (N > 1)
 def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=None,
-                      rg_bytes=None):
+                      rg_bytes=None, config_fn=None, cpu_fn=None, traffic=None):
     """bench.py leg for torchrun N > 1: strong scaling of the iterated SpMV.
     ``clock_cls`` / ``peaks`` / ``rg_bytes`` are bench.py's NVML clock sampler,
-    measured HBM peak and algorithmic-bytes function."""
+    measured HBM peak and algorithmic-bytes function; ``config_fn(n, exchange)``
+    the config dict both bench arms print; ``cpu_fn()`` the CPU reference
+    baseline (rank 0, after the GPU timing); ``traffic`` the committed ncu DRAM
+    bytes of the single-GPU kernel on this workload."""
     import torch
     import torch.distributed as dist
 
@@ -709,9 +727,10 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "description": desc, "format": "rgcsr",
-                       "group_size": G,
-                       "parallelism": (f"row-slab x{world}, halo of x stored into peer windows "
+            "config": (config_fn(world, getattr(args, "exchange", "fused")) if config_fn else
+                       {"workload": args.workload, "description": desc}),
+            "exchange": {"used": exchange,
+                       "how": (f"row-slab x{world}, halo of x stored into peer windows "
                                        "by the SpMV epilogue (NVLink P2P) + device flag barrier"
                                        if exchange == "fused" else
                                        f"row-slab x{world}, NCCL {exchange} of x"),
@@ -723,13 +742,16 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
                        "exchange_fallback": fallback,
                        "shared_gpu": (f"SPMVK_SHARE_GPU=1: all {world} ranks on GPU 0 (gloo "
                                       "plumbing; a correctness run, not a scaling number)"
-                                      if share else None),
-                       "l2": "per-rank slab streamed from HBM each step (no flush)"},
+                                      if share else None)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved and peak else None,
                          "peak_kind": peak_kind, "bytes_per_launch": slab_bytes,
                          "kernel_us": k_s * 1e6, "scope": "rank-0 slab SpMV, max over ranks",
-                         "traffic": None},
+                         "traffic": traffic,
+                         "traffic_note": ("ncu DRAM bytes per launch of the whole-matrix "
+                                          "kernel at N = 1 (profiles/traffic.json); a slab "
+                                          "moves ~1/N of it") if traffic else None},
+            "cpu_baseline": cpu_fn() if cpu_fn else None,
             "e2e": {"value": 2.0 * tot_nnz.item() / e2e_s.item() / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": 8 * me.rows * world,
                     "d2h_bytes_per_step": 8 * me.rows * world,
@@ -739,4 +761,5 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             "gpu_launches": args.steps * (2 if exchange == "fused" and world > 1 else 1),
             "x_bits_checksum": int(sums.sum().item()),
         }), flush=True)
+    dist.barrier()  # the other ranks wait for rank 0's CPU baseline
     dist.destroy_process_group()

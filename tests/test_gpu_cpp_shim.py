@@ -13,7 +13,17 @@ DRIVER = os.path.join(ROOT, "oracle", "_ref", "parity_driver")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.skipif(not os.path.exists(DRIVER), reason="oracle/_ref/parity_driver not built")
+def _driver_fresh():
+    """The driver compiles the header-only shim in; it is only meaningful when
+    built after the last change to the headers it includes."""
+    if not os.path.exists(DRIVER):
+        return False
+    t = os.path.getmtime(DRIVER)
+    heads = [os.path.join(ROOT, "include", h) for h in ("spmvkit_gpu.hpp", "spmvk.h")]
+    return all(os.path.getmtime(h) <= t for h in heads)
+
+
+@pytest.mark.skipif(not _driver_fresh(), reason="oracle/_ref/parity_driver not built from this checkout")
 def test_reference_inputs_through_cpp_shim(cuda):
     r = subprocess.run([DRIVER], capture_output=True, text=True, timeout=600)
     print(r.stdout)

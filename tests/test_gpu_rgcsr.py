@@ -17,9 +17,8 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-VARIANTS = ["auto", "lite", "lite8", "lite8_full", "lite8_l2pf", "lite_l2pf", "vec2", "vec4", "pipe", "pipe_hi", "pipe8",
-            "ldg", "ldg_pf", "tma", "wtma", "lite_mpf", "lite8_mpf", "lite8_full_mpf",
-            "grp4", "grp6", "grp7", "grp7_mpf", "grp8", "grp8_r64", "grp8_len", "grpx", "grpx8"]
+VARIANTS = ["auto", "grp6", "grp7_mpf", "grp8", "grp8_r64", "lite", "lite8", "lite8_full",
+            "vec2", "pipe"]
 
 
 def dev(x):
