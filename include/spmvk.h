@@ -55,6 +55,8 @@ typedef struct spmvk_rgcsr spmvk_rgcsr;
 typedef struct spmvk_hybrid spmvk_hybrid;
 typedef struct spmvk_window spmvk_window;
 typedef struct spmvk_dist spmvk_dist;
+typedef struct spmvk_comm spmvk_comm;           /* an NCCL communicator (one rank) */
+typedef struct spmvk_nccl_iter spmvk_nccl_iter; /* NCCL iterated product of one slab */
 
 /* Thread-local message of the last failing call on this thread. */
 const char* spmvk_last_error(void);
@@ -187,6 +189,8 @@ int spmvk_rgcsr_spmv_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, floa
  * same kernel, x_next[i] = y[i] * scale (x_next may be NULL). */
 int spmvk_rgcsr_spmv_scaled_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
                                 uint64_t ny, double* x_next, double scale, void* stream);
+int spmvk_rgcsr_spmv_scaled_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                                uint64_t ny, float* x_next, float scale, void* stream);
 /* Span overloads on HOST memory: H2D(x), SpMV, D2H(y), synchronous.
  * multiply_add_count (may be NULL) receives the reference's madds count
  * (rgcsr.hpp:72-74: one per stored nonzero). */
@@ -402,6 +406,82 @@ int spmvk_dist_set_timeout_ms(spmvk_dist* d, uint64_t ms);
  * rank) if a barrier of this rank's window timed out, else SPMVK_OK. */
 int spmvk_dist_status(const spmvk_dist* d, void* stream);
 void spmvk_dist_destroy(spmvk_dist* d);
+
+/* ------------------------------------------------------------------ partition planning
+ * contiguous row slabs whose boundaries are multiples of the
+ * group size G, so a slab's RgCSR is exactly the global arrays' slice and
+ * every row keeps the reference's accumulation order.  Pure host code (no
+ * device needed).  `bounds` has parts + 1 entries: slab p = rows
+ * [bounds[p], bounds[p + 1]). */
+typedef enum { SPMVK_EXCHANGE_ALLGATHER = 0, SPMVK_EXCHANGE_HALO = 1 } spmvk_exchange;
+/* Equal slabs of S = ceil(groups / parts) * G rows (*slab_rows = S; the last
+ * slabs may be short or empty): bounds[p] = min(rows, p * S). */
+int spmvk_plan_slabs(uint64_t rows, uint64_t group_size, int parts, uint64_t* bounds,
+                     uint64_t* slab_rows);
+/* Slot-balanced cuts for skewed matrices (the power-law config): cut p is
+ * the first group boundary where the running RgCSR slot count reaches p/parts
+ * of the total.  row_lengths: host array of `rows` entries. */
+int spmvk_plan_slabs_weighted(const uint32_t* row_lengths, uint64_t rows, uint64_t group_size,
+                              int parts, uint64_t* bounds);
+/* Global rows [receive[2q], receive[2q+1]) rank q must hold every step: all
+ * of x (ALLGATHER) or its own rows plus the columns its slab reads (HALO;
+ * column_ranges[2q], [2q+1] = min, max column of slab q, min > max if the
+ * slab has no entries -- spmvk_csr_column_range).  This is what
+ * spmvk_dist_set_rows takes. */
+int spmvk_plan_receive(int parts, const uint64_t* bounds, const uint64_t* column_ranges, int mode,
+                       uint64_t* receive);
+/* Halo lists of `rank` (arrays of up to parts - 1 triples, ascending peer):
+ * recv[3k..3k+2] = (peer, c0, c1): columns [c0, c1) this slab reads that the
+ * peer owns; send[...] = (peer, c0, c1): this slab's rows the peer reads. */
+int spmvk_plan_halo(int rank, int parts, const uint64_t* bounds, const uint64_t* column_ranges,
+                    uint64_t* recv, int* n_recv, uint64_t* send, int* n_send);
+
+/* ------------------------------------------------------------------ NCCL iterated product
+ * x_{k+1} = (A_slab x_k) * scale per rank (scale fused into
+ * the SpMV epilogue), then the x exchange over NCCL: an in-place
+ * ncclAllGather of every rank's slab (equal slabs from spmvk_plan_slabs), or
+ * grouped ncclSend / ncclRecv of only the column ranges each slab reads
+ * (HALO).  Stream ordered, double-buffered x; the iterate is bitwise the
+ * single-GPU iterate.  NCCL is bound at run time (dlopen libnccl.so.2 or
+ * $SPMVK_NCCL_LIB); SPMVK_ENCCL if it is missing or a call fails.
+ *
+ * Communicators: one process per GPU -> rank 0 calls spmvk_nccl_unique_id,
+ * the 128 bytes travel out of band (MPI, a file, torch.distributed), every
+ * rank calls spmvk_comm_init_rank (ncclCommInitRank).  One process driving
+ * several GPUs -> spmvk_comm_init_all (ncclCommInitAll); it must then bracket
+ * the per-rank calls of one step with spmvk_nccl_group_start / _end. */
+#define SPMVK_NCCL_ID_BYTES 128
+int spmvk_nccl_version(int* version);
+int spmvk_nccl_unique_id(unsigned char* id_out);
+int spmvk_comm_init_rank(const unsigned char* id, int world, int rank, int device,
+                         spmvk_comm** out);
+/* out: ndev handles, rank i on devices[i] (devices NULL -> 0..ndev-1). */
+int spmvk_comm_init_all(int ndev, const int* devices, spmvk_comm** out);
+int spmvk_comm_info(const spmvk_comm* c, int* rank, int* world, int* device);
+void spmvk_comm_destroy(spmvk_comm* c);
+int spmvk_nccl_group_start(void);
+int spmvk_nccl_group_end(void);
+/* Collective over the communicator (every rank calls it): this rank's slab =
+ * global rows [row_begin, row_end) with `slab` its RgCSR (global columns), n
+ * the global length of x.  ALLGATHER needs row_begin = rank * slab_rows (the
+ * spmvk_plan_slabs layout); HALO takes any contiguous slabs in rank order.
+ * The ranks' plans (rows, column ranges) are exchanged with one ncclAllGather. */
+int spmvk_nccl_iter_create(spmvk_comm* comm, const spmvk_rgcsr* slab, uint64_t row_begin,
+                           uint64_t row_end, uint64_t slab_rows, uint64_t n, int mode,
+                           spmvk_nccl_iter** out);
+/* Device pointer (and length) of x buffer 0 / 1; write x_0 into the buffer
+ * spmvk_nccl_iter_current names before the first step. */
+int spmvk_nccl_iter_x(const spmvk_nccl_iter* it, int buffer, void** out, uint64_t* length);
+int spmvk_nccl_iter_current(const spmvk_nccl_iter* it, int* buffer);
+/* Entries of x this rank receives per step (halo: the columns it reads from
+ * peers; all-gather: the other ranks' slabs). */
+int spmvk_nccl_iter_halo_entries(const spmvk_nccl_iter* it, uint64_t* entries);
+/* One step: y (slab-local, device) = A_slab x[cur]; x[1-cur] gets this slab's
+ * x_next = y * scale and, after the exchange, every entry this rank reads;
+ * cur flips. */
+int spmvk_nccl_iter_step_f64(spmvk_nccl_iter* it, double scale, double* y, void* stream);
+int spmvk_nccl_iter_step_f32(spmvk_nccl_iter* it, float scale, float* y, void* stream);
+void spmvk_nccl_iter_destroy(spmvk_nccl_iter* it);
 
 /* ------------------------------------------------------------------ host generators
  * Seeded, platform-independent generators (std::mt19937_64 draws, the

@@ -350,6 +350,8 @@ def R():
             "ref_slabs_spmv": (ci, [vp, vp, vp]),
             "ref_slabs_spmv_serial": (ci, [vp, vp, vp]),
             "ref_slabs_free": (None, [vp]),
+            "ref_slabs_rgcsr_part": (ci, [vp, u64, vp, vp, vp, vp, vp]),
+            "ref_slabs_count": (u64, [vp]),
             "ref_mm_parse": (ci, [C.c_char_p, u64, pp, C.POINTER(C.c_uint64)]),
             "ref_mm_write": (u64, [vp, C.c_char_p, u64]),
         }
@@ -502,3 +504,57 @@ class RefMatrix:
         if getattr(self, "h", None) and self.h.value and _R is not None:
             _R.ref_tm_free(self.h)
             self.h = C.c_void_p()
+
+
+class RefSlabs:
+    """The reference's own templates over group-aligned row slabs (one
+    std::thread each in spmv(); in sequence in spmv_serial()), built from a
+    RefMatrix: fmt 0 = spmv_csr, 1 = spmv_rgcsr (group size G), 2 =
+    spmv_hybrid.  Bitwise equal to one thread (every row keeps its order)."""
+
+    def __init__(self, ref: RefMatrix, fmt=1, G=32, prec=8, threads=None, k1=-1):
+        self.h = C.c_void_p()
+        self.prec, self.rows, self.cols = prec, ref.rows, ref.cols
+        threads = threads or len(os.sched_getaffinity(0)) or 1
+        _rcheck(R().ref_slabs_build(ref.h, fmt, G, k1, prec, threads, C.byref(self.h)))
+
+    def _dt(self):
+        return np.float64 if self.prec == 8 else np.float32
+
+    def spmv(self, x, y=None):
+        x = np.ascontiguousarray(x, self._dt())
+        y = np.empty(self.rows, self._dt()) if y is None else y
+        _rcheck(R().ref_slabs_spmv(self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def spmv_serial(self, x, y=None):
+        x = np.ascontiguousarray(x, self._dt())
+        y = np.empty(self.rows, self._dt()) if y is None else y
+        _rcheck(R().ref_slabs_spmv_serial(self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def __len__(self):
+        return int(R().ref_slabs_count(self.h))
+
+    def rgcsr_part(self, t, arrays=True):
+        """(row_begin, row_end, dict of the slab's four reference arrays)."""
+        info = np.zeros(4, np.uint64)
+        _rcheck(R().ref_slabs_rgcsr_part(self.h, t, _ptr(info), None, None, None, None))
+        r0, r1, slots, groups = (int(v) for v in info)
+        if not arrays:
+            return r0, r1, {"slots": slots, "groups": groups}
+        out = dict(values=np.empty(slots, self._dt()), columns=np.empty(slots, np.uint32),
+                   group_pointers=np.empty(groups + 1, np.uint32),
+                   row_lengths=np.empty(r1 - r0, np.uint32))
+        _rcheck(R().ref_slabs_rgcsr_part(self.h, t, _ptr(info), _ptr(out["values"]),
+                                         _ptr(out["columns"]), _ptr(out["group_pointers"]),
+                                         _ptr(out["row_lengths"])))
+        return r0, r1, out
+
+    def free(self):
+        if self.h and self.h.value and _R is not None:
+            _R.ref_slabs_free(self.h)
+        self.h = C.c_void_p()
+
+    def __del__(self):
+        self.free()

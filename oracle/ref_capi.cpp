@@ -522,6 +522,35 @@ int ref_slabs_spmv_serial(const void* h, const void* x, void* y) {
   });
 }
 
+// Slab t of an RgCSR slab set (fmt 1): info[0..3] = row_begin, row_end,
+// slots, groups; then (when the pointers are non-null) the reference's four
+// arrays of that slab, so a config-scale comparison needs one slab at a time.
+int ref_slabs_rgcsr_part(const void* h, uint64_t t, uint64_t* info, void* values,
+                         uint32_t* columns, uint32_t* group_pointers, uint32_t* row_lengths) {
+  return guard([&] {
+    const auto* s = static_cast<const RefSlabs*>(h);
+    if (s->fmt != 1) throw std::invalid_argument("ref_slabs_rgcsr_part: not an RgCSR slab set");
+    if (t + 1 >= s->row_begin.size()) throw std::invalid_argument("ref_slabs_rgcsr_part: slab");
+    auto put = [&](const auto& a) {
+      info[0] = s->row_begin[t];
+      info[1] = s->row_begin[t + 1];
+      info[2] = a.values.size();
+      info[3] = a.group_pointers.size() - 1;
+      if (values) std::copy(a.values.begin(), a.values.end(),
+                            static_cast<typename std::decay_t<decltype(a.values)>::value_type*>(values));
+      if (columns) std::copy(a.columns.begin(), a.columns.end(), columns);
+      if (group_pointers) std::copy(a.group_pointers.begin(), a.group_pointers.end(), group_pointers);
+      if (row_lengths) std::copy(a.row_lengths.begin(), a.row_lengths.end(), row_lengths);
+    };
+    if (s->prec == 4) put(s->rf[t]);
+    else put(s->rd[t]);
+  });
+}
+
+uint64_t ref_slabs_count(const void* h) {
+  return static_cast<const RefSlabs*>(h)->row_begin.size() - 1;
+}
+
 void ref_slabs_free(void* h) { delete static_cast<RefSlabs*>(h); }
 
 }  // extern "C"

@@ -116,6 +116,27 @@ SIGNATURES = {
     "spmvk_dist_step_f32": (cint, [vp, vp, C.c_float, vp, cint, vp]),
     "spmvk_dist_cg_direction_f64": (cint, [vp, vp, vp, vp, C.c_int, vp]),
     "spmvk_dist_current": (cint, [vp, C.POINTER(cint)]),
+    "spmvk_rgcsr_spmv_scaled_f32": (cint, [vp, vp, u64, vp, u64, vp, C.c_float, vp]),
+    "spmvk_plan_slabs": (cint, [u64, u64, cint, u64p, u64p]),
+    "spmvk_plan_slabs_weighted": (cint, [vp, u64, u64, cint, u64p]),
+    "spmvk_plan_receive": (cint, [cint, u64p, u64p, cint, u64p]),
+    "spmvk_plan_halo": (cint, [cint, cint, u64p, u64p, u64p, C.POINTER(cint), u64p,
+                                C.POINTER(cint)]),
+    "spmvk_nccl_version": (cint, [C.POINTER(cint)]),
+    "spmvk_nccl_unique_id": (cint, [vp]),
+    "spmvk_comm_init_rank": (cint, [vp, cint, cint, cint, C.POINTER(vp)]),
+    "spmvk_comm_init_all": (cint, [cint, vp, vp]),
+    "spmvk_comm_info": (cint, [vp, C.POINTER(cint), C.POINTER(cint), C.POINTER(cint)]),
+    "spmvk_comm_destroy": (None, [vp]),
+    "spmvk_nccl_group_start": (cint, []),
+    "spmvk_nccl_group_end": (cint, []),
+    "spmvk_nccl_iter_create": (cint, [vp, vp, u64, u64, u64, u64, cint, C.POINTER(vp)]),
+    "spmvk_nccl_iter_x": (cint, [vp, cint, C.POINTER(vp), u64p]),
+    "spmvk_nccl_iter_current": (cint, [vp, C.POINTER(cint)]),
+    "spmvk_nccl_iter_halo_entries": (cint, [vp, u64p]),
+    "spmvk_nccl_iter_step_f64": (cint, [vp, C.c_double, vp, vp]),
+    "spmvk_nccl_iter_step_f32": (cint, [vp, C.c_float, vp, vp]),
+    "spmvk_nccl_iter_destroy": (None, [vp]),
     "spmvk_dist_set_timeout_ms": (cint, [vp, u64]),
     "spmvk_dist_status": (cint, [vp, vp]),
     "spmvk_dist_destroy": (None, [vp]),

@@ -851,6 +851,17 @@ int spmvk_rgcsr_spmv_scaled_f64(const spmvk_rgcsr* h, const double* x, uint64_t 
   });
 }
 
+int spmvk_rgcsr_spmv_scaled_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx, float* y,
+                                uint64_t ny, float* x_next, float scale, void* stream) {
+  return guarded([&] {
+    check_spmv_args<float>(h, nx, ny);
+    if (x_next)
+      launch_spmv<float, true>(h, x, y, x_next, scale, as_stream(stream));
+    else
+      launch_spmv<float, false>(h, x, y, nullptr, 0.0f, as_stream(stream));
+  });
+}
+
 int spmvk_rgcsr_spmv_host_f64(const spmvk_rgcsr* h, const double* x, uint64_t nx, double* y,
                               uint64_t ny, uint64_t* multiply_add_count) {
   return guarded([&] { spmv_host<double>(h, x, nx, y, ny, multiply_add_count); });

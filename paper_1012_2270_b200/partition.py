@@ -44,54 +44,63 @@ class Slab:
         return self.row_end - self.row_begin
 
 
+def _u64(values):
+    import ctypes as C
+    vals = list(values)
+    return (C.c_uint64 * max(1, len(vals)))(*vals)
+
+
+def _plan_check(rc):
+    if rc:
+        from . import spmvkit as sk
+        sk._check(rc)
+
+
 def slab_bounds(num_rows: int, group_size: int, parts: int) -> List[Slab]:
-    """Equal, group-aligned slabs: S = ceil(groups / P) * G rows each."""
+    """Equal, group-aligned slabs: S = ceil(groups / P) * G rows each
+    (spmvk_plan_slabs, csrc/nccl_dist.cu)."""
+    import ctypes as C
+
+    from ._lib import lib
     if group_size <= 0 or parts <= 0:
         raise ValueError("group size and part count must be positive")
-    groups = (num_rows + group_size - 1) // group_size
-    per = (groups + parts - 1) // parts
-    S = per * group_size
-    out = []
-    for p in range(parts):
-        b = min(num_rows, p * S)
-        e = min(num_rows, (p + 1) * S)
-        out.append(Slab(p, b, e, S))
-    return out
+    b = _u64([0] * (parts + 1))
+    S = C.c_uint64()
+    _plan_check(lib().spmvk_plan_slabs(num_rows, group_size, parts, b, C.byref(S)))
+    return [Slab(p, int(b[p]), int(b[p + 1]), int(S.value)) for p in range(parts)]
 
 
 def weighted_slab_bounds(row_lengths: Sequence[int], group_size: int, parts: int) -> List[tuple]:
     """Group-aligned cuts balancing stored slots (for skewed matrices such as
     the power-law config): cut p sits at the first group boundary where the
-    running slot count reaches p/P of the total.  Returns [(r0, r1)]."""
-    lens = np.asarray(row_lengths, dtype=np.int64)
-    n = lens.size
-    G = group_size
-    groups = (n + G - 1) // G
-    pad = np.zeros(groups * G, np.int64)
-    pad[:n] = lens
-    width = pad.reshape(groups, G).max(axis=1)
-    s = np.minimum(G, n - np.arange(groups) * G)
-    slots = np.cumsum(width * s)
-    total = int(slots[-1]) if groups else 0
-    cuts = [0]
-    for p in range(1, parts):
-        g = int(np.searchsorted(slots, total * p / parts, side="left")) + 1 if total else 0
-        cuts.append(min(n, max(cuts[-1], g * G)))
-    cuts.append(n)
-    return list(zip(cuts, cuts[1:]))
+    running slot count reaches p/P of the total (spmvk_plan_slabs_weighted).
+    Returns [(r0, r1)]."""
+    from ._lib import lib
+    lens = np.ascontiguousarray(row_lengths, dtype=np.uint32)
+    b = _u64([0] * (parts + 1))
+    _plan_check(lib().spmvk_plan_slabs_weighted(lens.ctypes.data if lens.size else None,
+                                                lens.size, group_size, parts, b))
+    return [(int(b[p]), int(b[p + 1])) for p in range(parts)]
 
 
 def halo_plan(slab: Slab, column_min: int, column_max: int, slabs: Sequence[Slab]):
     """Ranks whose x slab intersects [column_min, column_max] of this slab's
-    columns and the intersecting ranges: [(rank, c0, c1)] excluding self."""
-    plan = []
-    for s in slabs:
-        if s.rank == slab.rank or s.rows == 0:
-            continue
-        c0, c1 = max(column_min, s.row_begin), min(column_max + 1, s.row_end)
-        if c0 < c1:
-            plan.append((s.rank, c0, c1))
-    return plan
+    columns and the intersecting ranges: [(rank, c0, c1)] excluding self
+    (the receive list of spmvk_plan_halo)."""
+    import ctypes as C
+
+    from ._lib import lib
+    P = len(slabs)
+    bounds = _u64([s.row_begin for s in slabs] + [slabs[-1].row_end])
+    ranges = [(1, 0)] * P
+    ranges[slab.rank] = (column_min, column_max)
+    cr = _u64([v for r in ranges for v in r])
+    recv, send = _u64([0] * (3 * P)), _u64([0] * (3 * P))
+    nr, ns = C.c_int(), C.c_int()
+    _plan_check(lib().spmvk_plan_halo(slab.rank, P, bounds, cr, recv, C.byref(nr), send,
+                                      C.byref(ns)))
+    return [(int(recv[3 * k]), int(recv[3 * k + 1]), int(recv[3 * k + 2]))
+            for k in range(nr.value)]
 
 
 class IteratedSpmv:
@@ -385,19 +394,16 @@ def fused_receive_ranges(slabs: Sequence[Slab], ranges, mode: str) -> List[tuple
     """Global rows [lo, hi) each rank's window must receive every step of the
     fused path (spmvk_dist_set_rows): the whole x for "allgather"; for "halo"
     the span of its own slab and the columns its slab reads (``ranges[q]`` =
-    (cmin, cmax), cmin > cmax for a slab without entries)."""
-    n = max((s.row_end for s in slabs), default=0)
-    out = []
-    for s in slabs:
-        if mode == "allgather":
-            out.append((0, n))
-            continue
-        cmin, cmax = ranges[s.rank]
-        lo, hi = s.row_begin, s.row_end
-        if cmin <= cmax:
-            lo, hi = min(lo, cmin), max(hi, cmax + 1)
-        out.append((lo, hi) if lo < hi else (0, 0))
-    return out
+    (cmin, cmax), cmin > cmax for a slab without entries).  spmvk_plan_receive."""
+    from ._lib import lib
+    P = len(slabs)
+    if mode not in ("allgather", "halo"):
+        raise ValueError(f"unknown exchange mode {mode!r}")
+    bounds = _u64([s.row_begin for s in slabs] + [slabs[-1].row_end if slabs else 0])
+    cr = _u64([v for r in (ranges if mode == "halo" else [(1, 0)] * P) for v in r])
+    out = _u64([0] * (2 * P))
+    _plan_check(lib().spmvk_plan_receive(P, bounds, cr, 0 if mode == "allgather" else 1, out))
+    return [(int(out[2 * q]), int(out[2 * q + 1])) for q in range(P)]
 
 
 def simulate_fused_routing(slabs, receive, slab_matvec, x0, steps: int):
@@ -536,6 +542,119 @@ class FusedIteratedSpmv:
             self._d = None
 
 
+class NcclComm:
+    """spmvk_comm: an NCCL communicator made by the C-ABI (ncclCommInitRank
+    with the 128-byte unique id, or ncclCommInitAll via ``init_all``)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        buf = (C.c_ubyte * 128)()
+        sk._check(lib().spmvk_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def init_rank(cls, uid: bytes, world: int, rank: int, device: int) -> "NcclComm":
+        import ctypes as C
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        h = C.c_void_p()
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        sk._check(lib().spmvk_comm_init_rank(buf, world, rank, device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def init_all(cls, devices) -> list:
+        import ctypes as C
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        n = len(devices)
+        hs = (C.c_void_p * n)()
+        sk._check(lib().spmvk_comm_init_all(n, (C.c_int * n)(*devices), hs))
+        return [cls(C.c_void_p(h)) for h in hs]
+
+    def close(self):
+        if self._h:
+            from ._lib import lib
+            lib().spmvk_comm_destroy(self._h)
+            self._h = None
+
+
+class NcclIteratedSpmv:
+    """The iterated product with the x exchange over NCCL, all in the C-ABI
+    (spmvk_nccl_iter_*, csrc/nccl_dist.cu): scaled slab SpMV, then an in-place
+    ncclAllGather ("allgather", equal slabs) or grouped ncclSend/ncclRecv of
+    the column ranges each slab reads ("halo").  Creating it is collective."""
+
+    def __init__(self, comm: NcclComm, slab: Slab, a, n: int, mode: str, stream: int,
+                 scale: float = 0.0625):
+        import ctypes as C
+
+        import torch
+
+        from . import spmvkit as sk
+        from ._lib import lib
+        self._L, self.slab, self.a, self.stream, self.scale = lib(), slab, a, stream, scale
+        self.num_cols = a.num_cols
+        h = C.c_void_p()
+        sk._check(self._L.spmvk_nccl_iter_create(comm._h, a._h, slab.row_begin, slab.row_end,
+                                                 slab.pad_rows, n,
+                                                 0 if mode == "allgather" else 1, C.byref(h)))
+        self._h = h
+        self.xbuf = []
+        for b in range(2):
+            p, ln = C.c_void_p(), C.c_uint64()
+            sk._check(self._L.spmvk_nccl_iter_x(h, b, C.byref(p), C.byref(ln)))
+            self.xbuf.append(torch.as_tensor(
+                _DevArray(p.value, ln.value, "<f8" if a.precision == 8 else "<f4"), device="cuda"))
+        dt = torch.float64 if a.precision == 8 else torch.float32
+        self.y = torch.zeros(max(slab.rows, 1), dtype=dt, device="cuda")
+        self._step = self._L.spmvk_nccl_iter_step_f64 if a.precision == 8 else \
+            self._L.spmvk_nccl_iter_step_f32
+
+    @property
+    def cur(self) -> int:
+        import ctypes as C
+        c = C.c_int()
+        self._L.spmvk_nccl_iter_current(self._h, C.byref(c))
+        return c.value
+
+    @property
+    def x(self):
+        return self.xbuf
+
+    @property
+    def x_current(self):
+        return self.xbuf[self.cur][: self.num_cols]
+
+    def set_x(self, x_full):
+        self.xbuf[self.cur][: x_full.numel()].copy_(x_full)
+
+    def halo_entries(self) -> int:
+        import ctypes as C
+        v = C.c_uint64()
+        self._L.spmvk_nccl_iter_halo_entries(self._h, C.byref(v))
+        return v.value
+
+    def step(self):
+        from . import spmvkit as sk
+        sk._check(self._step(self._h, self.scale, self.y.data_ptr(), self.stream))
+
+    def close(self):
+        if self._h:
+            self.xbuf = []
+            self._L.spmvk_nccl_iter_destroy(self._h)
+            self._h = None
+
+
 # ---------------------------------------------------------------- bench (N > 1)
 def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=None,
                       rg_bytes=None, config_fn=None, cpu_fn=None, traffic=None):
@@ -643,12 +762,18 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             if win is not None:
                 win.close()
             exchange = "halo"
+    comm = None
     if exchange == "fused":
         pass
-    elif exchange == "halo":
-        it = HaloIteratedSpmv(me, slabs, ranges, a.num_cols, slab_spmv, p2p, x0)
-    else:
-        it = IteratedSpmv(me, a.num_cols, world, slab_spmv, all_gather, x0)
+    elif share:  # gloo plumbing: the torch.distributed forms of the exchanges
+        it = (HaloIteratedSpmv(me, slabs, ranges, a.num_cols, slab_spmv, p2p, x0)
+              if exchange == "halo" else IteratedSpmv(me, a.num_cols, world, slab_spmv,
+                                                      all_gather, x0))
+    else:  # NCCL driven from the C-ABI (spmvk_comm_init_rank + spmvk_nccl_iter_*)
+        uid = [NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NcclComm.init_rank(uid[0], world, rank, local)
+        it = NcclIteratedSpmv(comm, me, a, slabs[-1].row_end, exchange, sp)
     with torch.cuda.stream(stream):
         it.set_x(x0)
     stream.synchronize()
@@ -674,14 +799,14 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     # iterations (bitwise across P: the slab arrays are global slices and
     # every row keeps the reference's order) -- taken before the e2e leg,
     # which re-uploads each rank's own x slab only
-    xf = it.x[: a.num_cols] if exchange == "allgather" else it.x_current
+    xf = it.x[: a.num_cols] if isinstance(it, IteratedSpmv) else it.x_current
     # order-independent bit checksum: wrapping int64 sum of the raw bits
     part_sum = xf[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
     sums = gather_flat(part_sum)
     tot_nnz = reduce_scalar(float(nnz_local), dist.ReduceOp.SUM)
 
     # kernel-only time of this rank's slab SpMV (roofline of the dominant kernel)
-    xs = (it.x[: a.num_cols] if exchange == "allgather" else it.x_current).clone()
+    xs = (it.x[: a.num_cols] if isinstance(it, IteratedSpmv) else it.x_current).clone()
     ys = torch.empty(max(a.num_rows, 1), dtype=torch.float64, device="cuda")
     xn = torch.empty_like(ys)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -706,7 +831,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         with torch.cuda.stream(stream):
-            cur = it.x if exchange == "allgather" else it.x[it.cur]
+            cur = it.x if isinstance(it, IteratedSpmv) else it.x[it.cur]
             cur[me.row_begin:me.row_end].copy_(xh, non_blocking=True)
         it.step()
         with torch.cuda.stream(stream):
@@ -718,7 +843,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     if rank == 0:
         step_ms = ms.item() / args.steps
         value = 2.0 * tot_nnz.item() / (step_ms * 1e-3) / 1e9
-        halo = it.halo_entries() if exchange in ("halo", "fused") else None
+        halo = it.halo_entries() if hasattr(it, "halo_entries") else None
         k_s = kern_ms.item() * 1e-3
         achieved = slab_bytes / k_s / 1e9 if slab_bytes else None
         peak, peak_kind = peaks if peaks else (None, None)
@@ -762,4 +887,8 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             "x_bits_checksum": int(sums.sum().item()),
         }), flush=True)
     dist.barrier()  # the other ranks wait for rank 0's CPU baseline
+    if hasattr(it, "close"):
+        it.close()
+    if comm is not None:
+        comm.close()
     dist.destroy_process_group()

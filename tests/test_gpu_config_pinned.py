@@ -1,0 +1,199 @@
+"""Config-scale parity pinned to the reference itself (not to this repo).
+
+* Config 5 (BASELINE configs[4], 3D 7-point 512^3, 937,951,232 nnz, fp64,
+  G = 32) against the UNMODIFIED reference compiled in place (oracle/_ref):
+  the converted RgCSR arrays, compared slab by slab with the reference's own
+  build_rgcsr of each group-aligned slab (rgcsr.hpp:38-70); the full y of one
+  SpMV (rgcsr.hpp:75-97, reference on all host threads as row slabs, bitwise
+  equal to one thread); and x after 100 iterations of x <- (A x) * 2^-4,
+  for the single-GPU scaled kernel AND the P = 1 fused distributed step.
+* Config 3 (power-law, 8M rows, 128 M nnz) at full size: the complete
+  RgCSR G = 32 arrays and Hybrid ELL/COO arrays and both y against the
+  plain-C oracle (pinned to the reference by tests/test_oracle_pinned.py),
+  fp64 and fp32.
+* Config 2 (27-point 128^3) at G = 64, 128, 256 (G = 32 is in
+  test_gpu_rgcsr.py for every kernel variant).
+* Config 4: a 20-seed subset of the 200-matrix sweep (every class, 10^4 to
+  1.5 * 10^6 rows) -- every format's arrays and y against the oracle.
+
+Bar: bitwise (integers, values and y), stronger than north_star's 1e-12 /
+1e-5 relative L2.  These need tens of GB of host memory and a few minutes.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from helpers import HY_KEYS, RG_KEYS, bitwise
+from paper_1012_2270_b200 import generators as gen
+from paper_1012_2270_b200 import partition as pt
+from paper_1012_2270_b200 import spmvkit as sk
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+needs_ref = pytest.mark.skipif(not orc.ref_available(),
+                               reason="oracle/_ref (the reference compiled in place) not built")
+SHAPES = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "shapes.json")))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def product_csr(om: orc.Csr, prec=8):
+    """The product's device CSR of exactly the oracle's host arrays."""
+    return sk.build_csr(sk.TripletMatrix(om.rows, om.cols, om.rp, om.col, om.val, validate=False),
+                        prec)
+
+
+@needs_ref
+def test_config5_7pt_512_vs_reference(cuda):
+    n, G, iters = 512, 32, 100
+    om = orc.stencil(7, n)
+    N = om.rows
+    assert om.nnz == 937_951_232
+    csr = product_csr(om)
+    ref = orc.RefMatrix.from_csr(om)
+    del om
+    slabs = orc.RefSlabs(ref, fmt=1, G=G, prec=8)
+    del ref
+    a = sk.build_rgcsr(csr, G)
+    assert a.slot_count() == 938_475_520
+    # converted arrays: the product's global build, slab by slab against the
+    # reference's build of the same group-aligned slab (gp rebased)
+    got = a.to_host()
+    for t in range(len(slabs)):
+        r0, r1, want = slabs.rgcsr_part(t)
+        g0, g1 = r0 // G, (r1 + G - 1) // G
+        gp = got["group_pointers"]
+        s0, s1 = int(gp[g0]), int(gp[g1])
+        assert bitwise((gp[g0:g1 + 1] - gp[g0]).astype(np.uint32), want["group_pointers"]), t
+        assert bitwise(got["row_lengths"][r0:r1], want["row_lengths"]), t
+        assert bitwise(got["columns"][s0:s1], want["columns"]), t
+        assert bitwise(got["values"][s0:s1], want["values"]), t
+    del got
+    # one SpMV: full y
+    xh = orc.random_vector(N, 1)
+    x = dev(xh)
+    y = sk.spmv_rgcsr(a, x).cpu().numpy()
+    assert bitwise(y, slabs.spmv(xh))
+    # 100 iterations of x <- (A x) * 2^-4 (exact power-of-two scale)
+    xr = xh.copy()
+    for _ in range(iters):
+        xr = slabs.spmv(xr) * 0.0625
+    slabs.free()
+    from paper_1012_2270_b200._lib import lib
+    L = lib()
+    xs = [x.clone(), torch.empty_like(x)]
+    yd = torch.empty_like(x)
+    for k in range(iters):
+        sk._check(L.spmvk_rgcsr_spmv_scaled_f64(a._h, xs[k % 2].data_ptr(), N, yd.data_ptr(), N,
+                                                xs[1 - k % 2].data_ptr(), 0.0625, None))
+    assert bitwise(xs[iters % 2].cpu().numpy(), xr), "single-GPU iterate"
+    del xs, yd
+    # the same iterate through the fused distributed step at P = 1
+    sl = pt.slab_bounds(N, G, 1)[0]
+    win = pt.ExchangeWindow(N, 8)
+    s = torch.cuda.current_stream().cuda_stream
+    it = pt.FusedIteratedSpmv(sl, [(0, N)], a, win, 1, s, local_windows=[win], barrier=False)
+    it.set_x(x)
+    for _ in range(iters):
+        it.step()
+    torch.cuda.synchronize()
+    assert bitwise(it.x_current[:N].cpu().numpy(), xr), "fused P = 1 iterate"
+    it.close()
+    win.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_config3_powerlaw_8M_arrays_vs_oracle(cuda, prec):
+    e = SHAPES["powerlaw_8M"]
+    om = orc.powerlaw(8_000_000, 7)
+    assert om.nnz == e["nnz"]
+    csr = product_csr(om, prec)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    # RgCSR G = 32: 563,945,728 slots
+    a = sk.build_rgcsr(csr, 32, prec)
+    want = orc.build_rgcsr(om, 32, prec)
+    assert a.slot_count() == e["rg32"]["slots"] == want["values"].size
+    got = a.to_host()
+    for k in RG_KEYS:
+        assert bitwise(got[k], want[k]), k
+    del got
+    y = sk.spmv_rgcsr(a, dev(x)).cpu().numpy()
+    assert bitwise(y, orc.spmv_rgcsr(want, x)[0])
+    if prec == 8:
+        assert float(np.cumsum(y)[-1]) == e["rg32"]["checksum_f64"]
+    del a, want
+    # Hybrid: K1 = choose_ell_width (the reference's, golden), ELL + COO arrays
+    h = sk.build_hybrid(csr, None, prec)
+    assert h.slots_per_row == e["hybrid"]["k1"]
+    hw = orc.build_hybrid(om, e["hybrid"]["k1"], prec)
+    assert h.coo_nnz() == e["hybrid"]["coo"] == hw["coo_rows"].size
+    got = h.to_host()
+    for k in HY_KEYS:
+        assert bitwise(got[k], hw[k]), k
+    yh = sk.spmv_hybrid(h, dev(x)).cpu().numpy()
+    assert bitwise(yh, orc.spmv_hybrid(hw, x))
+    assert bitwise(yh, y)
+
+
+@pytest.mark.parametrize("G", [64, 128, 256])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_config2_27pt_128_group_sizes(cuda, G, prec):
+    om = orc.stencil(27, 128)
+    a = sk.build_rgcsr(sk.CsrMatrix.stencil(27, 128), G, prec)
+    want = orc.build_rgcsr(om, G, prec)
+    got = a.to_host()
+    for k in RG_KEYS:
+        assert bitwise(got[k], want[k]), k
+    e = SHAPES["27pt_128"][f"rg{G}"]
+    assert a.slot_count() == e["slots"]
+    f = sk.fill_report(a)
+    assert (f.artificial_zeros, f.bytes_single, f.bytes_double) == (
+        e["artificial_zeros"], e["bytes_single"], e["bytes_double"])
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    y = sk.spmv_rgcsr(a, dev(x)).cpu().numpy()
+    assert bitwise(y, orc.spmv_rgcsr(want, x)[0])
+    if prec == 8:
+        assert float(np.cumsum(y)[-1]) == SHAPES["27pt_128"]["checksum_reference"]
+
+
+# 20 of the 200 sweep seeds (scripts/sweep200.py): every 7th seed in row-count
+# order among those with <= 2.2 M rows -- 7 random, 5 banded, 8 block
+# matrices from 10,282 to 1,539,952 rows.
+SWEEP_SEEDS = [0, 23, 32, 34, 35, 38, 44, 48, 58, 71, 75, 81, 85, 96, 128, 138, 145, 164, 186,
+               193]
+
+
+@pytest.mark.parametrize("seed", SWEEP_SEEDS)
+def test_config4_sweep_subset_vs_oracle(cuda, seed):
+    name, m = gen.sweep_case(seed)
+    om = orc.Csr(m.num_rows, m.num_cols, m.row_ptr, m.col, m.val)
+    xh = gen.random_vector(m.num_cols, seed + 1)
+    k1 = orc.choose_ell_width(om.lens())
+    for prec in (8, 4):
+        dt = np.float64 if prec == 8 else np.float32
+        x = xh.astype(dt)
+        csr = sk.build_csr(m, prec)
+        ycsr = sk.spmv_csr(csr, dev(x)).cpu().numpy()
+        assert bitwise(ycsr, orc.spmv_csr(om, x, prec)), (name, prec, "csr")
+        for G in (32, 64, 128, 256):
+            a = sk.build_rgcsr(csr, G, prec)
+            want = orc.build_rgcsr(om, G, prec)
+            got = a.to_host()
+            for k in RG_KEYS:
+                assert bitwise(got[k], want[k]), (name, prec, G, k)
+            y = sk.spmv_rgcsr(a, dev(x)).cpu().numpy()
+            assert bitwise(y, orc.spmv_rgcsr(want, x)[0]), (name, prec, G)
+        h = sk.build_hybrid(csr, None, prec)
+        assert h.slots_per_row == k1, name
+        hw = orc.build_hybrid(om, k1, prec)
+        got = h.to_host()
+        for k in HY_KEYS:
+            assert bitwise(got[k], hw[k]), (name, prec, "hybrid", k)
+        assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(), orc.spmv_hybrid(hw, x)), name

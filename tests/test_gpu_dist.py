@@ -212,6 +212,13 @@ def _bench_json(world, workload, steps=6):
     return json.loads(lines[0])
 
 
+def _bench_ref_config(world, workload):
+    """The config dict the reference arm prints for the same run."""
+    sys.path.insert(0, ROOT)
+    import bench
+    return bench.bench_config(workload, world, "fused")
+
+
 @pytest.mark.parametrize("workload", ["27pt-128"])
 def test_bench_distributed_shared_gpu_bitwise(cuda, workload):
     """The driver's scaling run path (bench.py under torchrun, N ranks, fused
@@ -221,8 +228,9 @@ def test_bench_distributed_shared_gpu_bitwise(cuda, workload):
     assert ref["n_gpus"] == 1 and ref["x_bits_checksum"] != 0
     for world in (2, 3):
         d = _bench_json(world, workload)
-        assert d["n_gpus"] == world and d["config"]["exchange_fallback"] is None
-        assert d["config"]["shared_gpu"]
+        assert d["n_gpus"] == world and d["exchange"]["exchange_fallback"] is None
+        assert d["exchange"]["shared_gpu"]
+        assert d["config"] == _bench_ref_config(world, workload)
         assert d["x_bits_checksum"] == ref["x_bits_checksum"], world
         assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 2 * d["steps"]
 
