@@ -154,18 +154,35 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_apply(uint64_t* __rest
 
 }  // namespace
 
-uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s) {
-  if (n == 0) return 0;
+namespace {
+__global__ void copy_u64(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst) {
+  *dst = *src;
+}
+}  // namespace
+
+void exclusive_scan_u64_dev(uint64_t* d, uint64_t n, cudaStream_t s, uint64_t* total_dev) {
+  if (n == 0) {
+    SPMVK_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), s));
+    return;
+  }
   const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-  DevBuf<uint64_t> part(nb + 1);
+  TmpBuf<uint64_t> part(nb + 1, s);
   scan_tile_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(d, n, part.p);
   SPMVK_LAUNCH("scan_tile_reduce");
   scan_partials<<<1, kScanThreads, 0, s>>>(part.p, nb);
   SPMVK_LAUNCH("scan_partials");
   scan_tile_apply<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(d, n, part.p);
   SPMVK_LAUNCH("scan_tile_apply");
+  copy_u64<<<1, 1, 0, s>>>(part.p + nb, total_dev);
+  SPMVK_LAUNCH("copy_u64");
+}
+
+uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s) {
+  if (n == 0) return 0;
+  TmpBuf<uint64_t> tot(1, s);
+  exclusive_scan_u64_dev(d, n, s, tot.p);
   uint64_t total = 0;
-  SPMVK_CUDA(cudaMemcpyAsync(&total, part.p + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
   return total;
 }

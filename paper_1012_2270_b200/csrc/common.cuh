@@ -87,6 +87,24 @@ struct DevBuf {
   uint64_t bytes() const { return n * sizeof(T); }
 };
 
+// Stream-ordered temporary (cudaMallocAsync / cudaFreeAsync from the
+// device's default memory pool): no device-wide synchronisation on alloc or
+// free, so a converter's scratch arrays cost no host round trips.
+template <class T>
+struct TmpBuf {
+  T* p = nullptr;
+  uint64_t n = 0;
+  cudaStream_t s = nullptr;
+  TmpBuf(uint64_t count, cudaStream_t st) : n(count), s(st) {
+    SPMVK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count + 64, st));
+  }
+  TmpBuf(const TmpBuf&) = delete;
+  TmpBuf& operator=(const TmpBuf&) = delete;
+  ~TmpBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 // Number of SMs of the current device (cached per device).
 int sm_count();
 // Ensures the current device is usable (throws ECUDA otherwise).
@@ -184,6 +202,31 @@ __device__ __forceinline__ float ld_x(const float* p, uint64_t pol) {
   return v;
 }
 
+// Load helper with optional L2 eviction hints: kHint -> slot streams
+// evict_first, gathered x evict_last (createpolicy once per thread; uniform,
+// so ptxas keeps the policies in uniform registers), else the register-lean
+// unhinted forms.
+template <bool kHint>
+struct Ldr {
+  uint64_t pf = 0, pl = 0;
+  __device__ __forceinline__ Ldr() {
+    if constexpr (kHint) {
+      pf = policy_evict_first();
+      pl = policy_evict_last();
+    }
+  }
+  template <class T>
+  __device__ __forceinline__ T s(const T* p) const {
+    if constexpr (kHint) return ld_stream(p, pf);
+    else return ld_stream(p);
+  }
+  template <class T>
+  __device__ __forceinline__ T x(const T* p) const {
+    if constexpr (kHint) return ld_x(p, pl);
+    else return ld_x(p);
+  }
+};
+
 // 1D bulk prefetch of [src, src + bytes) into L2 through the TMA unit (no
 // completion tracking); src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
@@ -216,6 +259,8 @@ inline unsigned persistent_grid(uint64_t work_ctas, int per_sm) {
 // Exclusive prefix sum of n uint64 values in place; returns the total (synchronises
 // the stream to read it back).  Used for group pointers and COO offsets.
 uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s);
+// The same scan without the host round trip: the total goes to *total_dev.
+void exclusive_scan_u64_dev(uint64_t* d, uint64_t n, cudaStream_t s, uint64_t* total_dev);
 
 // Per-thread staging (stream + x/y device buffers) for the host-span
 // overloads (*_spmv_host_*), reused across calls.

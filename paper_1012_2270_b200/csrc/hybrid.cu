@@ -406,12 +406,13 @@ constexpr uint32_t kWalkCoo = 16 * kCooTile;
 // skips them): one thread would need run/4 dependent round trips.
 constexpr uint32_t kHeavyRun = 256;
 
-template <class T>
+template <class T, bool kHint = false>
 __device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
                                           const uint32_t* __restrict__ crp,
                                           const uint32_t* __restrict__ cc,
                                           const T* __restrict__ cv, const T* __restrict__ x) {
   if (!live) return acc;
+  const Ldr<kHint> ld;
   const uint32_t cb = crp[r], ce = crp[r + 1];
   if (ce - cb > kHeavyRun) return acc;  // added later by hybrid_heavy_rows
   constexpr int U = 4;  // fits the 32-register budget of the 8-CTA/SM kernels
@@ -420,12 +421,12 @@ __device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
     T v[U], xv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      c[u] = k + u < ce ? ld_stream(cc + k + u) : 0u;
-      v[u] = k + u < ce ? ld_stream(cv + k + u) : T(0);
+      c[u] = k + u < ce ? ld.s(cc + k + u) : 0u;
+      v[u] = k + u < ce ? ld.s(cv + k + u) : T(0);
     }
     __syncwarp(__activemask());  // scheduling fence: loads before gathers
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = k + u < ce ? ld_x(x + c[u]) : T(0);
+    for (int u = 0; u < U; ++u) xv[u] = k + u < ce ? ld.x(x + c[u]) : T(0);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < ce) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -433,7 +434,7 @@ __device__ __forceinline__ T coo_row_walk(uint32_t r, bool live, T acc,
   return acc;
 }
 
-template <class T>
+template <class T, bool kHint = false>
 __device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool live, T acc,
                                                  const uint32_t* __restrict__ tile_ptr,
                                                  const uint32_t* __restrict__ cr,
@@ -443,11 +444,12 @@ __device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool
   __shared__ T prod[kCooTile];
   __shared__ uint32_t prow[kCooTile];
   const uint32_t c0 = tile_ptr[tile], c1 = tile_ptr[tile + 1];
+  const Ldr<kHint> ld;
   for (uint32_t t0 = c0; t0 < c1; t0 += kCooTile) {
     const uint32_t n = min((uint32_t)kCooTile, c1 - t0);
     for (uint32_t i = threadIdx.x; i < n; i += kRowsPerTile) {
-      prow[i] = ld_stream(cr + t0 + i);
-      prod[i] = mul_rn(ld_stream(cv + t0 + i), ld_x(x + ld_stream(cc + t0 + i)));
+      prow[i] = ld.s(cr + t0 + i);
+      prod[i] = mul_rn(ld.s(cv + t0 + i), ld.x(x + ld.s(cc + t0 + i)));
     }
     __syncthreads();
     if (live) {
@@ -481,7 +483,7 @@ __device__ __forceinline__ T coo_tile_accumulate(uint32_t tile, uint32_t r, bool
 // row loads 256 consecutive COO entries per round (8 per lane, coalesced),
 // forms the products in parallel, stages them in shared memory, and lane 0
 // adds them in array order onto y[r] -- the reference's rounding sequence.
-template <class T>
+template <class T, bool kHint = false>
 __global__ void __launch_bounds__(256) hybrid_heavy_rows(uint32_t n, const uint32_t* __restrict__ rows,
                                                          const uint32_t* __restrict__ crp,
                                                          const uint32_t* __restrict__ cc,
@@ -491,6 +493,7 @@ __global__ void __launch_bounds__(256) hybrid_heavy_rows(uint32_t n, const uint3
   constexpr int K = 8, W = 32 * K;
   __shared__ T prod[8][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Ldr<kHint> ld;
   for (uint32_t i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
     const uint32_t r = rows[i];
     const uint32_t cb = crp[r], ce = crp[r + 1];
@@ -501,14 +504,14 @@ __global__ void __launch_bounds__(256) hybrid_heavy_rows(uint32_t n, const uint3
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t e = k0 + lane + 32 * k;
-        c[k] = e < ce ? ld_stream(cc + e) : 0u;
-        v[k] = e < ce ? ld_stream(cv + e) : T(0);
+        c[k] = e < ce ? ld.s(cc + e) : 0u;
+        v[k] = e < ce ? ld.s(cv + e) : T(0);
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t e = k0 + lane + 32 * k;
-        if (e < ce) prod[warp][lane + 32 * k] = mul_rn(v[k], ld_x(x + c[k]));
+        if (e < ce) prod[warp][lane + 32 * k] = mul_rn(v[k], ld.x(x + c[k]));
       }
       __syncwarp();
       if (lane == 0) {
@@ -534,7 +537,8 @@ __global__ void __launch_bounds__(256) hybrid_heavy_rows(uint32_t n, const uint3
 // U*rows instead of recomputing 64-bit indices, and MINB resident CTAs per
 // SM.  Same per-row rounding sequence (all K1 ELL slots including pads, then
 // the row's COO entries in array order) -> y bitwise spmv_hybrid's.
-template <class T, int U, int MINB, bool kAccum, bool kCoo, bool kFence = false>
+template <class T, int U, int MINB, bool kAccum, bool kCoo, bool kFence = false,
+          bool kHint = false>
 __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ cr,
@@ -542,6 +546,7 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
     T* __restrict__ y, const uint32_t* __restrict__ crp) {
   const uint32_t ntiles = (rows + kRowsPerTile - 1) / kRowsPerTile;
   const size_t step = (size_t)U * rows;
+  const Ldr<kHint> ld;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t r = tile * kRowsPerTile + threadIdx.x;
     const bool live = r < rows;
@@ -556,12 +561,12 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
         T v[U], xv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          c[u] = ld_stream(cp + (size_t)u * rows);
-          v[u] = ld_stream(vp + (size_t)u * rows);
+          c[u] = ld.s(cp + (size_t)u * rows);
+          v[u] = ld.s(vp + (size_t)u * rows);
         }
         if (kFence) __syncwarp(__activemask());  // slot loads ahead of the gathers
 #pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
+        for (int u = 0; u < U; ++u) xv[u] = ld.x(x + c[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
         cp += step;
@@ -575,13 +580,13 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
           c[u] = 0;
           v[u] = T(0);
           if (j + u < k1) {
-            c[u] = ld_stream(cp + (size_t)u * rows);
-            v[u] = ld_stream(vp + (size_t)u * rows);
+            c[u] = ld.s(cp + (size_t)u * rows);
+            v[u] = ld.s(vp + (size_t)u * rows);
           }
         }
         if (kFence) __syncwarp(__activemask());
 #pragma unroll
-        for (int u = 0; u < U - 1; ++u) xv[u] = j + u < k1 ? ld_x(x + c[u]) : T(0);
+        for (int u = 0; u < U - 1; ++u) xv[u] = j + u < k1 ? ld.x(x + c[u]) : T(0);
 #pragma unroll
         for (int u = 0; u < U - 1; ++u)
           if (j + u < k1) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -589,9 +594,9 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
     }
     if constexpr (kCoo) {
       if (crp && tile_ptr[tile + 1] - tile_ptr[tile] > kWalkCoo)  // CTA-uniform
-        acc = coo_row_walk<T>(r, live, acc, crp, cc, cv, x);
+        acc = coo_row_walk<T, kHint>(r, live, acc, crp, cc, cv, x);
       else
-        acc = coo_tile_accumulate<T>(tile, r, live, acc, tile_ptr, cr, cc, cv, x);
+        acc = coo_tile_accumulate<T, kHint>(tile, r, live, acc, tile_ptr, cr, cc, cv, x);
     }
     if (live) y[r] = acc;
   }
@@ -601,7 +606,12 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
 // "v4": hybrid_spmv_kernel (policy-hinted loads, 4-deep, 8 CTAs / SM);
 // "lite" / "lite8" / "lite8_full": hybrid_spmv_lite with 4-deep batches at
 // 8 CTAs / SM, 8-deep at 5, 8-deep at 8.  All bitwise identical.
-enum class HK { kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F };
+// "g6" / "g7" / "g8" / "g8r": the fenced walk with the RgCSR group walk's
+// batch shapes (U = 6, 7, 8 at 5 CTAs / SM; U = 8 at 4) for pure-ELL
+// matrices, where every row walks the same K1 slots like a group.
+// "litefh": litef with L2 eviction hints (ELL / COO streams evict_first, x
+// evict_last) in the main kernel and the heavy-row tails.
+enum class HK { kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F, kG6, kG7, kG8, kG8R, kLiteFH };
 
 std::atomic<int>& hk_slot() {
   static std::atomic<int> k{[] {
@@ -610,7 +620,8 @@ std::atomic<int>& hk_slot() {
       const std::string s(e);
       v = s == "v4" ? HK::kV4 : s == "lite" ? HK::kLite : s == "lite8" ? HK::kLite8
         : s == "lite8_full" ? HK::kLite8Full : s == "litef" ? HK::kLiteF
-        : s == "lite8f" ? HK::kLite8F : HK::kAuto;
+        : s == "lite8f" ? HK::kLite8F : s == "g6" ? HK::kG6 : s == "g7" ? HK::kG7
+        : s == "g8" ? HK::kG8 : s == "g8r" ? HK::kG8R : s == "litefh" ? HK::kLiteFH : HK::kAuto;
     }
     return static_cast<int>(v);
   }()};
@@ -768,7 +779,8 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     const auto& hr = h->heavy_rows_host;
     const uint64_t n = std::lower_bound(hr.begin(), hr.end(), rows) - hr.begin();
     if (!n) return;
-    hybrid_heavy_rows<T><<<persistent_grid((n + 7) / 8, 8), 256, 0, s>>>(
+    auto hk = k == HK::kLiteFH ? hybrid_heavy_rows<T, true> : hybrid_heavy_rows<T, false>;
+    hk<<<persistent_grid((n + 7) / 8, 8), 256, 0, s>>>(
         static_cast<uint32_t>(n), h->heavy_rows.p, h->coo_row_ptr.p, h->coo_columns.p,
         reinterpret_cast<const T*>(h->coo_values.p), x, y);
     SPMVK_LAUNCH("hybrid_heavy_rows");
@@ -792,9 +804,35 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
       else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
       else run(hybrid_spmv_lite<T, 4, 8, false, false, true>);
       break;
+    case HK::kLiteFH:  // fp64 + COO: 6 CTAs / SM (the policies spill at 8)
+      if (acc) run(hybrid_spmv_lite<T, 4, sizeof(T) == 8 ? 6 : 8, true, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, sizeof(T) == 8 ? 6 : 8, false, true, true, true>);
+      else run(hybrid_spmv_lite<T, 4, 8, false, false, true, true>);
+      break;
     case HK::kLite8F:
       if (acc) run(hybrid_spmv_lite<T, 8, 4, true, true, true>);
       else if (coo) run(hybrid_spmv_lite<T, 8, 4, false, true, true>);
+      else run(hybrid_spmv_lite<T, 8, 4, false, false, true>);
+      break;
+    // group-walk shapes: pure ELL launches only (a COO part keeps liteF)
+    case HK::kG6:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
+      else run(hybrid_spmv_lite<T, 6, 5, false, false, true>);
+      break;
+    case HK::kG7:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
+      else run(hybrid_spmv_lite<T, 7, 5, false, false, true>);
+      break;
+    case HK::kG8:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
+      else run(hybrid_spmv_lite<T, 8, 5, false, false, true>);
+      break;
+    case HK::kG8R:
+      if (acc) run(hybrid_spmv_lite<T, 4, 8, true, true, true>);
+      else if (coo) run(hybrid_spmv_lite<T, 4, 8, false, true, true>);
       else run(hybrid_spmv_lite<T, 8, 4, false, false, true>);
       break;
     default:
@@ -867,9 +905,15 @@ int spmvk_set_hybrid_kernel(const char* name) {
     else if (v == "lite8_full") k = HK::kLite8Full;
     else if (v == "litef") k = HK::kLiteF;
     else if (v == "lite8f") k = HK::kLite8F;
+    else if (v == "g6") k = HK::kG6;
+    else if (v == "g7") k = HK::kG7;
+    else if (v == "g8") k = HK::kG8;
+    else if (v == "g8r") k = HK::kG8R;
+    else if (v == "litefh") k = HK::kLiteFH;
     else
       fail(SPMVK_EINVAL, "unknown Hybrid kernel variant '" + v +
-                             "' (auto | v4 | lite | lite8 | lite8_full | litef | lite8f)");
+                             "' (auto | v4 | lite | lite8 | lite8_full | litef | lite8f | g6 | "
+                             "g7 | g8 | g8r | litefh)");
     hk_slot().store(static_cast<int>(k));
   });
 }

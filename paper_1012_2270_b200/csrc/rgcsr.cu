@@ -6,6 +6,8 @@
 // t sits at gp[g] + t + j*s, pads hold (0, column 0).  For one step j the s
 // rows of a group read s CONTIGUOUS slots, so a warp of consecutive rows
 // issues fully coalesced loads with one thread per row.
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -21,16 +23,29 @@ namespace spmvk {
 namespace {
 
 // ------------------------------------------------------------ K1: layout
-// slots[g] = s_g * max_{t<s_g} lens[g*G + t]
-__global__ void group_slots(uint64_t rows, uint64_t G, uint64_t groups,
-                            const uint32_t* __restrict__ lens, uint64_t* __restrict__ slots) {
+// Per group g (s_g rows): slots[g] = s_g * max_t lens[g*G + t] and
+// nlong[g] = how many of its rows are longer than the long-row cut.
+__global__ void group_layout(uint64_t rows, uint64_t G, uint64_t groups, uint32_t cut,
+                             const uint32_t* __restrict__ lens, uint64_t* __restrict__ slots,
+                             uint64_t* __restrict__ nlong) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r0 = g * G, s = min(G, rows - r0);
-    uint32_t w = 0;
-    for (uint64_t t = 0; t < s; ++t) w = max(w, lens[r0 + t]);
+    uint32_t w = 0, nl = 0;
+    for (uint64_t t = 0; t < s; ++t) {
+      const uint32_t l = lens[r0 + t];
+      w = max(w, l);
+      nl += l > cut;
+    }
     slots[g] = s * w;
+    nlong[g] = nl;
   }
+}
+
+// out[0] = row_ptr[r1] - row_ptr[r0] (the slab's nnz)
+__global__ void slab_nnz(const uint32_t* __restrict__ rp, uint64_t r0, uint64_t r1,
+                         uint64_t* __restrict__ out) {
+  *out = (uint64_t)rp[r1] - rp[r0];
 }
 
 __global__ void narrow_pointers(uint64_t groups, const uint64_t* __restrict__ gp64,
@@ -40,18 +55,18 @@ __global__ void narrow_pointers(uint64_t groups, const uint64_t* __restrict__ gp
     gp[g] = (uint32_t)(g == groups ? total : gp64[g]);
 }
 
-__global__ void long_row_flags(uint64_t rows, uint32_t cut, const uint32_t* __restrict__ lens,
-                               uint64_t* __restrict__ flag) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (uint64_t)gridDim.x * blockDim.x)
-    flag[r] = lens[r] > cut ? 1 : 0;
-}
-
-__global__ void long_row_scatter(uint64_t rows, uint32_t cut, const uint32_t* __restrict__ lens,
-                                 const uint64_t* __restrict__ pos, uint32_t* __restrict__ out) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (uint64_t)gridDim.x * blockDim.x)
-    if (lens[r] > cut) out[pos[r]] = (uint32_t)r;
+// The long rows in ascending order: group g writes its rows longer than the
+// cut at its scanned offset off[g].
+__global__ void long_rows_by_group(uint64_t rows, uint64_t G, uint64_t groups, uint32_t cut,
+                                   const uint32_t* __restrict__ lens,
+                                   const uint64_t* __restrict__ off, uint32_t* __restrict__ out) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r0 = g * G, s = min(G, rows - r0);
+    uint64_t o = off[g];
+    for (uint64_t t = 0; t < s; ++t)
+      if (lens[r0 + t] > cut) out[o++] = (uint32_t)(r0 + t);
+  }
 }
 
 // ------------------------------------------------------------ to_triplets
@@ -138,68 +153,91 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
 // 4096-slot row would be its critical path).  SPMVK_LONG_QUADS=0 disables.
 constexpr uint32_t kQuadMaxLen = 1024;
 
-__global__ void gather_u32(uint64_t n, const uint32_t* __restrict__ idx,
-                           const uint32_t* __restrict__ src, uint32_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = src[idx[i]];
+// Long row i (ascending ids lr[]): is it the first row of a quad (rows r..r+3,
+// r % 4 == 0, all long, each shorter than kQuadMaxLen, inside one full group
+// of a G % 4 == 0 matrix), and does it belong to any quad?  A quad starts on
+// a multiple of 4 and covers 4 consecutive ids, so membership of row r is
+// the quad test of r & ~3.  Sort keys put the singles first, longest first
+// (stable: ties keep ascending ids), the quad members after them.
+__device__ __forceinline__ bool quad_at(uint64_t i, uint64_t n, const uint32_t* __restrict__ lr,
+                                        const uint32_t* __restrict__ lens, uint64_t rows,
+                                        uint64_t G) {
+  const uint32_t r = lr[i];
+  if (r % 4 || G % 4 || i + 3 >= n) return false;
+  const uint64_t g = r / G;
+  if ((g + 1) * G > rows || (r + 3) / G != g) return false;
+  for (int k = 0; k < 4; ++k)
+    if (lr[i + k] != r + k || lens[r + k] >= kQuadMaxLen) return false;
+  return true;
 }
 
-void split_long_rows(spmvk_rgcsr* h, uint32_t G, cudaStream_t s) {
+__global__ void long_split(uint64_t n, uint64_t rows, uint64_t G, int quads_on,
+                           const uint32_t* __restrict__ lr, const uint32_t* __restrict__ lens,
+                           uint64_t* __restrict__ qflag, uint32_t* __restrict__ key) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = lr[i];
+    const bool start = quads_on && quad_at(i, n, lr, lens, rows, G);
+    bool member = start;
+    if (quads_on && !start && r % 4) {  // the quad test of r & ~3, at index i - r % 4
+      const uint64_t d = r % 4;
+      member = i >= d && lr[i - d] == r - d && quad_at(i - d, n, lr, lens, rows, G);
+    }
+    qflag[i] = start ? 1 : 0;
+    key[i] = member ? 0xffffffffu : 0xfffffffeu - lens[r];
+  }
+}
+
+__global__ void count_singles(uint64_t n, uint64_t* __restrict__ counts) {
+  counts[1] = n - 4 * counts[0];
+}
+
+__global__ void quad_scatter(uint64_t n, const uint32_t* __restrict__ lr,
+                             const uint64_t* __restrict__ qflag, const uint64_t* __restrict__ qpos,
+                             uint32_t* __restrict__ quads) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (qflag[i]) quads[qpos[i]] = lr[i];
+}
+
+// Device split of the long rows (lr, ascending) into quads and singles
+// (longest first) for rgcsr_spmv_long_mixed.  The two counts land in
+// counts_dev[0] (quads) and counts_dev[1] (singles).
+void split_long_rows(spmvk_rgcsr* h, uint32_t G, uint64_t* counts_dev, cudaStream_t s) {
   static const bool on = [] {
     const char* e = std::getenv("SPMVK_LONG_QUADS");
     return !e || std::atoi(e) != 0;
   }();
-  std::vector<uint32_t> lr(h->n_long), len(h->n_long);
-  SPMVK_CUDA(cudaStreamSynchronize(s));
-  SPMVK_CUDA(cudaMemcpy(lr.data(), h->long_rows.p, 4 * h->n_long, cudaMemcpyDeviceToHost));
-  {
-    DevBuf<uint32_t> d(h->n_long);
-    gather_u32<<<persistent_grid((h->n_long + 255) / 256, 8), 256, 0, s>>>(
-        h->n_long, h->long_rows.p, h->row_lengths.p, d.p);
-    SPMVK_LAUNCH("gather_u32");
-    SPMVK_CUDA(cudaMemcpyAsync(len.data(), d.p, 4 * h->n_long, cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaStreamSynchronize(s));
-  }
-  std::vector<uint32_t> quads, singles;
-  for (uint64_t i = 0; i < h->n_long;) {
-    const uint32_t r = lr[i];
-    const uint64_t g = r / G;
-    const bool full = (g + 1) * G <= h->rows;
-    bool quad = on && G % 4 == 0 && r % 4 == 0 && full && i + 3 < h->n_long &&
-                (r + 3) / G == g;
-    for (int k = 0; quad && k < 4; ++k) quad = lr[i + k] == r + k && len[i + k] < kQuadMaxLen;
-    if (quad) {
-      quads.push_back(r);
-      i += 4;
-    } else {
-      singles.push_back(r);
-      ++i;
-    }
-  }
-  // singles longest first: the longest rows bound the phase, start them early
-  std::vector<uint64_t> order(singles.size());
-  for (uint64_t k = 0; k < order.size(); ++k) order[k] = k;
-  std::vector<uint32_t> slen(singles.size());
-  for (uint64_t k = 0, i = 0; k < singles.size(); ++k) {
-    while (lr[i] != singles[k]) ++i;
-    slen[k] = len[i];
-  }
-  std::stable_sort(order.begin(), order.end(),
-                   [&](uint64_t a, uint64_t b) { return slen[a] > slen[b]; });
-  std::vector<uint32_t> sorted(singles.size());
-  for (uint64_t k = 0; k < order.size(); ++k) sorted[k] = singles[order[k]];
-  h->n_quads = quads.size();
-  h->n_singles = sorted.size();
-  h->long_quads.alloc(h->n_quads);
-  h->long_singles.alloc(h->n_singles);
-  if (h->n_quads)
-    SPMVK_CUDA(cudaMemcpy(h->long_quads.p, quads.data(), 4 * h->n_quads, cudaMemcpyHostToDevice));
-  if (h->n_singles)
-    SPMVK_CUDA(cudaMemcpy(h->long_singles.p, sorted.data(), 4 * h->n_singles,
-                          cudaMemcpyHostToDevice));
+  const uint64_t n = h->n_long;
+  const unsigned grid = persistent_grid((n + 255) / 256, 8);
+  TmpBuf<uint64_t> qflag(n, s);
+  TmpBuf<uint32_t> key(n, s), key2(n, s);
+  long_split<<<grid, 256, 0, s>>>(n, h->rows, G, on ? 1 : 0, h->long_rows.p, h->row_lengths.p,
+                                  qflag.p, key.p);
+  SPMVK_LAUNCH("long_split");
+  // singles first (longest first, stable), quad members last
+  h->long_singles.alloc(n);
+  size_t tmp_bytes = 0;
+  SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key2.p, h->long_rows.p,
+                                             h->long_singles.p, static_cast<int>(n), 0, 32, s));
+  TmpBuf<unsigned char> tmp(tmp_bytes, s);
+  SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key.p, key2.p, h->long_rows.p,
+                                             h->long_singles.p, static_cast<int>(n), 0, 32, s));
+  // quads: compaction of the starts (ascending)
+  TmpBuf<uint64_t> qpos(n, s);
+  SPMVK_CUDA(cudaMemcpyAsync(qpos.p, qflag.p, 8 * n, cudaMemcpyDeviceToDevice, s));
+  exclusive_scan_u64_dev(qpos.p, n, s, counts_dev);
+  h->long_quads.alloc(n / 4 + 1);
+  quad_scatter<<<grid, 256, 0, s>>>(n, h->long_rows.p, qflag.p, qpos.p, h->long_quads.p);
+  SPMVK_LAUNCH("quad_scatter");
+  count_singles<<<1, 1, 0, s>>>(n, counts_dev);
+  SPMVK_LAUNCH("count_singles");
 }
 
+// K1 on the device with two host round trips: the slot total, long-row
+// count and nnz (one 24-byte readback, needed to size the arrays and to
+// report a uint32 overflow before writing), and the quad / single counts at
+// the end.  Scratch arrays are stream-ordered (no device-wide syncs).
 spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int prec,
                    cudaStream_t s) {
   if (!a) fail(SPMVK_EINVAL, "null CSR handle");
@@ -216,52 +254,38 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
   h->group_size = G;
   h->prec = prec;
   h->groups = (h->rows + G - 1) / G;
+  h->long_cut = long_cut_slot().load();
   h->row_lengths.alloc(h->rows);
   h->group_pointers.alloc(h->groups + 1);
   const unsigned rgrid = persistent_grid((h->rows + 255) / 256, 8);
+  const unsigned ggrid = persistent_grid((h->groups + 255) / 256, 8);
+  TmpBuf<uint64_t> tot(5, s);  // slots, long rows, nnz | quads, singles
+  TmpBuf<uint64_t> slots(h->groups, s), nlong(h->groups, s);
   if (h->rows) {
     csr_row_lengths<<<rgrid, 256, 0, s>>>(r0, h->rows, a->row_ptr.p, h->row_lengths.p);
     SPMVK_LAUNCH("csr_row_lengths");
+    group_layout<<<ggrid, 256, 0, s>>>(h->rows, G, h->groups, h->long_cut, h->row_lengths.p,
+                                       slots.p, nlong.p);
+    SPMVK_LAUNCH("group_layout");
   }
-  uint64_t total = 0;
-  {
-    DevBuf<uint64_t> slots(h->groups);
-    if (h->groups) {
-      group_slots<<<persistent_grid((h->groups + 255) / 256, 8), 256, 0, s>>>(
-          h->rows, G, h->groups, h->row_lengths.p, slots.p);
-      SPMVK_LAUNCH("group_slots");
-    }
-    total = exclusive_scan_u64(slots.p, h->groups, s);
-    if (total > 0xffffffffull)
-      fail(SPMVK_ERANGE, "build_rgcsr: " + std::to_string(total) +
-                             " slots overflow the 32-bit group pointers (group size " +
-                             std::to_string(G) + ")");
-    narrow_pointers<<<persistent_grid((h->groups + 256) / 256, 8), 256, 0, s>>>(
-        h->groups, slots.p, total, h->group_pointers.p);
-    SPMVK_LAUNCH("narrow_pointers");
-    SPMVK_CUDA(cudaStreamSynchronize(s));
-  }
+  exclusive_scan_u64_dev(slots.p, h->groups, s, tot.p);
+  exclusive_scan_u64_dev(nlong.p, h->groups, s, tot.p + 1);
+  slab_nnz<<<1, 1, 0, s>>>(a->row_ptr.p, r0, r1, tot.p + 2);
+  SPMVK_LAUNCH("slab_nnz");
+  uint64_t t3[3];
+  SPMVK_CUDA(cudaMemcpyAsync(t3, tot.p, sizeof(t3), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  const uint64_t total = t3[0];
+  if (total > 0xffffffffull)
+    fail(SPMVK_ERANGE, "build_rgcsr: " + std::to_string(total) +
+                           " slots overflow the 32-bit group pointers (group size " +
+                           std::to_string(G) + ")");
   h->slots = total;
-  {
-    uint32_t b = 0, e = 0;
-    SPMVK_CUDA(cudaMemcpy(&b, a->row_ptr.p + r0, 4, cudaMemcpyDeviceToHost));
-    SPMVK_CUDA(cudaMemcpy(&e, a->row_ptr.p + r1, 4, cudaMemcpyDeviceToHost));
-    h->nnz = e - b;
-  }
-  if (h->rows) {  // long-row list (ascending): flag, scan, scatter
-    DevBuf<uint64_t> pos(h->rows);
-    h->long_cut = long_cut_slot().load();
-    long_row_flags<<<rgrid, 256, 0, s>>>(h->rows, h->long_cut, h->row_lengths.p, pos.p);
-    SPMVK_LAUNCH("long_row_flags");
-    h->n_long = exclusive_scan_u64(pos.p, h->rows, s);
-    h->long_rows.alloc(h->n_long);
-    if (h->n_long) {
-      long_row_scatter<<<rgrid, 256, 0, s>>>(h->rows, h->long_cut, h->row_lengths.p, pos.p,
-                                             h->long_rows.p);
-      SPMVK_LAUNCH("long_row_scatter");
-      split_long_rows(h.get(), G, s);
-    }
-  }
+  h->n_long = t3[1];
+  h->nnz = t3[2];
+  narrow_pointers<<<persistent_grid((h->groups + 256) / 256, 8), 256, 0, s>>>(
+      h->groups, slots.p, total, h->group_pointers.p);
+  SPMVK_LAUNCH("narrow_pointers");
   h->values.alloc(total * static_cast<uint64_t>(prec));
   h->columns.alloc(total);
   if (h->groups) {
@@ -284,7 +308,20 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
     }
     SPMVK_LAUNCH("rgcsr_scatter");
   }
-  SPMVK_CUDA(cudaStreamSynchronize(s));
+  h->long_rows.alloc(h->n_long);
+  if (h->n_long) {  // long-row list (ascending), split into quads and singles
+    long_rows_by_group<<<ggrid, 256, 0, s>>>(h->rows, G, h->groups, h->long_cut,
+                                             h->row_lengths.p, nlong.p, h->long_rows.p);
+    SPMVK_LAUNCH("long_rows_by_group");
+    split_long_rows(h.get(), static_cast<uint32_t>(G), tot.p + 3, s);
+    uint64_t qs[2];
+    SPMVK_CUDA(cudaMemcpyAsync(qs, tot.p + 3, sizeof(qs), cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+    h->n_quads = qs[0];
+    h->n_singles = qs[1];
+  } else {
+    SPMVK_CUDA(cudaStreamSynchronize(s));
+  }
   return h.release();
 }
 
@@ -301,7 +338,12 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // Round 2 pruned the variants that never won a measured case (TMA rings,
 // L2 bulk prefetch, x staged in shared memory, policy-hinted ldg, deeper
 // pipes; numbers in profiles/r02_k2_pruned.md).
-enum class K2 { kAuto, kPipe, kLite, kLite8, kLite8Full, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64 };
+// "liteh" / "lite8h": lite / lite8 with L2 eviction hints (slot streams
+// evict_first, x evict_last), for matrices whose x competes with a large
+// slot stream for L2 (power-law).
+enum class K2 {
+  kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64
+};
 
 // "auto" (default): the variant that measured fastest on B200 across the
 // stencil shapes (profiles/r01_k2_sweep.md): the register-lean tile kernel —
@@ -345,7 +387,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"auto", K2::kAuto},         {"pipe", K2::kPipe},         {"lite", K2::kLite},
       {"lite8", K2::kLite8},       {"lite8_full", K2::kLite8Full}, {"vec2", K2::kVec2},
       {"grp6", K2::kGrp6},         {"grp7_mpf", K2::kGrp7Mpf},  {"grp8", K2::kGrp8},
-      {"grp8_r64", K2::kGrp8R64}};
+      {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -368,11 +410,20 @@ K2 k2_choice() { return static_cast<K2>(k2_slot().load(std::memory_order_relaxed
 
 // The rows past the long-row cut: singles (warp per row, longest first) and
 // quads (four rows per warp) in one launch after the thread-per-row kernel.
+// hint: L2 eviction hints on the long rows' slot streams and x gathers
+// (SPMVK_LONG_HINT=0/1 forces them off/on).
 template <class T, bool kScaled>
 void launch_long(const spmvk_rgcsr* h, uint32_t G, int sh, const T* x, T* y, T* x_next, T scale,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool hint) {
+  static const int env = [] {
+    const char* e = std::getenv("SPMVK_LONG_HINT");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (env >= 0) hint = env > 0;
   const uint64_t items = h->n_singles + h->n_quads;
-  rgcsr_spmv_long_mixed<T, kScaled><<<persistent_grid((items + 7) / 8, 8), 256, 0, s>>>(
+  auto kern = hint ? rgcsr_spmv_long_mixed<T, kScaled, true>
+                   : rgcsr_spmv_long_mixed<T, kScaled, false>;
+  kern<<<persistent_grid((items + 7) / 8, 8), 256, 0, s>>>(
       static_cast<uint32_t>(h->n_singles), h->long_singles.p, static_cast<uint32_t>(h->n_quads),
       h->long_quads.p, static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
       h->row_lengths.p, reinterpret_cast<const T*>(h->values.p), h->columns.p, x, y, x_next,
@@ -404,6 +455,10 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   constexpr bool f64 = sizeof(T) == 8;
   K2 k = k2_choice();
   if (k == K2::kAuto) k = auto_k2(h, f64);
+  // the group-uniform walk has no long-row split: matrices with long rows
+  // (and, for now, any request on them) take the lite kernel instead
+  if (k >= K2::kGrp6 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
+  const bool hinted = k == K2::kLiteH || k == K2::kLite8H || k == K2::kPipe;
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
   constexpr int U = sizeof(T) == 8 ? 4 : 8;
@@ -446,7 +501,7 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale, long_cut);
     SPMVK_LAUNCH("rgcsr_spmv (thread per row)");
-    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s);
+    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s, hinted);
   };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
   auto run_vec = [&](auto kern) {
@@ -459,11 +514,11 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale, long_cut);
     SPMVK_LAUNCH("rgcsr_spmv_vec");
-    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s);
+    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s, false);
   };
   // the group-uniform walk has no long-row split: matrices with long rows
   // (and, for now, any request on them) take the lite kernel instead
-  if (k >= K2::kGrp6 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
+
   switch (k) {
     // group-uniform walk: <T, kScaled, U, MINB, kNoLen, kMpf>
     case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
@@ -473,6 +528,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
+    case K2::kLiteH: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
+    case K2::kLite8H: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
     default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
   }
@@ -895,7 +952,7 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
                              "' (auto | grp6 | grp7_mpf | grp8 | grp8_r64 | lite | lite8 | "
-                             "lite8_full | vec2 | pipe)");
+                             "lite8_full | liteh | lite8h | vec2 | pipe)");
     k2_slot().store(static_cast<int>(k));
   });
 }

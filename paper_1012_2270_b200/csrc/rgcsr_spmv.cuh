@@ -152,12 +152,13 @@ struct PeerEpi {
   }
 };
 
-template <class T, int U, class Epi>
+template <class T, int U, class Epi, bool kHint = false>
 __device__ __forceinline__ void lite_tiles_epi(
     uint32_t tile_begin, uint32_t tile_end, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
     uint32_t long_cut, const Epi& epi) {
+  const Ldr<kHint> ld;
   for (uint32_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     const uint32_t r = tile * 256 + threadIdx.x;
     if (r >= rows) continue;
@@ -180,11 +181,11 @@ __device__ __forceinline__ void lite_tiles_epi(
       T v[U], xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        c[u] = ld_stream(cp + u * s);
-        v[u] = ld_stream(vp + u * s);
+        c[u] = ld.s(cp + u * s);
+        v[u] = ld.s(vp + u * s);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = ld_x(x + c[u]);
+      for (int u = 0; u < U; ++u) xv[u] = ld.x(x + c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
       cp += U * s;
@@ -198,12 +199,12 @@ __device__ __forceinline__ void lite_tiles_epi(
         c[u] = 0;
         v[u] = T(0);
         if (j + u < len) {
-          c[u] = ld_stream(cp + u * s);
-          v[u] = ld_stream(vp + u * s);
+          c[u] = ld.s(cp + u * s);
+          v[u] = ld.s(vp + u * s);
         }
       }
 #pragma unroll
-      for (int u = 0; u < U - 1; ++u) xv[u] = j + u < len ? ld_x(x + c[u]) : T(0);
+      for (int u = 0; u < U - 1; ++u) xv[u] = j + u < len ? ld.x(x + c[u]) : T(0);
 #pragma unroll
       for (int u = 0; u < U - 1; ++u)
         if (j + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -222,13 +223,13 @@ __device__ __forceinline__ void lite_tiles(
                                     columns, x, long_cut, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
-template <class T, bool kScaled, int U, int MINB>
+template <class T, bool kScaled, int U, int MINB, bool kHint = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t long_cut) {
-  lite_tiles_epi<T, U, StoreEpi<T, kScaled>>(
+  lite_tiles_epi<T, U, StoreEpi<T, kScaled>, kHint>(
       0, (rows + 255) / 256, rows, G, g_shift, gp, lens, values, columns, x, long_cut,
       StoreEpi<T, kScaled>{y, x_next, scale});
 }
@@ -674,7 +675,7 @@ __device__ __forceinline__ void long_rows_epi(
 // slot order, so y stays bitwise.  Singles (the other long rows) take the
 // warp-per-row path above.  One kernel for both lists: item i < n_single is
 // single row single_rows[i], else quad quads[i - n_single].
-template <class T, class Epi>
+template <class T, class Epi, bool kHint = false>
 __device__ __forceinline__ void long_mixed_epi(
     uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
     const uint32_t* __restrict__ quads, uint32_t rows, uint32_t G, int g_shift,
@@ -685,6 +686,7 @@ __device__ __forceinline__ void long_mixed_epi(
   __shared__ T prod[8][W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t items = n_single + n_quad;
+  const Ldr<kHint> ld;
   for (uint32_t i = blockIdx.x * 8 + warp; i < items; i += gridDim.x * 8) {
     if (i < n_single) {  // one row per warp (as long_rows_epi)
       const uint32_t r = single_rows[i];
@@ -701,14 +703,14 @@ __device__ __forceinline__ void long_mixed_epi(
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const uint32_t j = j0 + lane + 32 * k;
-          c[k] = j < len ? ld_stream(cp + (size_t)j * s) : 0u;
-          v[k] = j < len ? ld_stream(vp + (size_t)j * s) : T(0);
+          c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
+          v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
         }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const uint32_t j = j0 + lane + 32 * k;
-          if (j < len) prod[warp][lane + 32 * k] = mul_rn(v[k], ld_x(x + c[k]));
+          if (j < len) prod[warp][lane + 32 * k] = mul_rn(v[k], ld.x(x + c[k]));
         }
         __syncwarp();
         if (lane == 0) {
@@ -749,14 +751,14 @@ __device__ __forceinline__ void long_mixed_epi(
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t j = j0 + l + 8 * k;
-        c[k] = j < len ? ld_stream(cp + (size_t)j * s) : 0u;
-        v[k] = j < len ? ld_stream(vp + (size_t)j * s) : T(0);
+        c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
+        v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
       }
       __syncwarp();  // scheduling fence: every slot load before the gathers
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t j = j0 + l + 8 * k;
-        if (j < len) pq[l + 8 * k] = mul_rn(v[k], ld_x(x + c[k]));
+        if (j < len) pq[l + 8 * k] = mul_rn(v[k], ld.x(x + c[k]));
       }
       __syncwarp();
       if (l == 0 && j0 < len) {
@@ -777,14 +779,15 @@ __device__ __forceinline__ void long_mixed_epi(
   }
 }
 
-template <class T, bool kScaled>
+template <class T, bool kScaled, bool kHint = false>
 __global__ void __launch_bounds__(256) rgcsr_spmv_long_mixed(
     uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
     const uint32_t* __restrict__ quads, uint32_t rows, uint32_t G, int g_shift,
     const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
     const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
     T* __restrict__ y, T* __restrict__ x_next, T scale) {
-  long_mixed_epi<T>(n_single, single_rows, n_quad, quads, rows, G, g_shift, gp, lens, values,
+  long_mixed_epi<T, StoreEpi<T, kScaled>, kHint>(n_single, single_rows, n_quad, quads, rows, G,
+                                                 g_shift, gp, lens, values,
                     columns, x, StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
