@@ -757,10 +757,16 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
   const uint32_t* tp = part != Part::kEll && h->coo ? h->tile_ptr.p : nullptr;
   HK k = static_cast<HK>(hk_slot().load(std::memory_order_relaxed));
   if (k == HK::kAuto) {
-    // measured (scripts/ab_formats.py, profiles/r01_hybrid_variants.md): the
-    // fenced 4-deep lite kernel is best or within 2 % everywhere (7-pt 256^3
-    // fp64 239 vs v4 248 us, fp32 173 vs 180; power-law fp64 748 vs 801)
-    k = HK::kLiteF;
+    // measured (scripts/ab_formats.py; profiles/r01_hybrid_variants.md,
+    // profiles/r02_ab.md): with a COO part the fenced 4-deep lite kernel
+    // (power-law fp64 736 us; fp32 with L2 hints 675 vs 690); pure ELL takes
+    // the group-walk batch shape matching K1 -- 5-point (K1 = 5) U = 6:
+    // fp64 47.1 vs 49.3 us, fp32 31.8 vs 34.9 (5-pt 2048^2); 27-point U = 7:
+    // fp64 105.2 vs 106.8, fp32 76.1 vs 77.7; 7-point keeps U = 4 (fp32
+    // 172.4 vs 172.7 for U = 7, 174.5 for U = 8).
+    const bool pure_ell = part == Part::kEll || !h->coo;
+    if (pure_ell) k = k1 <= 6 ? HK::kG6 : k1 <= 12 ? HK::kLiteF : HK::kG7;
+    else k = sizeof(T) == 4 ? HK::kLiteFH : HK::kLiteF;
   }
   auto run = [&](auto kern) {
     int per_sm = 0;

@@ -83,6 +83,10 @@ def main():
             for key in KEYS:
                 if key in k:
                     lines.append(f"| {key} | {k[key][0]} | {k[key][1]} |")
+            # request-path utilisation (the floor of gather-bound kernels)
+            for key in sorted(k):
+                if ("xbar_req" in key or "l1tex__lsu_writeback" in key) and key not in KEYS:
+                    lines.append(f"| {key} | {k[key][0]} | {k[key][1]} |")
             rd = float(k["dram__bytes_read.sum"][0].replace(",", ""))
             wr = float(k["dram__bytes_write.sum"][0].replace(",", ""))
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--prec", type=int, default=8)
     ap.add_argument("--variant", default="pipe")
     ap.add_argument("--format", default="rgcsr")
+    ap.add_argument("--hvariant", default="auto", help="Hybrid kernel variant")
     ap.add_argument("--launches", type=int, default=4)
     ap.add_argument("--reorder", action="store_true", help="descending row reordering first")
     a = ap.parse_args()
@@ -28,6 +29,7 @@ def main():
     L = lib()
     assert L.spmvk_init(0) == 0
     assert L.spmvk_set_rgcsr_kernel(a.variant.encode()) == 0
+    assert L.spmvk_set_hybrid_kernel(a.hvariant.encode()) == 0
     kind, n, G = (int(v) for v in a.case.split(":"))
     if kind == 0:
         csr = sk.build_csr(gen.powerlaw(n, 7), a.prec)

@@ -1,206 +1,10 @@
-"""ncu-backed replacement of the reference's `spmvkit simulate`.
-
-The reference models a GTX 280: it replays the RgCSR/CSR/ELL address streams
-per half-warp, counts 128-byte segment transactions per array and runs an LRU
-texture-cache simulation (src/memsim.cpp:92-199, tools/main.cpp:274-317).
-Here the same report is filled from REAL counters of the B200 kernel: one
-`ncu --section SourceCounters` pass over one SpMV launch gives, per SASS
-memory instruction, the L2 sectors it touched ("L2 Theoretical Sectors
-Global") and the ideal count for its bytes; instructions are attributed to
-arrays by their cache operator and width:
-
-  values   LDG.NA (no-allocate) of the scalar width     (RgCSR / ELL slots)
-  columns  LDG.NA 32-bit                                 (fp32: values and columns
-           have identical index patterns, so the NA.32 sectors split evenly)
-  x        LDG (L1-allocating, read-only) of the scalar width
-  output   STG
-  (row lengths / group pointers: the remaining LDG.32, reported as "metadata")
-
-and the x "cache" is the L1: hits / misses of the global-load lookups
-(`l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_{hit,miss}`; the NA
-slot loads never allocate, so the hits are x's).  Units are 32-byte sectors,
-B200's transaction granularity, instead of the model's 128-byte segments.
-
-    python scripts/simulate.py --case 27:128 --format rgcsr --group-size 32 \
-        --precision double [--out report.json]        (needs ncu + a GPU)
-"""
-import argparse
-import csv
-import io
-import json
+"""Thin wrapper: the ncu-backed `simulate` report lives in the package
+(paper_1012_2270_b200/simulate.py; python -m paper_1012_2270_b200.simulate)."""
 import os
-import subprocess
 import sys
-import tempfile
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
-
-KERNELS = {"rgcsr": "rgcsr_spmv", "ellpack": "hybrid_spmv", "csr": "csr_spmv"}
-
-
-def child(a):
-    import torch
-
-    from paper_1012_2270_b200 import generators as gen
-    from paper_1012_2270_b200 import spmvkit as sk
-    from paper_1012_2270_b200._lib import lib
-    torch.cuda.set_device(0)
-    assert lib().spmvk_init(0) == 0
-    prec = 8 if a.precision == "double" else 4
-    csr = load(a, sk, gen)
-    if prec == 4:
-        rp, col, val = csr.to_host()
-        csr = sk.build_csr(sk.TripletMatrix(csr.num_rows, csr.num_cols, rp, col, val), 4)
-    if a.format == "rgcsr":
-        h = sk.build_rgcsr(csr, a.group_size, prec)
-        fn = sk.spmv_rgcsr
-        az = sk.fill_report(h).artificial_zeros
-    elif a.format == "ellpack":  # Hybrid at K1 = max row length is plain ELLPACK
-        h = sk.build_hybrid(csr, csr.row_length_range()[0], prec)
-        fn = sk.spmv_hybrid
-        az = sk.fill_report(h).artificial_zeros
-    else:
-        h, fn, az = csr, sk.spmv_csr, 0
-    dt = torch.float64 if prec == 8 else torch.float32
-    x = torch.from_numpy(gen.random_vector(csr.num_cols, a.seed)).cuda().to(dt)
-    fn(h, x)  # ONE SpMV: every kernel it launches is profiled (ncu flushes caches)
-    torch.cuda.synchronize()
-    with open(a.meta, "w") as f:
-        json.dump({"nnz": csr.nnz(), "artificial_zeros": az, "rows": csr.num_rows}, f)
-
-
-def load(a, sk, gen):
-    if a.mtx:
-        return sk.load_matrix_market(a.mtx)
-    kind, n = (int(v) for v in a.case.split(":"))
-    if kind == 0:
-        return sk.build_csr(gen.powerlaw(n, 7))
-    return sk.CsrMatrix.stencil(kind, n)
-
-
-def classify(rows, sv, meta_sectors=0):
-    """Sum per-instruction sectors over every profiled kernel's section of the
-    `--page source --csv` output (each section: a "Kernel Name" row, a header
-    row, then one row per SASS instruction)."""
-    out = {k: [0, 0] for k in ("values", "columns", "x", "output", "metadata", "na32")}
-    ix, i = None, 0
-    while i < len(rows):
-        r = rows[i]
-        i += 1
-        if r and r[0] == "Kernel Name":
-            h = rows[i]
-            i += 1
-            ix = {k: h.index(k) for k in ("Source", "Access Operation", "Access Size",
-                                          "L2 Theoretical Sectors Global",
-                                          "L2 Theoretical Sectors Global Ideal")}
-            continue
-        if ix is None or len(r) <= max(ix.values()):
-            continue
-        op = r[ix["Access Operation"]]
-        if op not in ("Load", "Store"):
-            continue
-        src = r[ix["Source"]]
-        size = int(r[ix["Access Size"]] or 0)
-        sec = int(float(r[ix["L2 Theoretical Sectors Global"]] or 0))
-        ideal = int(float(r[ix["L2 Theoretical Sectors Global Ideal"]] or 0))
-        if op == "Store":
-            key = "output"
-        elif "LDG" not in src:
-            continue
-        elif ".NA" in src:  # streamed slots (L1 no-allocate)
-            if sv == 8:
-                key = "values" if size == 64 else "columns"
-            else:
-                key = "na32"
-        elif size == 8 * sv:
-            key = "x"
-        else:
-            key = "metadata"
-        out[key][0] += sec
-        out[key][1] += ideal
-    if sv == 4:  # fp32: values and columns share one index pattern and width
-        s, i = out.pop("na32")
-        out["values"] = [s // 2, i // 2]
-        out["columns"] = [s - s // 2, i - i // 2]
-        # the 32-bit L1-allocating loads are x gathers AND the per-row metadata
-        # (row length, group pointer); move the metadata's coalesced sector count
-        meta = min(meta_sectors, out["x"][0])
-        out["x"] = [out["x"][0] - meta, max(0, out["x"][1] - meta)]
-        out["metadata"] = [out["metadata"][0] + meta, out["metadata"][1] + meta]
-    else:
-        out.pop("na32")
-    return out
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="27:128")
-    ap.add_argument("--mtx")
-    ap.add_argument("--format", default="rgcsr", choices=sorted(KERNELS))
-    ap.add_argument("--group-size", type=int, default=32)
-    ap.add_argument("--precision", default="double", choices=["single", "double"])
-    ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--out")
-    ap.add_argument("--child", action="store_true")
-    ap.add_argument("--meta")
-    a = ap.parse_args()
-    if a.child:
-        return child(a)
-    sv = 8 if a.precision == "double" else 4
-    with tempfile.TemporaryDirectory() as d:
-        rep, meta = os.path.join(d, "sim"), os.path.join(d, "meta.json")
-        argv = [sys.executable, os.path.abspath(__file__), "--child", "--meta", meta,
-                "--format", a.format, "--group-size", str(a.group_size), "--precision",
-                a.precision, "--seed", str(a.seed)] + (["--mtx", a.mtx] if a.mtx else
-                                                        ["--case", a.case])
-        subprocess.run(["ncu", "--section", "SourceCounters", "--import-source", "on",
-                        "--metrics", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum,"
-                        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum",
-                        "--clock-control", "none", "-k", f"regex:{KERNELS[a.format]}",
-                        "-o", rep] + argv, check=True,
-                       stdout=subprocess.DEVNULL)
-        src = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "source", "--csv",
-                              "--print-source", "sass"], capture_output=True, text=True,
-                             check=True).stdout
-        raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv"],
-                             capture_output=True, text=True, check=True).stdout
-        m = json.load(open(meta))
-    meta_sec = 0
-    if sv == 4 and a.format == "rgcsr":  # coalesced row lengths + one group pointer per warp
-        meta_sec = (m["rows"] * 4 + 31) // 32 + (m["rows"] + 31) // 32
-    tx = classify(list(csv.reader(io.StringIO(src))), sv, meta_sec)
-    rr = list(csv.reader(io.StringIO(raw)))
-    hdr = rr[0]
-
-    def total_of(metric):  # summed over the profiled kernels (one raw row each)
-        j = hdr.index(metric)
-        return sum(int(float(v[j].replace(",", ""))) for v in rr[2:] if len(v) > j and v[j])
-    hits = total_of("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum")
-    miss_all = total_of("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum")
-    kernels = [v[hdr.index("Kernel Name")] for v in rr[2:] if len(v) > 1]
-    total = sum(v[0] for v in tx.values())
-    ideal = sum(v[1] for v in tx.values())
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-        bw = float(json.load(f)["hbm_gbs"])
-    bytes_per_nnz = 4 + sv  # x cached, as the reference's simulate (cached_x=true)
-    doc = {"matrix": a.mtx or f"synthetic:{a.case}", "format": a.format,
-           "precision": a.precision, "nnz": m["nnz"], "artificial_zeros": m["artificial_zeros"],
-           "transactions": {k: tx[k][0] for k in ("values", "columns", "x", "output")},
-           "min_possible": ideal, "efficiency": ideal / total if total else 1.0,
-           "cache": {"hits": hits, "misses": max(0, tx["x"][0] - hits)},
-           "peak": {"bytes_per_nnz": bytes_per_nnz, "gflops": 2.0 * bw / bytes_per_nnz},
-           "metadata_sectors": tx["metadata"][0],
-           "units": "32-byte L2 sectors per launch (ncu SourceCounters), B200; "
-                    "cache = L1 global-load lookup hits of the x gathers",
-           "all_load_lookup_misses": miss_all, "kernels": kernels}
-    if a.format == "rgcsr":
-        doc["group_size"] = a.group_size
-    text = json.dumps(doc, indent=2)
-    if a.out:
-        open(a.out, "w").write(text + "\n")
-    print(text)
-
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1012_2270_b200.simulate import main  # noqa: E402
 
 if __name__ == "__main__":
     main()

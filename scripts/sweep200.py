@@ -4,10 +4,13 @@ and fp64, RgCSR G in {32, 64, 128, 256} vs Hybrid ELL+COO — the B200 analogue
 of the paper's 1,596-matrix study.
 
 For each matrix and precision: conversion + SpMV time (L2 flushed before
-every timed launch), GFLOP/s, and a parity gate: every format's y must be
-bitwise equal to the device CSR kernel's y (all accumulate in the reference's
-order), and 64 sampled rows must equal the host recomputation.  One JSON line
-per (matrix, precision); `--summary` renders the statistics table.
+every timed launch), GFLOP/s, and a parity gate against the ORACLE
+(oracle/oracle.c, pinned to the unmodified reference by
+tests/test_oracle_pinned.py): every format's y must be bitwise the oracle's
+spmv_csr y (all formats accumulate each row in the reference's order), and
+for matrices up to --array-nnz entries the converted RgCSR (G = 32) and
+Hybrid arrays must be bitwise the oracle's build_rgcsr / build_hybrid.  One
+JSON line per (matrix, precision); `--summary` renders the statistics table.
 
     python scripts/sweep200.py [--first 0 --count 200 --max-rows 10000000]
     python scripts/sweep200.py --summary gpurun_out/sweep200.jsonl
@@ -46,6 +49,7 @@ def timed(fn, stream, scratch, reps):
 def run(args):
     import torch
 
+    import oracle as orc
     from paper_1012_2270_b200 import generators as gen
     from paper_1012_2270_b200 import spmvkit as sk
     from paper_1012_2270_b200._lib import lib
@@ -62,25 +66,23 @@ def run(args):
         t_gen = time.perf_counter() - t0
         csr = sk.build_csr(m, 8, stream=sp)
         xh = gen.random_vector(m.num_cols, seed + 1)
-        sample = rng.integers(0, m.num_rows, 64)
+        om = orc.Csr(m.num_rows, m.num_cols, m.row_ptr, m.col, m.val)
         for prec in (8, 4):
             dt = torch.float64 if prec == 8 else torch.float32
             npdt = np.float64 if prec == 8 else np.float32
             x = torch.from_numpy(xh.astype(npdt)).cuda()
             c = csr if prec == 8 else sk.build_csr(m, 4, stream=sp)
-            yref = sk.spmv_csr(c, x)
+            yo = orc.spmv_csr(om, xh.astype(npdt), prec)  # the oracle's y
+            yref = torch.from_numpy(yo).cuda()
+            ycsr = sk.spmv_csr(c, x)
             torch.cuda.synchronize()
-            # host recomputation of sampled rows in the reference's order
-            yh = yref[torch.from_numpy(sample).cuda()].cpu().numpy()
-            xs = xh.astype(npdt)
-            ok = True
-            for k, r in enumerate(sample.tolist()):
-                acc = npdt(0)
-                for j in range(int(m.row_ptr[r]), int(m.row_ptr[r + 1])):
-                    acc = npdt(acc + npdt(npdt(m.val[j]) * xs[m.col[j]]))
-                ok &= acc.tobytes() == yh[k].tobytes()
             rec = {"seed": seed, "matrix": name, "rows": m.num_rows, "nnz": m.nnz, "prec": prec,
-                   "gen_s": round(t_gen, 2), "sampled_rows_bitwise": bool(ok)}
+                   "gen_s": round(t_gen, 2), "parity": "oracle",
+                   "csr_bitwise": bool(torch.equal(ycsr.view(torch.int64 if prec == 8 else
+                                                             torch.int32),
+                                                   yref.view(torch.int64 if prec == 8 else
+                                                             torch.int32)))}
+            arrays = m.nnz <= args.array_nnz
             iv = torch.int64 if prec == 8 else torch.int32
             for fmt in FORMATS:
                 y = torch.empty(m.num_rows, dtype=dt, device="cuda")
@@ -96,11 +98,19 @@ def run(args):
                     fill = sk.fill_report(h).fill_percent
                 torch.cuda.synchronize()
                 conv = (time.perf_counter() - t) * 1e3
+                same_arrays = None
+                if arrays and fmt in ("rgcsr32", "hybrid"):
+                    got = h.to_host()
+                    want = (orc.build_hybrid(om, h.slots_per_row, prec) if fmt == "hybrid"
+                            else orc.build_rgcsr(om, 32, prec))
+                    same_arrays = all(got[k].tobytes() == want[k].tobytes() for k in got
+                                      if k in want)
                 us = timed(lambda: fn(h._h, x.data_ptr(), m.num_cols, y.data_ptr(), m.num_rows, sp),
                            stream, scratch, args.reps)
                 rec[fmt] = {"gflops": round(2 * m.nnz / us / 1e3, 2), "us": round(us, 2),
                             "fill": round(fill, 2), "convert_ms": round(conv, 2),
-                            "bitwise": bool(torch.equal(y.view(iv), yref.view(iv)))}
+                            "bitwise": bool(torch.equal(y.view(iv), yref.view(iv))),
+                            "arrays_bitwise": same_arrays}
                 del h
             print(json.dumps(rec), flush=True)
             if prec == 4:
@@ -121,7 +131,9 @@ def summary(path):
         for fmt in FORMATS:
             g = [r[fmt]["gflops"] for r in rs]
             fill = [r[fmt]["fill"] for r in rs]
-            bit = all(r[fmt]["bitwise"] for r in rs) and all(r["sampled_rows_bitwise"] for r in rs)
+            bit = all(r[fmt]["bitwise"] for r in rs) and all(
+                r.get("sampled_rows_bitwise", r.get("csr_bitwise", False)) for r in rs) and all(
+                r[fmt].get("arrays_bitwise") is not False for r in rs)
             if fmt == "hybrid":
                 out.append(f"| {fmt} | {statistics.mean(g):.1f} | {max(g):.1f} | "
                            f"{statistics.mean(fill):.1f} | — | — | {bit} |")
@@ -141,6 +153,8 @@ def main():
     ap.add_argument("--count", type=int, default=200)
     ap.add_argument("--max-rows", type=int, default=10_000_000)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--array-nnz", type=int, default=60_000_000,
+                    help="compare converted arrays with the oracle up to this many entries")
     ap.add_argument("--summary")
     a = ap.parse_args()
     if a.summary:

@@ -1,11 +1,7 @@
-"""scripts/simulate.py attribution of ncu per-instruction sectors to the
-reference `simulate` report's arrays (values / columns / x / output), CPU only."""
-import os
-import sys
-
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                "scripts"))
-import simulate  # noqa: E402
+"""paper_1012_2270_b200.simulate: attribution of ncu per-instruction sectors
+to the reference `simulate` report's arrays (values / columns / x / output),
+CPU only."""
+from paper_1012_2270_b200 import simulate
 
 HDR = ["Address", "Source", "Access Operation", "Access Size", "L2 Theoretical Sectors Global",
        "L2 Theoretical Sectors Global Ideal"]
