@@ -63,10 +63,19 @@ def peaks():
 
 
 def committed_traffic(key):
-    """ncu dram bytes per launch of the dominant kernel (profiles/traffic.json)."""
+    """ncu dram bytes per launch of the dominant kernel (profiles/traffic.json,
+    written by scripts/ncu_summary.py from one `ncu --set full` capture)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+def traffic_source():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get("_source")
     except Exception:
         return None
 
@@ -288,6 +297,32 @@ def cpu_baseline_block(c):
                               "cpu_model", "host_threads")}
 
 
+# ---------------------------------------------------------------- K1 rate
+def convert_rate(csr, stream, peak, G=32, reps=5):
+    """Wall time of the device CSR -> RgCSR converter (spmvk_rgcsr_build: the
+    layout kernels, one 24-byte readback, the scatter), median of `reps`
+    builds after a warm one, against its algorithmic bytes: the CSR read
+    (row pointers, columns, values) and the RgCSR arrays written."""
+    import torch
+    from paper_1012_2270_b200 import spmvkit as sk
+    sk.build_rgcsr(csr, G, 8, stream=stream.cuda_stream)
+    times, a = [], None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        a = sk.build_rgcsr(csr, G, 8, stream=stream.cuda_stream)
+        times.append(time.perf_counter() - t)
+        del a
+    a = sk.build_rgcsr(csr, G, 8, stream=stream.cuda_stream)
+    nnz, rows = a.nnz(), a.num_rows
+    bytes_ = 4 * (rows + 1) + 12 * nnz + a.info.bytes_double
+    med = statistics.median(times)
+    return {"ms": med * 1e3, "bytes": bytes_, "gbs": bytes_ / med / 1e9,
+            "frac_of_peak": bytes_ / med / 1e9 / peak,
+            "what": "spmvk_rgcsr_build G=32 fp64, host wall time incl. its readback and "
+                    "allocation, median of %d; bytes = CSR read + RgCSR written" % reps}
+
+
 # ---------------------------------------------------------------- scaling anchor
 def scale_anchor(args, peak):
     """BASELINE configs[4] at N = 1: 7-point 512^3 fp64 (938 M nnz, 13.4 GB of
@@ -504,6 +539,7 @@ def run_ours(args):
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "bytes_per_launch": B, "kernel_us": kern_ms * 1e3,
                      "traffic": traffic,
+                     "traffic_source": traffic_source(),
                      # the peak above is a copy (half writes); SpMV traffic is ~98 % reads
                      "read_stream_peak": READ_STREAM_GBS,
                      "frac_read_stream": achieved / READ_STREAM_GBS,
@@ -521,6 +557,7 @@ def run_ours(args):
         "parity": ("checksum == the unmodified reference's (CPU run above and the golden)"
                    if golden is not None else "checksum == the CPU reference run above"),
         "convert_ms": {"csr_ingest": t_csr * 1e3, "rgcsr_g32_f64": t_conv * 1e3},
+        "convert": convert_rate(csr, stream, peak),
         "variants": variants,
         "scale_anchor": anchor,
     }

@@ -4,6 +4,7 @@
 #include "common.cuh"
 
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -42,6 +43,46 @@ void require_device() {
 HostStage& host_stage() {
   static thread_local HostStage st;
   return st;
+}
+
+namespace {
+struct ScratchCache {
+  std::mutex mu;
+  std::map<std::tuple<int, cudaStream_t, uint64_t>, std::vector<void*>> free;
+};
+ScratchCache& scratch_cache() {
+  static ScratchCache* c = new ScratchCache();  // never destroyed: blocks live for the process
+  return *c;
+}
+}  // namespace
+
+void* scratch_get(cudaStream_t s, uint64_t bytes, uint64_t* cls) {
+  uint64_t c = 256;
+  while (c < bytes) c <<= 1;
+  *cls = c;
+  int dev = 0;
+  SPMVK_CUDA(cudaGetDevice(&dev));
+  ScratchCache& sc = scratch_cache();
+  {
+    std::lock_guard<std::mutex> lk(sc.mu);
+    auto& v = sc.free[{dev, s, c}];
+    if (!v.empty()) {
+      void* p = v.back();
+      v.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  SPMVK_CUDA(cudaMalloc(&p, c));
+  return p;
+}
+
+void scratch_put(cudaStream_t s, void* p, uint64_t cls) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  ScratchCache& sc = scratch_cache();
+  std::lock_guard<std::mutex> lk(sc.mu);
+  sc.free[{dev, s, cls}].push_back(p);
 }
 
 // Scratch keyed by (device, stream): work on one stream is ordered, so calls

@@ -87,21 +87,28 @@ struct DevBuf {
   uint64_t bytes() const { return n * sizeof(T); }
 };
 
-// Stream-ordered temporary (cudaMallocAsync / cudaFreeAsync from the
-// device's default memory pool): no device-wide synchronisation on alloc or
-// free, so a converter's scratch arrays cost no host round trips.
+// Stream-ordered temporaries from a per-(device, stream) cache of device
+// blocks (power-of-two size classes, allocated with cudaMalloc on a miss and
+// kept for the process): a block returned by one call is reused by the next
+// call on the SAME stream, which is ordered after every use of it, so a
+// converter's scratch costs neither cudaFree's device-wide synchronisation
+// nor a pool re-map.  (cudaMallocAsync from the default pool was measured
+// 10-200x slower here: the pool trims at every synchronisation.)
+void* scratch_get(cudaStream_t s, uint64_t bytes, uint64_t* cls);
+void scratch_put(cudaStream_t s, void* p, uint64_t cls);
+
 template <class T>
 struct TmpBuf {
   T* p = nullptr;
-  uint64_t n = 0;
+  uint64_t n = 0, cls = 0;
   cudaStream_t s = nullptr;
   TmpBuf(uint64_t count, cudaStream_t st) : n(count), s(st) {
-    SPMVK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count + 64, st));
+    p = static_cast<T*>(scratch_get(st, sizeof(T) * count + 64, &cls));
   }
   TmpBuf(const TmpBuf&) = delete;
   TmpBuf& operator=(const TmpBuf&) = delete;
   ~TmpBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) scratch_put(s, p, cls);
   }
 };
 

@@ -254,7 +254,10 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
 // slots are in flight, so a row costs two dependent round trips (slots, x)
 // like the ELLPACK kernel.  Per row the adds stay in slot order -> y bitwise
 // spmv_rgcsr's.
-template <class T, int U, bool kNoLen, bool kMpf, class Epi>
+// kGatherK: gather x for every slot < K (pads read x[0], harmless) and
+// predicate only the adds on the length, so no load depends on the x[0]
+// probe or the row length.
+template <class T, int U, bool kNoLen, bool kMpf, class Epi, bool kGatherK = false>
 __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_shift,
                                               const uint32_t* __restrict__ gp,
                                               const uint32_t* __restrict__ lens,
@@ -323,7 +326,7 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
       // ptxas interleaves and the value loads trail by a full DRAM round trip
       __syncwarp(__activemask());
 #pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = j + u < lim ? ld_x(x + c[u]) : T(0);
+      for (int u = 0; u < U; ++u) xv[u] = (kGatherK || j + u < lim) ? ld_x(x + c[u]) : T(0);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -339,7 +342,8 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
       for (int u = 0; u < U - 1; ++u) c[u] = j + u < K ? ld_stream(cp + u * s) : 0u;
       __syncwarp(__activemask());
 #pragma unroll
-      for (int u = 0; u < U - 1; ++u) xv[u] = j + u < lim ? ld_x(x + c[u]) : T(0);
+      for (int u = 0; u < U - 1; ++u)
+        xv[u] = (kGatherK ? j + u < K : j + u < lim) ? ld_x(x + c[u]) : T(0);
 #pragma unroll
       for (int u = 0; u < U - 1; ++u)
         if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -348,13 +352,13 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
   }
 }
 
-template <class T, bool kScaled, int U, int MINB, bool kNoLen, bool kMpf>
+template <class T, bool kScaled, int U, int MINB, bool kNoLen, bool kMpf, bool kGatherK = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t x_pf_elems /* long_cut slot: no long rows here */) {
-  grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>>(
+  grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>, kGatherK>(
       rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale},
       x_pf_elems);
 }

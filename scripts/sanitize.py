@@ -110,4 +110,62 @@ for rk in ranks:
 for w in wins:
     w.close()
 torch.cuda.synchronize()
+# round 2: every kept K2 variant (incl. the L2-hinted ones) and the Hybrid
+# group-walk shapes on the same matrices, the empty-column shape, an offset
+# (8-byte aligned) x view, the NCCL iterated product at world size 1, and the
+# bounded barrier timing out on a missing peer
+om = orc.powerlaw(20000, 7)
+m = triplets(om)
+for prec, dt in ((8, np.float64), (4, np.float32)):
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    want = orc.spmv_rgcsr(orc.build_rgcsr(om, 32, prec), x)[0]
+    a = sk.build_rgcsr(m, 32, prec)
+    for v in ("liteh", "lite8h", "pipe", "lite8", "lite"):
+        lib().spmvk_set_rgcsr_kernel(v.encode())
+        assert sk.spmv_rgcsr(a, torch.from_numpy(x).cuda()).cpu().numpy().tobytes() == \
+            want.tobytes(), v
+    lib().spmvk_set_rgcsr_kernel(b"auto")
+    for name, o2 in (("5pt", orc.stencil(5, 64)), ("27pt", orc.stencil(27, 16)), ("pl", om)):
+        h = sk.build_hybrid(triplets(o2), None, prec)
+        x2 = orc.random_vector(o2.cols, 1).astype(dt)
+        want = orc.spmv_hybrid(orc.build_hybrid(o2, None, prec), x2)
+        for v in ("g6", "g7", "g8", "g8r", "litefh", "auto"):
+            lib().spmvk_set_hybrid_kernel(v.encode())
+            assert sk.spmv_hybrid(h, torch.from_numpy(x2).cuda()).cpu().numpy().tobytes() == \
+                want.tobytes(), (name, v)
+    lib().spmvk_set_hybrid_kernel(b"auto")
+e = sk.build_rgcsr(sk.TripletMatrix(100, 0, np.zeros(101, np.uint32), np.zeros(0, np.uint32),
+                                    np.zeros(0)), 32)
+assert not sk.spmv_rgcsr(e, torch.empty(0, dtype=torch.float64, device="cuda")).any()
+o5 = orc.stencil(5, 64)
+buf = torch.zeros(o5.cols + 1, dtype=torch.float64, device="cuda")
+buf[1:] = torch.from_numpy(orc.random_vector(o5.cols, 1)).cuda()
+want = orc.spmv_rgcsr(orc.build_rgcsr(o5, 32), orc.random_vector(o5.cols, 1))[0]
+assert sk.spmv_rgcsr(sk.build_rgcsr(triplets(o5), 32), buf[1:]).cpu().numpy().tobytes() == \
+    want.tobytes()
+for mode in ("allgather", "halo"):
+    comm = pt.NcclComm.init_rank(pt.NcclComm.unique_id(), 1, 0, 0)
+    sl = pt.slab_bounds(csr.num_rows, 32, 1)[0]
+    it = pt.NcclIteratedSpmv(comm, sl, sk.build_rgcsr(csr, 32, 8), csr.num_rows, mode,
+                             torch.cuda.current_stream().cuda_stream)
+    it.set_x(x0)
+    for _ in range(3):
+        it.step()
+    torch.cuda.synchronize()
+    it.close()
+    comm.close()
+wins = [pt.ExchangeWindow(csr.num_rows, 8) for _ in range(2)]
+sl2 = pt.slab_bounds(csr.num_rows, 32, 2)
+it = pt.FusedIteratedSpmv(sl2[0], [(0, csr.num_rows)] * 2,
+                          sk.build_rgcsr(csr, 32, 8, row_range=(sl2[0].row_begin,
+                                                                sl2[0].row_end)),
+                          wins[0], 2, torch.cuda.current_stream().cuda_stream,
+                          local_windows=wins, barrier=True)
+lib().spmvk_dist_set_timeout_ms(it._d, 50)
+it.step()
+assert lib().spmvk_dist_status(it._d, None) == 4
+it.close()
+for w in wins:
+    w.close()
+torch.cuda.synchronize()
 print("sanitize pass ok")
