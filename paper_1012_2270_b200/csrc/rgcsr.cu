@@ -343,8 +343,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // evict_first, x evict_last), for matrices whose x competes with a large
 // slot stream for L2 (power-law).
 enum class K2 {
-  kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64,
-  kGrp6O, kGrp7O, kGrp8O, kGrp6U, kGrp7U, kGrp8U, kGrp8RU, kGrp6N
+  kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -389,10 +388,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"auto", K2::kAuto},         {"pipe", K2::kPipe},         {"lite", K2::kLite},
       {"lite8", K2::kLite8},       {"lite8_full", K2::kLite8Full}, {"vec2", K2::kVec2},
       {"grp6", K2::kGrp6},         {"grp7_mpf", K2::kGrp7Mpf},  {"grp8", K2::kGrp8},
-      {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H},
-      {"grp6o", K2::kGrp6O},       {"grp7o", K2::kGrp7O},       {"grp8o", K2::kGrp8O},
-      {"grp6u", K2::kGrp6U},       {"grp7u", K2::kGrp7U},       {"grp8u", K2::kGrp8U},
-      {"grp8ru", K2::kGrp8RU},     {"grp6n", K2::kGrp6N}};
+      {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -448,27 +444,6 @@ __global__ void spmv_empty(uint64_t rows, T* __restrict__ y, T* __restrict__ x_n
   }
 }
 
-// A non-blocking side stream + fork / join events per (device, stream).
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-
-SideStream& side_stream(cudaStream_t user) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, SideStream> m;
-  int dev = 0;
-  SPMVK_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lk(mu);
-  SideStream& ss = m[{dev, user}];
-  if (!ss.s) {
-    SPMVK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
-    SPMVK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
-    SPMVK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
-  }
-  return ss;
-}
-
 template <class T, bool kScaled>
 void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cudaStream_t s) {
   if (h->rows == 0) return;
@@ -519,30 +494,17 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     SPMVK_LAUNCH("rgcsr_spmv_grp");
   };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
-  // SPMVK_LONG_OVERLAP=1: the long-row kernel runs on a forked side stream,
-  // launched FIRST, concurrently with the thread-per-row kernel (they write
-  // disjoint rows of y), joined back into s before the call returns
-  static const bool overlap = [] {
-    const char* e = std::getenv("SPMVK_LONG_OVERLAP");
-    return e && std::atoi(e) != 0;
-  }();
   auto run = [&](auto kern) {
     int per_sm = 0;
     SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
-    SideStream* side = (h->n_long && overlap) ? &side_stream(s) : nullptr;
-    if (side) {
-      SPMVK_CUDA(cudaEventRecord(side->fork, s));
-      SPMVK_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
-      launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, side->s, hinted);
-      SPMVK_CUDA(cudaEventRecord(side->join, side->s));
-    }
     kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
                               h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
                               h->columns.p, x, y, x_next, scale, long_cut);
     SPMVK_LAUNCH("rgcsr_spmv (thread per row)");
-    if (side) SPMVK_CUDA(cudaStreamWaitEvent(s, side->join, 0));
-    else if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s, hinted);
+    // the long rows after it on the same stream (a forked concurrent launch
+    // was measured 13 % slower: profiles/r02_ab.md)
+    if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s, hinted);
   };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
   auto run_vec = [&](auto kern) {
@@ -562,19 +524,13 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
 
   switch (k) {
     // group-uniform walk: <T, kScaled, U, MINB, kNoLen, kMpf>
-    case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true>); break;
-    case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true>); break;
+    // grp6 / grp7_mpf gather x for every slot < K (kGatherK): 5-pt 2048^2
+    // fp32 35.1 vs 35.5 us, fp64 47.3 vs 47.4; 27-pt fp32 75.5 vs 75.7
+    // (profiles/r02_ab.md); 6 CTAs / SM or no metadata prefetch lost 4-11 %
+    case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true>); break;
+    case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true>); break;
     case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
     case K2::kGrp8R64: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
-    // one more resident CTA per SM (register cap 40 / 40 / 40)
-    case K2::kGrp6O: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 6, true, true>); break;
-    case K2::kGrp7O: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 6, true, true>); break;
-    case K2::kGrp8O: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 6, true, true>); break;
-    case K2::kGrp6U: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true>); break;
-    case K2::kGrp7U: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true>); break;
-    case K2::kGrp8U: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true, true>); break;
-    case K2::kGrp8RU: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true, true>); break;
-    case K2::kGrp6N: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, false>); break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
@@ -1002,7 +958,7 @@ int spmvk_set_rgcsr_kernel(const char* name) {
     if (!name || !parse_k2(name, &k))
       fail(SPMVK_EINVAL, std::string("unknown RgCSR kernel variant '") + (name ? name : "") +
                              "' (auto | grp6 | grp7_mpf | grp8 | grp8_r64 | lite | lite8 | "
-                             "lite8_full | liteh | lite8h | vec2 | pipe | grp6o | grp7o | grp8o)");
+                             "lite8_full | liteh | lite8h | vec2 | pipe)");
     k2_slot().store(static_cast<int>(k));
   });
 }
