@@ -483,16 +483,33 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   const bool xpf = x_aligned && (xpf_env >= 0 ? xpf_env > 0
                                               : (2 * h->slots <= 11 * h->rows &&
                                                  h->cols * sizeof(T) <= (48ull << 20)));
-  auto run_grp = [&](auto kern) {
+  // SPMVK_PDL=1: the grp kernels with programmatic dependent launch
+  static const bool pdl = [] {
+    const char* e = std::getenv("SPMVK_PDL");
+    return e && std::atoi(e) != 0;
+  }();
+  auto launch_grp = [&](auto kern, bool programmatic) {
     int per_sm = 0;
     SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
-    kern<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
-                              h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
-                              h->columns.p, x, y, x_next, scale,
-                              xpf ? static_cast<uint32_t>(h->cols) : 0u);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = programmatic ? 1 : 0;
+    SPMVK_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<uint32_t>(h->rows), G, sh,
+                                  (const uint32_t*)h->group_pointers.p,
+                                  (const uint32_t*)h->row_lengths.p,
+                                  reinterpret_cast<const T*>(h->values.p),
+                                  (const uint32_t*)h->columns.p, x, y, x_next, scale,
+                                  xpf ? static_cast<uint32_t>(h->cols) : 0u));
     SPMVK_LAUNCH("rgcsr_spmv_grp");
   };
+  auto run_grp = [&](auto kern) { launch_grp(kern, false); };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -530,7 +547,10 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true>); break;
     case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true>); break;
     case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
-    case K2::kGrp8R64: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>); break;
+    case K2::kGrp8R64:
+      if (pdl) launch_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true, false, true>, true);
+      else run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>);
+      break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;

@@ -257,7 +257,13 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
 // kGatherK: gather x for every slot < K (pads read x[0], harmless) and
 // predicate only the adds on the length, so no load depends on the x[0]
 // probe or the row length.
-template <class T, int U, bool kNoLen, bool kMpf, class Epi, bool kGatherK = false>
+// kPdl: launched with programmatic stream serialisation -- the grid lets
+// the next launch's CTAs start as its own retire (griddepcontrol
+// .launch_dependents), and waits for the previous grid (griddepcontrol.wait:
+// complete and its memory visible) before its first access to x or y; only
+// the immutable matrix metadata is read before that.
+template <class T, int U, bool kNoLen, bool kMpf, class Epi, bool kGatherK = false,
+          bool kPdl = false>
 __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_shift,
                                               const uint32_t* __restrict__ gp,
                                               const uint32_t* __restrict__ lens,
@@ -276,11 +282,22 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
     for (uint64_t o = b0; o < b1; o += 65536)
       bulk_prefetch_l2(reinterpret_cast<const char*>(x) + o, (uint32_t)min((uint64_t)65536, b1 - o));
   }
-  const bool use_len = !kNoLen || !isfinite(__ldg(x));
   const uint32_t ntiles = (rows + 255) / 256;
   struct Meta {
     uint32_t b0, b1, len;
   };
+  uint32_t pre_b0 = 0, pre_b1 = 0;  // kPdl: the first row's group pointers, before the wait
+  if constexpr (kPdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t r0 = blockIdx.x * 256 + threadIdx.x;
+    if (blockIdx.x < ntiles && r0 < rows) {
+      const uint32_t g0 = g_shift >= 0 ? (r0 >> g_shift) : r0 / G;
+      pre_b0 = ld_stream(gp + g0);
+      pre_b1 = ld_stream(gp + g0 + 1);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  const bool use_len = !kNoLen || !isfinite(__ldg(x));
   auto load_meta = [&](uint32_t r) {
     const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
     Meta m;
@@ -292,7 +309,10 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
   Meta nxt{0, 0, 0};
   if (kMpf) {
     const uint32_t r0 = blockIdx.x * 256 + threadIdx.x;
-    if (blockIdx.x < ntiles && r0 < rows) nxt = load_meta(r0);
+    if (blockIdx.x < ntiles && r0 < rows) {
+      if constexpr (kPdl) nxt = Meta{pre_b0, pre_b1, use_len ? ld_stream(lens + r0) : 0u};
+      else nxt = load_meta(r0);
+    }
   }
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t r = tile * 256 + threadIdx.x;
@@ -352,13 +372,14 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
   }
 }
 
-template <class T, bool kScaled, int U, int MINB, bool kNoLen, bool kMpf, bool kGatherK = false>
+template <class T, bool kScaled, int U, int MINB, bool kNoLen, bool kMpf, bool kGatherK = false,
+          bool kPdl = false>
 __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
     T* __restrict__ x_next, T scale, uint32_t x_pf_elems /* long_cut slot: no long rows here */) {
-  grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>, kGatherK>(
+  grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>, kGatherK, kPdl>(
       rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale},
       x_pf_elems);
 }
@@ -679,6 +700,79 @@ __device__ __forceinline__ void long_rows_epi(
 // slot order, so y stays bitwise.  Singles (the other long rows) take the
 // warp-per-row path above.  One kernel for both lists: item i < n_single is
 // single row single_rows[i], else quad quads[i - n_single].
+// Sequential sum of n staged products p[0..n) onto acc, in order; the next
+// 8 products are loaded from shared memory while the current 8 are added.
+template <class T>
+__device__ __forceinline__ T ordered_sum(const T* __restrict__ p, uint32_t n, T acc) {
+  uint32_t q = 0;
+  if (n >= 8) {
+    T a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = p[u];
+    for (q = 8; q + 8 <= n; q += 8) {
+      T b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) b[u] = p[q + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = add_rn(acc, a[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = b[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = add_rn(acc, a[u]);
+  }
+  for (; q < n; ++q) acc = add_rn(acc, p[q]);
+  return acc;
+}
+
+// One long row per L lanes (L = 32: a single; L = 8: one of a quad's four
+// rows), K slots per lane per round, software-pipelined: the next round's
+// slot loads are issued before this round's ordered adds, so the DRAM
+// latency of the slot stream hides behind the sequential add chain.  Lane l
+// of the row handles slots j0 + l + L*k; products go to pr[l + L*k]; lane
+// l == 0 adds them in slot order (the reference's rounding sequence).
+template <class T, int L, int K, bool kHint>
+__device__ __forceinline__ T long_row_walk(uint32_t len, uint32_t lmax, int l,
+                                           const T* __restrict__ vp,
+                                           const uint32_t* __restrict__ cp, uint32_t s,
+                                           const T* __restrict__ x, T* __restrict__ pr,
+                                           const Ldr<kHint>& ld) {
+  constexpr uint32_t W = L * K;
+  uint32_t c[K];
+  T v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t j = l + L * k;
+    c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
+    v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
+  }
+  T acc = T(0);
+  for (uint32_t j0 = 0; j0 < lmax; j0 += W) {
+    __syncwarp();  // scheduling fence, and the previous round's adds are done
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t j = j0 + l + L * k;
+      if (j < len) pr[l + L * k] = mul_rn(v[k], ld.x(x + c[k]));
+    }
+    const uint32_t jn = j0 + W;  // next round's slots, in flight during the adds
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t j = jn + l + L * k;
+      c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
+      v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
+    }
+    __syncwarp();
+    if (l == 0 && j0 < len) acc = ordered_sum(pr, min(W, len - j0), acc);
+  }
+  __syncwarp();
+  return acc;
+}
+
+// The rows past the long-row cut, one launch, two work lists: item i <
+// n_single is row single_rows[i] (warp per row, longest first), else quad
+// quads[i - n_single]: four consecutive long rows of one group (r0 % 4 == 0),
+// lane 8 q + l on row q's slots l, l+8, ..., so the four rows' slot j is ONE
+// 32-byte sector (a quarter of the uncoalesced requests of one row per warp).
 template <class T, class Epi, bool kHint = false>
 __device__ __forceinline__ void long_mixed_epi(
     uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
@@ -692,49 +786,18 @@ __device__ __forceinline__ void long_mixed_epi(
   const uint32_t items = n_single + n_quad;
   const Ldr<kHint> ld;
   for (uint32_t i = blockIdx.x * 8 + warp; i < items; i += gridDim.x * 8) {
-    if (i < n_single) {  // one row per warp (as long_rows_epi)
+    if (i < n_single) {  // one row per warp
       const uint32_t r = single_rows[i];
       const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-      const uint32_t t = r - g * G;
       const uint32_t s = min(G, rows - g * G);
       const uint32_t len = lens[r];
-      const T* __restrict__ vp = values + gp[g] + t;
-      const uint32_t* __restrict__ cp = columns + gp[g] + t;
-      T acc = T(0);
-      for (uint32_t j0 = 0; j0 < len; j0 += W) {
-        uint32_t c[K];
-        T v[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const uint32_t j = j0 + lane + 32 * k;
-          c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
-          v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const uint32_t j = j0 + lane + 32 * k;
-          if (j < len) prod[warp][lane + 32 * k] = mul_rn(v[k], ld.x(x + c[k]));
-        }
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t n = min((uint32_t)W, len - j0);
-          uint32_t q = 0;
-          for (; q + 8 <= n; q += 8) {
-            T p[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) p[u] = prod[warp][q + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
-          }
-          for (; q < n; ++q) acc = add_rn(acc, prod[warp][q]);
-        }
-        __syncwarp();
-      }
+      const uint32_t off = gp[g] + (r - g * G);
+      const T acc = long_row_walk<T, 32, K, kHint>(len, len, lane, values + off, columns + off,
+                                                   s, x, prod[warp], ld);
       if (lane == 0) epi(r, acc);
       continue;
     }
-    // quad: rows r0..r0+3 of one group
+    // quad: rows r0..r0+3 of one group, 8 lanes per row, 64 slots per round
     const uint32_t r0 = quads[i - n_single];
     const int q = lane >> 3, l = lane & 7;
     const uint32_t r = r0 + q;
@@ -745,40 +808,8 @@ __device__ __forceinline__ void long_mixed_epi(
 #pragma unroll
     for (int o = 8; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     const uint32_t off = gp[g] + (r - g * G);
-    const T* __restrict__ vp = values + off;
-    const uint32_t* __restrict__ cp = columns + off;
-    T* pq = &prod[warp][q * (W / 4)];  // 64 products of row q per round
-    T acc = T(0);
-    for (uint32_t j0 = 0; j0 < lmax; j0 += W / 4) {
-      uint32_t c[K];
-      T v[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t j = j0 + l + 8 * k;
-        c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
-        v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
-      }
-      __syncwarp();  // scheduling fence: every slot load before the gathers
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t j = j0 + l + 8 * k;
-        if (j < len) pq[l + 8 * k] = mul_rn(v[k], ld.x(x + c[k]));
-      }
-      __syncwarp();
-      if (l == 0 && j0 < len) {
-        const uint32_t n = min((uint32_t)(W / 4), len - j0);
-        uint32_t u0 = 0;
-        for (; u0 + 8 <= n; u0 += 8) {
-          T p[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) p[u] = pq[u0 + u];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc = add_rn(acc, p[u]);
-        }
-        for (; u0 < n; ++u0) acc = add_rn(acc, pq[u0]);
-      }
-      __syncwarp();
-    }
+    const T acc = long_row_walk<T, 8, K, kHint>(len, lmax, l, values + off, columns + off, s, x,
+                                                &prod[warp][q * (W / 4)], ld);
     if (l == 0) epi(r, acc);
   }
 }
