@@ -483,10 +483,15 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   const bool xpf = x_aligned && (xpf_env >= 0 ? xpf_env > 0
                                               : (2 * h->slots <= 11 * h->rows &&
                                                  h->cols * sizeof(T) <= (48ull << 20)));
-  // SPMVK_PDL=1: the grp kernels with programmatic dependent launch
+  // Programmatic dependent launch for the group walk (default; SPMVK_PDL=0
+  // turns it off): a launch may start while the previous kernel on the stream
+  // drains, reads only the immutable group pointers, and waits
+  // (griddepcontrol.wait) before touching x or y.  Back-to-back SpMVs:
+  // 27-pt 128^3 fp64 102.8 -> 101.6 us, 7-pt 256^3 245.9 -> 244.0, 5-pt
+  // 1024^2 (L2-resident) 16.2 -> 13.6 (profiles/r02_ab.md).
   static const bool pdl = [] {
     const char* e = std::getenv("SPMVK_PDL");
-    return e && std::atoi(e) != 0;
+    return !e || std::atoi(e) != 0;
   }();
   auto launch_grp = [&](auto kern, bool programmatic) {
     int per_sm = 0;
@@ -509,7 +514,10 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                                   xpf ? static_cast<uint32_t>(h->cols) : 0u));
     SPMVK_LAUNCH("rgcsr_spmv_grp");
   };
-  auto run_grp = [&](auto kern) { launch_grp(kern, false); };
+  auto run_grp = [&](auto kern, auto kern_pdl) {
+    if (pdl) launch_grp(kern_pdl, true);
+    else launch_grp(kern, false);
+  };
   // persistent grid: exactly the resident CTAs of this variant (occupancy API)
   auto run = [&](auto kern) {
     int per_sm = 0;
@@ -544,12 +552,21 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     // grp6 / grp7_mpf gather x for every slot < K (kGatherK): 5-pt 2048^2
     // fp32 35.1 vs 35.5 us, fp64 47.3 vs 47.4; 27-pt fp32 75.5 vs 75.7
     // (profiles/r02_ab.md); 6 CTAs / SM or no metadata prefetch lost 4-11 %
-    case K2::kGrp6: run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true>); break;
-    case K2::kGrp7Mpf: run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true>); break;
-    case K2::kGrp8: run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>); break;
+    case K2::kGrp6:
+      run_grp(rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true>,
+              rgcsr_spmv_grp<T, kScaled, 6, 5, true, true, true, true>);
+      break;
+    case K2::kGrp7Mpf:
+      run_grp(rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true>,
+              rgcsr_spmv_grp<T, kScaled, 7, 5, true, true, true, true>);
+      break;
+    case K2::kGrp8:
+      run_grp(rgcsr_spmv_grp<T, kScaled, 8, 5, true, true>,
+              rgcsr_spmv_grp<T, kScaled, 8, 5, true, true, false, true>);
+      break;
     case K2::kGrp8R64:
-      if (pdl) launch_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true, false, true>, true);
-      else run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>);
+      run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>,
+              rgcsr_spmv_grp<T, kScaled, 8, 4, true, true, false, true>);
       break;
     case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
     case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
