@@ -210,23 +210,20 @@ void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
  * y.  (No reference counterpart: the CPU reference has no cache control.) */
 int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double hit_ratio,
                            uint64_t* granted);
-/* Tuning knob (process-wide): which K2 kernel runs -- "auto" (default: for
- * matrices without long rows and <= 10 % padding the group-uniform walk,
- * grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf (fp32);
- * otherwise lite8 for fp64, lite or pipe for fp32), "grp4" / "grp6" /
- * "grp7" / "grp7_mpf" / "grp8" / "grp8_r64" / "grp8_len" (group-uniform
- * walk: U-deep slot batches bound by the group width, scheduling fence
- * before the x gathers, row_lengths skipped when x[0] is finite; _mpf
- * prefetches the next row's group pointers; grp8_len predicates on
- * row_lengths), "grpx" / "grpx8" (same walk with x staged in shared memory
- * per 256-row tile, for banded matrices; measured slower), "lite" / "lite8" /
- * "lite8_full" / "lite*_mpf" (register-lean
- * thread per row), "vec2" / "vec4" (128-bit loads of 2 / 4 rows),
- * "lite_l2pf" / "lite8_l2pf" (+ bulk L2 prefetch of the next tile), "pipe" /
- * "pipe_hi" / "pipe8" (row-metadata prefetch, predicated batches), "ldg" /
- * "ldg_pf" (first kernels), "tma" (CTA-wide bulk-async-copy ring), "wtma"
- * (per-warp bulk-async-copy streams).  All give bitwise identical y; the
- * measured comparison is in DESIGN.md §3.  Also read from SPMVK_RGCSR_KERNEL. */
+/* Tuning knob (process-wide): which K2 kernel runs.  "auto" (default:
+ * without long rows and with <= 10 % padding the group-uniform walk --
+ * grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf (fp32),
+ * launched with programmatic dependent launch unless SPMVK_PDL=0; otherwise
+ * lite8 for fp64, lite or pipe for fp32, plus the long-row kernel),
+ * "grp6" / "grp7_mpf" / "grp8" / "grp8_r64" (group-uniform walk: U-deep slot
+ * batches bound by the group width, scheduling fence before the x gathers,
+ * row_lengths skipped when x[0] is finite, next row's group pointers
+ * prefetched), "lite" / "lite8" / "lite8_full" (register-lean thread per
+ * row), "liteh" / "lite8h" (same with L2 eviction hints), "vec2" (128-bit
+ * loads of 2 / 4 rows), "pipe" (row-metadata prefetch, predicated batches,
+ * L2 hints).  All give bitwise identical y; the measured comparison (and the
+ * variants removed in round 2) are in DESIGN.md §3 and
+ * profiles/r02_k2_pruned.md.  Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
 /* Tuning knob (process-wide, read at build): rows with more than `cut` slots
  * (default 128) are handled by a warp-per-row kernel instead of one thread
@@ -234,13 +231,16 @@ int spmvk_set_rgcsr_kernel(const char* name);
 int spmvk_set_long_row_cut(uint32_t cut);
 
 /* ------------------------------------------------------------------ Hybrid */
-/* Tuning knob (process-wide): Hybrid SpMV kernel variant, "auto" (default:
- * "litef"), "v4" (first kernel: policy-hinted loads, 4-deep), "lite" /
- * "lite8" / "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at
- * 8 / 5 / 8 CTAs per SM), "litef" / "lite8f" (same, 4-deep at 8 / 8-deep
- * at 4 CTAs per SM, with a scheduling fence that issues every slot load
- * before the x gathers).  All give bitwise identical y.  Also read from
- * SPMVK_HYBRID_KERNEL. */
+/* Tuning knob (process-wide): Hybrid SpMV kernel variant.  "auto" (default:
+ * pure ELL -> the group-walk batch shape matching K1: "g6" for K1 <= 6,
+ * "litef" up to 12, "g7" beyond; with a COO part "litef", fp32 "litefh"),
+ * "v4" (first kernel: policy-hinted loads, 4-deep), "lite" / "lite8" /
+ * "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at 8 / 5 / 8
+ * CTAs per SM), "litef" / "lite8f" (same, 4-deep at 8 / 8-deep at 4 CTAs per
+ * SM, with a scheduling fence that issues every slot load before the x
+ * gathers), "g6" / "g7" / "g8" / "g8r" (fenced, U = 6 / 7 / 8 at 5 CTAs per
+ * SM, U = 8 at 4; pure-ELL launches only), "litefh" (litef with L2 eviction
+ * hints).  All give bitwise identical y.  Also read from SPMVK_HYBRID_KERNEL. */
 int spmvk_set_hybrid_kernel(const char* name);
 typedef struct {
   uint64_t num_rows, num_cols;
@@ -327,6 +327,9 @@ void spmvk_hybrid_destroy(spmvk_hybrid* h);
 int spmvk_cg_solve_f64(const spmvk_rgcsr* a, const double* b, double* x, uint64_t n, double tol,
                        uint64_t max_iter, uint64_t check_every, uint64_t* iters,
                        double* rel_residual, void* stream);
+/* Reductions (the dots below, spmv_dot, cg_solve) use device scratch private
+ * to the (device, stream) pair, so calls on different streams -- from one
+ * host thread or many -- never share partial sums. */
 /* y = A x and dot_out (device scalar) = sum_r x[x_offset + r] * y[r] -- CG's
  * p.q fused into the SpMV's row epilogue (rows of a square matrix or of a row
  * slab whose rows start at global row x_offset).  Deterministic (fixed
