@@ -64,6 +64,15 @@ int spmvk_abi_version(void);
 /* Selects the CUDA device for subsequent calls on this thread and checks it
  * is an sm_100-class part. */
 int spmvk_init(int device);
+/* Handle arrays (format values / columns / pointers, >= 1 MiB) released by
+ * *_destroy are kept in a per-device block cache and reused by the next
+ * build of a similar size (no cudaMalloc page mapping, no cudaFree device
+ * synchronisation; a reused block is handed out after a device
+ * synchronisation).  At most SPMVK_ALLOC_CACHE_MB (default 16384, 0 = off)
+ * per device; emptied automatically when cudaMalloc runs out of memory.
+ * spmvk_empty_cache returns every cached block to the driver (device < 0:
+ * all devices), like torch.cuda.empty_cache for the caching allocator. */
+int spmvk_empty_cache(int device);
 
 /* ------------------------------------------------------------------ CSR ingest
  * Replaces TripletMatrix(num_rows, num_cols, entries) validation
@@ -229,6 +238,11 @@ int spmvk_set_rgcsr_kernel(const char* name);
  * (default 128) are handled by a warp-per-row kernel instead of one thread
  * (power-law tails).  Does not change y. */
 int spmvk_set_long_row_cut(uint32_t cut);
+/* Tuning knob (process-wide, read at launch): 1 (default) fuses the long rows
+ * into the thread-per-row kernel (its warps take the long-row items first,
+ * dynamically, then their tiles; one launch), 0 runs them as a separate
+ * launch after it.  Does not change y.  Also read from SPMVK_LONG_FUSED. */
+int spmvk_set_long_fused(int on);
 
 /* ------------------------------------------------------------------ Hybrid */
 /* Tuning knob (process-wide): Hybrid SpMV kernel variant.  "auto" (default:

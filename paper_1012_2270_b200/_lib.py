@@ -44,6 +44,7 @@ SIGNATURES = {
     "spmvk_last_error": (C.c_char_p, []),
     "spmvk_abi_version": (cint, []),
     "spmvk_init": (cint, [cint]),
+    "spmvk_empty_cache": (cint, [cint]),
     "spmvk_csr_upload": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
     "spmvk_csr_upload_device": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
     "spmvk_csr_stencil": (cint, [cint, u64, vp, C.POINTER(vp)]),
@@ -79,6 +80,7 @@ SIGNATURES = {
     "spmvk_set_hybrid_kernel": (cint, [C.c_char_p]),
     "spmvk_stream_persist_x": (cint, [vp, vp, u64, C.c_double, u64p]),
     "spmvk_set_long_row_cut": (cint, [C.c_uint32]),
+    "spmvk_set_long_fused": (cint, [cint]),
     "spmvk_csr_choose_ell_width": (cint, [vp, u64p]),
     "spmvk_choose_ell_width": (u64, [vp, u64]),
     "spmvk_hybrid_split_cost": (u64, [vp, u64, u64]),

@@ -3,6 +3,7 @@
 // checks, and the uint64 exclusive scan used for group pointers / COO offsets.
 #include "common.cuh"
 
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <mutex>
@@ -56,6 +57,94 @@ ScratchCache& scratch_cache() {
 }
 }  // namespace
 
+namespace {
+constexpr uint64_t kCacheMin = 1ull << 20;
+struct BlockCache {
+  std::mutex mu;
+  std::map<int, std::multimap<uint64_t, void*>> free;  // device -> (size, block)
+  std::map<int, uint64_t> held;
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();
+  return *c;
+}
+uint64_t cache_limit() {
+  static const uint64_t lim = [] {
+    const char* e = std::getenv("SPMVK_ALLOC_CACHE_MB");
+    return (e ? std::strtoull(e, nullptr, 10) : 16384ull) << 20;
+  }();
+  return lim;
+}
+}  // namespace
+
+void dev_cache_empty(int dev) {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& [d, m] : c.free) {
+    if (dev >= 0 && d != dev) continue;
+    if (m.empty()) continue;
+    cudaSetDevice(d);
+    for (auto& [sz, p] : m) cudaFree(p);
+    m.clear();
+    c.held[d] = 0;
+  }
+  cudaSetDevice(cur);
+}
+
+void* dev_alloc(uint64_t bytes, uint64_t* cap, int* dev) {
+  SPMVK_CUDA(cudaGetDevice(dev));
+  if (bytes >= kCacheMin && cache_limit()) {
+    void* hit = nullptr;
+    {
+      BlockCache& c = block_cache();
+      std::lock_guard<std::mutex> lk(c.mu);
+      auto& m = c.free[*dev];
+      auto it = m.lower_bound(bytes);
+      if (it != m.end() && it->first <= bytes + bytes / 4) {
+        hit = it->second;
+        *cap = it->first;
+        c.held[*dev] -= it->first;
+        m.erase(it);
+      }
+    }
+    if (hit) {
+      // kernels still reading the handle this block came from were queued
+      // before it was released: let them finish before it is rewritten
+      SPMVK_CUDA(cudaDeviceSynchronize());
+      return hit;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    dev_cache_empty(*dev);
+    e = cudaMalloc(&p, bytes);
+  }
+  SPMVK_CUDA(e);
+  *cap = bytes;
+  return p;
+}
+
+void dev_release(void* p, uint64_t cap, int dev) noexcept {
+  if (cap >= kCacheMin && cache_limit()) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (c.held[dev] + cap <= cache_limit()) {
+      c.free[dev].emplace(cap, p);
+      c.held[dev] += cap;
+      return;
+    }
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaFree(p);
+  if (cur != dev) cudaSetDevice(cur);
+}
+
 void* scratch_get(cudaStream_t s, uint64_t bytes, uint64_t* cls) {
   uint64_t c = 256;
   while (c < bytes) c <<= 1;
@@ -103,6 +192,30 @@ double* stream_scratch(cudaStream_t s, uint64_t n) {
       fail(SPMVK_EINVAL, "first reduction on this stream is inside a stream capture; "
                          "call it once eagerly first");
     b.alloc(n);
+  }
+  return b.p;
+}
+
+// Four 32-bit work counters per (device, stream), zero between launches: the
+// fused long-row kernels take items from word 0, row slices from word 2, and
+// count finished warps in word 1; the last warp resets them (rgcsr_spmv.cuh
+// LongList).  Launches
+// on one stream are ordered, so they never share a live pair.
+uint32_t* stream_counters(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, DevBuf<uint32_t>> bufs;
+  int dev = 0;
+  SPMVK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  DevBuf<uint32_t>& b = bufs[{dev, s}];
+  if (!b.p) {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    SPMVK_CUDA(cudaStreamIsCapturing(s, &cst));
+    if (cst != cudaStreamCaptureStatusNone)
+      fail(SPMVK_EINVAL, "first long-row SpMV on this stream is inside a stream capture; "
+                         "call it once eagerly first");
+    b.alloc(4);
+    SPMVK_CUDA(cudaMemsetAsync(b.p, 0, 4 * sizeof(uint32_t), s));
   }
   return b.p;
 }
@@ -246,6 +359,10 @@ int spmvk_init(int device) {
       spmvk::fail(SPMVK_ECUDA, std::string("spmvk is built for sm_100a; device ") + p.name +
                                    " is sm_" + std::to_string(p.major * 10 + p.minor));
   });
+}
+
+int spmvk_empty_cache(int device) {
+  return spmvk::guarded([&] { spmvk::dev_cache_empty(device); });
 }
 
 int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double hit_ratio,

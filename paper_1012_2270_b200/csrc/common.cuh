@@ -58,31 +58,55 @@ int guarded(F&& f) {
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // ---------------------------------------------------------------- device buffer
+// Handle arrays come from a per-device cache of released blocks (best fit,
+// at most 25 % larger than the request): rebuilding a format of the same
+// shape -- the converter in a solver loop, the bench's K1 rate -- reuses the
+// previous arrays instead of paying cudaMalloc's page mapping (~1-10 ms for
+// the 680 MB headline arrays) and cudaFree's device-wide synchronisation.
+// A reused block is handed out only after a device synchronisation, so a
+// kernel still reading the handle it came from has finished (the guarantee
+// cudaFree gives).  Blocks under 1 MiB bypass the cache; the cache holds at
+// most SPMVK_ALLOC_CACHE_MB (default 16384; 0 disables) per device, is
+// emptied and the allocation retried when cudaMalloc runs out of memory, and
+// spmvk_empty_cache() returns it to the driver.
+void* dev_alloc(uint64_t bytes, uint64_t* cap, int* dev);
+void dev_release(void* p, uint64_t cap, int dev) noexcept;
+void dev_cache_empty(int dev);  // dev < 0: every device
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
-  uint64_t n = 0;
+  uint64_t n = 0, cap = 0;
+  int dev = 0;
   DevBuf() = default;
   explicit DevBuf(uint64_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap), dev(o.dev) {
+    o.p = nullptr;
+    o.n = o.cap = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; cap = o.cap; dev = o.dev;
+      o.p = nullptr;
+      o.n = o.cap = 0;
+    }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(uint64_t count) {
     release();
-    n = count;
     // 64 spare bytes: zero-sized arrays stay valid, and 16-byte-aligned bulk
     // copies may round a range end up to 3 elements past the last one
-    SPMVK_CUDA(cudaMalloc(&p, sizeof(T) * count + 64));
+    p = static_cast<T*>(dev_alloc(sizeof(T) * count + 64, &cap, &dev));
+    n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_release(p, cap, dev);
     p = nullptr;
-    n = 0;
+    n = cap = 0;
   }
   uint64_t bytes() const { return n * sizeof(T); }
 };
@@ -286,6 +310,7 @@ struct HostStage {
 HostStage& host_stage();
 // Device scratch of >= n doubles private to (current device, stream s).
 double* stream_scratch(cudaStream_t s, uint64_t n);
+uint32_t* stream_counters(cudaStream_t s);
 
 }  // namespace spmvk
 

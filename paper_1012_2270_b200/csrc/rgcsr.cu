@@ -370,12 +370,13 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
   // 128-bit value loads win (5-pt 4096^2: fp64 220 vs 232 us, fp32 152 vs
   // 163 us); from 7 slots on they lose (profiles/r01_k2_sweep3.md)
   if (!h->n_long && 2 * h->slots <= 11 * h->rows) return K2::kVec2;
-  // long rows: the row-pipelined kernel when the rows are sorted into groups
-  // of similar length (<= 10 % padding, e.g. after descending reordering:
-  // power-law fp64 611 vs 632 us), lite8 for fp64 otherwise (1,425 vs 1,479)
-  if (h->n_long && h->slots * 10 <= h->nnz * 11) return K2::kPipe;
-  if (f64) return K2::kLite8;
+  // long rows: the row-pipelined kernel with the long rows fused in and its
+  // rows taken in dynamic 128-row slices (rgcsr_spmv_pipe_fl).  Config-3
+  // power-law 8M, best of 5 x 20 back-to-back (profiles/r02_long_fused.md):
+  // original order fp64 1,222 us (was lite8 + separate long-row launch
+  // 1,419), fp32 925 (1,044); descending order fp64 557 (607), fp32 511 (564)
   if (h->n_long) return K2::kPipe;
+  if (f64) return K2::kLite8;
   // fp32, short rows (<= ~12 slots): one 8-deep batch per row at full
   // occupancy (32 registers, no spills) keeps more slot bytes in flight
   // (7-pt 256^3: 193 vs 201 us; 5-pt 1024^2: 14.6 vs 16.7 us); longer rows
@@ -442,6 +443,16 @@ __global__ void spmv_empty(uint64_t rows, T* __restrict__ y, T* __restrict__ x_n
     y[r] = T(0);
     if (kScaled) x_next[r] = mul_rn(T(0), scale);
   }
+}
+
+// Long rows fused into the tile kernel (default) or a separate launch after
+// it: spmvk_set_long_fused() / SPMVK_LONG_FUSED=0.
+std::atomic<int>& long_fused_slot() {
+  static std::atomic<int> v{[] {
+    const char* e = std::getenv("SPMVK_LONG_FUSED");
+    return (!e || std::atoi(e) != 0) ? 1 : 0;
+  }()};
+  return v;
 }
 
 template <class T, bool kScaled>
@@ -531,6 +542,26 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
     // was measured 13 % slower: profiles/r02_ab.md)
     if (h->n_long) launch_long<T, kScaled>(h, G, sh, x, y, x_next, scale, s, hinted);
   };
+  // the long rows fused into the tile kernel (default; SPMVK_LONG_FUSED=0
+  // restores the separate launch): warps take the long-row items first, then
+  // their tiles (rgcsr_spmv.cuh long_items_dynamic)
+  auto run_fl = [&](auto kern, auto kern_fl) {
+    if (!h->n_long || !long_fused_slot().load(std::memory_order_relaxed)) return run(kern);
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_fl, 256, 0));
+    const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
+    static const uint32_t lw = [] {
+      const char* e = std::getenv("SPMVK_LONG_WARPS");
+      const int v = e ? std::atoi(e) : 2;  // 2 / 4 / 8 measured: 2 best (r02_long_fused.md)
+      return static_cast<uint32_t>(v < 1 ? 1 : v > 8 ? 8 : v);
+    }();
+    const LongList ll{static_cast<uint32_t>(h->n_singles), static_cast<uint32_t>(h->n_quads),
+                      h->long_singles.p, h->long_quads.p, stream_counters(s), lw};
+    kern_fl<<<grid, 256, 0, s>>>(static_cast<uint32_t>(h->rows), G, sh, h->group_pointers.p,
+                                 h->row_lengths.p, reinterpret_cast<const T*>(h->values.p),
+                                 h->columns.p, x, y, x_next, scale, long_cut, ll);
+    SPMVK_LAUNCH("rgcsr_spmv (long rows fused)");
+  };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
   auto run_vec = [&](auto kern) {
     constexpr uint64_t R = sizeof(T) == 8 ? 2 : 4;
@@ -568,13 +599,21 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       run_grp(rgcsr_spmv_grp<T, kScaled, 8, 4, true, true>,
               rgcsr_spmv_grp<T, kScaled, 8, 4, true, true, false, true>);
       break;
-    case K2::kLite: run(rgcsr_spmv_lite<T, kScaled, 4, 8>); break;
-    case K2::kLite8: run(rgcsr_spmv_lite<T, kScaled, 8, 5>); break;
+    case K2::kLite:
+      run_fl(rgcsr_spmv_lite<T, kScaled, 4, 8>, rgcsr_spmv_lite_fl<T, kScaled, 4, 8, false>);
+      break;
+    case K2::kLite8:
+      run_fl(rgcsr_spmv_lite<T, kScaled, 8, 5>, rgcsr_spmv_lite_fl<T, kScaled, 8, 5, false>);
+      break;
     case K2::kLite8Full: run(rgcsr_spmv_lite<T, kScaled, 8, 8>); break;
-    case K2::kLiteH: run(rgcsr_spmv_lite<T, kScaled, 4, 8, true>); break;
-    case K2::kLite8H: run(rgcsr_spmv_lite<T, kScaled, 8, 5, true>); break;
+    case K2::kLiteH:
+      run_fl(rgcsr_spmv_lite<T, kScaled, 4, 8, true>, rgcsr_spmv_lite_fl<T, kScaled, 4, 8, true>);
+      break;
+    case K2::kLite8H:
+      run_fl(rgcsr_spmv_lite<T, kScaled, 8, 5, true>, rgcsr_spmv_lite_fl<T, kScaled, 8, 5, true>);
+      break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
-    default: run(rgcsr_spmv_pipe<T, kScaled, U, 4>); break;
+    default: run_fl(rgcsr_spmv_pipe<T, kScaled, U, 4>, rgcsr_spmv_pipe_fl<T, kScaled, U, 4>); break;
   }
 }
 
@@ -973,6 +1012,10 @@ int spmvk_rgcsr_spmv_host_f32(const spmvk_rgcsr* h, const float* x, uint64_t nx,
 }
 
 void spmvk_rgcsr_destroy(spmvk_rgcsr* h) { delete h; }
+
+int spmvk_set_long_fused(int on) {
+  return guarded([&] { long_fused_slot().store(on ? 1 : 0); });
+}
 
 int spmvk_set_long_row_cut(uint32_t cut) {
   return guarded([&] {

@@ -20,6 +20,18 @@
 
 namespace spmvk {
 
+// Row epilogue of the plain / iterated SpMV: y, and x_next = y * scale.
+template <class T, bool kScaled>
+struct StoreEpi {
+  T* __restrict__ y;
+  T* __restrict__ x_next;
+  T scale;
+  __device__ __forceinline__ void operator()(uint32_t r, T acc) const {
+    y[r] = acc;
+    if (kScaled) x_next[r] = mul_rn(acc, scale);
+  }
+};
+
 // Row- and batch-pipelined thread-per-row kernel (the default for short and
 // medium rows).  Three latencies sit on a row's critical path — (row length,
 // group pointer) -> (slot columns, values) -> x gathers — so both levels are
@@ -27,12 +39,56 @@ namespace spmvk {
 // the current row runs, and batch b+1's slots are loaded (predicated on the
 // row length, so short rows and tails cost no extra round trip) before batch
 // b's x gathers.  Accumulation stays strictly in slot order.
-template <class T, bool kScaled, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
+template <class T, int U>
+__device__ __forceinline__ T pipe_row(uint32_t len, uint32_t s, const T* __restrict__ vp,
+                                      const uint32_t* __restrict__ cp, const T* __restrict__ x,
+                                      uint64_t pf, uint64_t pl) {
+  uint32_t cA[U];
+  T vA[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    cA[u] = 0;
+    vA[u] = T(0);
+    if ((uint32_t)u < len) {
+      cA[u] = ld_stream(cp + (size_t)u * s, pf);
+      vA[u] = ld_stream(vp + (size_t)u * s, pf);
+    }
+  }
+  T acc = T(0);
+  for (uint32_t j = 0; j < len; j += U) {
+    const uint32_t jn = j + U;
+    uint32_t cB[U];
+    T vB[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cB[u] = 0;
+      vB[u] = T(0);
+      if (jn + u < len) {
+        cB[u] = ld_stream(cp + (size_t)(jn + u) * s, pf);
+        vB[u] = ld_stream(vp + (size_t)(jn + u) * s, pf);
+      }
+    }
+    T xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = j + u < len ? ld_x(x + cA[u], pl) : T(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j + u < len) acc = add_rn(acc, mul_rn(vA[u], xv[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cA[u] = cB[u];
+      vA[u] = vB[u];
+    }
+  }
+  return acc;
+}
+
+template <class T, int U, class Epi>
+__device__ __forceinline__ void pipe_rows_epi(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
-    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t long_cut) {
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, uint32_t long_cut,
+    const Epi& epi) {
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,51 +111,76 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
       len_n = lens[rn];
       base_n = gp[gn];
     }
-    if (len > long_cut) {  // handled by rgcsr_spmv_long
-      r = rn;
-      continue;
-    }
-    uint32_t cA[U];
-    T vA[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      cA[u] = 0;
-      vA[u] = T(0);
-      if ((uint32_t)u < len) {
-        cA[u] = ld_stream(cp + (size_t)u * s, pf);
-        vA[u] = ld_stream(vp + (size_t)u * s, pf);
-      }
-    }
-    T acc = T(0);
-    for (uint32_t j = 0; j < len; j += U) {
-      const uint32_t jn = j + U;
-      uint32_t cB[U];
-      T vB[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        cB[u] = 0;
-        vB[u] = T(0);
-        if (jn + u < len) {
-          cB[u] = ld_stream(cp + (size_t)(jn + u) * s, pf);
-          vB[u] = ld_stream(vp + (size_t)(jn + u) * s, pf);
-        }
-      }
-      T xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = j + u < len ? ld_x(x + cA[u], pl) : T(0);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (j + u < len) acc = add_rn(acc, mul_rn(vA[u], xv[u]));
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        cA[u] = cB[u];
-        vA[u] = vB[u];
-      }
-    }
-    y[r] = acc;
-    if (kScaled) x_next[r] = mul_rn(acc, scale);
+    if (len <= long_cut) epi(r, pipe_row<T, U>(len, s, vp, cp, x, pf, pl));  // else: long rows
     r = rn;
   }
+}
+
+// The same walk with rows taken dynamically: a warp grabs 128-row slices
+// (one atomicAdd on *slice_ctr each, the next slice grabbed one ahead so its
+// row metadata can be prefetched), so a warp that spent time on long-row
+// items simply takes fewer slices -- no tail of late warps.
+template <class T, int U, class Epi>
+__device__ __forceinline__ void pipe_rows_dyn(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, uint32_t long_cut,
+    uint32_t* slice_ctr, const Epi& epi) {
+  constexpr uint32_t kSub = 4;  // 32-row sub-slices per grab
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  const uint32_t lane = threadIdx.x & 31;
+  auto grab = [&]() -> uint64_t {
+    uint32_t q = 0;
+    if (lane == 0) q = atomicAdd(slice_ctr, 1u);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    return static_cast<uint64_t>(q) * (32 * kSub);
+  };
+  uint64_t cur = grab();
+  uint64_t nxt = cur < rows ? grab() : cur;
+  uint32_t sub = 0;
+  uint64_t r = cur + lane;
+  uint32_t len_n = 0, base_n = 0;
+  if (r < rows) {
+    const uint32_t g = g_shift >= 0 ? ((uint32_t)r >> g_shift) : (uint32_t)r / G;
+    len_n = lens[r];
+    base_n = gp[g];
+  }
+  while (cur < rows) {  // warp-uniform
+    uint64_t cur_n = cur;
+    uint32_t sub_n = sub + 1;
+    if (sub_n == kSub) {
+      sub_n = 0;
+      cur_n = nxt;
+    }
+    const uint64_t rn = cur_n + sub_n * 32 + lane;
+    const uint32_t len = len_n, b0 = base_n;
+    if (rn < rows) {
+      const uint32_t gn = g_shift >= 0 ? ((uint32_t)rn >> g_shift) : (uint32_t)rn / G;
+      len_n = lens[rn];
+      base_n = gp[gn];
+    }
+    if (r < rows && len <= long_cut) {
+      const uint32_t rr = static_cast<uint32_t>(r);
+      const uint32_t g = g_shift >= 0 ? (rr >> g_shift) : rr / G;
+      const uint32_t t = rr - g * G;
+      const uint32_t s = min(G, rows - g * G);
+      epi(rr, pipe_row<T, U>(len, s, values + b0 + t, columns + b0 + t, x, pf, pl));
+    }
+    if (sub_n == 0 && cur_n < rows) nxt = grab();
+    cur = cur_n;
+    sub = sub_n;
+    r = rn;
+  }
+}
+
+template <class T, bool kScaled, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut) {
+  pipe_rows_epi<T, U>(rows, G, g_shift, gp, lens, values, columns, x, long_cut,
+                      StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
 // Lean thread-per-row kernel built for occupancy (the default K2): a CTA
@@ -113,16 +194,6 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe(
 // plain / iterated form (y, and x_next = y * scale); PeerEpi (the fused
 // distributed step, dist.cu) also stores x_next into every peer window whose
 // receive range covers the row -- over NVLink when the peer is another GPU.
-template <class T, bool kScaled>
-struct StoreEpi {
-  T* __restrict__ y;
-  T* __restrict__ x_next;
-  T scale;
-  __device__ __forceinline__ void operator()(uint32_t r, T acc) const {
-    y[r] = acc;
-    if (kScaled) x_next[r] = mul_rn(acc, scale);
-  }
-};
 
 constexpr int kMaxPeers = 8;
 template <class T>
@@ -702,24 +773,24 @@ __device__ __forceinline__ void long_rows_epi(
 // single row single_rows[i], else quad quads[i - n_single].
 // Sequential sum of n staged products p[0..n) onto acc, in order; the next
 // 8 products are loaded from shared memory while the current 8 are added.
-template <class T>
+template <class T, int B = 8>
 __device__ __forceinline__ T ordered_sum(const T* __restrict__ p, uint32_t n, T acc) {
   uint32_t q = 0;
-  if (n >= 8) {
-    T a[8];
+  if (n >= B) {
+    T a[B];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = p[u];
-    for (q = 8; q + 8 <= n; q += 8) {
-      T b[8];
+    for (int u = 0; u < B; ++u) a[u] = p[u];
+    for (q = B; q + B <= n; q += B) {
+      T b[B];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) b[u] = p[q + u];
+      for (int u = 0; u < B; ++u) b[u] = p[q + u];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc = add_rn(acc, a[u]);
+      for (int u = 0; u < B; ++u) acc = add_rn(acc, a[u]);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = b[u];
+      for (int u = 0; u < B; ++u) a[u] = b[u];
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = add_rn(acc, a[u]);
+    for (int u = 0; u < B; ++u) acc = add_rn(acc, a[u]);
   }
   for (; q < n; ++q) acc = add_rn(acc, p[q]);
   return acc;
@@ -731,7 +802,7 @@ __device__ __forceinline__ T ordered_sum(const T* __restrict__ p, uint32_t n, T 
 // latency of the slot stream hides behind the sequential add chain.  Lane l
 // of the row handles slots j0 + l + L*k; products go to pr[l + L*k]; lane
 // l == 0 adds them in slot order (the reference's rounding sequence).
-template <class T, int L, int K, bool kHint>
+template <class T, int L, int K, bool kHint, int B = 8>
 __device__ __forceinline__ T long_row_walk(uint32_t len, uint32_t lmax, int l,
                                            const T* __restrict__ vp,
                                            const uint32_t* __restrict__ cp, uint32_t s,
@@ -762,17 +833,56 @@ __device__ __forceinline__ T long_row_walk(uint32_t len, uint32_t lmax, int l,
       v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
     }
     __syncwarp();
-    if (l == 0 && j0 < len) acc = ordered_sum(pr, min(W, len - j0), acc);
+    if (l == 0 && j0 < len) acc = ordered_sum<T, B>(pr, min(W, len - j0), acc);
   }
   __syncwarp();
   return acc;
 }
 
-// The rows past the long-row cut, one launch, two work lists: item i <
-// n_single is row single_rows[i] (warp per row, longest first), else quad
-// quads[i - n_single]: four consecutive long rows of one group (r0 % 4 == 0),
-// lane 8 q + l on row q's slots l, l+8, ..., so the four rows' slot j is ONE
-// 32-byte sector (a quarter of the uncoalesced requests of one row per warp).
+// One long-row work item: item i < n_single is row single_rows[i] (warp per
+// row), else quad quads[i - n_single]: four consecutive long rows of one group
+// (r0 % 4 == 0), lane 8 q + l on row q's slots l, l+8, ..., so the four rows'
+// slot j is ONE 32-byte sector (a quarter of the uncoalesced requests of one
+// row per warp).  pr: this warp's 256-entry product buffer in shared memory.
+template <class T, class Epi, bool kHint, int K = 8>
+__device__ __forceinline__ void long_item(
+    uint32_t i, uint32_t n_single, const uint32_t* __restrict__ single_rows,
+    const uint32_t* __restrict__ quads, uint32_t rows, uint32_t G, int g_shift,
+    const uint32_t* __restrict__ gp, const uint32_t* __restrict__ lens,
+    const T* __restrict__ values, const uint32_t* __restrict__ columns, const T* __restrict__ x,
+    T* __restrict__ pr, const Ldr<kHint>& ld, const Epi& epi) {
+  constexpr int W = 32 * K;
+  const int lane = threadIdx.x & 31;
+  if (i < n_single) {  // one row per warp
+    const uint32_t r = single_rows[i];
+    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+    const uint32_t s = min(G, rows - g * G);
+    const uint32_t len = lens[r];
+    const uint32_t off = gp[g] + (r - g * G);
+    const T acc = long_row_walk<T, 32, K, kHint, (K >= 8 ? 8 : 4)>(len, len, lane, values + off,
+                                                                  columns + off, s, x, pr, ld);
+    if (lane == 0) epi(r, acc);
+    return;
+  }
+  // quad: rows r0..r0+3 of one group, 8 lanes per row, 64 slots per round
+  const uint32_t r0 = quads[i - n_single];
+  const int q = lane >> 3, l = lane & 7;
+  const uint32_t r = r0 + q;
+  const uint32_t g = g_shift >= 0 ? (r0 >> g_shift) : r0 / G;
+  const uint32_t s = min(G, rows - g * G);
+  const uint32_t len = lens[r];
+  uint32_t lmax = len;
+#pragma unroll
+  for (int o = 8; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  const uint32_t off = gp[g] + (r - g * G);
+  const T acc = long_row_walk<T, 8, K, kHint, (K >= 8 ? 8 : 4)>(len, lmax, l, values + off,
+                                                                 columns + off, s, x,
+                                                                 pr + q * (W / 4), ld);
+  if (l == 0) epi(r, acc);
+}
+
+// The rows past the long-row cut, one launch, two work lists (long_item),
+// statically spread over the warps of the grid.
 template <class T, class Epi, bool kHint = false>
 __device__ __forceinline__ void long_mixed_epi(
     uint32_t n_single, const uint32_t* __restrict__ single_rows, uint32_t n_quad,
@@ -782,36 +892,97 @@ __device__ __forceinline__ void long_mixed_epi(
     const Epi& epi) {
   constexpr int K = 8, W = 32 * K;
   __shared__ T prod[8][W];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const uint32_t items = n_single + n_quad;
   const Ldr<kHint> ld;
-  for (uint32_t i = blockIdx.x * 8 + warp; i < items; i += gridDim.x * 8) {
-    if (i < n_single) {  // one row per warp
-      const uint32_t r = single_rows[i];
-      const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-      const uint32_t s = min(G, rows - g * G);
-      const uint32_t len = lens[r];
-      const uint32_t off = gp[g] + (r - g * G);
-      const T acc = long_row_walk<T, 32, K, kHint>(len, len, lane, values + off, columns + off,
-                                                   s, x, prod[warp], ld);
-      if (lane == 0) epi(r, acc);
-      continue;
-    }
-    // quad: rows r0..r0+3 of one group, 8 lanes per row, 64 slots per round
-    const uint32_t r0 = quads[i - n_single];
-    const int q = lane >> 3, l = lane & 7;
-    const uint32_t r = r0 + q;
-    const uint32_t g = g_shift >= 0 ? (r0 >> g_shift) : r0 / G;
-    const uint32_t s = min(G, rows - g * G);
-    const uint32_t len = lens[r];
-    uint32_t lmax = len;
-#pragma unroll
-    for (int o = 8; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    const uint32_t off = gp[g] + (r - g * G);
-    const T acc = long_row_walk<T, 8, K, kHint>(len, lmax, l, values + off, columns + off, s, x,
-                                                &prod[warp][q * (W / 4)], ld);
-    if (l == 0) epi(r, acc);
+  for (uint32_t i = blockIdx.x * 8 + warp; i < items; i += gridDim.x * 8)
+    long_item<T, Epi, kHint>(i, n_single, single_rows, quads, rows, G, g_shift, gp, lens, values,
+                             columns, x, prod[warp], ld, epi);
+}
+
+// The long-row work lists of a matrix, for the fused kernels below: the items
+// are taken dynamically (one atomicAdd per item on ctr[0], singles longest
+// first, then the quads), so the longest rows start first and no warp idles
+// while another holds several; ctr[1] counts the warps that are done, and the
+// last one resets every word for the next launch on the stream (ctr is the
+// stream's own counter block, stream_counters(); ctr[2] is the row-slice
+// counter of pipe_rows_dyn).
+struct LongList {
+  uint32_t n_single, n_quad;
+  const uint32_t* singles;
+  const uint32_t* quads;
+  uint32_t* ctr;
+  uint32_t warps;  // warps per CTA that take items (the first `warps`); the rest stream tiles
+};
+
+// Each warp first takes long-row items until none are left, then runs its
+// share of the thread-per-row tiles: the long rows' latency-bound ordered
+// adds overlap the tile streaming of the other warps instead of running as a
+// second, mostly idle kernel after it.
+template <class T, class Epi, bool kHint, int K>
+__device__ __forceinline__ void long_items_dynamic(
+    const LongList& ll, uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ pr,
+    const Epi& epi) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t items = ll.n_single + ll.n_quad;
+  if ((threadIdx.x >> 5) >= ll.warps) return;
+  const Ldr<kHint> ld;
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(ll.ctr, 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= items) break;
+    long_item<T, Epi, kHint, K>(i, ll.n_single, ll.singles, ll.quads, rows, G, g_shift, gp, lens,
+                                values, columns, x, pr, ld, epi);
   }
+}
+
+__device__ __forceinline__ void long_items_done(const LongList& ll) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();  // this warp's last fetch is ordered before its done count
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(ll.ctr + 1, 1u) == warps - 1) {
+      atomicExch(ll.ctr, 0u);
+      atomicExch(ll.ctr + 2, 0u);
+      atomicExch(ll.ctr + 1, 0u);
+    }
+  }
+}
+
+// lite with the long rows fused (long_items_dynamic first, then the tiles);
+// KL slots per lane per round of the long walk (4 keeps the register-capped
+// lite kernels free of spills).
+template <class T, bool kScaled, int U, int MINB, bool kHint, int KL = 4>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite_fl(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut, LongList ll) {
+  __shared__ T prod[8][32 * KL];
+  const StoreEpi<T, kScaled> epi{y, x_next, scale};
+  long_items_dynamic<T, StoreEpi<T, kScaled>, kHint, KL>(ll, rows, G, g_shift, gp, lens, values,
+                                                         columns, x, prod[threadIdx.x >> 5], epi);
+  lite_tiles_epi<T, U, StoreEpi<T, kScaled>, kHint>(0, (rows + 255) / 256, rows, G, g_shift, gp,
+                                                    lens, values, columns, x, long_cut, epi);
+  long_items_done(ll);
+}
+
+// pipe with the long rows fused (the reordered power-law default).
+template <class T, bool kScaled, int U, int MINB, int KL = 4>
+__global__ void __launch_bounds__(256, MINB) rgcsr_spmv_pipe_fl(
+    uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
+    const uint32_t* __restrict__ lens, const T* __restrict__ values,
+    const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
+    T* __restrict__ x_next, T scale, uint32_t long_cut, LongList ll) {
+  __shared__ T prod[8][32 * KL];
+  const StoreEpi<T, kScaled> epi{y, x_next, scale};
+  long_items_dynamic<T, StoreEpi<T, kScaled>, true, KL>(ll, rows, G, g_shift, gp, lens, values,
+                                                        columns, x, prod[threadIdx.x >> 5], epi);
+  pipe_rows_dyn<T, U>(rows, G, g_shift, gp, lens, values, columns, x, long_cut, ll.ctr + 2, epi);
+  long_items_done(ll);
 }
 
 template <class T, bool kScaled, bool kHint = false>

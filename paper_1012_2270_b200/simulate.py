@@ -16,7 +16,8 @@ arrays by their cache operator and width:
            have identical index patterns, so the NA.32 sectors split evenly)
   x        LDG (L1-allocating, read-only) of the scalar width
   output   STG
-  (row lengths / group pointers: the remaining LDG.32, reported as "metadata")
+  (row lengths / group pointers: the remaining LDG.32, and every warp-uniform
+   load -- one sector per executed warp instruction -- reported as "metadata")
 
 and the x "cache" is the L1: hits / misses of the global-load lookups
 (`l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_{hit,miss}`; the NA
@@ -92,7 +93,7 @@ def classify(rows, sv, meta_sectors=0):
     `--page source --csv` output (each section: a "Kernel Name" row, a header
     row, then one row per SASS instruction)."""
     out = {k: [0, 0] for k in ("values", "columns", "x", "output", "metadata", "na32")}
-    ix, i = None, 0
+    ix, ix_inst, i = None, None, 0
     while i < len(rows):
         r = rows[i]
         i += 1
@@ -102,6 +103,7 @@ def classify(rows, sv, meta_sectors=0):
             ix = {k: h.index(k) for k in ("Source", "Access Operation", "Access Size",
                                           "L2 Theoretical Sectors Global",
                                           "L2 Theoretical Sectors Global Ideal")}
+            ix_inst = h.index("Instructions Executed") if "Instructions Executed" in h else None
             continue
         if ix is None or len(r) <= max(ix.values()):
             continue
@@ -116,6 +118,10 @@ def classify(rows, sv, meta_sectors=0):
             key = "output"
         elif "LDG" not in src:
             continue
+        elif ix_inst is not None and 0 < sec <= int(float(r[ix_inst] or 0)):
+            # warp-uniform loads (one sector per warp instruction): the group
+            # pointers and tile bounds, never a slot stream or an x gather
+            key = "metadata"
         elif ".NA" in src:  # streamed slots (L1 no-allocate)
             if sv == 8:
                 key = "values" if size == 64 else "columns"
@@ -172,10 +178,7 @@ def simulate(case: str = "27:128", mtx: str = None, format: str = "rgcsr",
         raw = subprocess.run([ncu, "-i", rep + ".ncu-rep", "--page", "raw", "--csv"],
                              capture_output=True, text=True, check=True).stdout
         m = json.load(open(meta))
-    meta_sec = 0
-    if sv == 4 and format == "rgcsr":  # coalesced row lengths + one group pointer per warp
-        meta_sec = (m["rows"] * 4 + 31) // 32 + (m["rows"] + 31) // 32
-    tx = classify(list(csv.reader(io.StringIO(src))), sv, meta_sec)
+    tx = classify(list(csv.reader(io.StringIO(src))), sv)
     rr = list(csv.reader(io.StringIO(raw)))
     hdr = rr[0]
 

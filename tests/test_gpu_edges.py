@@ -158,3 +158,34 @@ def test_barrier_times_out_on_a_missing_peer(cuda):
     L.spmvk_dist_destroy(d)
     for w in wins:
         w.close()
+
+
+def test_block_cache_reuse_keeps_inflight_spmv_and_arrays(cuda):
+    """Handle arrays released by destroy are reused by the next build of a
+    similar size (spmvk.h spmvk_empty_cache): a SpMV still queued on the
+    destroyed handle must finish before its block is rewritten, and a rebuilt
+    (smaller, reusing the larger block) format is bitwise the oracle's."""
+    big = sk.CsrMatrix.stencil(27, 40)
+    small = sk.CsrMatrix.stencil(27, 38)
+    x_big = torch.from_numpy(gen.random_vector(big.num_cols, 1)).cuda()
+    want_big = sk.spmv_rgcsr(sk.build_rgcsr(big, 32), x_big).cpu().numpy()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        a = sk.build_rgcsr(big, 32)
+        y = torch.empty_like(x_big)
+        with torch.cuda.stream(s1):
+            for _ in range(20):  # queue work on the handle, then release it at once
+                sk.spmv_rgcsr(a, x_big, y)
+        del a
+        b = sk.build_rgcsr(small, 32, stream=s2.cuda_stream)
+        torch.cuda.synchronize()
+        assert bitwise(y.cpu().numpy(), want_big)
+        rp, col, val = small.to_host()
+        want = orc.build_rgcsr(orc.Csr(small.num_rows, small.num_cols, rp, col, val), 32)
+        got = b.to_host()
+        for k in ("values", "columns", "group_pointers", "row_lengths"):
+            assert np.array_equal(got[k], want[k]), k
+        del b
+    assert lib().spmvk_empty_cache(-1) == 0
+    c = sk.build_rgcsr(big, 32)
+    assert bitwise(sk.spmv_rgcsr(c, x_big).cpu().numpy(), want_big)

@@ -385,3 +385,54 @@ def test_l2_persistence_window_keeps_results(cuda):
         sk.spmv_rgcsr(a, x, y)
     s.synchronize()
     assert bitwise(y.cpu().numpy(), want)
+
+
+@pytest.fixture(scope="module")
+def powerlaw_pair():
+    """A 300k-row power-law matrix in original and descending order (singles,
+    quads and short rows all present), as device CSR + oracle CSR."""
+    csr = sk.build_csr(triplets(orc.powerlaw(300_000, 7)))
+    out = {}
+    for name, c in (("orig", csr), ("desc", sk.apply_descending_permutation(csr)[0])):
+        rp, col, val = c.to_host()
+        out[name] = (c, orc.Csr(c.num_rows, c.num_cols, rp, col, val))
+    return out
+
+
+@pytest.mark.parametrize("variant", ["lite", "lite8", "liteh", "lite8h", "pipe"])
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_long_rows_fused_into_tile_kernel(cuda, powerlaw_pair, variant, fused, prec):
+    """Long rows taken by the tile kernel's warps (dynamic items, one launch)
+    or by the separate long-row launch: y and the scaled iterate bitwise the
+    oracle's, over repeated back-to-back launches (the per-stream item counter
+    must reset itself) and on two streams at once."""
+    from paper_1012_2270_b200._lib import lib
+    L = lib()
+    assert L.spmvk_set_rgcsr_kernel(variant.encode()) == 0
+    assert L.spmvk_set_long_fused(fused) == 0
+    dt = np.float64 if prec == 8 else np.float32
+    try:
+        for order in ("orig", "desc"):
+            c, om = powerlaw_pair[order]
+            a = sk.build_rgcsr(c, 32, prec)
+            want = orc.spmv_rgcsr(orc.build_rgcsr(om, 32, prec), orc.random_vector(om.cols, 1)
+                                  .astype(dt))[0]
+            x = dev(orc.random_vector(om.cols, 1).astype(dt))
+            streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+            ys = [torch.empty_like(x) for _ in range(4)]
+            for k in range(4):
+                with torch.cuda.stream(streams[k % 2]):
+                    sk.spmv_rgcsr(a, x, ys[k])
+            torch.cuda.synchronize()
+            for y in ys:
+                assert bitwise(y.cpu().numpy(), want), (order, variant)
+            if prec == 8:
+                y, xn = torch.empty_like(x), torch.empty_like(x)
+                assert L.spmvk_rgcsr_spmv_scaled_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(),
+                                                     y.numel(), xn.data_ptr(), 0.0625, None) == 0
+                torch.cuda.synchronize()
+                assert bitwise(y.cpu().numpy(), want) and bitwise(xn.cpu().numpy(), want * 0.0625)
+    finally:
+        L.spmvk_set_rgcsr_kernel(b"auto")
+        L.spmvk_set_long_fused(1)

@@ -39,3 +39,17 @@ def test_sums_every_kernel_section():
              ("STG.E.64 [R10.64], R12", "Store", 64, 2, 2))
     t = simulate.classify(a + b, 8)
     assert t["values"] == [88, 84] and t["output"] == [2, 2]
+
+
+def test_warp_uniform_loads_are_metadata():
+    """A load with at most one sector per executed warp instruction is a
+    warp-uniform read (the group pointers), never a slot stream or a gather."""
+    hdr = HDR + ["Instructions Executed"]
+    r = [["Kernel Name", "k"], hdr,
+         ["0x0", "LDG.E.NA.CONSTANT R10, [R4.64]", "Load", "32", "3456", "3456", "3456"],
+         ["0x0", "LDG.E.NA.CONSTANT R11, [R20.64]", "Load", "32", "13824", "13824", "3456"],
+         ["0x0", "LDG.E.NA.64.CONSTANT R28, [R24.64]", "Load", "64", "27648", "27648", "3456"],
+         ["0x0", "LDG.E.CONSTANT R2, [R4.64+0x4]", "Load", "32", "3456", "3456", "3456"]]
+    t = simulate.classify(r, 8)
+    assert t["metadata"] == [6912, 6912] and t["columns"] == [13824, 13824]
+    assert t["values"] == [27648, 27648]
