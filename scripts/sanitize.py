@@ -168,4 +168,37 @@ it.close()
 for w in wins:
     w.close()
 torch.cuda.synchronize()
+# round 2 (later): long rows fused into the row-pipelined kernel (dynamic
+# items + dynamic row slices) and the separate launch, both orders, repeated
+# launches on one stream (the per-stream counters reset themselves); the
+# handle-array block cache reusing a released block under a queued SpMV
+for order in ("orig", "desc"):
+    c = sk.build_csr(m) if order == "orig" else sk.apply_descending_permutation(sk.build_csr(m))[0]
+    rp, col, val = c.to_host()
+    oc = orc.Csr(c.num_rows, c.num_cols, rp, col, val)
+    for prec, dt in ((8, np.float64), (4, np.float32)):
+        x = orc.random_vector(oc.cols, 1).astype(dt)
+        want = orc.spmv_rgcsr(orc.build_rgcsr(oc, 32, prec), x)[0]
+        a = sk.build_rgcsr(c, 32, prec)
+        for fused in (1, 0):
+            lib().spmvk_set_long_fused(fused)
+            for v in ("pipe", "lite8", "lite8h", "auto"):
+                lib().spmvk_set_rgcsr_kernel(v.encode())
+                for _ in range(2):
+                    assert sk.spmv_rgcsr(a, torch.from_numpy(x).cuda()).cpu().numpy().tobytes() \
+                        == want.tobytes(), (order, prec, fused, v)
+        lib().spmvk_set_long_fused(1)
+        lib().spmvk_set_rgcsr_kernel(b"auto")
+big = sk.CsrMatrix.stencil(27, 40)
+xb = torch.from_numpy(orc.random_vector(big.num_cols, 1)).cuda()
+a = sk.build_rgcsr(big, 32)
+want = sk.spmv_rgcsr(a, xb).cpu().numpy()
+yb = torch.empty_like(xb)
+for _ in range(5):
+    sk.spmv_rgcsr(a, xb, yb)
+del a
+a = sk.build_rgcsr(big, 32)
+assert yb.cpu().numpy().tobytes() == want.tobytes()
+assert sk.spmv_rgcsr(a, xb).cpu().numpy().tobytes() == want.tobytes()
+torch.cuda.synchronize()
 print("sanitize pass ok")
