@@ -247,14 +247,19 @@ int spmvk_set_long_fused(int on);
 /* ------------------------------------------------------------------ Hybrid */
 /* Tuning knob (process-wide): Hybrid SpMV kernel variant.  "auto" (default:
  * pure ELL -> the group-walk batch shape matching K1: "g6" for K1 <= 6,
- * "litef" up to 12, "g7" beyond; with a COO part "litef", fp32 "litefh"),
+ * "litef" up to 12, "g7" beyond; with a COO part "dyn" for spmv_hybrid and
+ * "litef", fp32 "litefh" for the spmv_coo part alone),
  * "v4" (first kernel: policy-hinted loads, 4-deep), "lite" / "lite8" /
  * "lite8_full" (register-lean ELL loop, 4- or 8-deep batches at 8 / 5 / 8
  * CTAs per SM), "litef" / "lite8f" (same, 4-deep at 8 / 8-deep at 4 CTAs per
  * SM, with a scheduling fence that issues every slot load before the x
  * gathers), "g6" / "g7" / "g8" / "g8r" (fenced, U = 6 / 7 / 8 at 5 CTAs per
  * SM, U = 8 at 4; pure-ELL launches only), "litefh" (litef with L2 eviction
- * hints).  All give bitwise identical y.  Also read from SPMVK_HYBRID_KERNEL. */
+ * hints), "dyn" (spmv_hybrid with a COO part: rows in dynamic 128-row slices,
+ * each 32-row slice's COO range staged per warp -- no block barrier, no row
+ * search -- and rows with COO runs over 256 entries as warp work items taken
+ * first, longest first; other parts fall back to "litef").  All give bitwise
+ * identical y.  Also read from SPMVK_HYBRID_KERNEL. */
 int spmvk_set_hybrid_kernel(const char* name);
 typedef struct {
   uint64_t num_rows, num_cols;

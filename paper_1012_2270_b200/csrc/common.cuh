@@ -373,4 +373,8 @@ struct spmvk_hybrid {
   spmvk::DevBuf<uint32_t> heavy_rows;
   std::vector<uint32_t> heavy_rows_host;  // the same list, to clip it to a row limit
   uint64_t n_heavy = 0;
+  // Every row whose COO run exceeds kHeavyDyn, longest first: the work items
+  // of hybrid_spmv_dyn (kernel metadata).
+  spmvk::DevBuf<uint32_t> dyn_heavy;
+  uint64_t n_dyn_heavy = 0;
 };

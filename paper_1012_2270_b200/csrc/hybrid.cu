@@ -12,8 +12,11 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.cuh"
+#include "rgcsr_spmv.cuh"  // long_row_walk, LongList, long_items_done
 
 namespace spmvk {
 namespace {
@@ -602,6 +605,154 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
   }
 }
 
+// ---------------------------------------------------------------------------
+// hybrid_spmv_dyn -- Hybrid with a COO part, without block barriers.
+//
+// The staged-tile kernel above spends ~22 % of its stall samples at the
+// __syncthreads of its COO staging and another ~7 % in the per-row binary
+// search of the staged rows (ncu, power-law 8M fp64,
+// profiles/r02b_ncu_hyb_pl8m_p8.md), and a row with a long COO tail holds its
+// whole CTA at the barrier while one thread adds.  Here:
+//  * rows are taken in dynamic 128-row slices (four 32-row sub-slices per
+//    grab from a per-stream counter), thread per row for the K1 ELL slots
+//    (pads included, as spmv_ellpack) in U-deep fenced batches;
+//  * the COO entries of a 32-row sub-slice are one contiguous range
+//    [crp[r0], crp[r0 + 32]) (COO is sorted by row): the warp stages it in
+//    chunks of 32 KC entries -- coalesced column / value loads, products
+//    formed in parallel into the warp's shared buffer -- and each lane adds
+//    the part of ITS row's run [crp[r], crp[r + 1]) inside the chunk, in
+//    array order; warp-level syncs only, no row search, and the COO row array
+//    is never read;
+//  * rows whose COO run exceeds kHeavyDyn are work items taken first
+//    (longest first) by `warps` warps per CTA: a warp walks the row's K1 ELL
+//    slots and then its COO run (long_row_walk, lane 0 adding in order), so
+//    the longest add chains start at once instead of forming the tail; the
+//    sub-slice pass skips those rows and their COO ranges.
+// Per row: ELL slots 0..K1-1, then the COO run in array order, products and
+// sums rounded separately -> y bitwise spmv_hybrid's.
+constexpr uint32_t kHeavyDyn = 256;
+
+template <class T, int U, int MINB, int KC, bool kHint>
+__global__ void __launch_bounds__(256, MINB) hybrid_spmv_dyn(
+    uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
+    const uint32_t* __restrict__ crp, const uint32_t* __restrict__ cc, const T* __restrict__ cv,
+    const T* __restrict__ x, T* __restrict__ y, LongList hl) {
+  constexpr uint32_t W = 32 * KC, kSub = 4;
+  __shared__ T prod[8][W];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* __restrict__ pr = prod[warp];
+  const Ldr<kHint> ld;
+  if (warp < hl.warps) {  // heavy rows first, longest first
+    for (;;) {
+      uint32_t i = 0;
+      if (lane == 0) i = atomicAdd(hl.ctr, 1u);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= hl.n_single) break;
+      const uint32_t r = hl.singles[i];
+      const uint32_t cb = crp[r], ce = crp[r + 1];
+      T acc = long_row_walk<T, 32, KC, kHint, 4>(k1, k1, lane, ev + r, ec + r, rows, x, pr, ld);
+      acc = long_row_walk<T, 32, KC, kHint, 4>(ce - cb, ce - cb, lane, cv + cb, cc + cb, 1u, x,
+                                               pr, ld, acc);
+      if (lane == 0) y[r] = acc;
+    }
+  }
+  const size_t step = (size_t)U * rows;
+  auto grab = [&]() -> uint64_t {
+    uint32_t q = 0;
+    if (lane == 0) q = atomicAdd(hl.ctr + 2, 1u);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    return static_cast<uint64_t>(q) * (32 * kSub);
+  };
+  for (uint64_t base = grab(); base < rows; base = grab()) {
+    for (uint32_t sub = 0; sub < kSub; ++sub) {
+      const uint64_t r0 = base + sub * 32;
+      if (r0 >= rows) break;  // warp-uniform
+      const uint32_t r = static_cast<uint32_t>(r0) + lane;
+      const bool live = r < rows;
+      const uint32_t rb = live ? crp[r] : 0u, re = live ? crp[r + 1] : 0u;
+      const bool heavy = live && re - rb > kHeavyDyn;
+      const bool mine = live && !heavy;
+      T acc = T(0);
+      if (mine) {  // ELL: all K1 slots, pads included
+        const T* __restrict__ vp = ev + r;
+        const uint32_t* __restrict__ cp = ec + r;
+        uint32_t j = 0;
+        for (; j + U <= k1; j += U) {
+          uint32_t c[U];
+          T v[U], xv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            c[u] = ld.s(cp + (size_t)u * rows);
+            v[u] = ld.s(vp + (size_t)u * rows);
+          }
+          __syncwarp(__activemask());  // slot loads ahead of the gathers
+#pragma unroll
+          for (int u = 0; u < U; ++u) xv[u] = ld.x(x + c[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+          cp += step;
+          vp += step;
+        }
+        if (j < k1) {
+          uint32_t c[U - 1];
+          T v[U - 1], xv[U - 1];
+#pragma unroll
+          for (int u = 0; u < U - 1; ++u) {
+            c[u] = j + u < k1 ? ld.s(cp + (size_t)u * rows) : 0u;
+            v[u] = j + u < k1 ? ld.s(vp + (size_t)u * rows) : T(0);
+          }
+          __syncwarp(__activemask());
+#pragma unroll
+          for (int u = 0; u < U - 1; ++u) xv[u] = j + u < k1 ? ld.x(x + c[u]) : T(0);
+#pragma unroll
+          for (int u = 0; u < U - 1; ++u)
+            if (j + u < k1) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+        }
+      }
+      // COO: the sub-slice's range minus the heavy runs, staged per chunk
+      const uint32_t last = min(31u, static_cast<uint32_t>(rows - r0 - 1));
+      const uint32_t wb = __shfl_sync(0xffffffffu, rb, 0);
+      const uint32_t we = __shfl_sync(0xffffffffu, re, last);
+      uint32_t hm = __ballot_sync(0xffffffffu, heavy);
+      uint32_t cursor = wb;
+      for (;;) {
+        const int h = hm ? __ffs(hm) - 1 : -1;
+        const uint32_t hb = __shfl_sync(0xffffffffu, rb, h < 0 ? 0 : h);
+        const uint32_t he = __shfl_sync(0xffffffffu, re, h < 0 ? 0 : h);
+        const uint32_t seg_end = h < 0 ? we : hb;
+        for (uint32_t c0 = cursor; c0 < seg_end; c0 += W) {
+          const uint32_t n = min(W, seg_end - c0);
+          uint32_t c[KC];
+          T v[KC];
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const uint32_t e = lane + 32 * k;
+            c[k] = e < n ? ld.s(cc + c0 + e) : 0u;
+            v[k] = e < n ? ld.s(cv + c0 + e) : T(0);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const uint32_t e = lane + 32 * k;
+            if (e < n) pr[e] = mul_rn(v[k], ld.x(x + c[k]));
+          }
+          __syncwarp();
+          if (mine) {
+            const uint32_t lo = max(rb, c0), hi = min(re, c0 + n);
+            for (uint32_t e = lo; e < hi; ++e) acc = add_rn(acc, pr[e - c0]);
+          }
+          __syncwarp();
+        }
+        if (h < 0) break;
+        cursor = he;
+        hm &= hm - 1;
+      }
+      if (mine) y[r] = acc;
+    }
+  }
+  long_items_done(hl);
+}
+
 // Hybrid SpMV kernel choice: spmvk_set_hybrid_kernel() or SPMVK_HYBRID_KERNEL.
 // "v4": hybrid_spmv_kernel (policy-hinted loads, 4-deep, 8 CTAs / SM);
 // "lite" / "lite8" / "lite8_full": hybrid_spmv_lite with 4-deep batches at
@@ -611,7 +762,9 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
 // matrices, where every row walks the same K1 slots like a group.
 // "litefh": litef with L2 eviction hints (ELL / COO streams evict_first, x
 // evict_last) in the main kernel and the heavy-row tails.
-enum class HK { kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F, kG6, kG7, kG8, kG8R, kLiteFH };
+enum class HK {
+  kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F, kG6, kG7, kG8, kG8R, kLiteFH, kDyn
+};
 
 std::atomic<int>& hk_slot() {
   static std::atomic<int> k{[] {
@@ -621,11 +774,50 @@ std::atomic<int>& hk_slot() {
       v = s == "v4" ? HK::kV4 : s == "lite" ? HK::kLite : s == "lite8" ? HK::kLite8
         : s == "lite8_full" ? HK::kLite8Full : s == "litef" ? HK::kLiteF
         : s == "lite8f" ? HK::kLite8F : s == "g6" ? HK::kG6 : s == "g7" ? HK::kG7
-        : s == "g8" ? HK::kG8 : s == "g8r" ? HK::kG8R : s == "litefh" ? HK::kLiteFH : HK::kAuto;
+        : s == "g8" ? HK::kG8 : s == "g8r" ? HK::kG8R : s == "litefh" ? HK::kLiteFH
+        : s == "dyn" ? HK::kDyn : HK::kAuto;
     }
     return static_cast<int>(v);
   }()};
   return k;
+}
+
+// Rows whose COO run exceeds thr (unordered; sorted longest first after).
+__global__ void heavy_collect(uint64_t rows, const uint32_t* __restrict__ crp, uint32_t thr,
+                              uint32_t* __restrict__ list, uint32_t* __restrict__ key,
+                              unsigned* __restrict__ count) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t run = crp[r + 1] - crp[r];
+    if (run > thr) {
+      const unsigned i = atomicAdd(count, 1u);
+      list[i] = static_cast<uint32_t>(r);
+      key[i] = ~run;
+    }
+  }
+}
+
+// h->dyn_heavy: the rows of hybrid_spmv_dyn's work list, longest run first.
+void collect_dyn_heavy(spmvk_hybrid* h, cudaStream_t s) {
+  const uint64_t cap = h->coo / (kHeavyDyn + 1) + 1;
+  TmpBuf<uint32_t> list(cap, s), key(cap, s), key2(cap, s);
+  TmpBuf<unsigned> cnt(1, s);
+  SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned), s));
+  heavy_collect<<<persistent_grid((h->rows + 255) / 256, 8), 256, 0, s>>>(
+      h->rows, h->coo_row_ptr.p, kHeavyDyn, list.p, key.p, cnt.p);
+  SPMVK_LAUNCH("heavy_collect");
+  unsigned n = 0;
+  SPMVK_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(n), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaStreamSynchronize(s));
+  h->n_dyn_heavy = n;
+  h->dyn_heavy.alloc(n);
+  if (!n) return;
+  size_t tmp_bytes = 0;
+  SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key2.p, list.p,
+                                             h->dyn_heavy.p, static_cast<int>(n), 0, 32, s));
+  TmpBuf<unsigned char> tmp(tmp_bytes, s);
+  SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key.p, key2.p, list.p,
+                                             h->dyn_heavy.p, static_cast<int>(n), 0, 32, s));
 }
 
 template <class T, class V>
@@ -677,6 +869,7 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
     h->heavy_rows.alloc(h->n_heavy);
     if (h->n_heavy)
       SPMVK_CUDA(cudaMemcpy(h->heavy_rows.p, heavy.data(), 4 * h->n_heavy, cudaMemcpyHostToDevice));
+    collect_dyn_heavy(h, s);
   }
   DevBuf<unsigned long long> cnt(1);
   SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
@@ -764,8 +957,13 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     // fp64 47.1 vs 49.3 us, fp32 31.8 vs 34.9 (5-pt 2048^2); 27-point U = 7:
     // fp64 105.2 vs 106.8, fp32 76.1 vs 77.7; 7-point keeps U = 4 (fp32
     // 172.4 vs 172.7 for U = 7, 174.5 for U = 8).
+    // With a COO part, spmv_hybrid takes hybrid_spmv_dyn (config-3 power-law
+    // 8M, original order: fp64 617 vs 744 us, fp32 533 vs 677; descending
+    // order 837 vs 846 / 733 vs 726 -- profiles/r02_hybrid_dyn.md); the
+    // spmv_coo / spmv_ellpack parts keep the staged-tile kernels.
     const bool pure_ell = part == Part::kEll || !h->coo;
     if (pure_ell) k = k1 <= 6 ? HK::kG6 : k1 <= 12 ? HK::kLiteF : HK::kG7;
+    else if (part == Part::kBoth) k = HK::kDyn;
     else k = sizeof(T) == 4 ? HK::kLiteFH : HK::kLiteF;
   }
   auto run = [&](auto kern) {
@@ -778,6 +976,27 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     SPMVK_LAUNCH("hybrid_spmv");
   };
   const bool acc = part == Part::kCoo, coo = tp != nullptr;
+  // spmv_hybrid with a COO part: dynamic slices, warp-staged COO, heavy rows
+  // as work items (one launch; other variants / parts fall through below)
+  if (k == HK::kDyn && part == Part::kBoth && coo && rows == h->rows) {
+    static const uint32_t hw = [] {
+      const char* e = std::getenv("SPMVK_HYB_HEAVY_WARPS");
+      const int v = e ? std::atoi(e) : 2;
+      return static_cast<uint32_t>(v < 1 ? 1 : v > 8 ? 8 : v);
+    }();
+    auto kern = sizeof(T) == 4 ? hybrid_spmv_dyn<T, 4, 6, 4, true> : hybrid_spmv_dyn<T, 4, 5, 4, false>;
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const LongList hl{static_cast<uint32_t>(h->n_dyn_heavy), 0u, h->dyn_heavy.p, nullptr,
+                      stream_counters(s), hw};
+    kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
+        static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
+        h->ell_columns.p, h->coo_row_ptr.p, h->coo_columns.p,
+        reinterpret_cast<const T*>(h->coo_values.p), x, y, hl);
+    SPMVK_LAUNCH("hybrid_spmv_dyn");
+    return;
+  }
+  if (k == HK::kDyn) k = HK::kLiteF;
   // after the main kernel (any variant but v4, which stages every tile): the
   // heavy rows' COO tails, warp per row, onto the y the main kernel stored
   auto heavy = [&]() {
@@ -916,10 +1135,11 @@ int spmvk_set_hybrid_kernel(const char* name) {
     else if (v == "g8") k = HK::kG8;
     else if (v == "g8r") k = HK::kG8R;
     else if (v == "litefh") k = HK::kLiteFH;
+    else if (v == "dyn") k = HK::kDyn;
     else
       fail(SPMVK_EINVAL, "unknown Hybrid kernel variant '" + v +
                              "' (auto | v4 | lite | lite8 | lite8_full | litef | lite8f | g6 | "
-                             "g7 | g8 | g8r | litefh)");
+                             "g7 | g8 | g8r | litefh | dyn)");
     hk_slot().store(static_cast<int>(k));
   });
 }

@@ -807,7 +807,7 @@ __device__ __forceinline__ T long_row_walk(uint32_t len, uint32_t lmax, int l,
                                            const T* __restrict__ vp,
                                            const uint32_t* __restrict__ cp, uint32_t s,
                                            const T* __restrict__ x, T* __restrict__ pr,
-                                           const Ldr<kHint>& ld) {
+                                           const Ldr<kHint>& ld, T acc0 = T(0)) {
   constexpr uint32_t W = L * K;
   uint32_t c[K];
   T v[K];
@@ -817,7 +817,7 @@ __device__ __forceinline__ T long_row_walk(uint32_t len, uint32_t lmax, int l,
     c[k] = j < len ? ld.s(cp + (size_t)j * s) : 0u;
     v[k] = j < len ? ld.s(vp + (size_t)j * s) : T(0);
   }
-  T acc = T(0);
+  T acc = acc0;  // meaningful in the adding lane (l == 0)
   for (uint32_t j0 = 0; j0 < lmax; j0 += W) {
     __syncwarp();  // scheduling fence, and the previous round's adds are done
 #pragma unroll

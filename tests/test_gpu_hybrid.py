@@ -15,7 +15,7 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-HYBRID_VARIANTS = ["auto", "v4", "lite", "lite8", "lite8_full", "litef", "lite8f"]
+HYBRID_VARIANTS = ["auto", "v4", "lite", "lite8", "lite8_full", "litef", "lite8f", "dyn"]
 
 
 @pytest.fixture(params=HYBRID_VARIANTS)
@@ -341,3 +341,34 @@ def test_parts_compose_on_heavy_tiles(cuda, hk):
     y = sk.spmv_ellpack(h, x)
     sk.spmv_coo(h, x, y)
     assert bitwise(y.cpu().numpy(), sk.spmv_hybrid(h, x).cpu().numpy())
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("order", ["orig", "desc"])
+def test_dyn_repeated_launches_two_streams(cuda, prec, order):
+    """hybrid_spmv_dyn takes rows and heavy rows from per-stream counters that
+    the last warp resets: back-to-back launches alternating over two streams
+    must all give the oracle's y bitwise (heavy rows present in both
+    orders)."""
+    from paper_1012_2270_b200._lib import lib
+    csr = sk.build_csr(triplets(orc.powerlaw(300_000, 7)))
+    c = csr if order == "orig" else sk.apply_descending_permutation(csr)[0]
+    rp, col, val = c.to_host()
+    om = orc.Csr(c.num_rows, c.num_cols, rp, col, val)
+    h = sk.build_hybrid(c, None, prec)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(om.cols, 1).astype(dt)
+    want = orc.spmv_hybrid(orc.build_hybrid(om, None, prec), x)
+    assert lib().spmvk_set_hybrid_kernel(b"dyn") == 0
+    try:
+        xd = dev(x)
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        ys = [torch.empty_like(xd) for _ in range(4)]
+        for k in range(4):
+            with torch.cuda.stream(streams[k % 2]):
+                sk.spmv_hybrid(h, xd, ys[k])
+        torch.cuda.synchronize()
+        for y in ys:
+            assert bitwise(y.cpu().numpy(), want)
+    finally:
+        lib().spmvk_set_hybrid_kernel(b"auto")
