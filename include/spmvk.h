@@ -257,7 +257,7 @@ int spmvk_set_long_fused(int on);
  * SM, U = 8 at 4; pure-ELL launches only), "litefh" (litef with L2 eviction
  * hints), "dyn" (spmv_hybrid with a COO part: rows in dynamic 128-row slices,
  * each 32-row slice's COO range staged per warp -- no block barrier, no row
- * search -- and rows with COO runs over 256 entries as warp work items taken
+ * search -- and rows with COO runs over 128 entries as warp work items taken
  * first, longest first; other parts fall back to "litef").  All give bitwise
  * identical y.  Also read from SPMVK_HYBRID_KERNEL. */
 int spmvk_set_hybrid_kernel(const char* name);

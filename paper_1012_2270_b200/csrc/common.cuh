@@ -377,4 +377,5 @@ struct spmvk_hybrid {
   // of hybrid_spmv_dyn (kernel metadata).
   spmvk::DevBuf<uint32_t> dyn_heavy;
   uint64_t n_dyn_heavy = 0;
+  uint32_t dyn_heavy_run = 128;
 };

@@ -623,20 +623,30 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
 //    the part of ITS row's run [crp[r], crp[r + 1]) inside the chunk, in
 //    array order; warp-level syncs only, no row search, and the COO row array
 //    is never read;
-//  * rows whose COO run exceeds kHeavyDyn are work items taken first
+//  * rows whose COO run exceeds kHeavyDyn (128) are work items taken first
 //    (longest first) by `warps` warps per CTA: a warp walks the row's K1 ELL
 //    slots and then its COO run (long_row_walk, lane 0 adding in order), so
 //    the longest add chains start at once instead of forming the tail; the
 //    sub-slice pass skips those rows and their COO ranges.
 // Per row: ELL slots 0..K1-1, then the COO run in array order, products and
 // sums rounded separately -> y bitwise spmv_hybrid's.
-constexpr uint32_t kHeavyDyn = 256;
+constexpr uint32_t kHeavyDyn = 128;
+// SPMVK_HYB_HEAVY_RUN overrides the run length that makes a row a work item
+// (read at build; the list and the kernel use the handle's value).
+uint32_t heavy_dyn_run() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("SPMVK_HYB_HEAVY_RUN");
+    const long n = e ? std::atol(e) : 0;
+    return n > 0 ? static_cast<uint32_t>(n) : kHeavyDyn;
+  }();
+  return v;
+}
 
 template <class T, int U, int MINB, int KC, bool kHint>
 __global__ void __launch_bounds__(256, MINB) hybrid_spmv_dyn(
     uint32_t rows, uint32_t k1, const T* __restrict__ ev, const uint32_t* __restrict__ ec,
     const uint32_t* __restrict__ crp, const uint32_t* __restrict__ cc, const T* __restrict__ cv,
-    const T* __restrict__ x, T* __restrict__ y, LongList hl) {
+    const T* __restrict__ x, T* __restrict__ y, uint32_t heavy_run, LongList hl) {
   constexpr uint32_t W = 32 * KC, kSub = 4;
   __shared__ T prod[8][W];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -670,7 +680,7 @@ __global__ void __launch_bounds__(256, MINB) hybrid_spmv_dyn(
       const uint32_t r = static_cast<uint32_t>(r0) + lane;
       const bool live = r < rows;
       const uint32_t rb = live ? crp[r] : 0u, re = live ? crp[r + 1] : 0u;
-      const bool heavy = live && re - rb > kHeavyDyn;
+      const bool heavy = live && re - rb > heavy_run;
       const bool mine = live && !heavy;
       T acc = T(0);
       if (mine) {  // ELL: all K1 slots, pads included
@@ -799,12 +809,13 @@ __global__ void heavy_collect(uint64_t rows, const uint32_t* __restrict__ crp, u
 
 // h->dyn_heavy: the rows of hybrid_spmv_dyn's work list, longest run first.
 void collect_dyn_heavy(spmvk_hybrid* h, cudaStream_t s) {
-  const uint64_t cap = h->coo / (kHeavyDyn + 1) + 1;
+  h->dyn_heavy_run = heavy_dyn_run();
+  const uint64_t cap = h->coo / (h->dyn_heavy_run + 1) + 1;
   TmpBuf<uint32_t> list(cap, s), key(cap, s), key2(cap, s);
   TmpBuf<unsigned> cnt(1, s);
   SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned), s));
   heavy_collect<<<persistent_grid((h->rows + 255) / 256, 8), 256, 0, s>>>(
-      h->rows, h->coo_row_ptr.p, kHeavyDyn, list.p, key.p, cnt.p);
+      h->rows, h->coo_row_ptr.p, h->dyn_heavy_run, list.p, key.p, cnt.p);
   SPMVK_LAUNCH("heavy_collect");
   unsigned n = 0;
   SPMVK_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(n), cudaMemcpyDeviceToHost, s));
@@ -992,7 +1003,7 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     kern<<<persistent_grid(ntiles, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
         static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
         h->ell_columns.p, h->coo_row_ptr.p, h->coo_columns.p,
-        reinterpret_cast<const T*>(h->coo_values.p), x, y, hl);
+        reinterpret_cast<const T*>(h->coo_values.p), x, y, h->dyn_heavy_run, hl);
     SPMVK_LAUNCH("hybrid_spmv_dyn");
     return;
   }
