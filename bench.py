@@ -323,6 +323,63 @@ def convert_rate(csr, stream, peak, G=32, reps=5):
                     "allocation, median of %d; bytes = CSR read + RgCSR written" % reps}
 
 
+# ---------------------------------------------------------------- config 3
+def powerlaw_block(args, peak):
+    """BASELINE configs[2] at full size (8M rows, power-law lengths, 128 M nnz),
+    fp64: RgCSR G = 32 in the original and the descending row order, and the
+    paper's Hybrid ELL+COO in both, each timed like the headline (back-to-back
+    launches, CUDA events on the launching stream).  Roofline on B_min
+    (format-independent: every nonzero's value + column once, x and y) and on
+    the format's own bytes.  Parity gate: the sequential sum of every y (the
+    descending ones mapped back to the original rows) must equal the unmodified
+    reference's checksum (tests/golden/shapes.json)."""
+    import torch
+    from paper_1012_2270_b200 import generators as gen
+    from paper_1012_2270_b200 import spmvkit as sk
+    from paper_1012_2270_b200._lib import lib
+    L = lib()
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    t0 = time.perf_counter()
+    csr = make_csr("powerlaw-8M")
+    desc, pmap = sk.apply_descending_permutation(csr)
+    perm = sk.Permutation(pmap)
+    rows, nnz = csr.num_rows, csr.nnz()
+    x = torch.from_numpy(gen.random_vector(csr.num_cols, 1)).cuda()
+    y = torch.empty(rows, dtype=torch.float64, device="cuda")
+    golden = golden_checksum("powerlaw-8M")
+    b_min = nnz * 12 + 8 * (rows + csr.num_cols)
+    out = {"workload": "powerlaw-8M", "description": WORKLOADS["powerlaw-8M"][3],
+           "precision": "fp64", "nnz": nnz, "b_min": b_min,
+           "reference_checksum": golden}
+    steps = max(5, min(args.steps, 50))
+    for label, mat, fmt, reordered in (("rgcsr_g32_original", csr, "rg", False),
+                                       ("rgcsr_g32_descending", desc, "rg", True),
+                                       ("hybrid_original", csr, "hy", False),
+                                       ("hybrid_descending", desc, "hy", True)):
+        if fmt == "rg":
+            h = sk.build_rgcsr(mat, 32, 8, stream=sp)
+            fn, bf = L.spmvk_rgcsr_spmv_f64, rg_bytes(h.info, 8)
+        else:
+            h = sk.build_hybrid(mat, None, 8, stream=sp)
+            fn, bf = L.spmvk_hybrid_spmv_f64, hy_bytes(h.info, 8)
+        _, km = time_launches(lambda: fn(h._h, x.data_ptr(), h.num_cols, y.data_ptr(), rows, sp),
+                              stream, steps, max(3, args.warmup))
+        yy = sk.permute_vector(perm, y, inverse=True) if reordered else y
+        ysum = float(np.cumsum(yy.cpu().numpy())[-1])
+        if golden is not None and ysum != golden:
+            raise SystemExit(f"parity gate failed: powerlaw {label} checksum {ysum!r} != "
+                             f"reference {golden!r}")
+        out[label] = {"kernel_us": km * 1e3, "gflops": 2.0 * nnz / (km * 1e-3) / 1e9,
+                      "frac_b_min": b_min / (km * 1e-3) / 1e9 / peak,
+                      "format_bytes": bf, "frac_format_bytes": bf / (km * 1e-3) / 1e9 / peak,
+                      "checksum": ysum}
+        del h
+    out["parity"] = "every checksum == the unmodified reference's (descending y mapped back)"
+    out["setup_s"] = time.perf_counter() - t0
+    return out
+
+
 # ---------------------------------------------------------------- scaling anchor
 def scale_anchor(args, peak):
     """BASELINE configs[4] at N = 1: 7-point 512^3 fp64 (938 M nnz, 13.4 GB of
@@ -524,6 +581,7 @@ def run_ours(args):
             del h
 
     anchor = scale_anchor(args, peak) if args.workload != "7pt-512" else None
+    plaw = powerlaw_block(args, peak) if args.powerlaw else None
     cpu = cpu_reference(args.workload, args.cpu_reps)
     if cpu["checksum"] != ysum:
         raise SystemExit(f"parity gate failed: GPU checksum {ysum!r} != CPU reference "
@@ -560,6 +618,7 @@ def run_ours(args):
         "convert": convert_rate(csr, stream, peak),
         "variants": variants,
         "scale_anchor": anchor,
+        "config3_powerlaw": plaw,
     }
     print(json.dumps(line), flush=True)
 
@@ -574,6 +633,8 @@ def main():
                     help="default: 27pt-128 (configs[1]) on one GPU; 7pt-512 (configs[4], the "
                          "iterated, row-slab sharded config) under torchrun with N > 1")
     ap.add_argument("--cpu-reps", type=int, default=10)
+    ap.add_argument("--no-powerlaw", dest="powerlaw", action="store_false",
+                    help="skip the BASELINE configs[2] (power-law 8M) block of the N = 1 line")
     ap.add_argument("--distributed", action="store_true",
                     help="use the row-slab + NCCL path even at world size 1 (under torchrun)")
     ap.add_argument("--exchange", default="fused", choices=["allgather", "halo", "fused"],

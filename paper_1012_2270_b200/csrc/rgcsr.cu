@@ -15,6 +15,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -102,7 +103,11 @@ __global__ void rgcsr_gather_rows(uint64_t rows, uint64_t G, uint64_t nnz,
 
 // Rows longer than this go to the warp-per-row kernel (spmvk_set_long_row_cut).
 std::atomic<uint32_t>& long_cut_slot() {
-  static std::atomic<uint32_t> v{kLongRow};
+  static std::atomic<uint32_t> v{[] {
+    const char* e = std::getenv("SPMVK_LONG_CUT");  // A/B only; default kLongRow
+    const long n = e ? std::atol(e) : 0;
+    return n > 0 ? static_cast<uint32_t>(n) : kLongRow;
+  }()};
   return v;
 }
 
@@ -110,6 +115,13 @@ std::atomic<uint32_t>& long_cut_slot() {
 // One warp per group.  Lane t owns local row t (+32 per chunk) and walks its
 // slots j = 0..K_g-1; for a fixed j the warp writes 32 contiguous slots, and
 // every pad slot is written (0, 0), so no separate zero-fill pass is needed.
+// A group's CSR entries [rp[g G], rp[g G + s]) are contiguous: when they fit
+// the warp's shared-memory stage (kStage entries) they are first copied in
+// with coalesced loads, and the slot-major writes read them from there --
+// instead of 32 scattered row streams per load instruction, which cost one
+// L1 tag lookup per lane.  Larger groups (long rows) read CSR directly.
+constexpr uint32_t kStage = 1024;
+
 template <class T, class V>
 __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows, uint64_t G,
                                                      uint64_t groups,
@@ -120,13 +132,37 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
                                                      const uint32_t* __restrict__ lens,
                                                      T* __restrict__ values,
                                                      uint32_t* __restrict__ columns) {
-  const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) unsigned char stage_raw[];  // 8 warps x kStage (T + u32)
+  T* sv_all = reinterpret_cast<T*>(stage_raw);
+  uint32_t* sc_all = reinterpret_cast<uint32_t*>(sv_all + 8 * kStage);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* sv = sv_all + warp * kStage;
+  uint32_t* sc = sc_all + warp * kStage;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < groups;
-       g += warps) {
+  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp; g < groups; g += warps) {
     const uint64_t s = min(G, rows - g * G);
     const uint32_t base = gp[g];
     const uint64_t width = s ? (gp[g + 1] - base) / s : 0;
+    const uint32_t e0 = rp[r0 + g * G], e1 = rp[r0 + g * G + s];
+    if (s <= 32 && e1 - e0 <= kStage) {  // warp-uniform
+      for (uint32_t i = lane; i < e1 - e0; i += 32) {
+        sv[i] = static_cast<T>(val[e0 + i]);
+        sc[i] = col[e0 + i];
+      }
+      __syncwarp();
+      const bool live = (uint64_t)lane < s;
+      const uint64_t row = g * G + lane;
+      const uint32_t len = live ? lens[row] : 0;
+      const uint32_t off = live ? rp[r0 + row] - e0 : 0;
+      if (live)
+        for (uint64_t j = 0; j < width; ++j) {
+          const uint64_t idx = base + lane + j * s;
+          values[idx] = j < len ? sv[off + j] : T(0);
+          columns[idx] = j < len ? sc[off + j] : 0u;
+        }
+      __syncwarp();
+      continue;
+    }
     for (uint64_t t0 = 0; t0 < s; t0 += 32) {
       const uint64_t t = t0 + lane;
       const bool live = t < s;
@@ -290,24 +326,28 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
   h->values.alloc(total * static_cast<uint64_t>(prec));
   h->columns.alloc(total);
   if (h->groups) {
-    const unsigned sgrid = persistent_grid((h->groups + 7) / 8, 16);
-    if (prec == SPMVK_F64) {
-      rgcsr_scatter<double, double><<<sgrid, 256, 0, s>>>(
-          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
-          reinterpret_cast<const double*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
-          reinterpret_cast<double*>(h->values.p), h->columns.p);
-    } else if (a->val_prec == SPMVK_F64) {
-      rgcsr_scatter<float, double><<<sgrid, 256, 0, s>>>(
-          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
-          reinterpret_cast<const double*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
-          reinterpret_cast<float*>(h->values.p), h->columns.p);
-    } else {
-      rgcsr_scatter<float, float><<<sgrid, 256, 0, s>>>(
-          r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p,
-          reinterpret_cast<const float*>(a->val.p), h->group_pointers.p, h->row_lengths.p,
-          reinterpret_cast<float*>(h->values.p), h->columns.p);
-    }
-    SPMVK_LAUNCH("rgcsr_scatter");
+    auto scatter = [&](auto kern, auto* vals_in, auto* vals_out) {
+      using TO = std::remove_pointer_t<decltype(vals_out)>;
+      const size_t smem = 8 * kStage * (sizeof(TO) + sizeof(uint32_t));
+      SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      int per_sm = 0;
+      SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+      const unsigned sgrid = persistent_grid((h->groups + 7) / 8, per_sm > 0 ? per_sm : 1);
+      kern<<<sgrid, 256, smem, s>>>(r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p, vals_in,
+                                    h->group_pointers.p, h->row_lengths.p, vals_out,
+                                    h->columns.p);
+      SPMVK_LAUNCH("rgcsr_scatter");
+    };
+    if (prec == SPMVK_F64)
+      scatter(rgcsr_scatter<double, double>, reinterpret_cast<const double*>(a->val.p),
+              reinterpret_cast<double*>(h->values.p));
+    else if (a->val_prec == SPMVK_F64)
+      scatter(rgcsr_scatter<float, double>, reinterpret_cast<const double*>(a->val.p),
+              reinterpret_cast<float*>(h->values.p));
+    else
+      scatter(rgcsr_scatter<float, float>, reinterpret_cast<const float*>(a->val.p),
+              reinterpret_cast<float*>(h->values.p));
   }
   h->long_rows.alloc(h->n_long);
   if (h->n_long) {  // long-row list (ascending), split into quads and singles
