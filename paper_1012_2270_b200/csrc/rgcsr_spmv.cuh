@@ -305,6 +305,61 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_lite(
       StoreEpi<T, kScaled>{y, x_next, scale});
 }
 
+// One row of the group walk (group pointers b0, b1 and, if use_len, the row
+// length already loaded): returns the row's sum in slot order.
+template <class T, int U, bool kGatherK>
+__device__ __forceinline__ T grp_row(uint32_t r, uint32_t b0, uint32_t b1, uint32_t len,
+                                     bool use_len, uint32_t rows, uint32_t G, int g_shift,
+                                     const T* __restrict__ values,
+                                     const uint32_t* __restrict__ columns,
+                                     const T* __restrict__ x) {
+  const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
+  const uint32_t s = min(G, rows - g * G);
+  const uint32_t width = b1 - b0;
+  const uint32_t K = (s == G && g_shift >= 0) ? (width >> g_shift) : width / s;
+  const uint32_t lim = use_len ? len : K;
+  const uint32_t off = b0 + (r - g * G);
+  const T* __restrict__ vp = values + off;
+  const uint32_t* __restrict__ cp = columns + off;
+  T acc = T(0);
+  uint32_t j = 0;
+  for (; j + U <= K; j += U) {
+    uint32_t c[U];
+    T v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + u * s);
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = ld_stream(cp + u * s);
+    // warp barrier = a ptxas scheduling fence: every slot load (columns AND
+    // values) issues before the first gather waits on a column; without it
+    // ptxas interleaves and the value loads trail by a full DRAM round trip
+    __syncwarp(__activemask());
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = (kGatherK || j + u < lim) ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+    cp += U * s;
+    vp += U * s;
+  }
+  if (j < K) {  // predicated last batch (< U slots)
+    uint32_t c[U - 1];
+    T v[U - 1], xv[U - 1];
+#pragma unroll
+    for (int u = 0; u < U - 1; ++u) v[u] = j + u < K ? ld_stream(vp + u * s) : T(0);
+#pragma unroll
+    for (int u = 0; u < U - 1; ++u) c[u] = j + u < K ? ld_stream(cp + u * s) : 0u;
+    __syncwarp(__activemask());
+#pragma unroll
+    for (int u = 0; u < U - 1; ++u)
+      xv[u] = (kGatherK ? j + u < K : j + u < lim) ? ld_x(x + c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < U - 1; ++u)
+      if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // rgcsr_spmv_grp -- group-uniform walk for matrices without long rows.
 //
@@ -395,51 +450,8 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
     }
     if (r >= rows) continue;
     if (!kMpf) m = load_meta(r);
-    const uint32_t g = g_shift >= 0 ? (r >> g_shift) : r / G;
-    const uint32_t s = min(G, rows - g * G);
-    const uint32_t width = m.b1 - m.b0;
-    const uint32_t K = (s == G && g_shift >= 0) ? (width >> g_shift) : width / s;
-    const uint32_t lim = use_len ? m.len : K;
-    const uint32_t off = m.b0 + (r - g * G);
-    const T* __restrict__ vp = values + off;
-    const uint32_t* __restrict__ cp = columns + off;
-    T acc = T(0);
-    uint32_t j = 0;
-    for (; j + U <= K; j += U) {
-      uint32_t c[U];
-      T v[U], xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + u * s);
-#pragma unroll
-      for (int u = 0; u < U; ++u) c[u] = ld_stream(cp + u * s);
-      // warp barrier = a ptxas scheduling fence: every slot load (columns AND
-      // values) issues before the first gather waits on a column; without it
-      // ptxas interleaves and the value loads trail by a full DRAM round trip
-      __syncwarp(__activemask());
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = (kGatherK || j + u < lim) ? ld_x(x + c[u]) : T(0);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
-      cp += U * s;
-      vp += U * s;
-    }
-    if (j < K) {  // predicated last batch (< U slots)
-      uint32_t c[U - 1];
-      T v[U - 1], xv[U - 1];
-#pragma unroll
-      for (int u = 0; u < U - 1; ++u) v[u] = j + u < K ? ld_stream(vp + u * s) : T(0);
-#pragma unroll
-      for (int u = 0; u < U - 1; ++u) c[u] = j + u < K ? ld_stream(cp + u * s) : 0u;
-      __syncwarp(__activemask());
-#pragma unroll
-      for (int u = 0; u < U - 1; ++u)
-        xv[u] = (kGatherK ? j + u < K : j + u < lim) ? ld_x(x + c[u]) : T(0);
-#pragma unroll
-      for (int u = 0; u < U - 1; ++u)
-        if (j + u < lim) acc = add_rn(acc, mul_rn(v[u], xv[u]));
-    }
-    epi(r, acc);
+    epi(r, grp_row<T, U, kGatherK>(r, m.b0, m.b1, m.len, use_len, rows, G, g_shift, values,
+                                   columns, x));
   }
 }
 
