@@ -606,6 +606,70 @@ __global__ void __launch_bounds__(kRowsPerTile, MINB) hybrid_spmv_lite(
 }
 
 // ---------------------------------------------------------------------------
+// hybrid_ell_vec -- pure ELL with 128-bit slot loads: a thread owns R = 16 B /
+// sizeof(T) consecutive rows (fp32: 4, fp64: 2), so slot j of its rows is one
+// aligned float4 / double2 value vector and one uint4 / uint2 column vector
+// (rows % R == 0 keeps every slot's row block 16-byte aligned); a warp reads
+// 32 R consecutive rows of a slot -- 512 B per slot stream instead of 128 B
+// (fp32), a quarter of the concurrent slot streams per byte.  Each row adds
+// its K1 products in slot order (pads included) -> bitwise spmv_ellpack.
+template <class T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) hybrid_ell_vec(uint32_t rows, uint32_t k1,
+                                                            const T* __restrict__ ev,
+                                                            const uint32_t* __restrict__ ec,
+                                                            const T* __restrict__ x,
+                                                            T* __restrict__ y) {
+  constexpr int R = 16 / sizeof(T);
+  using Wv = VecOf<T, R>;
+  using V = typename Wv::V;
+  using Cv = typename Wv::C;
+  const uint32_t tiles = (rows + 256 * R - 1) / (256 * R);
+  const size_t vstep = rows / R;  // one slot, in vectors
+  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint32_t r0 = tile * 256 * R + threadIdx.x * R;
+    if (r0 >= rows) continue;
+    const V* __restrict__ vp = reinterpret_cast<const V*>(ev + r0);
+    const Cv* __restrict__ cp = reinterpret_cast<const Cv*>(ec + r0);
+    T acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = T(0);
+    uint32_t j = 0;
+    for (; j + U <= k1; j += U) {
+      V v[U];
+      Cv c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = ld_stream_v(vp + u * vstep);
+        c[u] = ld_stream_v(cp + u * vstep);
+      }
+      __syncwarp(__activemask());  // every slot load before the gathers
+      T xv[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < R; ++i) xv[u][i] = ld_x(x + Wv::col(c[u], i));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[i] = add_rn(acc[i], mul_rn(Wv::get(v[u], i), xv[u][i]));
+      vp += U * vstep;
+      cp += U * vstep;
+    }
+    for (; j < k1; ++j) {
+      const V v = ld_stream_v(vp);
+      const Cv c = ld_stream_v(cp);
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        acc[i] = add_rn(acc[i], mul_rn(Wv::get(v, i), ld_x(x + Wv::col(c, i))));
+      vp += vstep;
+      cp += vstep;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) y[r0 + i] = acc[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // hybrid_spmv_dyn -- Hybrid with a COO part, without block barriers.
 //
 // The staged-tile kernel above spends ~22 % of its stall samples at the
@@ -773,7 +837,8 @@ __global__ void __launch_bounds__(256, MINB) hybrid_spmv_dyn(
 // "litefh": litef with L2 eviction hints (ELL / COO streams evict_first, x
 // evict_last) in the main kernel and the heavy-row tails.
 enum class HK {
-  kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F, kG6, kG7, kG8, kG8R, kLiteFH, kDyn
+  kAuto, kV4, kLite, kLite8, kLite8Full, kLiteF, kLite8F, kG6, kG7, kG8, kG8R, kLiteFH, kDyn,
+  kVec
 };
 
 std::atomic<int>& hk_slot() {
@@ -785,7 +850,7 @@ std::atomic<int>& hk_slot() {
         : s == "lite8_full" ? HK::kLite8Full : s == "litef" ? HK::kLiteF
         : s == "lite8f" ? HK::kLite8F : s == "g6" ? HK::kG6 : s == "g7" ? HK::kG7
         : s == "g8" ? HK::kG8 : s == "g8r" ? HK::kG8R : s == "litefh" ? HK::kLiteFH
-        : s == "dyn" ? HK::kDyn : HK::kAuto;
+        : s == "dyn" ? HK::kDyn : s == "vec" ? HK::kVec : HK::kAuto;
     }
     return static_cast<int>(v);
   }()};
@@ -972,8 +1037,13 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     // 8M, original order: fp64 617 vs 744 us, fp32 533 vs 677; descending
     // order 837 vs 846 / 733 vs 726 -- profiles/r02_hybrid_dyn.md); the
     // spmv_coo / spmv_ellpack parts keep the staged-tile kernels.
+    // fp32 pure ELL takes the 128-bit slot loads (4 rows per thread): 27-pt
+    // 128^3 77.4 -> 71.3 us, 5-pt 2048^2 32.3 -> 28.9, 7-pt 256^3 172.5 ->
+    // 171.2; fp64 gains nothing (108.2 vs 108.0, 7-pt 242 vs 253) and keeps
+    // the scalar shapes (profiles/r02_hybrid_dyn.md)
     const bool pure_ell = part == Part::kEll || !h->coo;
-    if (pure_ell) k = k1 <= 6 ? HK::kG6 : k1 <= 12 ? HK::kLiteF : HK::kG7;
+    if (pure_ell && sizeof(T) == 4 && h->rows % 4 == 0 && part == Part::kBoth) k = HK::kVec;
+    else if (pure_ell) k = k1 <= 6 ? HK::kG6 : k1 <= 12 ? HK::kLiteF : HK::kG7;
     else if (part == Part::kBoth) k = HK::kDyn;
     else k = sizeof(T) == 4 ? HK::kLiteFH : HK::kLiteF;
   }
@@ -1008,6 +1078,21 @@ void launch(const spmvk_hybrid* h, const T* x, T* y, cudaStream_t s, Part part =
     return;
   }
   if (k == HK::kDyn) k = HK::kLiteF;
+  // pure ELL with 128-bit slot loads (rows % R == 0 keeps the vectors aligned)
+  if (k == HK::kVec) {
+    constexpr uint64_t R = 16 / sizeof(T);
+    if (!coo && !acc && rows == h->rows && rows % R == 0) {
+      auto kern = hybrid_ell_vec<T, 4, sizeof(T) == 8 ? 5 : 4>;
+      int per_sm = 0;
+      SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+      kern<<<persistent_grid((rows + 256 * R - 1) / (256 * R), per_sm > 0 ? per_sm : 1), 256, 0,
+             s>>>(static_cast<uint32_t>(rows), k1, reinterpret_cast<const T*>(h->ell_values.p),
+                  h->ell_columns.p, x, y);
+      SPMVK_LAUNCH("hybrid_ell_vec");
+      return;
+    }
+    k = HK::kLiteF;
+  }
   // after the main kernel (any variant but v4, which stages every tile): the
   // heavy rows' COO tails, warp per row, onto the y the main kernel stored
   auto heavy = [&]() {
@@ -1147,10 +1232,11 @@ int spmvk_set_hybrid_kernel(const char* name) {
     else if (v == "g8r") k = HK::kG8R;
     else if (v == "litefh") k = HK::kLiteFH;
     else if (v == "dyn") k = HK::kDyn;
+    else if (v == "vec") k = HK::kVec;
     else
       fail(SPMVK_EINVAL, "unknown Hybrid kernel variant '" + v +
                              "' (auto | v4 | lite | lite8 | lite8_full | litef | lite8f | g6 | "
-                             "g7 | g8 | g8r | litefh | dyn)");
+                             "g7 | g8 | g8r | litefh | dyn | vec)");
     hk_slot().store(static_cast<int>(k));
   });
 }

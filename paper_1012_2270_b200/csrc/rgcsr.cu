@@ -383,7 +383,8 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // evict_first, x evict_last), for matrices whose x competes with a large
 // slot stream for L2 (power-law).
 enum class K2 {
-  kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64
+  kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64,
+  kGrpV4, kGrpV2
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -402,6 +403,12 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
   // (vec2), fp32 35.5 vs 35.7; 7-pt 384^3 fp64 842 vs 934 (lite8), fp32
   // 607 vs 651 (lite); 27-pt 128^3 fp64 102.6 vs 105.5, fp32 75.5 vs 80.7.
   if (!h->n_long && h->slots * 10 <= h->nnz * 11) {
+    // fp32 with <= 12 slots per row (5- and 7-point class): the group walk
+    // with 128-bit slot loads, 4 rows per thread (rgcsr_spmv_grpv): 5-pt
+    // 2048^2 32.9 vs 34.7 us, 7-pt 256^3 175.0 vs 180.8, 7-pt 384^3 567 vs
+    // 600, 5-pt 1024^2 11.2 vs 11.3; 27-pt 72.8 vs 71.5 and every fp64 case
+    // lose (profiles/r02_grpv.md)
+    if (!f64 && h->slots <= 12 * h->rows && h->group_size % 4 == 0) return K2::kGrpV4;
     if (2 * h->slots <= 11 * h->rows) return K2::kGrp6;
     if (f64) return K2::kGrp8R64;
     return h->slots <= 12 * h->rows ? K2::kGrp8 : K2::kGrp7Mpf;
@@ -429,7 +436,8 @@ bool parse_k2(const std::string& v, K2* out) {
       {"auto", K2::kAuto},         {"pipe", K2::kPipe},         {"lite", K2::kLite},
       {"lite8", K2::kLite8},       {"lite8_full", K2::kLite8Full}, {"vec2", K2::kVec2},
       {"grp6", K2::kGrp6},         {"grp7_mpf", K2::kGrp7Mpf},  {"grp8", K2::kGrp8},
-      {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H}};
+      {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H},
+      {"grpv4", K2::kGrpV4},       {"grpv2", K2::kGrpV2}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -510,6 +518,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   // the group-uniform walk has no long-row split: matrices with long rows
   // (and, for now, any request on them) take the lite kernel instead
   if (k >= K2::kGrp6 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
+  // the vector walk needs groups of whole vectors
+  if ((k == K2::kGrpV4 || k == K2::kGrpV2) && h->group_size % (16 / sizeof(T)) != 0)
+    k = f64 ? K2::kGrp8R64 : K2::kGrp8;
   const bool hinted = k == K2::kLiteH || k == K2::kLite8H || k == K2::kPipe;
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
   const int sh = pow2_shift(h->group_size);
@@ -602,6 +613,28 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                                  h->columns.p, x, y, x_next, scale, long_cut, ll);
     SPMVK_LAUNCH("rgcsr_spmv (long rows fused)");
   };
+  auto run_grpv = [&](auto kern) {
+    constexpr uint64_t R = 16 / sizeof(T);
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const unsigned grid = persistent_grid((h->rows + 256 * R - 1) / (256 * R),
+                                          per_sm > 0 ? per_sm : 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    SPMVK_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<uint32_t>(h->rows), G, sh,
+                                  (const uint32_t*)h->group_pointers.p,
+                                  (const uint32_t*)h->row_lengths.p,
+                                  reinterpret_cast<const T*>(h->values.p),
+                                  (const uint32_t*)h->columns.p, x, y, x_next, scale, 0u));
+    SPMVK_LAUNCH("rgcsr_spmv_grpv");
+  };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))
   auto run_vec = [&](auto kern) {
     constexpr uint64_t R = sizeof(T) == 8 ? 2 : 4;
@@ -653,6 +686,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       run_fl(rgcsr_spmv_lite<T, kScaled, 8, 5, true>, rgcsr_spmv_lite_fl<T, kScaled, 8, 5, true>);
       break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
+    case K2::kGrpV4: run_grpv(rgcsr_spmv_grpv<T, kScaled, 4, 4>); break;
+    case K2::kGrpV2: run_grpv(rgcsr_spmv_grpv<T, kScaled, 2, 4>); break;
     default: run_fl(rgcsr_spmv_pipe<T, kScaled, U, 4>, rgcsr_spmv_pipe_fl<T, kScaled, U, 4>); break;
   }
 }

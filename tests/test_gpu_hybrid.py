@@ -15,7 +15,7 @@ from paper_1012_2270_b200 import spmvkit as sk
 pytestmark = pytest.mark.gpu
 
 
-HYBRID_VARIANTS = ["auto", "v4", "lite", "lite8", "lite8_full", "litef", "lite8f", "dyn"]
+HYBRID_VARIANTS = ["auto", "v4", "lite", "lite8", "lite8_full", "litef", "lite8f", "dyn", "vec"]
 
 
 @pytest.fixture(params=HYBRID_VARIANTS)
