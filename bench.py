@@ -42,6 +42,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# x up and y down at once over PCIe Gen5 x16: 2 x 16 MiB in 344 us, measured with two
+# concurrent copy-engine transfers (scripts/probes/pcie_sm.cu)
+PCIE_BIDIR_GBS = 2 * 16 * 1048576 / 344e-6 / 1e9
+
 METRIC = "SpMV GFLOP/s and achieved HBM GB/s (% of roofline) fp32/fp64 at 1/2/4/8 B200"
 
 WORKLOADS = {
@@ -608,6 +612,12 @@ def run_ours(args):
         "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,
                 "ms_per_step": e2e_s * 1e3,
+                "pcie_gbs": 8 * (a.num_cols + a.num_rows) / e2e_s / 1e9,
+                "pcie_peak_gbs": PCIE_BIDIR_GBS,
+                "frac_pcie": 8 * (a.num_cols + a.num_rows) / e2e_s / 1e9 / PCIE_BIDIR_GBS,
+                "pcie_peak_source": "16 MB up + 16 MB down as two concurrent copy-engine "
+                                    "transfers, 344 us (scripts/probes/pcie_sm.cu, "
+                                    "profiles/r01_e2e_pipeline.md)",
                 "path": "spmvk_rgcsr_spmv_host_f64 (pinned host x,y; H2D + SpMV + D2H)"},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
