@@ -241,7 +241,12 @@ int spmvk_set_long_row_cut(uint32_t cut);
 /* Tuning knob (process-wide, read at launch): 1 (default) fuses the long rows
  * into the thread-per-row kernel (its warps take the long-row items first,
  * dynamically, then their tiles; one launch), 0 runs them as a separate
- * launch after it.  Does not change y.  Also read from SPMVK_LONG_FUSED. */
+ * launch after it.  Does not change y.  Also read from SPMVK_LONG_FUSED.
+ * The fused kernels (and the Hybrid "dyn" kernel) take work from four 32-bit
+ * counters per (device, stream) that the last warp of each launch resets:
+ * launches on one stream are ordered, so they never share live counters --
+ * do not destroy a stream and recreate one while work it queued on those
+ * kernels is still running (a recycled handle would share them). */
 int spmvk_set_long_fused(int on);
 
 /* ------------------------------------------------------------------ Hybrid */
