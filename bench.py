@@ -390,8 +390,8 @@ def scale_anchor(args, peak):
     RgCSR), the matrix the N > 1 scaling runs shard.  One step is the
     iterated product's x <- (A x) * 2^-4 (the scaled K2 epilogue), 100 steps
     as the config names, timed like the headline; the iterate's bit checksum
-    is compared with the device CSR kernel's iterate (an independent kernel;
-    the reference comparison of this iterate is tests/test_gpu_config5.py)."""
+    must equal the unmodified reference's (tests/golden/iterate_7pt512.json,
+    oracle/make_iterate_golden.py) and the device CSR kernel's iterate."""
     import torch
     from paper_1012_2270_b200 import generators as gen
     from paper_1012_2270_b200 import spmvkit as sk
@@ -434,6 +434,8 @@ def scale_anchor(args, peak):
             torch.mul(yc, 0.0625, out=xc)
     torch.cuda.synchronize()
     bits_csr = int(xc.view(torch.int64).sum().item())
+    with open(os.path.join(ROOT, "tests", "golden", "iterate_7pt512.json")) as f:
+        bits_ref = int(json.load(f)["bits_sum_int64_after"][str(iters)])
     B = rg_bytes(a.info, 8)
     nnz = a.nnz()
     out = {"workload": "7pt-512", "description": WORKLOADS["7pt-512"][3], "n_gpus": 1,
@@ -441,13 +443,15 @@ def scale_anchor(args, peak):
            "gflops": 2.0 * nnz / (per * 1e-3) / 1e9,
            "roofline": {"achieved": B / (per * 1e-3) / 1e9, "peak": peak,
                         "frac": B / (per * 1e-3) / 1e9 / peak, "bytes_per_launch": B},
-           "build_s": t_build, "x_bits_checksum": bits,
-           "parity": "bitwise == device spmv_csr iterate" if bits == bits_csr else "MISMATCH",
+           "build_s": t_build, "x_bits_checksum": bits, "reference_bits": bits_ref,
+           "parity": ("bitwise == the unmodified reference's iterate and the device spmv_csr "
+                      "iterate" if bits == bits_csr == bits_ref else "MISMATCH"),
            "sm_mhz": clk.summary().get("sm_mhz")}
     del a, csr, xs, y, xc, yc
     torch.cuda.empty_cache()
-    if bits != bits_csr:
-        raise SystemExit("parity gate failed: 7pt-512 iterate differs from the CSR kernel's")
+    if not bits == bits_csr == bits_ref:
+        raise SystemExit(f"parity gate failed: 7pt-512 iterate bits {bits} (CSR kernel "
+                         f"{bits_csr}, reference {bits_ref})")
     return out
 
 

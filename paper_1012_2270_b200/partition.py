@@ -536,6 +536,16 @@ class FusedIteratedSpmv:
         sk._check(self._step(self._d, self.a._h, self.scale, self.y.data_ptr(),
                              1 if self.barrier else 0, self.stream))
 
+    def status(self) -> tuple:
+        """(0, "") while every flag barrier so far completed; else the
+        SPMVK_ENCCL code and the message naming the rank that never arrived
+        (spmvk_dist_status: synchronises the stream)."""
+        import ctypes as C
+
+        from ._lib import lib
+        rc = self._L.spmvk_dist_status(self._d, C.c_void_p(self.stream))
+        return rc, (lib().spmvk_last_error().decode() if rc else "")
+
     def close(self):
         if self._d:
             self._L.spmvk_dist_destroy(self._d)
@@ -795,6 +805,15 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     if clocks:
         clocks.__exit__(None, None, None)
     ms = reduce_scalar(e0.elapsed_time(e1), dist.ReduceOp.MAX)
+    # a flag barrier that timed out makes every later step return at once: a
+    # time measured across one is not a step time -- fail instead
+    if exchange == "fused" and world > 1:
+        rc, why = it.status()
+        bad = reduce_scalar(1 if rc else 0, dist.ReduceOp.MAX, torch.int64)
+        if bad.item():
+            whys = [None] * world
+            dist.all_gather_object(whys, f"rank {rank}: {why}" if rc else "")
+            raise SystemExit("fused exchange failed: " + "; ".join(w for w in whys if w))
     # checksum of this rank's rows of the iterate after warmup + steps
     # iterations (bitwise across P: the slab arrays are global slices and
     # every row keeps the reference's order) -- taken before the e2e leg,
@@ -804,6 +823,35 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
     part_sum = xf[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
     sums = gather_flat(part_sum)
     tot_nnz = reduce_scalar(float(nnz_local), dist.ReduceOp.SUM)
+
+    # parity gate: from x0 again, exactly 100 iterations, and the wrapping
+    # int64 sum of the iterate's raw bits over all ranks must equal the
+    # unmodified reference's (tests/golden/iterate_7pt512.json, made by
+    # oracle/make_iterate_golden.py) -- the P-GPU iterate bitwise the CPU one
+    parity = None
+    golden_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "tests", "golden", "iterate_7pt512.json")
+    if args.workload == "7pt-512" and os.path.exists(golden_path):
+        with open(golden_path) as f:
+            want = int(json.load(f)["bits_sum_int64_after"]["100"])
+        with torch.cuda.stream(stream):
+            it.set_x(x0)
+        stream.synchronize()
+        dist.barrier()
+        for _ in range(100):
+            it.step()
+        torch.cuda.synchronize()
+        if exchange == "fused" and world > 1 and it.status()[0]:
+            raise SystemExit(f"fused exchange failed in the parity pass: {it.status()[1]}")
+        xp = it.x[: a.num_cols] if isinstance(it, IteratedSpmv) else it.x_current
+        mine = xp[me.row_begin:me.row_end].contiguous().view(torch.int64).sum().reshape(1)
+        got = int(gather_flat(mine).sum().item())
+        got = (got + 2 ** 63) % 2 ** 64 - 2 ** 63
+        parity = {"iterations": 100, "bits_sum_int64": got, "reference": want,
+                  "bitwise": got == want, "golden": "tests/golden/iterate_7pt512.json"}
+        if got != want:
+            raise SystemExit(f"parity gate failed: {world}-GPU iterate bit sum {got} != "
+                             f"reference {want}")
 
     # kernel-only time of this rank's slab SpMV (roofline of the dominant kernel)
     xs = (it.x[: a.num_cols] if isinstance(it, IteratedSpmv) else it.x_current).clone()
@@ -885,6 +933,7 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
             "clocks": clocks.summary() if clocks else None,
             "gpu_launches": args.steps * (2 if exchange == "fused" and world > 1 else 1),
             "x_bits_checksum": int(sums.sum().item()),
+            "parity": parity,
         }), flush=True)
     dist.barrier()  # the other ranks wait for rank 0's CPU baseline
     if hasattr(it, "close"):

@@ -92,6 +92,11 @@ def test_config5_7pt_512_vs_reference(cuda):
         sk._check(L.spmvk_rgcsr_spmv_scaled_f64(a._h, xs[k % 2].data_ptr(), N, yd.data_ptr(), N,
                                                 xs[1 - k % 2].data_ptr(), 0.0625, None))
     assert bitwise(xs[iters % 2].cpu().numpy(), xr), "single-GPU iterate"
+    # the committed golden bit sum (bench.py's N > 1 parity gate) is this iterate's
+    gp_ = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "iterate_7pt512.json")
+    with open(gp_) as f:
+        gold = int(json.load(f)["bits_sum_int64_after"]["100"])
+    assert int(xr.view(np.int64).sum(dtype=np.int64)) == gold
     del xs, yd
     # the same iterate through the fused distributed step at P = 1
     sl = pt.slab_bounds(N, G, 1)[0]
