@@ -545,6 +545,21 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   const bool xpf = x_aligned && (xpf_env >= 0 ? xpf_env > 0
                                               : (2 * h->slots <= 11 * h->rows &&
                                                  h->cols * sizeof(T) <= (48ull << 20)));
+  // small matrices (format + x <= 24 MB, a fifth of L2): prefetch the slot
+  // arrays, the group pointers and x at launch, whatever the row shape -- a
+  // cold launch of a small SpMV is one dependent chain of three DRAM round
+  // trips otherwise (profiles/r02b_sweep200.md: 10^4-row banded matrices
+  // ran 10.2 vs 8.2 us for ELL, which has no group pointers).
+  // SPMVK_SMALL_PREFETCH=0 turns it off.
+  static const int small_env = [] {
+    const char* e = std::getenv("SPMVK_SMALL_PREFETCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  const uint64_t fmt_bytes = h->slots * (sizeof(T) + 4) + 4 * (h->groups + 1) +
+                             sizeof(T) * h->cols;
+  const bool small = x_aligned && small_env != 0 && fmt_bytes <= (24ull << 20) &&
+                     (reinterpret_cast<uintptr_t>(h->values.p) & 15) == 0;
+  const bool xpf_small = xpf || small;
   // Programmatic dependent launch for the group walk (default; SPMVK_PDL=0
   // turns it off): a launch may start while the previous kernel on the stream
   // drains, reads only the immutable group pointers, and waits
@@ -573,7 +588,8 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                                   (const uint32_t*)h->row_lengths.p,
                                   reinterpret_cast<const T*>(h->values.p),
                                   (const uint32_t*)h->columns.p, x, y, x_next, scale,
-                                  xpf ? static_cast<uint32_t>(h->cols) : 0u));
+                                  xpf_small ? static_cast<uint32_t>(h->cols) : 0u,
+                                  small ? static_cast<uint32_t>(h->slots) : 0u));
     SPMVK_LAUNCH("rgcsr_spmv_grp");
   };
   auto run_grp = [&](auto kern, auto kern_pdl) {
@@ -632,7 +648,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
                                   (const uint32_t*)h->group_pointers.p,
                                   (const uint32_t*)h->row_lengths.p,
                                   reinterpret_cast<const T*>(h->values.p),
-                                  (const uint32_t*)h->columns.p, x, y, x_next, scale, 0u));
+                                  (const uint32_t*)h->columns.p, x, y, x_next, scale,
+                                  small ? static_cast<uint32_t>(h->cols) : 0u,
+                                  small ? static_cast<uint32_t>(h->slots) : 0u));
     SPMVK_LAUNCH("rgcsr_spmv_grpv");
   };
   // vectorised kernels: tiles of 256 * R rows (R = 16 bytes / sizeof(T))

@@ -418,7 +418,8 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
                                               const T* __restrict__ values,
                                               const uint32_t* __restrict__ columns,
                                               const T* __restrict__ x, const Epi& epi,
-                                              uint32_t x_pf_elems = 0) {
+                                              uint32_t x_pf_elems = 0,
+                                              uint32_t pf_slots = 0) {
   // x_pf_elems > 0 (matrices that fit in L2): every CTA first bulk-prefetches
   // its 1/gridDim slice of x[0, x_pf_elems) into L2 (TMA unit, no completion
   // wait), so a cold launch's x gathers hit L2 instead of paying a second
@@ -429,6 +430,23 @@ __device__ __forceinline__ void grp_tiles_epi(uint32_t rows, uint32_t G, int g_s
     const uint64_t b0 = per * blockIdx.x, b1 = min((uint64_t)(bytes & ~15ull), b0 + per);
     for (uint64_t o = b0; o < b1; o += 65536)
       bulk_prefetch_l2(reinterpret_cast<const char*>(x) + o, (uint32_t)min((uint64_t)65536, b1 - o));
+  }
+  // pf_slots > 0 (small matrices, launched cold): the CTA also prefetches its
+  // slice of the slot arrays and the group pointers, so a cold launch's
+  // dependent chain (group pointers -> slots -> x) waits on DRAM once, not
+  // three times
+  if (pf_slots && threadIdx.x == 0) {
+    const uint64_t ngp = (uint64_t)(rows + G - 1) / G + 1;
+    const void* arr[3] = {values, columns, gp};
+    const uint64_t len[3] = {(uint64_t)pf_slots * sizeof(T), (uint64_t)pf_slots * 4, ngp * 4};
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t bytes = len[a] & ~15ull;
+      const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+      const uint64_t b0 = per * blockIdx.x, b1 = min(bytes, b0 + per);
+      for (uint64_t o = b0; o < b1; o += 65536)
+        bulk_prefetch_l2(reinterpret_cast<const char*>(arr[a]) + o,
+                         (uint32_t)min((uint64_t)65536, b1 - o));
+    }
   }
   const uint32_t ntiles = (rows + 255) / 256;
   struct Meta {
@@ -492,12 +510,26 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grpv(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t /*unused*/) {
+    T* __restrict__ x_next, T scale, uint32_t x_pf_elems, uint32_t pf_slots) {
   constexpr int R = 16 / sizeof(T);
   using Wv = VecOf<T, R>;
   using V = typename Wv::V;
   using Cv = typename Wv::C;
   const StoreEpi<T, kScaled> epi{y, x_next, scale};
+  if (threadIdx.x == 0 && (x_pf_elems || pf_slots)) {  // small matrices: as the scalar walk
+    const uint64_t ngp = pf_slots ? (uint64_t)(rows + G - 1) / G + 1 : 0;
+    const void* arr[4] = {x, values, columns, gp};
+    const uint64_t len[4] = {(uint64_t)x_pf_elems * sizeof(T), (uint64_t)pf_slots * sizeof(T),
+                             (uint64_t)pf_slots * 4, ngp * 4};
+    for (int a = 0; a < 4; ++a) {
+      const uint64_t bytes = len[a] & ~15ull;
+      const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+      const uint64_t b0 = per * blockIdx.x, b1 = min(bytes, b0 + per);
+      for (uint64_t o = b0; o < b1; o += 65536)
+        bulk_prefetch_l2(reinterpret_cast<const char*>(arr[a]) + o,
+                         (uint32_t)min((uint64_t)65536, b1 - o));
+    }
+  }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool use_len = !isfinite(__ldg(x));
@@ -590,10 +622,11 @@ __global__ void __launch_bounds__(256, MINB) rgcsr_spmv_grp(
     uint32_t rows, uint32_t G, int g_shift, const uint32_t* __restrict__ gp,
     const uint32_t* __restrict__ lens, const T* __restrict__ values,
     const uint32_t* __restrict__ columns, const T* __restrict__ x, T* __restrict__ y,
-    T* __restrict__ x_next, T scale, uint32_t x_pf_elems /* long_cut slot: no long rows here */) {
+    T* __restrict__ x_next, T scale, uint32_t x_pf_elems /* long_cut slot: no long rows here */,
+    uint32_t pf_slots) {
   grp_tiles_epi<T, U, kNoLen, kMpf, StoreEpi<T, kScaled>, kGatherK, kPdl>(
       rows, G, g_shift, gp, lens, values, columns, x, StoreEpi<T, kScaled>{y, x_next, scale},
-      x_pf_elems);
+      x_pf_elems, pf_slots);
 }
 
 // SpMV with the CG dot fused into the row epilogue: y = A x and, per CTA, the
