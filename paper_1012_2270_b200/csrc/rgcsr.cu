@@ -120,7 +120,7 @@ std::atomic<uint32_t>& long_cut_slot() {
 // with coalesced loads, and the slot-major writes read them from there --
 // instead of 32 scattered row streams per load instruction, which cost one
 // L1 tag lookup per lane.  Larger groups (long rows) read CSR directly.
-constexpr uint32_t kStage = 1024;
+constexpr uint32_t kStage = 512;
 
 template <class T, class V>
 __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows, uint64_t G,
@@ -143,6 +143,38 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
     const uint64_t s = min(G, rows - g * G);
     const uint32_t base = gp[g];
     const uint64_t width = s ? (gp[g + 1] - base) / s : 0;
+    if (s == 32) {  // full 32-row group: two 16-row halves, each staged if it fits
+      for (uint32_t c0 = 0; c0 < 32; c0 += 16) {
+        const uint64_t row = g * G + c0 + (lane & 15);
+        const uint32_t len = lens[row];
+        const uint32_t h0 = rp[r0 + g * G + c0], h1 = rp[r0 + g * G + c0 + 16];
+        const uint32_t start = rp[r0 + row];
+        const uint64_t t = c0 + (lane & 15);
+        if (h1 - h0 <= kStage) {  // warp-uniform
+          for (uint32_t i = lane; i < h1 - h0; i += 32) {
+            sv[i] = static_cast<T>(val[h0 + i]);
+            sc[i] = col[h0 + i];
+          }
+          __syncwarp();
+          const uint32_t off = start - h0;
+          // lanes 0-15 write even slots, 16-31 odd: each store instruction
+          // covers two whole 16-row (128 B / 64 B) runs of the slab
+          for (uint64_t j = lane >> 4; j < width; j += 2) {
+            const uint64_t idx = base + t + j * 32;
+            values[idx] = j < len ? sv[off + j] : T(0);
+            columns[idx] = j < len ? sc[off + j] : 0u;
+          }
+          __syncwarp();
+        } else {
+          for (uint64_t j = lane >> 4; j < width; j += 2) {
+            const uint64_t idx = base + t + j * 32;
+            values[idx] = j < len ? static_cast<T>(val[start + j]) : T(0);
+            columns[idx] = j < len ? col[start + j] : 0u;
+          }
+        }
+      }
+      continue;
+    }
     const uint32_t e0 = rp[r0 + g * G], e1 = rp[r0 + g * G + s];
     if (s <= 32 && e1 - e0 <= kStage) {  // warp-uniform
       for (uint32_t i = lane; i < e1 - e0; i += 32) {
