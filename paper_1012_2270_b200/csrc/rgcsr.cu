@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "rgcsr_spmv.cuh"
+#include "tma.cuh"
 
 namespace spmvk {
 namespace {
@@ -216,6 +217,105 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
   }
 }
 
+// K1 scatter with 1D bulk async copies (TMA, cp.async.bulk + mbarrier):
+// each warp owns a static sequence of groups; a full 32-row group's CSR block
+// [rp[g G], rp[g G + 32]) (values, columns; rounded out to 16-byte bounds) is
+// brought into one of the warp's two shared-memory stages by two bulk copies
+// issued by lane 0, the NEXT group's block is in flight while this group's
+// slots are written (slot-major, coalesced, pads included) from the other
+// stage.  Partial groups and blocks that do not fit the stage are written
+// straight from CSR.  SPMVK_K1_BULK=1 selects it (A/B).
+constexpr uint32_t kBulkStage = 1024;  // entries per stage (+ 4 of alignment slack)
+
+template <class T, class V>
+__global__ void __launch_bounds__(128) rgcsr_scatter_bulk(uint64_t r0, uint64_t rows, uint64_t G,
+                                                          uint64_t groups,
+                                                          const uint32_t* __restrict__ rp,
+                                                          const uint32_t* __restrict__ col,
+                                                          const V* __restrict__ val,
+                                                          const uint32_t* __restrict__ gp,
+                                                          const uint32_t* __restrict__ lens,
+                                                          T* __restrict__ values,
+                                                          uint32_t* __restrict__ columns) {
+  constexpr uint32_t SV = (kBulkStage + 4) * sizeof(V), SC = (kBulkStage + 4) * 4;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wbase = sm + (size_t)warp * 2 * (SV + SC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)4 * 2 * (SV + SC)) + warp * 2;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t first = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  // stage b of group g: returns whether a copy was issued
+  auto full_and_fits = [&](uint64_t g) {
+    if (g >= groups || (g + 1) * G > rows || G != 32) return false;
+    return rp[r0 + g * G + 32] - rp[r0 + g * G] <= kBulkStage;
+  };
+  auto issue = [&](uint64_t g, int b) {
+    const uint32_t e0 = rp[r0 + g * G], e1 = rp[r0 + g * G + 32];
+    const uint64_t v0 = (uint64_t)e0 * sizeof(V) & ~15ull;
+    const uint64_t v1 = ((uint64_t)e1 * sizeof(V) + 15) & ~15ull;
+    const uint64_t c0 = (uint64_t)e0 * 4 & ~15ull, c1 = ((uint64_t)e1 * 4 + 15) & ~15ull;
+    unsigned char* sv = wbase + b * (SV + SC);
+    mbar_arrive_expect_tx(&bar[b], (uint32_t)(v1 - v0 + c1 - c0));
+    bulk_g2s(sv, reinterpret_cast<const unsigned char*>(val) + v0, (uint32_t)(v1 - v0), &bar[b]);
+    bulk_g2s(sv + SV, reinterpret_cast<const unsigned char*>(col) + c0, (uint32_t)(c1 - c0),
+             &bar[b]);
+  };
+  uint32_t phase[2] = {0, 0};
+  bool staged = first < groups && full_and_fits(first);
+  if (staged && lane == 0) issue(first, 0);
+  int b = 0;
+  for (uint64_t g = first; g < groups; g += warps, b ^= 1) {
+    const uint64_t gn = g + warps;
+    const bool staged_n = full_and_fits(gn);
+    if (staged_n && lane == 0) {
+      fence_proxy_async_smem();  // stage 1-b was read (generic proxy) by the previous group
+      issue(gn, b ^ 1);
+    }
+    const uint64_t s = min(G, rows - g * G);
+    const uint32_t base = gp[g];
+    const uint64_t width = s ? (gp[g + 1] - base) / s : 0;
+    if (staged) {
+      mbar_wait(&bar[b], phase[b]);
+      phase[b] ^= 1;
+      const uint32_t e0 = rp[r0 + g * G];
+      const V* sv = reinterpret_cast<const V*>(wbase + b * (SV + SC)) +
+                    ((uint64_t)e0 * sizeof(V) & 15) / sizeof(V);
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(wbase + b * (SV + SC) + SV) +
+                           ((uint64_t)e0 * 4 & 15) / 4;
+      const uint64_t row = g * G + lane;
+      const uint32_t len = lens[row];
+      const uint32_t off = rp[r0 + row] - e0;
+      for (uint64_t j = 0; j < width; ++j) {
+        const uint64_t idx = base + lane + j * 32;
+        values[idx] = j < len ? static_cast<T>(sv[off + j]) : T(0);
+        columns[idx] = j < len ? sc[off + j] : 0u;
+      }
+      __syncwarp();
+    } else {
+      for (uint64_t t0 = 0; t0 < s; t0 += 32) {
+        const uint64_t t = t0 + lane;
+        if (t >= s) continue;
+        const uint64_t row = g * G + t;
+        const uint32_t len = lens[row];
+        const uint32_t start = rp[r0 + row];
+        for (uint64_t j = 0; j < width; ++j) {
+          const uint64_t idx = base + t + j * s;
+          values[idx] = j < len ? static_cast<T>(val[start + j]) : T(0);
+          columns[idx] = j < len ? col[start + j] : 0u;
+        }
+      }
+      __syncwarp();
+    }
+    staged = staged_n;
+  }
+}
+
 // Quads for rgcsr_spmv_long_mixed: rows r..r+3 (r % 4 == 0) all long, in one
 // full group of a G % 4 == 0 matrix, each shorter than kQuadMaxLen (the
 // longest rows keep a warp each: a quad walks 64 slots per round, so a
@@ -371,7 +471,33 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
                                     h->columns.p);
       SPMVK_LAUNCH("rgcsr_scatter");
     };
-    if (prec == SPMVK_F64)
+    static const bool k1_bulk = [] {
+      const char* e = std::getenv("SPMVK_K1_BULK");
+      return e && std::atoi(e) != 0;
+    }();
+    auto scatter_bulk = [&](auto kern, auto* vals_in, auto* vals_out) {
+      using VI = std::remove_const_t<std::remove_pointer_t<decltype(vals_in)>>;
+      const size_t smem = 4 * 2 * ((kBulkStage + 4) * (sizeof(VI) + 4)) + 4 * 2 * 8;
+      SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      int per_sm = 0;
+      SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+      const unsigned sgrid = persistent_grid((h->groups + 3) / 4, per_sm > 0 ? per_sm : 1);
+      kern<<<sgrid, 128, smem, s>>>(r0, h->rows, G, h->groups, a->row_ptr.p, a->col.p, vals_in,
+                                    h->group_pointers.p, h->row_lengths.p, vals_out,
+                                    h->columns.p);
+      SPMVK_LAUNCH("rgcsr_scatter_bulk");
+    };
+    if (k1_bulk && prec == SPMVK_F64)
+      scatter_bulk(rgcsr_scatter_bulk<double, double>, reinterpret_cast<const double*>(a->val.p),
+                   reinterpret_cast<double*>(h->values.p));
+    else if (k1_bulk && a->val_prec == SPMVK_F64)
+      scatter_bulk(rgcsr_scatter_bulk<float, double>, reinterpret_cast<const double*>(a->val.p),
+                   reinterpret_cast<float*>(h->values.p));
+    else if (k1_bulk)
+      scatter_bulk(rgcsr_scatter_bulk<float, float>, reinterpret_cast<const float*>(a->val.p),
+                   reinterpret_cast<float*>(h->values.p));
+    else if (prec == SPMVK_F64)
       scatter(rgcsr_scatter<double, double>, reinterpret_cast<const double*>(a->val.p),
               reinterpret_cast<double*>(h->values.p));
     else if (a->val_prec == SPMVK_F64)

@@ -110,8 +110,8 @@ def main():
     out = open(args.out, "w") if args.out else None
     R = orc.R() if orc.ref_available() else None
     for wl in args.workloads.split(","):
-        rows, cols, rp, col, val = bench.host_csr(wl)
-        m = orc.Csr(rows, cols, rp, col, val)
+        m = bench.host_csr(wl)  # the oracle's generators (oracle.Csr)
+        rows, cols, rp, col, val = m.rows, m.cols, m.rp, m.col, m.val
         ref_m = orc.RefMatrix.from_csr(m) if R else None
         csr = bench.make_csr(wl)
         nnz = csr.nnz()
