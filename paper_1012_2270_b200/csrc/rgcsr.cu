@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256) rgcsr_scatter(uint64_t r0, uint64_t rows,
 // issued by lane 0, the NEXT group's block is in flight while this group's
 // slots are written (slot-major, coalesced, pads included) from the other
 // stage.  Partial groups and blocks that do not fit the stage are written
-// straight from CSR.  SPMVK_K1_BULK=1 selects it (A/B).
+// straight from CSR.  The default K1 scatter (SPMVK_K1_BULK=0 selects the
+// staged rgcsr_scatter above).
 constexpr uint32_t kBulkStage = 1024;  // entries per stage (+ 4 of alignment slack)
 
 template <class T, class V>
@@ -471,9 +472,11 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
                                     h->columns.p);
       SPMVK_LAUNCH("rgcsr_scatter");
     };
+    // bulk-copy scatter (default; SPMVK_K1_BULK=0 -> the shared-memory staged
+    // kernel): 27-pt 128^3 fp64 207 vs 271 us (profiles/r02b_ncu_k1_scatter.md)
     static const bool k1_bulk = [] {
       const char* e = std::getenv("SPMVK_K1_BULK");
-      return e && std::atoi(e) != 0;
+      return !e || std::atoi(e) != 0;
     }();
     auto scatter_bulk = [&](auto kern, auto* vals_in, auto* vals_out) {
       using VI = std::remove_const_t<std::remove_pointer_t<decltype(vals_in)>>;
