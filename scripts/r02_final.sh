@@ -18,7 +18,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rgcsr_spmv -s 3 -c 1 -o $O/prof_headline_$TAG python bench.py --steps 5 --warmup 3 --cpu-reps 1 --no-powerlaw > $O/ncu_headline_$TAG.log 2>&1; tail -1 $O/ncu_headline_$TAG.log
 timeout 1500 python scripts/records.py --out $O/records_$TAG.jsonl > $O/records_$TAG.log 2>&1; tail -2 $O/records_$TAG.log
 M=$(python -c "import sys; sys.path.insert(0,'scripts'); import records_ncu as r; print(r.METRICS)")
-timeout 1800 ncu --metrics $M --clock-control none --csv --log-file $O/rec_ncu_$TAG.csv -k regex:"rgcsr_spmv|hybrid_spmv|hybrid_ell|csr_spmv|dot_partials" python scripts/records_ncu.py run > $O/rec_ncu_$TAG.log 2>&1
+timeout 1800 ncu --metrics $M --clock-control none --csv --log-file $O/rec_ncu_$TAG.csv -k regex:"rgcsr_spmv|hybrid_spmv|hybrid_ell_vec|csr_spmv|dot_partials" python scripts/records_ncu.py run > $O/rec_ncu_$TAG.log 2>&1
 python scripts/records_ncu.py merge $O/rec_ncu_$TAG.csv $O/records_$TAG.jsonl
 timeout 900 compute-sanitizer --tool memcheck python scripts/sanitize.py > $O/san_${TAG}_memcheck.log 2>&1; tail -2 $O/san_${TAG}_memcheck.log
 ls $O | grep $TAG

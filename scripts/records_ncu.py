@@ -4,7 +4,8 @@ under `ncu --metrics`, cases separated by a marker kernel, then the
 per-case sums merged into the records .jsonl.
 
   ncu --metrics <METRICS> --csv --log-file gpurun_out/rec_ncu.csv \\
-      -k regex:"rgcsr_spmv|hybrid_spmv|csr_spmv|dot_partials" python scripts/records_ncu.py run
+      -k regex:"rgcsr_spmv|hybrid_spmv|hybrid_ell_vec|csr_spmv|dot_partials" \
+      python scripts/records_ncu.py run
   python scripts/records_ncu.py merge gpurun_out/rec_ncu.csv profiles/r01_records.jsonl
 
 Counters per record: DRAM bytes read + written (summed over the case's SpMV
@@ -93,7 +94,7 @@ def merge(csv_path, records_path):
             if cur is not None:
                 groups.append(cur)
             cur = []
-        elif cur is not None:
+        elif cur is not None and "_fill" not in k["name"]:  # a builder kernel, not a SpMV
             cur.append(k)
     per = {}
     for (wl, prec, fmt), ks in zip(cases(), groups):

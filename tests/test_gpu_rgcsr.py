@@ -436,3 +436,44 @@ def test_long_rows_fused_into_tile_kernel(cuda, powerlaw_pair, variant, fused, p
     finally:
         L.spmvk_set_rgcsr_kernel(b"auto")
         L.spmvk_set_long_fused(1)
+
+
+@pytest.mark.parametrize("bulk", ["1", "0"])
+def test_k1_scatter_variants_bitwise(cuda, bulk):
+    """Both K1 scatters (SPMVK_K1_BULK, read once per process, so each runs in
+    a child): the TMA bulk-copy kernel (default) and the shared-memory staged
+    one, on full and partial groups, G = 32 and 64, row slabs, fp64 and fp32
+    (double -> float cast), stencils and power-law rows past the stage size --
+    arrays bitwise the oracle's build_rgcsr."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np
+import oracle as orc
+from helpers import triplets
+from paper_1012_2270_b200 import spmvkit as sk
+mats = [orc.stencil(27, 21), orc.stencil(5, 301), orc.powerlaw(40000, 7), orc.banded(7777, 9, 3)]
+for om in mats:
+    m = sk.build_csr(triplets(om))
+    for G in (32, 64, 7):
+        for prec in (8, 4):
+            got = sk.build_rgcsr(m, G, prec).to_host()
+            want = orc.build_rgcsr(om, G, prec)
+            for k in ("values", "columns", "group_pointers", "row_lengths"):
+                assert np.array_equal(got[k], want[k]), (om.rows, G, prec, k)
+    r0 = 32 * (om.rows // 96)
+    part = sk.build_rgcsr(m, 32, 8, row_range=(r0, om.rows)).to_host()
+    full = orc.build_rgcsr(om, 32, 8)
+    gp = full["group_pointers"]
+    g0 = r0 // 32
+    assert np.array_equal(part["values"], full["values"][gp[g0]:])
+    assert np.array_equal(part["columns"], full["columns"][gp[g0]:])
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]),
+               SPMVK_K1_BULK=bulk)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
