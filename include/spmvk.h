@@ -220,19 +220,24 @@ void spmvk_rgcsr_destroy(spmvk_rgcsr* h);
 int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double hit_ratio,
                            uint64_t* granted);
 /* Tuning knob (process-wide): which K2 kernel runs.  "auto" (default:
- * without long rows and with <= 10 % padding the group-uniform walk --
- * grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf (fp32),
- * launched with programmatic dependent launch unless SPMVK_PDL=0; otherwise
- * lite8 for fp64, lite or pipe for fp32, plus the long-row kernel),
- * "grp6" / "grp7_mpf" / "grp8" / "grp8_r64" (group-uniform walk: U-deep slot
- * batches bound by the group width, scheduling fence before the x gathers,
- * row_lengths skipped when x[0] is finite, next row's group pointers
- * prefetched), "lite" / "lite8" / "lite8_full" (register-lean thread per
- * row), "liteh" / "lite8h" (same with L2 eviction hints), "vec2" (128-bit
- * loads of 2 / 4 rows), "pipe" (row-metadata prefetch, predicated batches,
- * L2 hints).  All give bitwise identical y; the measured comparison (and the
- * variants removed in round 2) are in DESIGN.md §3 and
- * profiles/r02_k2_pruned.md.  Also read from SPMVK_RGCSR_KERNEL. */
+ * without long rows and with <= 10 % padding the group-uniform walk -- fp32
+ * with <= 12 slots per row grpv4 (128-bit slot loads, 4 rows per thread),
+ * else grp6 (<= 5.5 slots per row) / grp8_r64 (fp64) / grp8 or grp7_mpf
+ * (fp32), launched with programmatic dependent launch unless SPMVK_PDL=0;
+ * with rows past the long-row cut the row-pipelined kernel with the long rows
+ * fused in (pipe_fl: long-row work items, then dynamic 128-row slices);
+ * heavily padded matrices without long rows lite8 for fp64, lite or
+ * lite8_full for fp32), "grp6" / "grp7_mpf" / "grp8" / "grp8_r64" (group-
+ * uniform walk: U-deep slot batches bound by the group width, scheduling
+ * fence before the x gathers, row_lengths skipped when x[0] is finite, next
+ * row's group pointers prefetched), "grpv4" / "grpv2" (the same walk with
+ * 128-bit slot vectors, U = 4 / 2), "lite" / "lite8" / "lite8_full"
+ * (register-lean thread per row), "liteh" / "lite8h" (same with L2 eviction
+ * hints), "vec2" (128-bit loads of 2 / 4 rows, per-row lengths), "pipe"
+ * (row-metadata prefetch, predicated batches, L2 hints).  All give bitwise
+ * identical y; the measured comparison (and the variants removed in round 2)
+ * are in DESIGN.md §3, profiles/r02_k2_pruned.md and profiles/r02_grpv.md.
+ * Also read from SPMVK_RGCSR_KERNEL. */
 int spmvk_set_rgcsr_kernel(const char* name);
 /* Tuning knob (process-wide, read at build): rows with more than `cut` slots
  * (default 128) are handled by a warp-per-row kernel instead of one thread
