@@ -230,8 +230,8 @@ int spmvk_stream_persist_x(void* stream, const void* x, uint64_t bytes, double h
  * lite8_full for fp32), "grp6" / "grp7_mpf" / "grp8" / "grp8_r64" (group-
  * uniform walk: U-deep slot batches bound by the group width, scheduling
  * fence before the x gathers, row_lengths skipped when x[0] is finite, next
- * row's group pointers prefetched), "grpv4" / "grpv2" (the same walk with
- * 128-bit slot vectors, U = 4 / 2), "lite" / "lite8" / "lite8_full"
+ * row's group pointers prefetched), "grpv4" (the same walk with 128-bit
+ * slot vectors, 4 rows per thread, U = 4), "lite" / "lite8" / "lite8_full"
  * (register-lean thread per row), "liteh" / "lite8h" (same with L2 eviction
  * hints), "vec2" (128-bit loads of 2 / 4 rows, per-row lengths), "pipe"
  * (row-metadata prefetch, predicated batches, L2 hints).  All give bitwise

@@ -545,7 +545,7 @@ void check_spmv_args(const spmvk_rgcsr* h, uint64_t nx, uint64_t ny) {
 // slot stream for L2 (power-law).
 enum class K2 {
   kAuto, kPipe, kLite, kLite8, kLite8Full, kLiteH, kLite8H, kVec2, kGrp6, kGrp7Mpf, kGrp8, kGrp8R64,
-  kGrpV4, kGrpV2
+  kGrpV4
 };
 
 // "auto" (default): the variant that measured fastest on B200 across the
@@ -598,7 +598,7 @@ bool parse_k2(const std::string& v, K2* out) {
       {"lite8", K2::kLite8},       {"lite8_full", K2::kLite8Full}, {"vec2", K2::kVec2},
       {"grp6", K2::kGrp6},         {"grp7_mpf", K2::kGrp7Mpf},  {"grp8", K2::kGrp8},
       {"grp8_r64", K2::kGrp8R64},  {"liteh", K2::kLiteH},      {"lite8h", K2::kLite8H},
-      {"grpv4", K2::kGrpV4},       {"grpv2", K2::kGrpV2}};
+      {"grpv4", K2::kGrpV4}};
   for (const auto& [n, k] : names)
     if (v == n) {
       *out = k;
@@ -680,7 +680,7 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   // (and, for now, any request on them) take the lite kernel instead
   if (k >= K2::kGrp6 && h->n_long) k = f64 ? K2::kLite8 : K2::kLite;
   // the vector walk needs groups of whole vectors
-  if ((k == K2::kGrpV4 || k == K2::kGrpV2) && h->group_size % (16 / sizeof(T)) != 0)
+  if (k == K2::kGrpV4 && h->group_size % (16 / sizeof(T)) != 0)
     k = f64 ? K2::kGrp8R64 : K2::kGrp8;
   const bool hinted = k == K2::kLiteH || k == K2::kLite8H || k == K2::kPipe;
   const uint32_t G = static_cast<uint32_t>(std::min<uint64_t>(h->group_size, 0xffffffffull));
@@ -866,7 +866,6 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
     case K2::kGrpV4: run_grpv(rgcsr_spmv_grpv<T, kScaled, 4, 4>); break;
-    case K2::kGrpV2: run_grpv(rgcsr_spmv_grpv<T, kScaled, 2, 4>); break;
     default: run_fl(rgcsr_spmv_pipe<T, kScaled, U, 4>, rgcsr_spmv_pipe_fl<T, kScaled, U, 4>); break;
   }
 }

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 
 VARIANTS = ["auto", "grp6", "grp7_mpf", "grp8", "grp8_r64", "lite", "lite8", "lite8_full",
-            "vec2", "pipe", "grpv4", "grpv2"]
+            "vec2", "pipe", "grpv4"]
 
 
 def dev(x):
