@@ -105,9 +105,14 @@ def test_kernel_variant_knobs_validate_names():
     """The tuning knobs accept their documented names and reject others
     (EINVAL with the list) -- host-only, no device needed."""
     L = _lib.lib()
-    for v in (b"auto", b"v4", b"lite", b"lite8", b"lite8_full", b"litef", b"lite8f"):
+    for v in (b"auto", b"v4", b"lite", b"lite8", b"lite8_full", b"litef", b"lite8f", b"g6",
+              b"g7", b"g8", b"g8r", b"litefh", b"dyn", b"vec"):
         assert L.spmvk_set_hybrid_kernel(v) == 0, v
     assert L.spmvk_set_hybrid_kernel(b"nope") == _lib.SPMVK_EINVAL
-    assert "lite8_full" in _lib.last_error()
+    assert "lite8_full" in _lib.last_error() and "dyn" in _lib.last_error()
+    for v in (b"auto", b"grp6", b"grp7_mpf", b"grp8", b"grp8_r64", b"grpv4", b"lite", b"lite8",
+              b"lite8_full", b"liteh", b"lite8h", b"vec2", b"pipe"):
+        assert L.spmvk_set_rgcsr_kernel(v) == 0, v
     assert L.spmvk_set_rgcsr_kernel(b"nope") == _lib.SPMVK_EINVAL
+    assert L.spmvk_set_long_fused(0) == 0 and L.spmvk_set_long_fused(1) == 0
     assert L.spmvk_set_hybrid_kernel(b"auto") == 0 and L.spmvk_set_rgcsr_kernel(b"auto") == 0
