@@ -106,3 +106,41 @@ def test_spmv_dot_fused(cuda):
     bad = torch.zeros(1, dtype=torch.float64, device="cuda")
     assert L.spmvk_rgcsr_spmv_dot_f64(a._h, x.data_ptr(), x.numel(), y.data_ptr(), y.numel(),
                                       x.numel(), bad.data_ptr(), None) != 0  # offset too large
+
+
+def test_cg_with_long_rows_graph_captured(cuda):
+    """CG on an SPD matrix with rows past the long-row cut (three dense hub
+    rows / columns on a 1-D Laplacian): its SpMV is the fused long-row kernel
+    (work counters per stream), run eagerly once and then replayed from the
+    CUDA graph CG captures -- the solution must match a direct solve."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    n = 20000
+    hubs = [0, 7000, 15000]
+    rng = np.random.default_rng(5)
+    rows, cols, vals = [], [], []
+    for i in range(n):  # 1-D Laplacian
+        rows += [i]
+        cols += [i]
+        vals += [4.0]
+        if i:
+            rows += [i, i - 1]
+            cols += [i - 1, i]
+            vals += [-1.0, -1.0]
+    for h in hubs:  # symmetric dense-ish hub row / column, diagonally dominated
+        js = rng.choice(np.setdiff1d(np.arange(n), [h - 1, h, h + 1]), 600, replace=False)
+        w = -rng.random(600) / 700.0
+        rows += [h] * 600 + list(js)
+        cols += list(js) + [h] * 600
+        vals += list(w) + list(w)
+    A = sp.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr()
+    A.sum_duplicates()
+    A.sort_indices()
+    om = orc.Csr(n, n, A.indptr.astype(np.uint32), A.indices.astype(np.uint32), A.data)
+    assert int(om.lens().max()) > 128
+    a = sk.build_rgcsr(triplets(om), 32)
+    bh = orc.random_vector(n, 9)
+    x, iters, rel = sk.cg(a, torch.from_numpy(bh).cuda(), tol=1e-10, max_iter=2000)
+    assert rel <= 1e-10 and 0 < iters < 2000
+    xs = spl.spsolve(A.tocsc(), bh)
+    assert np.linalg.norm(x.cpu().numpy() - xs) <= 1e-7 * np.linalg.norm(xs)
