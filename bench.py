@@ -84,7 +84,7 @@ def traffic_source():
         return None
 
 
-def measured_traffic(workload, timeout_s=240):
+def measured_traffic(workload, timeout_s=120):
     """DRAM bytes (read + write) of ONE launch of the headline kernel, measured
     in this run by ncu in a child process (scripts/prof_k2.py: the same
     matrix, the auto K2 kernel, third launch), after -- and apart from -- the
