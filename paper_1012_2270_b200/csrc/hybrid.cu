@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(256, MINB) hybrid_spmv_dyn(
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* __restrict__ pr = prod[warp];
   const Ldr<kHint> ld;
-  if (warp < hl.warps) {  // heavy rows first, longest first
+  if (hl.n_single && warp < hl.warps) {  // heavy rows first, longest first
     for (;;) {
       uint32_t i = 0;
       if (lane == 0) i = atomicAdd(hl.ctr, 1u);

@@ -584,6 +584,11 @@ K2 auto_k2(const spmvk_rgcsr* h, bool f64) {
   // original order fp64 1,222 us (was lite8 + separate long-row launch
   // 1,419), fp32 925 (1,044); descending order fp64 557 (607), fp32 511 (564)
   if (h->n_long) return K2::kPipe;
+  // ragged rows without long ones (> 10 % padding; the sweep's random class):
+  // the row-pipelined kernel, static rows (scripts/probes/random_ab.py:
+  // 0.8-7.2 M rows, mean 17-58, fp32 lite 124-2,321 us -> 96-1,833, fp64
+  // lite8 117-2,417 -> 113-2,246; 18 k rows equal; profiles/r02_long_fused.md)
+  if (h->rows >= (1u << 16)) return K2::kPipe;
   if (f64) return K2::kLite8;
   // fp32, short rows (<= ~12 slots): one 8-deep batch per row at full
   // occupancy (32 registers, no spills) keeps more slot bytes in flight
@@ -773,8 +778,16 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
   // the long rows fused into the tile kernel (default; SPMVK_LONG_FUSED=0
   // restores the separate launch): warps take the long-row items first, then
   // their tiles (rgcsr_spmv.cuh long_items_dynamic)
-  auto run_fl = [&](auto kern, auto kern_fl) {
-    if (!h->n_long || !long_fused_slot().load(std::memory_order_relaxed)) return run(kern);
+  // SPMVK_PIPE_DYN=1 (A/B): the pipe variant takes its rows in dynamic slices
+  // even without long rows
+  static const bool pipe_dyn_all = [] {
+    const char* e = std::getenv("SPMVK_PIPE_DYN");
+    return e && std::atoi(e) != 0;
+  }();
+  auto run_fl = [&](auto kern, auto kern_fl, bool dyn_ok = false) {
+    if (!(h->n_long || (dyn_ok && pipe_dyn_all)) ||
+        !long_fused_slot().load(std::memory_order_relaxed))
+      return run(kern);
     int per_sm = 0;
     SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_fl, 256, 0));
     const unsigned grid = persistent_grid((h->rows + 255) / 256, per_sm > 0 ? per_sm : 1);
@@ -866,7 +879,9 @@ void launch_spmv(const spmvk_rgcsr* h, const T* x, T* y, T* x_next, T scale, cud
       break;
     case K2::kVec2: run_vec(rgcsr_spmv_vec<T, kScaled, 2, 6>); break;
     case K2::kGrpV4: run_grpv(rgcsr_spmv_grpv<T, kScaled, 4, 4>); break;
-    default: run_fl(rgcsr_spmv_pipe<T, kScaled, U, 4>, rgcsr_spmv_pipe_fl<T, kScaled, U, 4>); break;
+    default:
+      run_fl(rgcsr_spmv_pipe<T, kScaled, U, 4>, rgcsr_spmv_pipe_fl<T, kScaled, U, 4>, true);
+      break;
   }
 }
 

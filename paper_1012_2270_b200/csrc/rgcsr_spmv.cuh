@@ -157,6 +157,10 @@ __device__ __forceinline__ void pipe_rows_dyn(
     q = __shfl_sync(0xffffffffu, q, 0);
     return static_cast<uint64_t>(q) * (32 * kSub);
   };
+  // every slice comes from the counter in grab order: warps that first took
+  // long-row items start on later slices, so the earliest slices -- the
+  // heaviest rows below the cut in a descending-sorted matrix -- are not held
+  // back behind the item phase (a static first slice per warp cost 2-10 %)
   uint64_t cur = grab();
   uint64_t nxt = cur < rows ? grab() : cur;
   uint32_t sub = 0;
@@ -1080,7 +1084,7 @@ __device__ __forceinline__ void long_items_dynamic(
     const Epi& epi) {
   const int lane = threadIdx.x & 31;
   const uint32_t items = ll.n_single + ll.n_quad;
-  if ((threadIdx.x >> 5) >= ll.warps) return;
+  if (items == 0 || (threadIdx.x >> 5) >= ll.warps) return;
   const Ldr<kHint> ld;
   for (;;) {
     uint32_t i = 0;
@@ -1092,12 +1096,14 @@ __device__ __forceinline__ void long_items_dynamic(
   }
 }
 
+// Counted per CTA (one atomic per CTA, not per warp: same-address atomics
+// serialise in L2): every warp of the CTA has made its last fetch before the
+// barrier, and the last CTA resets the counters for the next launch.
 __device__ __forceinline__ void long_items_done(const LongList& ll) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) {
-    __threadfence();  // this warp's last fetch is ordered before its done count
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    if (atomicAdd(ll.ctr + 1, 1u) == warps - 1) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // the CTA's last fetches are ordered before its done count
+    if (atomicAdd(ll.ctr + 1, 1u) == gridDim.x - 1) {
       atomicExch(ll.ctr, 0u);
       atomicExch(ll.ctr + 2, 0u);
       atomicExch(ll.ctr + 1, 0u);
