@@ -320,6 +320,12 @@ struct spmvk_csr {
   int val_prec = SPMVK_F64;
   spmvk::DevBuf<uint32_t> row_ptr, col;
   spmvk::DevBuf<unsigned char> val;  // nnz * val_prec bytes
+  // Lazily built launch metadata of the warp-staged CSR kernel: the rows with
+  // more than 128 entries, longest first (kernel metadata, not the reference's).
+  mutable std::mutex meta_mu;
+  mutable spmvk::DevBuf<uint32_t> heavy;
+  mutable uint64_t n_heavy = 0;
+  mutable bool heavy_ready = false;
 };
 
 struct spmvk_rgcsr {

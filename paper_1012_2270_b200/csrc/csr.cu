@@ -326,16 +326,24 @@ void csr_spmv(const spmvk_csr* a, const T* x, uint64_t nx, T* y, uint64_t ny, cu
   if (a->val_prec != static_cast<int>(sizeof(T)))
     fail(SPMVK_EINVAL, "spmv_csr: handle precision differs from the entry point");
   if (a->rows == 0) return;
-  // SPMVK_CSR_KERNEL: "staged" (default: CTA tile, 1,024-entry chunks, U = 4,
-  // 8 CTAs / SM), "warp" (per-warp chunks), "row" (first kernel, thread per
-  // row).  Measured (scripts/ab_formats.py, profiles/r01_csr.md): staged
+  // SPMVK_CSR_KERNEL: "" (default: "dyn" for matrices with rows past 128
+  // entries, else "staged"), "staged" (CTA tile, 1,024-entry chunks, U = 4,
+  // 8 CTAs / SM), "dyn" (hybrid_spmv_dyn's warp-staged walk), "warp"
+  // (per-warp chunks), "row" (first kernel, thread per row).  Measured (scripts/ab_formats.py, profiles/r01_csr.md): staged
   // 27-pt fp64 163 vs row 413 us, 7-pt 256^3 341 vs 852, power-law 803 vs
   // 2,090; 5-pt 2048^2 74 vs 74.
   static const int variant = [] {
     const char* e = std::getenv("SPMVK_CSR_KERNEL");
     const std::string v = e ? e : "";
-    return v == "row" ? 1 : v == "warp" ? 2 : 0;
+    return v == "row" ? 1 : v == "warp" ? 2 : v == "dyn" ? 4 : v == "staged" ? 3 : 0;
   }();
+  // default: matrices with rows past 128 entries take the warp-staged dyn
+  // kernel (power-law 8M fp64 802 -> 705 us, fp32 671 -> 580; on stencils it
+  // loses, 27-pt fp64 166 -> 213), the others the CTA-staged kernel
+  // (profiles/r01_csr.md)
+  if (variant == 4 || variant == 0) {
+    if (csr_spmv_dyn<T>(a, x, y, s, variant == 0)) return;
+  }
   if (variant == 1) {
     csr_spmv_kernel<T><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
         a->rows, a->row_ptr.p, a->col.p, reinterpret_cast<const T*>(a->val.p), x, y);

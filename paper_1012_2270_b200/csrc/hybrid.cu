@@ -1003,6 +1003,56 @@ spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
   return h.release();
 }
 
+}  // namespace
+
+// spmv_csr = the dyn kernel with K1 = 0: every entry is in the "COO" part,
+// row_ptr is the run pointer array; rows with more than kHeavyDyn entries are
+// the (longest-first) warp items.
+template <class T>
+bool csr_spmv_dyn(const spmvk_csr* a, const T* x, T* y, cudaStream_t s, bool only_if_heavy) {
+  {
+    std::lock_guard<std::mutex> lk(a->meta_mu);
+    if (!a->heavy_ready) {
+      const uint64_t cap = a->nnz / (kHeavyDyn + 1) + 1;
+      TmpBuf<uint32_t> list(cap, s), key(cap, s), key2(cap, s);
+      TmpBuf<unsigned> cnt(1, s);
+      SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned), s));
+      heavy_collect<<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
+          a->rows, a->row_ptr.p, kHeavyDyn, list.p, key.p, cnt.p);
+      SPMVK_LAUNCH("heavy_collect");
+      unsigned n = 0;
+      SPMVK_CUDA(cudaMemcpyAsync(&n, cnt.p, sizeof(n), cudaMemcpyDeviceToHost, s));
+      SPMVK_CUDA(cudaStreamSynchronize(s));
+      a->n_heavy = n;
+      a->heavy.alloc(n);
+      if (n) {
+        size_t tb = 0;
+        SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, list.p,
+                                                   a->heavy.p, static_cast<int>(n), 0, 32, s));
+        TmpBuf<unsigned char> tmp(tb, s);
+        SPMVK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, list.p, a->heavy.p,
+                                                   static_cast<int>(n), 0, 32, s));
+      }
+      a->heavy_ready = true;
+    }
+  }
+  if (only_if_heavy && a->n_heavy == 0) return false;
+  auto kern = sizeof(T) == 4 ? hybrid_spmv_dyn<T, 4, 6, 4, true> : hybrid_spmv_dyn<T, 4, 5, 4, false>;
+  int per_sm = 0;
+  SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  const LongList hl{static_cast<uint32_t>(a->n_heavy), 0u, a->heavy.p, nullptr,
+                    stream_counters(s), 2u};
+  kern<<<persistent_grid((a->rows + 255) / 256, per_sm > 0 ? per_sm : 1), 256, 0, s>>>(
+      static_cast<uint32_t>(a->rows), 0u, nullptr, nullptr, a->row_ptr.p, a->col.p,
+      reinterpret_cast<const T*>(a->val.p), x, y, kHeavyDyn, hl);
+  SPMVK_LAUNCH("hybrid_spmv_dyn (csr)");
+  return true;
+}
+template bool csr_spmv_dyn<double>(const spmvk_csr*, const double*, double*, cudaStream_t, bool);
+template bool csr_spmv_dyn<float>(const spmvk_csr*, const float*, float*, cudaStream_t, bool);
+
+namespace {
+
 template <class T>
 void check_args(const spmvk_hybrid* h, uint64_t nx, uint64_t ny) {
   if (!h) fail(SPMVK_EINVAL, "null Hybrid handle");

@@ -15,4 +15,11 @@ spmvk_csr* new_csr(uint64_t rows, uint64_t cols, uint64_t nnz, int val_prec);
 void row_length_range(const spmvk_csr* a, uint64_t r0, uint64_t r1, unsigned* mx, unsigned* mn,
                       cudaStream_t s);
 
+// spmv_csr through the warp-staged kernel of hybrid_spmv_dyn (every entry a
+// "COO" entry, row_ptr as the run pointers; hybrid.cu).  With only_if_heavy
+// it launches only when the matrix has rows past 128 entries (returns
+// whether it launched); the heavy-row list is built once per handle.
+template <class T>
+bool csr_spmv_dyn(const spmvk_csr* a, const T* x, T* y, cudaStream_t s, bool only_if_heavy);
+
 }  // namespace spmvk

@@ -17,7 +17,7 @@ from long_fused_ab import timed  # noqa: E402
 
 torch.cuda.set_device(0)
 assert lib().spmvk_init(0) == 0
-tag = os.environ.get("SPMVK_CSR_KERNEL", "bulk")
+tag = os.environ.get("SPMVK_CSR_KERNEL", "")
 for name in ("27:128", "7:256", "5:2048", "0:8000000"):
     kind, n = (int(v) for v in name.split(":"))
     c64 = sk.CsrMatrix.stencil(kind, n) if kind else sk.build_csr(gen.powerlaw(n, 7))
@@ -29,7 +29,7 @@ for name in ("27:128", "7:256", "5:2048", "0:8000000"):
         y = torch.empty(c.num_rows, dtype=dt, device="cuda")
         us = timed(lambda: sk.spmv_csr(c, x, y), reps=30)
         iv = torch.int64 if prec == 8 else torch.int32
-        print(json.dumps({"case": name, "prec": prec, "kernel": tag, "us": round(us, 2),
+        print(json.dumps({"case": name, "prec": prec, "kernel": tag or "default", "us": round(us, 2),
                           "gflops": round(2 * c.nnz() / us / 1e3, 1),
                           "bits": int(y.view(iv).sum().item())}), flush=True)
         if prec == 4:

@@ -240,7 +240,7 @@ def test_parts_compose_to_spmv_hybrid(cuda, hk, golden, prec):
             assert bitwise(yd.cpu().numpy(), want), (seed, k1)
 
 
-@pytest.mark.parametrize("kernel", ["staged", "warp", "row"])
+@pytest.mark.parametrize("kernel", ["", "dyn", "staged", "warp", "row"])
 def test_csr_kernels_bitwise_with_long_rows(kernel):
     """spmv_csr's three kernels (SPMVK_CSR_KERNEL, read once per process, so
     each runs in a child): stencils, a banded matrix and power-law rows up to
