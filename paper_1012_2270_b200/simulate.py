@@ -43,7 +43,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-KERNELS = {"rgcsr": "rgcsr_spmv", "ellpack": "hybrid_spmv|hybrid_ell", "csr": "csr_spmv"}
+KERNELS = {"rgcsr": "rgcsr_spmv", "ellpack": "hybrid_spmv|hybrid_ell", "csr": "csr_spmv|hybrid_spmv_dyn"}
 
 
 def child(a):
