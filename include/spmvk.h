@@ -149,7 +149,13 @@ int spmvk_permute_vector_f64(const uint32_t* map_dev, uint64_t n, const double* 
                              int inverse, void* stream);
 int spmvk_permute_vector_f32(const uint32_t* map_dev, uint64_t n, const float* in, float* out,
                              int inverse, void* stream);
-/* spmv_csr (spmvkit/csr.hpp:41-53): thread-per-row, same accumulation order. */
+/* spmv_csr (spmvkit/csr.hpp:41-53): each row accumulated in entry order from
+ * +0, products and sums rounded separately (bitwise the reference).  Matrices
+ * without rows past 128 entries take a CTA-staged kernel; with them, the
+ * warp-staged walk of the Hybrid kernel (dynamic row slices, long rows as
+ * work items) -- its long-row list is built once per handle on the first
+ * call, which synchronises the stream (make that first call outside a stream
+ * capture).  SPMVK_CSR_KERNEL = staged | dyn | warp | row forces a kernel. */
 int spmvk_csr_spmv_f64(const spmvk_csr* a, const double* x, uint64_t nx, double* y, uint64_t ny,
                        void* stream);
 int spmvk_csr_spmv_f32(const spmvk_csr* a, const float* x, uint64_t nx, float* y, uint64_t ny,
