@@ -372,3 +372,34 @@ def test_dyn_repeated_launches_two_streams(cuda, prec, order):
             assert bitwise(y.cpu().numpy(), want)
     finally:
         lib().spmvk_set_hybrid_kernel(b"auto")
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_dyn_walk_threshold_edges(cuda, prec):
+    """Rows of exactly 127-130 entries sit on the work-item cut of the dyn walk
+    (COO runs > 128 become warp items; CSR rows > 128 likewise), next to empty
+    rows, runs that straddle 128-entry chunks and 32-row sub-slice borders:
+    spmv_hybrid (K1 = 0 and chosen K1) and spmv_csr bitwise the oracle's."""
+    rng = np.random.default_rng(11)
+    n = 4099
+    lens = rng.integers(0, 9, n)
+    for i, l in zip(range(0, n, 37), [0, 1, 127, 128, 129, 130, 255, 256, 257, 31, 32, 33] * 20):
+        lens[i] = l
+    rp = np.zeros(n + 1, np.uint32)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(
+        np.uint32)
+    val = rng.uniform(-1, 1, int(rp[-1]))
+    om = orc.Csr(n, n, rp, col, val)
+    dt = np.float64 if prec == 8 else np.float32
+    x = orc.random_vector(n, 3).astype(dt)
+    m = triplets(om)
+    for k1 in (0, None):
+        h = sk.build_hybrid(m, k1, prec)
+        assert bitwise(sk.spmv_hybrid(h, dev(x)).cpu().numpy(),
+                       orc.spmv_hybrid(orc.build_hybrid(om, k1, prec), x)), k1
+    c = sk.build_csr(m, prec)
+    assert bitwise(sk.spmv_csr(c, dev(x)).cpu().numpy(), orc.spmv_csr(om, x, prec))
+    a = sk.build_rgcsr(m, 32, prec)
+    assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(),
+                   orc.spmv_rgcsr(orc.build_rgcsr(om, 32, prec), x)[0])
