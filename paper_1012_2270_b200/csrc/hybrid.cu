@@ -131,17 +131,44 @@ __global__ void hybrid_coo_fill(uint64_t rows, uint32_t k1, const uint32_t* __re
                                 const uint32_t* __restrict__ col, const V* __restrict__ val,
                                 const uint64_t* __restrict__ off, uint32_t* __restrict__ cr,
                                 uint32_t* __restrict__ cc, T* __restrict__ cv) {
+  // A warp per 32-row block: the block's COO entries are one contiguous output
+  // range [off[r0], off[r0 + 32]); the warp writes it 32 entries at a time
+  // (coalesced), each lane finding its entry's row among the block's 32 by a
+  // shuffle binary search over the rows' output offsets -- instead of a warp
+  // per row, which left most lanes idle on short COO tails.
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
-       r += warps) {
-    const uint32_t b = rp[r], len = rp[r + 1] - b;
-    if (len <= k1) continue;
-    const uint64_t o = off[r];
-    for (uint32_t i = lane; i < len - k1; i += 32) {
-      cr[o + i] = (uint32_t)r;
-      cc[o + i] = col[b + k1 + i];
-      cv[o + i] = static_cast<T>(val[b + k1 + i]);
+  const uint64_t blocks = (rows + 31) / 32;
+  for (uint64_t blk = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); blk < blocks;
+       blk += warps) {
+    const uint64_t r = blk * 32 + lane;
+    const bool live = r < rows;
+    const uint64_t o = live ? off[r] : 0;  // this row's first output entry
+    const uint32_t b = live ? rp[r] : 0;
+    const uint64_t last = min(rows, blk * 32 + 32) - 1;
+    const uint64_t o0 = __shfl_sync(0xffffffffu, o, 0);
+    const uint64_t o1 = (last + 1 == rows) ? off[last] + (rp[last + 1] - rp[last] > k1 ?
+                                                          rp[last + 1] - rp[last] - k1 : 0)
+                                           : off[last + 1];
+    for (uint64_t e0 = o0; e0 < o1; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      // the row of entry e: the largest lane q with off[q] <= e (rows with no
+      // COO entries share their successor's offset and are never chosen past it)
+      int q = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint64_t oq = __shfl_sync(0xffffffffu, o, q + step);
+        const bool ok = (uint64_t)(blk * 32 + q + step) < rows && oq <= e;
+        if (ok) q += step;
+      }
+      const uint64_t oq = __shfl_sync(0xffffffffu, o, q);
+      const uint32_t bq = __shfl_sync(0xffffffffu, b, q);
+      if (e < o1) {
+        const uint64_t src = (uint64_t)bq + k1 + (e - oq);
+        cr[e] = (uint32_t)(blk * 32 + q);
+        cc[e] = col[src];
+        cv[e] = static_cast<T>(val[src]);
+      }
     }
   }
 }
@@ -911,7 +938,7 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
   h->coo_columns.alloc(coo);
   h->coo_values.alloc(coo * sizeof(T));
   if (coo) {
-    hybrid_coo_fill<T, V><<<persistent_grid((a->rows + 7) / 8, 8), 256, 0, s>>>(
+    hybrid_coo_fill<T, V><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
         a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
         reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
         reinterpret_cast<T*>(h->coo_values.p));
