@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "rgcsr_spmv.cuh"  // long_row_walk, LongList, long_items_done
+#include "tma.cuh"
 
 namespace spmvk {
 namespace {
@@ -122,6 +123,90 @@ __global__ void hybrid_ell_fill(uint64_t rows, uint32_t k1, const uint32_t* __re
       }
     }
     overflow[r] = len > k1 ? len - k1 : 0;
+  }
+}
+
+// ELL fill with TMA bulk copies (the K1 scatter's design, rgcsr.cu): a warp
+// per 32-row block; the block's CSR entries (values + columns, rounded out to
+// 16 B) arrive in one of the warp's two shared-memory stages by two
+// cp.async.bulk copies on an mbarrier, the NEXT block in flight while this
+// one's K1 slots are written (slot j of the 32 rows is 32 contiguous entries
+// at j N + r0: coalesced), pads (0, column 0) in the same pass.  Blocks whose
+// entries do not fit a stage (or a partial last block) read CSR directly.
+constexpr uint32_t kEllStage = 1024;
+
+template <class T, class V>
+__global__ void __launch_bounds__(128) hybrid_ell_fill_bulk(
+    uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+    const V* __restrict__ val, T* __restrict__ ev, uint32_t* __restrict__ ec,
+    uint64_t* __restrict__ overflow) {
+  constexpr uint32_t SV = (kEllStage + 4) * sizeof(V), SC = (kEllStage + 4) * 4;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wbase = sm + (size_t)warp * 2 * (SV + SC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)4 * 2 * (SV + SC)) + warp * 2;
+  const uint64_t blocks = (rows + 31) / 32;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t first = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto fits = [&](uint64_t blk) {
+    if (blk >= blocks || blk * 32 + 32 > rows) return false;
+    return rp[blk * 32 + 32] - rp[blk * 32] <= kEllStage;
+  };
+  auto issue = [&](uint64_t blk, int b) {
+    const uint32_t e0 = rp[blk * 32], e1 = rp[blk * 32 + 32];
+    const uint64_t v0 = (uint64_t)e0 * sizeof(V) & ~15ull;
+    const uint64_t v1 = ((uint64_t)e1 * sizeof(V) + 15) & ~15ull;
+    const uint64_t c0 = (uint64_t)e0 * 4 & ~15ull, c1 = ((uint64_t)e1 * 4 + 15) & ~15ull;
+    unsigned char* sb = wbase + b * (SV + SC);
+    mbar_arrive_expect_tx(&bar[b], (uint32_t)(v1 - v0 + c1 - c0));
+    bulk_g2s(sb, reinterpret_cast<const unsigned char*>(val) + v0, (uint32_t)(v1 - v0), &bar[b]);
+    bulk_g2s(sb + SV, reinterpret_cast<const unsigned char*>(col) + c0, (uint32_t)(c1 - c0),
+             &bar[b]);
+  };
+  uint32_t phase[2] = {0, 0};
+  bool staged = fits(first);
+  if (staged && lane == 0) issue(first, 0);
+  int b = 0;
+  for (uint64_t blk = first; blk < blocks; blk += warps, b ^= 1) {
+    const uint64_t bn = blk + warps;
+    const bool staged_n = fits(bn);
+    if (staged_n && lane == 0) {
+      fence_proxy_async_smem();
+      issue(bn, b ^ 1);
+    }
+    const uint64_t r = blk * 32 + lane;
+    const bool live = r < rows;
+    const uint32_t start = live ? rp[r] : 0u, len = live ? rp[r + 1] - start : 0u;
+    if (live) overflow[r] = len > k1 ? len - k1 : 0;
+    if (staged) {
+      mbar_wait(&bar[b], phase[b]);
+      phase[b] ^= 1;
+      const uint32_t e0 = rp[blk * 32];
+      const V* sv = reinterpret_cast<const V*>(wbase + b * (SV + SC)) +
+                    ((uint64_t)e0 * sizeof(V) & 15) / sizeof(V);
+      const uint32_t* sc = reinterpret_cast<const uint32_t*>(wbase + b * (SV + SC) + SV) +
+                           ((uint64_t)e0 * 4 & 15) / 4;
+      const uint32_t off = start - e0;
+      for (uint32_t j = 0; j < k1; ++j) {
+        const uint64_t idx = (uint64_t)j * rows + r;
+        ev[idx] = j < len ? static_cast<T>(sv[off + j]) : T(0);
+        ec[idx] = j < len ? sc[off + j] : 0u;
+      }
+    } else if (live) {
+      for (uint32_t j = 0; j < k1; ++j) {
+        const uint64_t idx = (uint64_t)j * rows + r;
+        ev[idx] = j < len ? static_cast<T>(val[start + j]) : T(0);
+        ec[idx] = j < len ? col[start + j] : 0u;
+      }
+    }
+    __syncwarp();
+    staged = staged_n;
   }
 }
 
@@ -924,14 +1009,36 @@ void collect_dyn_heavy(spmvk_hybrid* h, cudaStream_t s) {
 }
 
 template <class T, class V>
-void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s) {
+void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len) {
   const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
   DevBuf<uint64_t> off(a->rows);
-  hybrid_ell_fill<T, V><<<grid, 256, 0, s>>>(
-      a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
-      reinterpret_cast<const V*>(a->val.p), reinterpret_cast<T*>(h->ell_values.p),
-      h->ell_columns.p, off.p);
-  SPMVK_LAUNCH("hybrid_ell_fill");
+  // bulk-copy fill for matrices whose 32-row blocks fit a stage (rows of at
+  // most 32 entries: 27-pt 405 -> 240 us); long-row matrices keep the
+  // thread-per-row fill (power-law 8M 361 vs 422 us).  SPMVK_ELL_BULK=0 / 1
+  // forces it off / on.
+  static const int bulk_env = [] {
+    const char* e = std::getenv("SPMVK_ELL_BULK");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (bulk_env > 0 || (bulk_env < 0 && max_len <= 32)) {
+    auto kern = hybrid_ell_fill_bulk<T, V>;
+    const size_t smem = 4 * 2 * ((kEllStage + 4) * (sizeof(V) + 4)) + 4 * 2 * 8;
+    SPMVK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    int per_sm = 0;
+    SPMVK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    kern<<<persistent_grid((a->rows + 127) / 128, per_sm > 0 ? per_sm : 1), 128, smem, s>>>(
+        a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+        reinterpret_cast<const V*>(a->val.p), reinterpret_cast<T*>(h->ell_values.p),
+        h->ell_columns.p, off.p);
+    SPMVK_LAUNCH("hybrid_ell_fill_bulk");
+  } else {
+    hybrid_ell_fill<T, V><<<grid, 256, 0, s>>>(
+        a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+        reinterpret_cast<const V*>(a->val.p), reinterpret_cast<T*>(h->ell_values.p),
+        h->ell_columns.p, off.p);
+    SPMVK_LAUNCH("hybrid_ell_fill");
+  }
   const uint64_t coo = exclusive_scan_u64(off.p, a->rows, s);
   h->coo = coo;
   h->coo_rows.alloc(coo);
@@ -1011,9 +1118,9 @@ spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
   h->nnz = a->nnz;
   h->ell_values.alloc(a->rows * width * prec);
   h->ell_columns.alloc(a->rows * width);
-  if (prec == SPMVK_F64) fill<double, double>(h.get(), a, s);
-  else if (a->val_prec == SPMVK_F64) fill<float, double>(h.get(), a, s);
-  else fill<float, float>(h.get(), a, s);
+  if (prec == SPMVK_F64) fill<double, double>(h.get(), a, s, mx);
+  else if (a->val_prec == SPMVK_F64) fill<float, double>(h.get(), a, s, mx);
+  else fill<float, float>(h.get(), a, s, mx);
   if (h->coo) {  // bounds of the COO part, for spmv_coo's check
     DevBuf<unsigned> mc(1);
     SPMVK_CUDA(cudaMemsetAsync(mc.p, 0, 4, s));
