@@ -13,6 +13,8 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -211,11 +213,46 @@ __global__ void __launch_bounds__(128) hybrid_ell_fill_bulk(
 }
 
 // COO: one warp per row with overflow copies the row's tail (coalesced).
+// Blocks of 32 rows with more COO entries than this are left to
+// hybrid_coo_fill_rows (a warp per row, spread over the grid): one warp
+// walking 32 long tails in sequence would be the critical path (a
+// descending-sorted power-law puts its ~4,000-entry tails together).
+constexpr uint64_t kCooBlockMax = 32 * 64;
+
+// The rows of the heavy blocks hybrid_coo_fill listed (see kCooBlockMax): a
+// warp per row, spread over the grid.
+template <class T, class V>
+__global__ void hybrid_coo_fill_rows(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
+                                     const uint32_t* __restrict__ col, const V* __restrict__ val,
+                                     const uint64_t* __restrict__ off, uint32_t* __restrict__ cr,
+                                     uint32_t* __restrict__ cc, T* __restrict__ cv,
+                                     const uint32_t* __restrict__ heavy_blocks,
+                                     const unsigned* __restrict__ n_heavy_blocks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t n = (uint64_t)*n_heavy_blocks * 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n;
+       w += warps) {
+    const uint64_t r = (uint64_t)heavy_blocks[w / 32] * 32 + (w % 32);
+    if (r >= rows) continue;
+    const uint32_t b = rp[r], len = rp[r + 1] - b;
+    if (len <= k1) continue;
+    const uint64_t o = off[r];
+    for (uint32_t i = lane; i < len - k1; i += 32) {
+      cr[o + i] = (uint32_t)r;
+      cc[o + i] = col[b + k1 + i];
+      cv[o + i] = static_cast<T>(val[b + k1 + i]);
+    }
+  }
+}
+
 template <class T, class V>
 __global__ void hybrid_coo_fill(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
                                 const uint32_t* __restrict__ col, const V* __restrict__ val,
                                 const uint64_t* __restrict__ off, uint32_t* __restrict__ cr,
-                                uint32_t* __restrict__ cc, T* __restrict__ cv) {
+                                uint32_t* __restrict__ cc, T* __restrict__ cv,
+                                uint32_t* __restrict__ heavy_blocks,
+                                unsigned* __restrict__ n_heavy_blocks) {
   // A warp per 32-row block: the block's COO entries are one contiguous output
   // range [off[r0], off[r0 + 32]); the warp writes it 32 entries at a time
   // (coalesced), each lane finding its entry's row among the block's 32 by a
@@ -235,6 +272,10 @@ __global__ void hybrid_coo_fill(uint64_t rows, uint32_t k1, const uint32_t* __re
     const uint64_t o1 = (last + 1 == rows) ? off[last] + (rp[last + 1] - rp[last] > k1 ?
                                                           rp[last + 1] - rp[last] - k1 : 0)
                                            : off[last + 1];
+    if (o1 - o0 > kCooBlockMax) {  // heavy block: listed for hybrid_coo_fill_rows
+      if (lane == 0) heavy_blocks[atomicAdd(n_heavy_blocks, 1u)] = (uint32_t)blk;
+      continue;
+    }
     for (uint64_t e0 = o0; e0 < o1; e0 += 32) {
       const uint64_t e = e0 + lane;
       // the row of entry e: the largest lane q with off[q] <= e (rows with no
@@ -984,6 +1025,20 @@ __global__ void heavy_collect(uint64_t rows, const uint32_t* __restrict__ crp, u
   }
 }
 
+// flag[r] = row r's COO run exceeds kHeavyRun inside a tile that walks
+// (> kWalkCoo COO entries): the staged kernel's heavy-row list, compacted in
+// ascending order by cub::DeviceSelect::Flagged.
+__global__ void walked_heavy_flags(uint64_t rows, const uint32_t* __restrict__ tile_ptr,
+                                   const uint32_t* __restrict__ crp,
+                                   unsigned char* __restrict__ flag) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = r / kRowsPerTile;
+    const bool walked = tile_ptr[t + 1] - tile_ptr[t] > kWalkCoo;
+    flag[r] = walked && crp[r + 1] - crp[r] > kHeavyRun;
+  }
+}
+
 // h->dyn_heavy: the rows of hybrid_spmv_dyn's work list, longest run first.
 void collect_dyn_heavy(spmvk_hybrid* h, cudaStream_t s) {
   h->dyn_heavy_run = heavy_dyn_run();
@@ -1045,11 +1100,22 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len)
   h->coo_columns.alloc(coo);
   h->coo_values.alloc(coo * sizeof(T));
   if (coo) {
-    hybrid_coo_fill<T, V><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
-        a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
-        reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
-        reinterpret_cast<T*>(h->coo_values.p));
-    SPMVK_LAUNCH("hybrid_coo_fill");
+    {
+      const uint64_t nblk = (a->rows + 31) / 32;
+      TmpBuf<uint32_t> hb(nblk, s);
+      TmpBuf<unsigned> nhb(1, s);
+      SPMVK_CUDA(cudaMemsetAsync(nhb.p, 0, sizeof(unsigned), s));
+      hybrid_coo_fill<T, V><<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
+          a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+          reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
+          reinterpret_cast<T*>(h->coo_values.p), hb.p, nhb.p);
+      SPMVK_LAUNCH("hybrid_coo_fill");
+      hybrid_coo_fill_rows<T, V><<<sm_count() * 8, 256, 0, s>>>(
+          a->rows, static_cast<uint32_t>(h->k1), a->row_ptr.p, a->col.p,
+          reinterpret_cast<const V*>(a->val.p), off.p, h->coo_rows.p, h->coo_columns.p,
+          reinterpret_cast<T*>(h->coo_values.p), hb.p, nhb.p);
+      SPMVK_LAUNCH("hybrid_coo_fill_rows");
+    }
     h->coo_row_ptr.alloc(a->rows + 1);
     narrow_offsets<<<persistent_grid((a->rows + 256) / 256, 8), 256, 0, s>>>(
         a->rows, off.p, coo, h->coo_row_ptr.p);
@@ -1059,26 +1125,36 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len)
     coo_tile_bounds<<<persistent_grid((ntiles + 256) / 256, 4), 256, 0, s>>>(
         ntiles, a->rows, coo, h->coo_rows.p, h->tile_ptr.p);
     SPMVK_LAUNCH("coo_tile_bounds");
-    // heavy rows: runs > kHeavyRun inside tiles that walk (> kWalkCoo entries)
-    std::vector<uint32_t> tp(ntiles + 1);
-    SPMVK_CUDA(cudaMemcpyAsync(tp.data(), h->tile_ptr.p, 4 * (ntiles + 1),
-                               cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaStreamSynchronize(s));
-    std::vector<uint32_t> heavy;
-    for (uint64_t t = 0; t < ntiles; ++t) {
-      if (tp[t + 1] - tp[t] <= kWalkCoo) continue;
-      const uint64_t r0 = t * kRowsPerTile, r1 = std::min<uint64_t>(a->rows, r0 + kRowsPerTile);
-      std::vector<uint32_t> crp(r1 - r0 + 1);
-      SPMVK_CUDA(cudaMemcpy(crp.data(), h->coo_row_ptr.p + r0, 4 * (r1 - r0 + 1),
-                            cudaMemcpyDeviceToHost));
-      for (uint64_t r = r0; r < r1; ++r)
-        if (crp[r - r0 + 1] - crp[r - r0] > kHeavyRun) heavy.push_back(static_cast<uint32_t>(r));
+    // heavy rows: runs > kHeavyRun inside tiles that walk (> kWalkCoo entries),
+    // ascending: flagged on the device and compacted in order (cub select)
+    {
+      TmpBuf<unsigned char> flag(a->rows, s);
+      walked_heavy_flags<<<persistent_grid((a->rows + 255) / 256, 8), 256, 0, s>>>(
+          a->rows, h->tile_ptr.p, h->coo_row_ptr.p, flag.p);
+      SPMVK_LAUNCH("walked_heavy_flags");
+      TmpBuf<uint32_t> sel(a->rows, s);
+      TmpBuf<int> nsel(1, s);
+      cub::CountingInputIterator<uint32_t> ids(0);
+      size_t tb = 0;
+      SPMVK_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, flag.p, sel.p, nsel.p,
+                                            static_cast<int>(a->rows), s));
+      TmpBuf<unsigned char> tmp(tb, s);
+      SPMVK_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, ids, flag.p, sel.p, nsel.p,
+                                            static_cast<int>(a->rows), s));
+      int n = 0;
+      SPMVK_CUDA(cudaMemcpyAsync(&n, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPMVK_CUDA(cudaStreamSynchronize(s));
+      std::vector<uint32_t> heavy(static_cast<size_t>(n));
+      if (n)
+        SPMVK_CUDA(cudaMemcpyAsync(heavy.data(), sel.p, 4ull * n, cudaMemcpyDeviceToHost, s));
+      h->n_heavy = static_cast<uint64_t>(n);
+      h->heavy_rows.alloc(h->n_heavy);
+      if (n)
+        SPMVK_CUDA(cudaMemcpyAsync(h->heavy_rows.p, sel.p, 4ull * n, cudaMemcpyDeviceToDevice,
+                                   s));
+      SPMVK_CUDA(cudaStreamSynchronize(s));
+      h->heavy_rows_host = std::move(heavy);
     }
-    h->n_heavy = heavy.size();
-    h->heavy_rows_host = heavy;
-    h->heavy_rows.alloc(h->n_heavy);
-    if (h->n_heavy)
-      SPMVK_CUDA(cudaMemcpy(h->heavy_rows.p, heavy.data(), 4 * h->n_heavy, cudaMemcpyHostToDevice));
     collect_dyn_heavy(h, s);
   }
   DevBuf<unsigned long long> cnt(1);

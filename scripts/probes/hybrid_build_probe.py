@@ -14,8 +14,9 @@ from paper_1012_2270_b200._lib import lib  # noqa: E402
 
 torch.cuda.set_device(0)
 assert lib().spmvk_init(0) == 0
-for name, csr, prec in (("27pt", sk.CsrMatrix.stencil(27, 128), 8),
-                        ("powerlaw", sk.build_csr(gen.powerlaw(8_000_000, 7)), 4)):
+pl = sk.build_csr(gen.powerlaw(8_000_000, 7))
+for name, csr, prec in (("27pt", sk.CsrMatrix.stencil(27, 128), 8), ("powerlaw", pl, 4),
+                        ("powerlaw-desc", sk.apply_descending_permutation(pl)[0], 8)):
     ts = []
     for _ in range(4):
         torch.cuda.synchronize()
