@@ -593,12 +593,19 @@ def run_ours(args):
         L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols, ypin.data_ptr(),
                                     a.num_rows, None)
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(e2e_steps):
-        rc = L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols, ypin.data_ptr(),
-                                         a.num_rows, None)
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t) / e2e_steps
+    # five rounds of back-to-back calls, the median round reported: a PCIe /
+    # host-memory hiccup from another tenant of the host moves one round,
+    # not the number (every round is in the line)
+    e2e_rounds = []
+    per_round = max(3, e2e_steps // 5)
+    for _ in range(5):
+        t = time.perf_counter()
+        for _ in range(per_round):
+            rc = L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols,
+                                             ypin.data_ptr(), a.num_rows, None)
+        torch.cuda.synchronize()
+        e2e_rounds.append((time.perf_counter() - t) / per_round)
+    e2e_s = statistics.median(e2e_rounds)
     assert rc == 0, sk._lib.last_error()
     assert float(np.cumsum(ypin.numpy())[-1]) == ysum
 
@@ -674,6 +681,8 @@ def run_ours(args):
         "e2e": {"value": 2.0 * nnz / e2e_s / 1e9, "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * a.num_cols, "d2h_bytes_per_step": 8 * a.num_rows,
                 "ms_per_step": e2e_s * 1e3,
+                "rounds_ms_per_step": [round(v * 1e3, 4) for v in e2e_rounds],
+                "timing": f"median of 5 rounds x {per_round} back-to-back calls",
                 "pcie_gbs": 8 * (a.num_cols + a.num_rows) / e2e_s / 1e9,
                 "pcie_peak_gbs": PCIE_BIDIR_GBS,
                 "frac_pcie": 8 * (a.num_cols + a.num_rows) / e2e_s / 1e9 / PCIE_BIDIR_GBS,
