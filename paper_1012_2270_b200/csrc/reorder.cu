@@ -45,23 +45,80 @@ __global__ void permuted_lengths(uint64_t rows, const uint32_t* __restrict__ map
 
 // inv != nullptr: symmetric mode, columns relabelled new = inv[old] (the
 // row's entries are then re-sorted by a segmented sort).
+constexpr uint64_t kPermBlockMax = 32 * 64;
 template <class V>
 __global__ void permuted_copy(uint64_t rows, uint64_t nnz, const uint32_t* __restrict__ map,
                               const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
                               const V* __restrict__ val, const uint64_t* __restrict__ off,
                               uint32_t* __restrict__ rp2, uint32_t* __restrict__ col2,
-                              V* __restrict__ val2, const uint32_t* __restrict__ inv) {
+                              V* __restrict__ val2, const uint32_t* __restrict__ inv,
+                              uint32_t* __restrict__ heavy_blocks,
+                              unsigned* __restrict__ n_heavy_blocks) {
+  // A warp per 32 output rows: their entries are one contiguous output range
+  // [off[i0], off[i0 + 32]), written 32 entries at a time (coalesced), each
+  // lane finding its entry's output row by a shuffle binary search over the
+  // rows' offsets.  Blocks of more than kPermBlockMax entries (long rows
+  // together, e.g. the first blocks of a descending order) are listed for
+  // permuted_copy_rows, a warp per row spread over the grid.
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < rows;
-       i += warps) {
-    const uint32_t o = map[i], b = rp[o], n = rp[o + 1] - b;
-    const uint64_t d = off[i];
-    if (lane == 0) {
+  const uint64_t blocks = (rows + 31) / 32;
+  for (uint64_t blk = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); blk < blocks;
+       blk += warps) {
+    const uint64_t i = blk * 32 + lane;
+    const bool live = i < rows;
+    const uint64_t d = live ? off[i] : 0;
+    const uint32_t src = live ? rp[map[i]] : 0;
+    if (live) {
       rp2[i] = (uint32_t)d;
       if (i + 1 == rows) rp2[rows] = (uint32_t)nnz;
     }
-    for (uint32_t k = lane; k < n; k += 32) {
+    const uint64_t last = min(rows, blk * 32 + 32) - 1;
+    const uint64_t d0 = __shfl_sync(0xffffffffu, d, 0);
+    const uint64_t d1 = last + 1 == rows ? nnz : off[last + 1];
+    if (d1 - d0 > kPermBlockMax) {
+      if (lane == 0) heavy_blocks[atomicAdd(n_heavy_blocks, 1u)] = (uint32_t)blk;
+      continue;
+    }
+    for (uint64_t e0 = d0; e0 < d1; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      int q = 0;  // the largest lane q with off[q] <= e (empty rows are skipped past)
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint64_t dq = __shfl_sync(0xffffffffu, d, q + step);
+        if ((uint64_t)(blk * 32 + q + step) < rows && dq <= e) q += step;
+      }
+      const uint64_t dq = __shfl_sync(0xffffffffu, d, q);
+      const uint32_t sq = __shfl_sync(0xffffffffu, src, q);
+      if (e < d1) {
+        const uint64_t k = (uint64_t)sq + (e - dq);
+        const uint32_t c = col[k];
+        col2[e] = inv ? inv[c] : c;
+        val2[e] = val[k];
+      }
+    }
+  }
+}
+
+// The rows of the listed heavy blocks: a warp per row.
+template <class V>
+__global__ void permuted_copy_rows(uint64_t rows, const uint32_t* __restrict__ map,
+                                   const uint32_t* __restrict__ rp,
+                                   const uint32_t* __restrict__ col, const V* __restrict__ val,
+                                   const uint64_t* __restrict__ off, uint32_t* __restrict__ col2,
+                                   V* __restrict__ val2, const uint32_t* __restrict__ inv,
+                                   const uint32_t* __restrict__ heavy_blocks,
+                                   const unsigned* __restrict__ n_heavy_blocks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t n = (uint64_t)*n_heavy_blocks * 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n;
+       w += warps) {
+    const uint64_t i = (uint64_t)heavy_blocks[w / 32] * 32 + (w % 32);
+    if (i >= rows) continue;
+    const uint32_t o = map[i], b = rp[o], len = rp[o + 1] - b;
+    const uint64_t d = off[i];
+    for (uint32_t k = lane; k < len; k += 32) {
       const uint32_t c = col[b + k];
       col2[d + k] = inv ? inv[c] : c;
       val2[d + k] = val[b + k];
@@ -114,7 +171,7 @@ spmvk_csr* permute_csr(const spmvk_csr* a, const uint32_t* d_map, bool symmetric
   permuted_lengths<<<grid, 256, 0, s>>>(a->rows, d_map, a->row_ptr.p, off.p);
   SPMVK_LAUNCH("permuted_lengths");
   exclusive_scan_u64(off.p, a->rows, s);
-  const unsigned wgrid = persistent_grid((a->rows + 7) / 8, 8);
+  const unsigned wgrid = persistent_grid((a->rows + 255) / 256, 8);  // a warp per 32 rows
   // symmetric: copy into scratch, then segmented-sort into b
   DevBuf<uint32_t> col_t(symmetric ? a->nnz : 0);
   DevBuf<unsigned char> val_t(symmetric ? a->nnz * static_cast<uint64_t>(a->val_prec) : 0);
@@ -122,11 +179,18 @@ spmvk_csr* permute_csr(const spmvk_csr* a, const uint32_t* d_map, bool symmetric
   unsigned char* val_dst = symmetric ? val_t.p : b->val.p;
   auto run = [&](auto tag) {
     using V = decltype(tag);
+    TmpBuf<uint32_t> hb((a->rows + 31) / 32, s);
+    TmpBuf<unsigned> nhb(1, s);
+    SPMVK_CUDA(cudaMemsetAsync(nhb.p, 0, sizeof(unsigned), s));
     permuted_copy<V><<<wgrid, 256, 0, s>>>(
         a->rows, a->nnz, d_map, a->row_ptr.p, a->col.p, reinterpret_cast<const V*>(a->val.p),
         off.p, b->row_ptr.p, col_dst, reinterpret_cast<V*>(val_dst),
-        symmetric ? inv.p : nullptr);
+        symmetric ? inv.p : nullptr, hb.p, nhb.p);
     SPMVK_LAUNCH("permuted_copy");
+    permuted_copy_rows<V><<<sm_count() * 8, 256, 0, s>>>(
+        a->rows, d_map, a->row_ptr.p, a->col.p, reinterpret_cast<const V*>(a->val.p), off.p,
+        col_dst, reinterpret_cast<V*>(val_dst), symmetric ? inv.p : nullptr, hb.p, nhb.p);
+    SPMVK_LAUNCH("permuted_copy_rows");
     if (!symmetric || a->nnz == 0) return;
     if (a->nnz > 0x7fffffffull) fail(SPMVK_ERANGE, "apply_permutation: nnz exceeds 2^31 - 1");
     size_t tmp_bytes = 0;
