@@ -45,6 +45,143 @@ __global__ void group_layout(uint64_t rows, uint64_t G, uint64_t groups, uint32_
   }
 }
 
+// Fused K1 layout (the default): two launches instead of row lengths +
+// group layout + two three-kernel scans + nnz + narrowing (twelve launches,
+// ~75 us of launch-bound host time on a 0.3 ms build).
+//   k1_layout: a CTA per tile of TG groups (<= kLayoutRows rows): row lengths
+//     (written, and staged in shared memory), then per group its slot count
+//     s*K_g and long-row count, and the tile's two sums in part[2b..2b+1].
+//     The last CTA to finish (ticket in the stream's counter word 3, reset
+//     by that CTA) scans the tile sums in place and writes the totals
+//     (slots, long rows, slab nnz) to tot[0..2].
+//   k1_layout_apply: a CTA per tile turns its groups' counts into the
+//     exclusive prefixes: group_pointers (u32) and the long-row offsets (u64).
+// Thread j of a tile owns its groups [j*q, (j+1)*q), q = ceil(TG/256), in
+// both kernels.
+constexpr uint32_t kLayoutRows = 8192;
+constexpr int kLayoutThreads = 256;
+
+__device__ __forceinline__ uint32_t lpad(uint64_t i) { return (uint32_t)(i + (i >> 5)); }
+
+// Block-wide exclusive scan of a pair; returns the block totals.
+__device__ __forceinline__ void block_scan_pair(uint64_t a, uint64_t b, uint64_t& ea,
+                                                uint64_t& eb, uint64_t& ta, uint64_t& tb) {
+  __shared__ uint64_t wt[2][kLayoutThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t xa = __shfl_up_sync(0xffffffffu, ia, o);
+    const uint64_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) ia += xa, ib += xb;
+  }
+  if (lane == 31) wt[0][warp] = ia, wt[1][warp] = ib;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t wa = lane < kLayoutThreads / 32 ? wt[0][lane] : 0;
+    uint64_t wb = lane < kLayoutThreads / 32 ? wt[1][lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t xa = __shfl_up_sync(0xffffffffu, wa, o);
+      const uint64_t xb = __shfl_up_sync(0xffffffffu, wb, o);
+      if (lane >= o) wa += xa, wb += xb;
+    }
+    if (lane < kLayoutThreads / 32) wt[0][lane] = wa, wt[1][lane] = wb;
+  }
+  __syncthreads();
+  ea = (warp ? wt[0][warp - 1] : 0) + ia - a;
+  eb = (warp ? wt[1][warp - 1] : 0) + ib - b;
+  ta = wt[0][kLayoutThreads / 32 - 1];
+  tb = wt[1][kLayoutThreads / 32 - 1];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kLayoutThreads) k1_layout(
+    uint64_t r0, uint64_t rows, uint64_t G, uint64_t groups, uint64_t TG, uint32_t cut,
+    const uint32_t* __restrict__ rp, uint32_t* __restrict__ lens, uint64_t* __restrict__ slots,
+    uint64_t* __restrict__ nlong, uint64_t* __restrict__ part, uint32_t* __restrict__ ticket,
+    uint64_t* __restrict__ tot) {
+  __shared__ uint32_t sl[kLayoutRows + kLayoutRows / 32];
+  __shared__ bool last;
+  const uint64_t g0 = blockIdx.x * TG, g1 = min(groups, g0 + TG);
+  const uint64_t rb = g0 * G, re = min(rows, g1 * G);
+  const bool staged = re - rb <= kLayoutRows;
+  for (uint64_t r = rb + threadIdx.x; r < re; r += kLayoutThreads) {
+    const uint32_t l = rp[r0 + r + 1] - rp[r0 + r];
+    lens[r] = l;
+    if (staged) sl[lpad(r - rb)] = l;
+  }
+  __syncthreads();
+  const uint64_t q = (g1 - g0 + kLayoutThreads - 1) / kLayoutThreads;
+  const uint64_t ga = min(g1, g0 + threadIdx.x * q), gb = min(g1, ga + q);
+  uint64_t ss = 0, ls = 0;
+  for (uint64_t g = ga; g < gb; ++g) {
+    const uint64_t gr = g * G, s = min(G, rows - gr);
+    uint32_t w = 0, nl = 0;
+    for (uint64_t t = 0; t < s; ++t) {
+      const uint32_t l = staged ? sl[lpad(gr - rb + t)] : lens[gr + t];
+      w = max(w, l);
+      nl += l > cut;
+    }
+    slots[g] = s * w;
+    nlong[g] = nl;
+    ss += s * w;
+    ls += nl;
+  }
+  uint64_t ea, eb, ta, tb;
+  block_scan_pair(ss, ls, ea, eb, ta, tb);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = ta;
+    part[2 * blockIdx.x + 1] = tb;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  // last CTA: exclusive scan of the tile sums in place, chunk by chunk
+  __threadfence();
+  const uint32_t nb = gridDim.x;
+  uint64_t ca = 0, cb = 0;
+  for (uint32_t c0 = 0; c0 < nb; c0 += kLayoutThreads) {
+    const uint32_t i = c0 + threadIdx.x;
+    const uint64_t va = i < nb ? __ldcg(part + 2 * i) : 0;
+    const uint64_t vb = i < nb ? __ldcg(part + 2 * i + 1) : 0;
+    block_scan_pair(va, vb, ea, eb, ta, tb);
+    if (i < nb) part[2 * i] = ca + ea, part[2 * i + 1] = cb + eb;
+    ca += ta;
+    cb += tb;
+  }
+  if (threadIdx.x == 0) {
+    tot[0] = ca;
+    tot[1] = cb;
+    tot[2] = (uint64_t)rp[r0 + rows] - rp[r0];
+    *ticket = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kLayoutThreads) k1_layout_apply(
+    uint64_t groups, uint64_t TG, const uint64_t* __restrict__ slots,
+    uint64_t* __restrict__ nlong, const uint64_t* __restrict__ part,
+    const uint64_t* __restrict__ tot, uint32_t* __restrict__ gp) {
+  const uint64_t g0 = blockIdx.x * TG, g1 = min(groups, g0 + TG);
+  const uint64_t q = (g1 - g0 + kLayoutThreads - 1) / kLayoutThreads;
+  const uint64_t ga = min(g1, g0 + threadIdx.x * q), gb = min(g1, ga + q);
+  uint64_t ss = 0, ls = 0;
+  for (uint64_t g = ga; g < gb; ++g) ss += slots[g], ls += nlong[g];
+  uint64_t ea, eb, ta, tb;
+  block_scan_pair(ss, ls, ea, eb, ta, tb);
+  ea += part[2 * blockIdx.x];
+  eb += part[2 * blockIdx.x + 1];
+  for (uint64_t g = ga; g < gb; ++g) {
+    const uint64_t sv = slots[g], lv = nlong[g];
+    gp[g] = (uint32_t)ea;
+    nlong[g] = eb;
+    ea += sv;
+    eb += lv;
+  }
+  if (g1 == groups && threadIdx.x == 0) gp[groups] = (uint32_t)tot[0];
+}
+
 // out[0] = row_ptr[r1] - row_ptr[r0] (the slab's nnz)
 __global__ void slab_nnz(const uint32_t* __restrict__ rp, uint64_t r0, uint64_t r1,
                          uint64_t* __restrict__ out) {
@@ -404,6 +541,14 @@ void split_long_rows(spmvk_rgcsr* h, uint32_t G, uint64_t* counts_dev, cudaStrea
   SPMVK_LAUNCH("count_singles");
 }
 
+// Pinned per-thread landing slot for the converter's small readbacks (a
+// pageable destination costs ~15 us of host time per cudaMemcpyAsync).
+uint64_t* readback_slot() {
+  static thread_local uint64_t* p = nullptr;  // 64 B, kept for the thread's life
+  if (!p) SPMVK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), 64, cudaHostAllocPortable));
+  return p;
+}
+
 // K1 on the device with two host round trips: the slot total, long-row
 // count and nnz (one 24-byte readback, needed to size the arrays and to
 // report a uint32 overflow before writing), and the quad / single counts at
@@ -431,19 +576,38 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
   const unsigned ggrid = persistent_grid((h->groups + 255) / 256, 8);
   TmpBuf<uint64_t> tot(5, s);  // slots, long rows, nnz | quads, singles
   TmpBuf<uint64_t> slots(h->groups, s), nlong(h->groups, s);
-  if (h->rows) {
-    csr_row_lengths<<<rgrid, 256, 0, s>>>(r0, h->rows, a->row_ptr.p, h->row_lengths.p);
-    SPMVK_LAUNCH("csr_row_lengths");
-    group_layout<<<ggrid, 256, 0, s>>>(h->rows, G, h->groups, h->long_cut, h->row_lengths.p,
-                                       slots.p, nlong.p);
-    SPMVK_LAUNCH("group_layout");
+  // SPMVK_K1_LAYOUT=0: the unfused layout kernels + scans (A/B only)
+  static const bool fused_layout = [] {
+    const char* e = std::getenv("SPMVK_K1_LAYOUT");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (fused_layout && h->groups) {
+    const uint64_t TG = std::max<uint64_t>(1, kLayoutRows / G);
+    const uint64_t ntiles = (h->groups + TG - 1) / TG;
+    if (ntiles > 0x7fffffffull) fail(SPMVK_ERANGE, "build_rgcsr: too many row tiles");
+    TmpBuf<uint64_t> part(2 * ntiles, s);
+    k1_layout<<<static_cast<unsigned>(ntiles), kLayoutThreads, 0, s>>>(
+        r0, h->rows, G, h->groups, TG, h->long_cut, a->row_ptr.p, h->row_lengths.p, slots.p,
+        nlong.p, part.p, stream_counters(s) + 3, tot.p);
+    SPMVK_LAUNCH("k1_layout");
+    k1_layout_apply<<<static_cast<unsigned>(ntiles), kLayoutThreads, 0, s>>>(
+        h->groups, TG, slots.p, nlong.p, part.p, tot.p, h->group_pointers.p);
+    SPMVK_LAUNCH("k1_layout_apply");
+  } else {
+    if (h->rows) {
+      csr_row_lengths<<<rgrid, 256, 0, s>>>(r0, h->rows, a->row_ptr.p, h->row_lengths.p);
+      SPMVK_LAUNCH("csr_row_lengths");
+      group_layout<<<ggrid, 256, 0, s>>>(h->rows, G, h->groups, h->long_cut, h->row_lengths.p,
+                                         slots.p, nlong.p);
+      SPMVK_LAUNCH("group_layout");
+    }
+    exclusive_scan_u64_dev(slots.p, h->groups, s, tot.p);
+    exclusive_scan_u64_dev(nlong.p, h->groups, s, tot.p + 1);
+    slab_nnz<<<1, 1, 0, s>>>(a->row_ptr.p, r0, r1, tot.p + 2);
+    SPMVK_LAUNCH("slab_nnz");
   }
-  exclusive_scan_u64_dev(slots.p, h->groups, s, tot.p);
-  exclusive_scan_u64_dev(nlong.p, h->groups, s, tot.p + 1);
-  slab_nnz<<<1, 1, 0, s>>>(a->row_ptr.p, r0, r1, tot.p + 2);
-  SPMVK_LAUNCH("slab_nnz");
-  uint64_t t3[3];
-  SPMVK_CUDA(cudaMemcpyAsync(t3, tot.p, sizeof(t3), cudaMemcpyDeviceToHost, s));
+  uint64_t* t3 = readback_slot();
+  SPMVK_CUDA(cudaMemcpyAsync(t3, tot.p, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
   const uint64_t total = t3[0];
   if (total > 0xffffffffull)
@@ -453,9 +617,11 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
   h->slots = total;
   h->n_long = t3[1];
   h->nnz = t3[2];
-  narrow_pointers<<<persistent_grid((h->groups + 256) / 256, 8), 256, 0, s>>>(
-      h->groups, slots.p, total, h->group_pointers.p);
-  SPMVK_LAUNCH("narrow_pointers");
+  if (!fused_layout || !h->groups) {
+    narrow_pointers<<<persistent_grid((h->groups + 256) / 256, 8), 256, 0, s>>>(
+        h->groups, slots.p, total, h->group_pointers.p);
+    SPMVK_LAUNCH("narrow_pointers");
+  }
   h->values.alloc(total * static_cast<uint64_t>(prec));
   h->columns.alloc(total);
   if (h->groups) {
@@ -516,8 +682,8 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
                                              h->row_lengths.p, nlong.p, h->long_rows.p);
     SPMVK_LAUNCH("long_rows_by_group");
     split_long_rows(h.get(), static_cast<uint32_t>(G), tot.p + 3, s);
-    uint64_t qs[2];
-    SPMVK_CUDA(cudaMemcpyAsync(qs, tot.p + 3, sizeof(qs), cudaMemcpyDeviceToHost, s));
+    uint64_t* qs = readback_slot() + 3;
+    SPMVK_CUDA(cudaMemcpyAsync(qs, tot.p + 3, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     SPMVK_CUDA(cudaStreamSynchronize(s));
     h->n_quads = qs[0];
     h->n_singles = qs[1];

@@ -477,3 +477,52 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=env, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_k1_layout_fused_and_unfused_bitwise(cuda, fused):
+    """Both K1 layout paths (SPMVK_K1_LAYOUT, read once per process, so each
+    runs in a child): the fused two-kernel layout (default; tiles of <= 8,192
+    rows, the last CTA scanning the tile sums) and the unfused kernels +
+    scans.  Group sizes that stage in shared memory with several groups per
+    thread (G = 1, 3), one (G = 32), partial tiles (G = 33, 256), one group
+    per tile (G = 8192) and groups past the staging size (G = 10000); more
+    than 256 tiles (the last CTA's scan crosses chunks); row slabs; long rows
+    (their offsets feed the long-row list: y must be the oracle's)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np
+import oracle as orc
+from helpers import triplets
+from paper_1012_2270_b200 import spmvkit as sk
+cases = [(orc.stencil(5, 1600), (1, 32, 33)), (orc.powerlaw(60000, 7), (1, 3, 32, 256, 8192, 10000)),
+         (orc.banded(20001, 5, 3), (3, 8192, 10000))]
+for om, Gs in cases:
+    m = sk.build_csr(triplets(om))
+    x = orc.random_vector(om.cols, 1)
+    for G in Gs:
+        a = sk.build_rgcsr(m, G, 8)
+        got = a.to_host()
+        want = orc.build_rgcsr(om, G, 8)
+        for k in ("values", "columns", "group_pointers", "row_lengths"):
+            assert np.array_equal(got[k], want[k]), (om.rows, G, k)
+        y = sk.spmv_rgcsr(a, x)
+        assert np.array_equal(y.view(np.uint64), orc.spmv_rgcsr(want, x)[0].view(np.uint64)), (om.rows, G)
+        r0 = G * ((om.rows // G) // 3)
+        if 0 < r0 < om.rows:
+            part = sk.build_rgcsr(m, G, 8, row_range=(r0, om.rows)).to_host()
+            gp = want["group_pointers"]
+            assert np.array_equal(part["values"], want["values"][gp[r0 // G]:]), (om.rows, G)
+            assert np.array_equal(part["row_lengths"], want["row_lengths"][r0:]), (om.rows, G)
+            assert np.array_equal(part["group_pointers"].astype(np.int64),
+                                  gp[r0 // G:].astype(np.int64) - int(gp[r0 // G])), (om.rows, G)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]),
+               SPMVK_K1_LAYOUT=fused)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=env, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
