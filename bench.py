@@ -586,8 +586,13 @@ def run_ours(args):
         raise SystemExit(f"parity gate failed: GPU checksum {ysum!r} != reference {golden!r}")
 
     # ---- e2e: reference-facing C-ABI span overload with pinned HOST buffers
-    xpin = torch.from_numpy(xh).pin_memory()
-    ypin = torch.empty(a.num_rows, dtype=torch.float64).pin_memory()
+    if args.e2e_host == "torch":  # A/B: torch's pinned host allocator
+        xpin = torch.from_numpy(xh).pin_memory()
+        ypin = torch.empty(a.num_rows, dtype=torch.float64).pin_memory()
+    else:  # the library's page-locked 2 MB-page host buffers (spmvk_host_alloc)
+        xpin, ypin = sk.host_array(a.num_cols), sk.host_array(a.num_rows)
+        xpin[:] = xh
+        xpin, ypin = torch.from_numpy(xpin), torch.from_numpy(ypin)
     e2e_steps = max(3, min(args.steps, 50))
     for _ in range(max(args.warmup, 10)):  # untimed: graph capture, first PCIe traffic
         L.spmvk_rgcsr_spmv_host_f64(a._h, xpin.data_ptr(), a.num_cols, ypin.data_ptr(),
@@ -689,7 +694,9 @@ def run_ours(args):
                 "pcie_peak_source": "16 MB up + 16 MB down as two concurrent copy-engine "
                                     "transfers, 344 us (scripts/probes/pcie_sm.cu, "
                                     "profiles/r01_e2e_pipeline.md)",
-                "path": "spmvk_rgcsr_spmv_host_f64 (pinned host x,y; H2D + SpMV + D2H)"},
+                "path": "spmvk_rgcsr_spmv_host_f64 (pinned host x,y; H2D + SpMV + D2H)",
+                "host_buffers": ("spmvk_host_alloc (page-locked, 2 MB pages)"
+                                 if args.e2e_host == "spmvk" else "torch pin_memory")},
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
         "checksum": ysum,
@@ -717,6 +724,9 @@ def main():
                     help="default: 27pt-128 (configs[1]) on one GPU; 7pt-512 (configs[4], the "
                          "iterated, row-slab sharded config) under torchrun with N > 1")
     ap.add_argument("--cpu-reps", type=int, default=10)
+    ap.add_argument("--e2e-host", choices=["spmvk", "torch"], default="spmvk",
+                    help="host x / y buffers of the e2e leg: spmvk_host_alloc (default) or "
+                         "torch pin_memory")
     ap.add_argument("--no-traffic-live", dest="traffic_live", action="store_false",
                     help="report the committed ncu capture instead of measuring the headline "
                          "kernel's DRAM bytes with ncu in a child process")

@@ -73,6 +73,16 @@ int spmvk_init(int device);
  * spmvk_empty_cache returns every cached block to the driver (device < 0:
  * all devices), like torch.cuda.empty_cache for the caching allocator. */
 int spmvk_empty_cache(int device);
+/* Host buffers for the span overloads (*_spmv_host_*): an anonymous mapping
+ * advised to transparent 2 MB huge pages, touched, and page-locked with
+ * cudaHostRegister (portable | mapped), so the pipelined host-span path can
+ * copy x up with the copy engine and store y straight into it.  Any pinned
+ * buffer (cudaHostAlloc, torch pin_memory) works; this one also skips the
+ * slow first calls measured on torch-pinned buffers (profiles/r02t_e2e_env.md).
+ * *out is 2 MB aligned; free with spmvk_host_free.  No reference
+ * counterpart (the reference's spans are over caller memory). */
+int spmvk_host_alloc(uint64_t bytes, void** out);
+int spmvk_host_free(void* p);
 
 /* ------------------------------------------------------------------ CSR ingest
  * Replaces TripletMatrix(num_rows, num_cols, entries) validation

@@ -45,6 +45,8 @@ SIGNATURES = {
     "spmvk_abi_version": (cint, []),
     "spmvk_init": (cint, [cint]),
     "spmvk_empty_cache": (cint, [cint]),
+    "spmvk_host_alloc": (cint, [u64, C.POINTER(vp)]),
+    "spmvk_host_free": (cint, [vp]),
     "spmvk_csr_upload": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
     "spmvk_csr_upload_device": (cint, [u64, u64, u64, vp, vp, vp, cint, vp, C.POINTER(vp)]),
     "spmvk_csr_stencil": (cint, [cint, u64, vp, C.POINTER(vp)]),

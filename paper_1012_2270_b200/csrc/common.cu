@@ -4,6 +4,8 @@
 #include "common.cuh"
 
 #include <cstdlib>
+#include <cstring>
+#include <sys/mman.h>
 #include <map>
 #include <tuple>
 #include <mutex>
@@ -341,6 +343,15 @@ uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s) {
   return total;
 }
 
+std::mutex& host_bufs_mu() {
+  static std::mutex m;
+  return m;
+}
+std::map<void*, uint64_t>& host_bufs() {
+  static std::map<void*, uint64_t> m;
+  return m;
+}
+
 }  // namespace spmvk
 
 extern "C" {
@@ -358,6 +369,53 @@ int spmvk_init(int device) {
     if (p.major != 10)
       spmvk::fail(SPMVK_ECUDA, std::string("spmvk is built for sm_100a; device ") + p.name +
                                    " is sm_" + std::to_string(p.major * 10 + p.minor));
+  });
+}
+
+int spmvk_host_alloc(uint64_t bytes, void** out) {
+  return spmvk::guarded([&] {
+    if (!out) spmvk::fail(SPMVK_EINVAL, "spmvk_host_alloc: null output pointer");
+    *out = nullptr;
+    spmvk::require_device();
+    constexpr uint64_t kHuge = 2ull << 20;
+    const uint64_t size = std::max<uint64_t>(kHuge, (bytes + kHuge - 1) / kHuge * kHuge);
+    void* raw = mmap(nullptr, size + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS,
+                     -1, 0);
+    if (raw == MAP_FAILED) spmvk::fail(SPMVK_ENOMEM, "spmvk_host_alloc: mmap failed");
+    const uintptr_t r = reinterpret_cast<uintptr_t>(raw);
+    const uintptr_t p = (r + kHuge - 1) / kHuge * kHuge;
+    if (p > r) munmap(raw, p - r);  // trim to a 2 MB aligned range
+    if (r + size + kHuge > p + size) munmap(reinterpret_cast<void*>(p + size), r + kHuge - p);
+    void* q = reinterpret_cast<void*>(p);
+    madvise(q, size, MADV_HUGEPAGE);  // advisory: fine if THP is off
+    std::memset(q, 0, size);          // populate before page-locking
+    const cudaError_t e = cudaHostRegister(q, size, cudaHostRegisterPortable |
+                                                        cudaHostRegisterMapped);
+    if (e != cudaSuccess) {
+      munmap(q, size);
+      spmvk::fail(SPMVK_ECUDA, std::string("spmvk_host_alloc: cudaHostRegister: ") +
+                                   cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> lk(spmvk::host_bufs_mu());
+    spmvk::host_bufs()[q] = size;
+    *out = q;
+  });
+}
+
+int spmvk_host_free(void* p) {
+  return spmvk::guarded([&] {
+    if (!p) return;
+    uint64_t size = 0;
+    {
+      std::lock_guard<std::mutex> lk(spmvk::host_bufs_mu());
+      auto it = spmvk::host_bufs().find(p);
+      if (it == spmvk::host_bufs().end())
+        spmvk::fail(SPMVK_EINVAL, "spmvk_host_free: not a spmvk_host_alloc buffer");
+      size = it->second;
+      spmvk::host_bufs().erase(it);
+    }
+    SPMVK_CUDA(cudaHostUnregister(p));
+    munmap(p, size);
   });
 }
 

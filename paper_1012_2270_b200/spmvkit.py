@@ -531,6 +531,32 @@ def build_rgcsr(m, group_size: int, precision=F64, stream: int = 0,
     return RgcsrMatrix(h.value)
 
 
+class _HostBuffer:
+    """Owner of one spmvk_host_alloc block; numpy arrays over it keep it alive."""
+
+    def __init__(self, ptr: int, nbytes: int, dtype: np.dtype, n: int):
+        self.ptr = ptr
+        self.__array_interface__ = {"shape": (n,), "typestr": dtype.str, "version": 3,
+                                    "data": (ptr, False)}
+
+    def __del__(self):
+        if self.ptr:
+            lib().spmvk_host_free(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+def host_array(n: int, dtype=np.float64) -> np.ndarray:
+    """A zeroed numpy array on page-locked 2 MB-page host memory
+    (spmvk_host_alloc) for the span overloads' x and y; freed when the last
+    array over it is collected.  Any pinned buffer works for the pipelined
+    host-span path; this one avoids the slow first calls of freshly pinned
+    4 KB pages (profiles/r02t_e2e_env.md)."""
+    dt = np.dtype(dtype)
+    p = C.c_void_p()
+    _check(lib().spmvk_host_alloc(max(1, n * dt.itemsize), C.byref(p)))
+    return np.asarray(_HostBuffer(p.value, n * dt.itemsize, dt, n))
+
+
 def spmv_rgcsr(a: RgcsrMatrix, x, y=None, multiply_add_count: bool = False,
                stream: Optional[int] = None):
     """spmv_rgcsr(a, x[, y][, &madds]) (rgcsr.hpp:75-105).

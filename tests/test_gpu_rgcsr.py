@@ -526,3 +526,27 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=env, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_host_array_buffers_through_the_span_overload(cuda):
+    """spmvk_host_alloc buffers (sk.host_array: page-locked, 2 MB pages) as x
+    and y of the pipelined host-span SpMV: y bitwise the device-resident
+    result; zero-length and odd sizes allocate; a foreign pointer is refused
+    on free."""
+    import ctypes as C
+    from paper_1012_2270_b200._lib import lib
+    csr = sk.CsrMatrix.stencil(27, 64)
+    a = sk.build_rgcsr(csr, 32)
+    xh = orc.random_vector(a.num_cols, 1)
+    x, y = sk.host_array(a.num_cols), sk.host_array(a.num_rows)
+    assert x.ctypes.data % (2 << 20) == 0 and not y.any()
+    x[:] = xh
+    assert lib().spmvk_rgcsr_spmv_host_f64(a._h, x.ctypes.data, a.num_cols, y.ctypes.data,
+                                           a.num_rows, None) == 0
+    assert bitwise(y, sk.spmv_rgcsr(a, dev(xh)).cpu().numpy())
+    for n in (0, 1, 3, (1 << 18) + 1):
+        z = sk.host_array(n, np.float32)
+        assert z.shape == (n,) and z.dtype == np.float32
+        del z
+    assert lib().spmvk_host_free(C.c_void_p(x.ctypes.data + 8)) != 0
+    del x, y
