@@ -541,7 +541,10 @@ class _HostBuffer:
 
     def __del__(self):
         if self.ptr:
-            lib().spmvk_host_free(C.c_void_p(self.ptr))
+            try:
+                lib().spmvk_host_free(C.c_void_p(self.ptr))
+            except Exception:  # noqa: BLE001 -- interpreter shutdown: the OS reclaims it
+                pass
             self.ptr = 0
 
 

@@ -17,8 +17,13 @@ torch.cuda.set_device(0)
 assert L.spmvk_init(0) == 0
 csr = sk.CsrMatrix.stencil(27, 128)
 a = sk.build_rgcsr(csr, 32, 8)
-xpin = torch.from_numpy(np.random.default_rng(1).random(csr.num_cols)).pin_memory()
-ypin = torch.empty(csr.num_rows, dtype=torch.float64).pin_memory()
+if os.environ.get("E2E_HOST", "spmvk") == "torch":
+    xpin = torch.from_numpy(np.random.default_rng(1).random(csr.num_cols)).pin_memory()
+    ypin = torch.empty(csr.num_rows, dtype=torch.float64).pin_memory()
+else:  # spmvk_host_alloc buffers (the bench default)
+    xpin = torch.from_numpy(sk.host_array(csr.num_cols))
+    xpin.numpy()[:] = np.random.default_rng(1).random(csr.num_cols)
+    ypin = torch.from_numpy(sk.host_array(csr.num_rows))
 
 
 def call():
@@ -45,5 +50,5 @@ ev = json.load(open("gpurun_out/e2e_trace.json"))["traceEvents"]
 gpu = [e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy")]
 gpu.sort(key=lambda e: e["ts"])
 t0 = gpu[0]["ts"]
-for e in gpu[:80]:
+for e in gpu[:int(os.environ.get('E2E_ROWS', '80'))]:
     print(f'{e["ts"]-t0:9.1f} {e["dur"]:7.1f} s{e["args"].get("stream")} {e["name"][:50]}')
