@@ -870,9 +870,12 @@ def bench_distributed(args, metric: str, workloads: dict, clock_cls=None, peaks=
 
     # e2e: every step each rank uploads its x slab from pinned host memory,
     # runs the exchange + slab SpMV, and downloads its y slab
-    xh = torch.from_numpy(gen.random_vector(a.num_cols, 1)[me.row_begin:me.row_end].copy())
-    xh = xh.pin_memory()
-    yh = torch.empty(max(a.num_rows, 1), dtype=torch.float64).pin_memory()
+    # (page-locked 2 MB-page host buffers, spmvk_host_alloc: no slow first
+    # calls, profiles/r02t_e2e_env.md)
+    xs_h = sk.host_array(me.row_end - me.row_begin)
+    xs_h[:] = gen.random_vector(a.num_cols, 1)[me.row_begin:me.row_end]
+    xh = torch.from_numpy(xs_h)
+    yh = torch.from_numpy(sk.host_array(max(a.num_rows, 1)))
     e2e_steps = max(3, min(args.steps, 50))
     dist.barrier()
     torch.cuda.synchronize()
