@@ -203,6 +203,12 @@ double* stream_scratch(cudaStream_t s, uint64_t n) {
 // count finished warps in word 1; the last warp resets them (rgcsr_spmv.cuh
 // LongList).  Launches
 // on one stream are ordered, so they never share a live pair.
+uint64_t* pinned_slot() {
+  static thread_local uint64_t* p = nullptr;  // kept for the thread's life
+  if (!p) SPMVK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), 64, cudaHostAllocPortable));
+  return p;
+}
+
 uint32_t* stream_counters(cudaStream_t s) {
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, DevBuf<uint32_t>> bufs;
@@ -337,10 +343,10 @@ uint64_t exclusive_scan_u64(uint64_t* d, uint64_t n, cudaStream_t s) {
   if (n == 0) return 0;
   TmpBuf<uint64_t> tot(1, s);
   exclusive_scan_u64_dev(d, n, s, tot.p);
-  uint64_t total = 0;
-  SPMVK_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  uint64_t* slot = pinned_slot();
+  SPMVK_CUDA(cudaMemcpyAsync(slot, tot.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
-  return total;
+  return slot[0];
 }
 
 std::mutex& host_bufs_mu() {

@@ -311,6 +311,10 @@ HostStage& host_stage();
 // Device scratch of >= n doubles private to (current device, stream s).
 double* stream_scratch(cudaStream_t s, uint64_t n);
 uint32_t* stream_counters(cudaStream_t s);
+// Pinned per-thread 64-byte landing slot for the converters' small
+// synchronous readbacks (a pageable destination costs ~15-30 us of host time
+// per cudaMemcpyAsync, profiles/r02t_k1_timeline.md).
+uint64_t* pinned_slot();
 
 }  // namespace spmvk
 

@@ -375,16 +375,17 @@ __global__ void csr_row_lengths(uint64_t r0, uint64_t rows, const uint32_t* __re
 
 void row_length_range(const spmvk_csr* a, uint64_t r0, uint64_t r1, unsigned* mx, unsigned* mn,
                       cudaStream_t s) {
-  DevBuf<unsigned> out(2);
-  unsigned init[2] = {0, 0xffffffffu};
-  SPMVK_CUDA(cudaMemcpyAsync(out.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  TmpBuf<unsigned> out(2, s);
+  unsigned* h = reinterpret_cast<unsigned*>(pinned_slot());
+  h[0] = 0;
+  h[1] = 0xffffffffu;
+  SPMVK_CUDA(cudaMemcpyAsync(out.p, h, 2 * sizeof(unsigned), cudaMemcpyHostToDevice, s));
   if (r1 > r0) {
     row_len_range<<<persistent_grid((r1 - r0 + 255) / 256, 8), 256, 0, s>>>(
         r1 - r0, a->row_ptr.p + r0, out.p);
     SPMVK_LAUNCH("row_len_range");
   }
-  unsigned h[2];
-  SPMVK_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaMemcpyAsync(h, out.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
   *mx = h[0];
   *mn = r1 > r0 ? h[1] : 0;

@@ -359,6 +359,28 @@ __global__ void ell_nnz_recount(uint64_t rows, uint32_t k1, const T* __restrict_
   if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
 }
 
+// The same count from the CSR the ELL part was filled from, without reading
+// the ELL arrays back (27-pt fp64: 110 us -> a pass over row_ptr): real
+// entries fill slots 0..n-1 (n = min(len, K1)) with strictly increasing
+// columns and pads carry (0, column 0), so the recount above stops exactly at
+// n -- except a row whose only ELL entry is a stored zero (after the cast to
+// the ELL precision) at column 0, which it counts as empty.
+template <class T, class V>
+__global__ void ell_nnz_from_csr(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
+                                 const uint32_t* __restrict__ col, const V* __restrict__ val,
+                                 unsigned long long* out) {
+  unsigned long long total = 0;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rp[r];
+    uint32_t n = min(rp[r + 1] - b, k1);
+    if (n == 1 && col[b] == 0 && static_cast<T>(val[b]) == T(0)) n = 0;
+    total += n;
+  }
+  for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
+}
+
 // ------------------------------------------------------------ to_triplets
 // ellpack.hpp:219-240: ELL rows through the ell_row_length recount, then the
 // COO overflow; per row the ELL columns precede the COO ones, so the result is
@@ -1160,14 +1182,27 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len)
   DevBuf<unsigned long long> cnt(1);
   SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
   if (h->k1 && a->rows) {
-    ell_nnz_recount<T><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
-                                            reinterpret_cast<const T*>(h->ell_values.p),
-                                            h->ell_columns.p, cnt.p);
-    SPMVK_LAUNCH("ell_nnz_recount");
+    // SPMVK_ELL_RECOUNT=1: recount from the written ELL arrays (A/B, tests)
+    static const bool recount = [] {
+      const char* e = std::getenv("SPMVK_ELL_RECOUNT");
+      return e && std::atoi(e) != 0;
+    }();
+    if (recount) {
+      ell_nnz_recount<T><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
+                                              reinterpret_cast<const T*>(h->ell_values.p),
+                                              h->ell_columns.p, cnt.p);
+      SPMVK_LAUNCH("ell_nnz_recount");
+    } else {
+      ell_nnz_from_csr<T, V><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
+                                                  a->row_ptr.p, a->col.p,
+                                                  reinterpret_cast<const V*>(a->val.p), cnt.p);
+      SPMVK_LAUNCH("ell_nnz_from_csr");
+    }
   }
-  unsigned long long ell_nnz = 0;
-  SPMVK_CUDA(cudaMemcpyAsync(&ell_nnz, cnt.p, sizeof(ell_nnz), cudaMemcpyDeviceToHost, s));
+  uint64_t* slot = pinned_slot();
+  SPMVK_CUDA(cudaMemcpyAsync(slot, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long ell_nnz = slot[0];
   h->fill_nnz = ell_nnz + coo;
 }
 
@@ -1203,10 +1238,11 @@ spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
     coo_max_column<<<persistent_grid((h->coo + 255) / 256, 4), 256, 0, s>>>(
         h->coo, h->coo_columns.p, mc.p);
     SPMVK_LAUNCH("coo_max_column");
-    uint32_t mr = 0, mcol = 0;
-    SPMVK_CUDA(cudaMemcpyAsync(&mr, h->coo_rows.p + h->coo - 1, 4, cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaMemcpyAsync(&mcol, mc.p, 4, cudaMemcpyDeviceToHost, s));
+    uint32_t* slot = reinterpret_cast<uint32_t*>(pinned_slot());
+    SPMVK_CUDA(cudaMemcpyAsync(slot, h->coo_rows.p + h->coo - 1, 4, cudaMemcpyDeviceToHost, s));
+    SPMVK_CUDA(cudaMemcpyAsync(slot + 1, mc.p, 4, cudaMemcpyDeviceToHost, s));
     SPMVK_CUDA(cudaStreamSynchronize(s));
+    const uint32_t mr = slot[0], mcol = slot[1];
     h->coo_max_row = mr;  // COO is sorted by row
     h->coo_max_col = mcol;
   }

@@ -541,14 +541,6 @@ void split_long_rows(spmvk_rgcsr* h, uint32_t G, uint64_t* counts_dev, cudaStrea
   SPMVK_LAUNCH("count_singles");
 }
 
-// Pinned per-thread landing slot for the converter's small readbacks (a
-// pageable destination costs ~15 us of host time per cudaMemcpyAsync).
-uint64_t* readback_slot() {
-  static thread_local uint64_t* p = nullptr;  // 64 B, kept for the thread's life
-  if (!p) SPMVK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), 64, cudaHostAllocPortable));
-  return p;
-}
-
 // K1 on the device with two host round trips: the slot total, long-row
 // count and nnz (one 24-byte readback, needed to size the arrays and to
 // report a uint32 overflow before writing), and the quad / single counts at
@@ -606,7 +598,7 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
     slab_nnz<<<1, 1, 0, s>>>(a->row_ptr.p, r0, r1, tot.p + 2);
     SPMVK_LAUNCH("slab_nnz");
   }
-  uint64_t* t3 = readback_slot();
+  uint64_t* t3 = pinned_slot();
   SPMVK_CUDA(cudaMemcpyAsync(t3, tot.p, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
   const uint64_t total = t3[0];
@@ -682,7 +674,7 @@ spmvk_rgcsr* build(const spmvk_csr* a, uint64_t r0, uint64_t r1, uint64_t G, int
                                              h->row_lengths.p, nlong.p, h->long_rows.p);
     SPMVK_LAUNCH("long_rows_by_group");
     split_long_rows(h.get(), static_cast<uint32_t>(G), tot.p + 3, s);
-    uint64_t* qs = readback_slot() + 3;
+    uint64_t* qs = pinned_slot() + 3;
     SPMVK_CUDA(cudaMemcpyAsync(qs, tot.p + 3, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     SPMVK_CUDA(cudaStreamSynchronize(s));
     h->n_quads = qs[0];

@@ -403,3 +403,47 @@ def test_dyn_walk_threshold_edges(cuda, prec):
     a = sk.build_rgcsr(m, 32, prec)
     assert bitwise(sk.spmv_rgcsr(a, dev(x)).cpu().numpy(),
                    orc.spmv_rgcsr(orc.build_rgcsr(om, 32, prec), x)[0])
+
+
+def _ell_row_length_ref(ev, ec, rows, k1):
+    """ellpack.hpp:55-72 (ell_row_length) over slot-major arrays, per row."""
+    out = np.zeros(rows, np.int64)
+    for r in range(rows):
+        n, prev = 0, 0
+        for slot in range(k1):
+            c, v = int(ec[slot * rows + r]), ev[slot * rows + r]
+            if slot > 0 and c <= prev:
+                break
+            if slot == 0 and c == 0 and v == 0:
+                if not (k1 > 1 and int(ec[rows + r]) > 0):
+                    break
+            n += 1
+            prev = c
+        out[r] = n
+    return out
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_ell_nnz_with_stored_zeros_at_column_0(cuda, prec):
+    """fill_report's ELL nnz is counted from the CSR (not by re-reading the
+    ELL arrays): rows whose only ELL entry is a stored zero at column 0 (also
+    -0.0, and 1e-50 which is zero only after the cast to fp32) count as empty,
+    exactly as the reference's ell_row_length recount of the layout; K1 = 1
+    truncates a stored zero at column 0 with a real successor to empty."""
+    rows_ = [[(0, 0.0)], [(0, 1.0)], [(0, 0.0), (5, 1.0)], [], [(3, 0.0)], [(0, -0.0)],
+             [(0, 1e-50)], [(c, 0.0 if c == 0 else 1.0) for c in range(0, 20, 2)],
+             [(1, 2.0), (2, 0.0)], [(0, 0.0), (1, 0.0), (2, 0.0)]]
+    rp = np.zeros(len(rows_) + 1, np.uint32)
+    col, val = [], []
+    for i, r in enumerate(rows_):
+        rp[i + 1] = rp[i] + len(r)
+        col += [c for c, _ in r]
+        val += [v for _, v in r]
+    om = orc.Csr(len(rows_), 24, rp, np.array(col, np.uint32), np.array(val, np.float64))
+    m = sk.build_csr(triplets(om))
+    for k1 in (1, 2, 3, 10):
+        h = sk.build_hybrid(m, k1, prec)
+        ref = orc.build_hybrid(om, k1, prec)
+        want = int(_ell_row_length_ref(ref["ell_values"], ref["ell_columns"], om.rows, k1).sum())
+        want += ref["coo_rows"].size
+        assert sk.fill_report(h).nnz == want, (k1, prec)
