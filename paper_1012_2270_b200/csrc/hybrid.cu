@@ -1088,7 +1088,7 @@ void collect_dyn_heavy(spmvk_hybrid* h, cudaStream_t s) {
 template <class T, class V>
 void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len) {
   const unsigned grid = persistent_grid((a->rows + 255) / 256, 8);
-  DevBuf<uint64_t> off(a->rows);
+  TmpBuf<uint64_t> off(a->rows, s);  // per-row COO counts (stream-ordered scratch)
   // bulk-copy fill for matrices whose 32-row blocks fit a stage (rows of at
   // most 32 entries: 27-pt 405 -> 240 us); long-row matrices keep the
   // thread-per-row fill (power-law 8M 361 vs 422 us).  SPMVK_ELL_BULK=0 / 1
@@ -1116,7 +1116,8 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len)
         h->ell_columns.p, off.p);
     SPMVK_LAUNCH("hybrid_ell_fill");
   }
-  const uint64_t coo = exclusive_scan_u64(off.p, a->rows, s);
+  // no row longer than K1 -> no COO part: skip the scan and its readback
+  const uint64_t coo = max_len <= h->k1 ? 0 : exclusive_scan_u64(off.p, a->rows, s);
   h->coo = coo;
   h->coo_rows.alloc(coo);
   h->coo_columns.alloc(coo);
