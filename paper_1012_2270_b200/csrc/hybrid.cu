@@ -322,63 +322,39 @@ __global__ void coo_tile_bounds(uint64_t ntiles, uint64_t rows, uint64_t n,
   }
 }
 
-__global__ void coo_max_column(uint64_t n, const uint32_t* __restrict__ cc, unsigned* out) {
-  unsigned m = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    m = max(m, cc[i]);
-  m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
-
 // FillReport's ELL nnz (fill.hpp:61-65 -> ell_nnz, ellpack.hpp:55-78): the
-// reference recounts real slots from the layout — the first non-increasing
+// reference recounts real slots from the layout -- the first non-increasing
 // column starts the pad region, and a lone stored zero at column 0 counts as
-// empty — so a stored zero can change fill_report.  Same recount, thread per row.
-template <class T>
-__global__ void ell_nnz_recount(uint64_t rows, uint32_t k1, const T* __restrict__ ev,
-                                const uint32_t* __restrict__ ec, unsigned long long* out) {
-  unsigned long long total = 0;
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
-       r += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t len = 0, prev = 0;
-    for (uint32_t slot = 0; slot < k1; ++slot) {
-      const uint64_t idx = (uint64_t)slot * rows + r;
-      const uint32_t c = ec[idx];
-      if (slot > 0 && c <= prev) break;
-      if (slot == 0 && c == 0 && ev[idx] == T(0)) {
-        const bool real_successor = k1 > 1 && ec[rows + r] > 0;
-        if (!real_successor) break;
-      }
-      ++len;
-      prev = c;
-    }
-    total += len;
-  }
-  for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-  if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
-}
-
+// empty -- so a stored zero can change fill_report.
 // The same count from the CSR the ELL part was filled from, without reading
 // the ELL arrays back (27-pt fp64: 110 us -> a pass over row_ptr): real
 // entries fill slots 0..n-1 (n = min(len, K1)) with strictly increasing
 // columns and pads carry (0, column 0), so the recount above stops exactly at
 // n -- except a row whose only ELL entry is a stored zero (after the cast to
 // the ELL precision) at column 0, which it counts as empty.
+// The same pass yields the COO part's largest column (out[1], for
+// spmv_coo's bounds check): a row's COO entries are its columns past K1, in
+// increasing order, so the row's last column.
 template <class T, class V>
 __global__ void ell_nnz_from_csr(uint64_t rows, uint32_t k1, const uint32_t* __restrict__ rp,
                                  const uint32_t* __restrict__ col, const V* __restrict__ val,
                                  unsigned long long* out) {
   unsigned long long total = 0;
+  uint32_t mc = 0;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = rp[r];
-    uint32_t n = min(rp[r + 1] - b, k1);
+    const uint32_t b = rp[r], len = rp[r + 1] - b;
+    uint32_t n = min(len, k1);
     if (n == 1 && col[b] == 0 && static_cast<T>(val[b]) == T(0)) n = 0;
     total += n;
+    if (len > k1) mc = max(mc, col[b + len - 1]);
   }
   for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-  if ((threadIdx.x & 31) == 0 && total) atomicAdd(out, total);
+  mc = __reduce_max_sync(0xffffffffu, mc);
+  if ((threadIdx.x & 31) == 0) {
+    if (total) atomicAdd(out, total);
+    if (mc) atomicMax(out + 1, (unsigned long long)mc);
+  }
 }
 
 // ------------------------------------------------------------ to_triplets
@@ -1180,30 +1156,26 @@ void fill(spmvk_hybrid* h, const spmvk_csr* a, cudaStream_t s, unsigned max_len)
     }
     collect_dyn_heavy(h, s);
   }
-  DevBuf<unsigned long long> cnt(1);
-  SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
-  if (h->k1 && a->rows) {
-    // SPMVK_ELL_RECOUNT=1: recount from the written ELL arrays (A/B, tests)
-    static const bool recount = [] {
-      const char* e = std::getenv("SPMVK_ELL_RECOUNT");
-      return e && std::atoi(e) != 0;
-    }();
-    if (recount) {
-      ell_nnz_recount<T><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
-                                              reinterpret_cast<const T*>(h->ell_values.p),
-                                              h->ell_columns.p, cnt.p);
-      SPMVK_LAUNCH("ell_nnz_recount");
-    } else {
-      ell_nnz_from_csr<T, V><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
-                                                  a->row_ptr.p, a->col.p,
-                                                  reinterpret_cast<const V*>(a->val.p), cnt.p);
-      SPMVK_LAUNCH("ell_nnz_from_csr");
-    }
+  TmpBuf<unsigned long long> cnt(2, s);  // ELL nnz, largest COO column
+  SPMVK_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
+  if (a->rows) {
+    ell_nnz_from_csr<T, V><<<grid, 256, 0, s>>>(a->rows, static_cast<uint32_t>(h->k1),
+                                                a->row_ptr.p, a->col.p,
+                                                reinterpret_cast<const V*>(a->val.p), cnt.p);
+    SPMVK_LAUNCH("ell_nnz_from_csr");
   }
   uint64_t* slot = pinned_slot();
-  SPMVK_CUDA(cudaMemcpyAsync(slot, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SPMVK_CUDA(cudaMemcpyAsync(slot, cnt.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             s));
+  if (coo)
+    SPMVK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(slot + 2), h->coo_rows.p + coo - 1, 4,
+                               cudaMemcpyDeviceToHost, s));
   SPMVK_CUDA(cudaStreamSynchronize(s));
   const unsigned long long ell_nnz = slot[0];
+  if (coo) {  // bounds of the COO part, for spmv_coo's check (COO is sorted by row)
+    h->coo_max_col = static_cast<uint32_t>(slot[1]);
+    h->coo_max_row = reinterpret_cast<const uint32_t*>(slot + 2)[0];
+  }
   h->fill_nnz = ell_nnz + coo;
 }
 
@@ -1233,20 +1205,6 @@ spmvk_hybrid* build(const spmvk_csr* a, int64_t k1, int prec, cudaStream_t s) {
   if (prec == SPMVK_F64) fill<double, double>(h.get(), a, s, mx);
   else if (a->val_prec == SPMVK_F64) fill<float, double>(h.get(), a, s, mx);
   else fill<float, float>(h.get(), a, s, mx);
-  if (h->coo) {  // bounds of the COO part, for spmv_coo's check
-    DevBuf<unsigned> mc(1);
-    SPMVK_CUDA(cudaMemsetAsync(mc.p, 0, 4, s));
-    coo_max_column<<<persistent_grid((h->coo + 255) / 256, 4), 256, 0, s>>>(
-        h->coo, h->coo_columns.p, mc.p);
-    SPMVK_LAUNCH("coo_max_column");
-    uint32_t* slot = reinterpret_cast<uint32_t*>(pinned_slot());
-    SPMVK_CUDA(cudaMemcpyAsync(slot, h->coo_rows.p + h->coo - 1, 4, cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaMemcpyAsync(slot + 1, mc.p, 4, cudaMemcpyDeviceToHost, s));
-    SPMVK_CUDA(cudaStreamSynchronize(s));
-    const uint32_t mr = slot[0], mcol = slot[1];
-    h->coo_max_row = mr;  // COO is sorted by row
-    h->coo_max_col = mcol;
-  }
   return h.release();
 }
 
